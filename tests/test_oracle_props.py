@@ -1,0 +1,385 @@
+"""Pins of the CPU oracle to closed forms, brute force, library routines and invariants
+(things the mathematics fixes, independent of the oracle's own code).  No CUDA."""
+import math
+
+import numpy as np
+import pytest
+from scipy import integrate, optimize
+
+from paper_2211_00705_b200 import workloads as W
+
+VAP, LIQ = 0, 1
+EOS = W.EOS_293K
+PRM = W.PARAMS
+
+
+@pytest.fixture(scope="module")
+def th(oracle_mod):
+    return oracle_mod.thresholds(EOS)
+
+
+# ---------------------------------------------------------------------------- EOS / thermo
+def test_phase_regions(oracle_mod, th):
+    # Omega_vap = (0, rho_t], Omega_spin = (rho_t, rho_min), Omega_liq = [rho_min, inf)
+    assert oracle_mod.phase(EOS, th["rho_tilde"]) == VAP
+    assert oracle_mod.phase(EOS, th["rho_min"]) == LIQ
+    assert oracle_mod.phase(EOS, 0.5 * (th["rho_tilde"] + th["rho_min"])) == 2
+    assert oracle_mod.phase(EOS, np.nextafter(th["rho_min"], 0)) == 2
+
+
+def test_thresholds_satisfy_equal_area(oracle_mod, th):
+    """R3: integral of v dp along liquid -> linear spinodal -> vapour between the two
+    saturation states vanishes; checked by adaptive quadrature of the piecewise EOS."""
+    a2, al2, r0, p0 = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"]
+    rmin, rt = th["rho_min"], th["rho_tilde"]
+    p_of = lambda r: (a2 * r if r <= rt else (p0 + al2 * (r - r0) if r >= rmin else
+                      EOS["p_min"] + (a2 * rt - EOS["p_min"]) * (r - rmin) / (rt - rmin)))
+    dp_dr = lambda r: (a2 if r <= rt else (al2 if r >= rmin else (a2 * rt - EOS["p_min"]) / (rt - rmin)))
+    f = lambda r: dp_dr(r) / r  # v dp = (1/rho) (dp/drho) drho
+    pts = [p0 / a2, rt, rmin, r0]
+    total = sum(integrate.quad(f, pts[i + 1], pts[i], limit=200, epsabs=1e-10)[0] for i in range(3))
+    assert abs(total) < 1e-6 * a2
+    assert p_of(rt) == pytest.approx(th["p_tilde"], rel=1e-14)
+    assert p_of(rmin) == pytest.approx(EOS["p_min"], abs=1e-6)
+
+
+@pytest.mark.parametrize("ph,p", [(VAP, 1000.0), (VAP, 4000.0), (LIQ, 1e5), (LIQ, -3e6)])
+def test_gibbs_is_integral_of_v_dp(oracle_mod, ph, p):
+    # P:127 g = f + p/rho => dg = v dp at constant T, g(p0) = 0; quadrature of v(p)
+    a2, al2, r0, p0 = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"]
+    v = (lambda q: a2 / q) if ph == VAP else (lambda q: 1.0 / (r0 + (q - p0) / al2))
+    ref = integrate.quad(v, p0, p, epsabs=1e-12, epsrel=1e-13)[0]
+    assert oracle_mod.gibbs(EOS, ph, p) == pytest.approx(ref, rel=1e-10, abs=1e-9)
+
+
+@pytest.mark.parametrize("ph,rs,rk", [(VAP, 0.01, 0.02), (LIQ, 995.0, 1001.0), (LIQ, 990.0, 999.0)])
+def test_rarefaction_branch_quadrature(oracle_mod, ph, rs, rk):
+    # f = int_{p_K}^{p*} v/a dzeta for p* <= p_K; numerical quadrature in pressure
+    a2, al2, r0, p0 = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"]
+    if ph == VAP:
+        rho_of, a, pK, ps = (lambda q: q / a2), math.sqrt(a2), a2 * rk, a2 * rs
+    else:
+        rho_of, a, pK, ps = (lambda q: r0 + (q - p0) / al2), math.sqrt(al2), p0 + al2 * (rk - r0), p0 + al2 * (rs - r0)
+    ref = integrate.quad(lambda q: 1.0 / (rho_of(q) * a), pK, ps, epsabs=1e-13, epsrel=1e-12)[0]
+    assert oracle_mod.wave_f(EOS, ph, rs, rk) == pytest.approx(ref, rel=1e-9)
+
+
+@pytest.mark.parametrize("ph,rk,rs", [(VAP, 0.01, 0.02), (LIQ, 999.0, 1001.0)])
+def test_shock_branch_rankine_hugoniot(oracle_mod, ph, rk, rs):
+    """Shock branch must give a state (rs, u*) joined to (rk, u) by a discontinuity
+    obeying the jump conditions: [[rho (u - S)]] = 0, rho(u-S)[[u]] + [[p]] = 0."""
+    u = 13.0
+    f = oracle_mod.wave_f(EOS, ph, rs, rk)
+    us = u - f  # left-facing shock: u* = u_K - f
+    pk, ps = oracle_mod.pressure(EOS, ph, rk), oracle_mod.pressure(EOS, ph, rs)
+    S = (rs * us - rk * u) / (rs - rk)  # from mass conservation
+    Q = rk * (u - S)
+    assert rs * (us - S) == pytest.approx(Q, rel=1e-12)
+    assert Q * (us - u) + (ps - pk) == pytest.approx(0.0, abs=1e-9 * abs(ps - pk))
+
+
+# ---------------------------------------------------------------------------- single phase
+@pytest.mark.parametrize("ph,r1,r2,du", [(LIQ, 1000.0, 999.0, 5.0), (VAP, 0.02, 0.025, 100.0)])
+def test_two_rarefactions_closed_form(oracle_mod, ph, r1, r2, du):
+    # both waves rarefactions: a ln(r*/r1) + a ln(r*/r2) + du = 0 => r* = sqrt(r1 r2) exp(-du/(2a))
+    a = EOS["a_l"] if ph == LIQ else math.sqrt(EOS["a_v2"])
+    rs = oracle_mod.single_phase_star(EOS, ph, r1, -du / 2, r2, du / 2)
+    assert rs == pytest.approx(math.sqrt(r1 * r2) * math.exp(-du / (2 * a)), rel=1e-13)
+
+
+@pytest.mark.parametrize("ph,r,s", [(LIQ, 1000.0, 3.0), (VAP, 0.02, 60.0)])
+def test_symmetric_two_shocks_closed_form(oracle_mod, ph, r, s):
+    # 2 a (r*-r)/sqrt(r r*) = 2s => sqrt(r*/r) = (x + sqrt(x^2 + 4))/2, x = s/a
+    a = EOS["a_l"] if ph == LIQ else math.sqrt(EOS["a_v2"])
+    x = s / a
+    rs = oracle_mod.single_phase_star(EOS, ph, r, s, r, -s)
+    assert rs == pytest.approx(r * ((x + math.sqrt(x * x + 4)) / 2) ** 2, rel=1e-13)
+
+
+def test_creation_trigger_equals_star_threshold(oracle_mod, th):
+    """App. B (i): p* < p_min (liquid) / p* > p_tilde (vapour) from the bisected single-phase
+    star state, against the oracle's monotone-function test (R7), 600 random edges."""
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        rl, rr = rng.uniform(994.5, 1003, 2)
+        ul, ur = rng.uniform(-30, 30, 2)
+        rs = oracle_mod.single_phase_star(EOS, LIQ, rl, ul, rr, ur)
+        assert oracle_mod.creation_trigger(EOS, LIQ, rl, ul, rr, ur) == (rs < th["rho_min"])
+    for _ in range(300):
+        rl, rr = rng.uniform(0.01, 0.032, 2)
+        ul, ur = rng.uniform(-150, 150, 2)
+        rs = oracle_mod.single_phase_star(EOS, VAP, rl, ul, rr, ur)
+        assert oracle_mod.creation_trigger(EOS, VAP, rl, ul, rr, ur) == (rs > th["rho_tilde"])
+
+
+# ---------------------------------------------------------------------------- HLL
+def test_hll_consistency_and_upwinding(oracle_mod):
+    a, p = EOS["a_l"], lambda r: EOS["p0"] + EOS["a_l"] ** 2 * (r - EOS["rho0"])
+    r, u = 1000.5, 12.0
+    F = oracle_mod.hll(EOS, r, r * u, r, r * u)
+    assert F[0] == pytest.approx(r * u, rel=1e-14)
+    assert F[1] == pytest.approx(r * u * u + p(r), rel=1e-14)
+    # supersonic to the right: pure upwind flux of the left state
+    rl, ul, rr, ur = 1000.0, 1600.0, 1001.0, 1700.0
+    F = oracle_mod.hll(EOS, rl, rl * ul, rr, rr * ur)
+    assert F == (rl * ul, rl * ul * ul + p(rl)) or F == pytest.approx((rl * ul, rl * ul * ul + p(rl)), rel=1e-15)
+
+
+def test_hll_integral_form(oracle_mod):
+    """HLL = flux of the single intermediate state U_hll obtained from the integral form of the
+    conservation law over the Riemann fan (Toro §10.3): F = F_L + S_L (U_hll - U_L)."""
+    a2 = EOS["a_v2"]
+    a = math.sqrt(a2)
+    rl, ul, rr, ur = 0.02, 30.0, 0.015, -20.0
+    UL, UR = np.array([rl, rl * ul]), np.array([rr, rr * ur])
+    FL, FR = np.array([rl * ul, rl * ul * ul + a2 * rl]), np.array([rr * ur, rr * ur * ur + a2 * rr])
+    SL, SR = min(ul, ur) - a, max(ul, ur) + a
+    Uh = (SR * UR - SL * UL - (FR - FL)) / (SR - SL)
+    F = oracle_mod.hll(EOS, rl, rl * ul, rr, rr * ur)
+    np.testing.assert_allclose(F, FL + SL * (Uh - UL), rtol=1e-12)
+    np.testing.assert_allclose(F, FR + SR * (Uh - UR), rtol=1e-12)
+
+
+# ---------------------------------------------------------------------------- interface
+def _iface_cases():
+    rng = np.random.default_rng(3)
+    out = [(1000.0, 0.0, 0.02, 0.0), (0.02, 0.0, 1000.0, 0.0), (998.5, -40.0, 0.01, 35.0)]
+    for _ in range(20):
+        rl, ul, rv = rng.uniform(995, 1002), rng.uniform(-150, 150), rng.uniform(0.003, 0.03)
+        uv = ul + rng.uniform(-200, 200)
+        out.append((rl, ul, rv, uv) if rng.random() < 0.5 else (rv, uv, rl, ul))
+    return out
+
+
+@pytest.mark.parametrize("case", _iface_cases())
+def test_interface_jump_conditions_and_entropy(oracle_mod, th, case):
+    """App. A solution obeys the jump conditions (P:198-199 -> P:1527-1528), the kinetic
+    relation (R2) re-evaluated here with numpy logs, and the entropy sign z[[g+e]] >= 0
+    (P:227-231)."""
+    rm, um, rp, up = case
+    s = oracle_mod.interface_solve(EOS, PRM, rm, um, rp, up)
+    z, w = s["z"], s["w"]
+    assert s["rho_minus"] * (s["u_minus"] - w) == pytest.approx(-z, rel=1e-9, abs=1e-12)
+    assert s["rho_plus"] * (s["u_plus"] - w) == pytest.approx(-z, rel=1e-9, abs=1e-12)
+    assert -z * s["u_minus"] + s["p_minus"] == pytest.approx(-z * s["u_plus"] + s["p_plus"], rel=1e-11)
+    # kinetic relation with interface-relative kinetic energy
+    a2, al2, r0, p0 = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"]
+    vap_minus = rm < 1.0
+    g = lambda r, vap: a2 * np.log(a2 * r / p0) if vap else al2 * np.log(r / r0)
+    gm, gp = g(s["rho_minus"], vap_minus), g(s["rho_plus"], not vap_minus)
+    em, ep = 0.5 * (s["u_minus"] - w) ** 2, 0.5 * (s["u_plus"] - w) ** 2
+    pV = s["p_minus"] if vap_minus else s["p_plus"]
+    jump = (gp + ep) - (gm + em)
+    assert z == pytest.approx(th["tau"] * pV * jump, rel=1e-8, abs=1e-12)
+    assert z * jump >= 0.0
+    # flux F_PB equals the physical flux relative to the moving boundary on both sides
+    for r_, u_, p_ in ((s["rho_minus"], s["u_minus"], s["p_minus"]), (s["rho_plus"], s["u_plus"], s["p_plus"])):
+        assert s["F0"] == pytest.approx(r_ * (u_ - w), rel=1e-9, abs=1e-12)
+        assert s["F1"] == pytest.approx(r_ * u_ * (u_ - w) + p_, rel=1e-10)
+
+
+def test_interface_mirror_and_galilean(oracle_mod):
+    base = oracle_mod.interface_solve(EOS, PRM, 1000.0, 10.0, 0.02, -5.0)
+    mir = oracle_mod.interface_solve(EOS, PRM, 0.02, 5.0, 1000.0, -10.0)
+    assert mir["z"] == pytest.approx(-base["z"], rel=1e-11)
+    assert mir["w"] == pytest.approx(-base["w"], rel=1e-11)
+    assert mir["p_minus"] == pytest.approx(base["p_plus"], rel=1e-13)
+    c = 37.5
+    sh = oracle_mod.interface_solve(EOS, PRM, 1000.0, 10.0 + c, 0.02, -5.0 + c)
+    assert sh["p_minus"] == pytest.approx(base["p_minus"], rel=1e-13)
+    assert sh["z"] == pytest.approx(base["z"], rel=1e-10)
+    assert sh["w"] == pytest.approx(base["w"] + c, rel=1e-12)
+
+
+def test_interface_against_scipy_root(oracle_mod):
+    """Brute force: the 2x2 system written independently with numpy/scipy (hybr)."""
+    a2, al2, r0, p0, al = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"], EOS["a_l"]
+    tau = oracle_mod.thresholds(EOS)["tau"]
+    rL, uL, rV, uV = 999.0, 20.0, 0.018, -30.0  # liquid minus, vapour plus
+
+    def fw(a, rs, rk):
+        return a * np.log(rs / rk) if rs <= rk else a * (rs - rk) / np.sqrt(rs * rk)
+
+    def G(x):
+        pV, pL = x
+        rVs, rLs = pV / a2, r0 + (pL - p0) / al2
+        jg = a2 * np.log(pV / p0) - al2 * np.log(rLs / r0)  # g_plus - g_minus (vapour plus)
+        jv, jv2 = 1 / rVs - 1 / rLs, 1 / rVs ** 2 - 1 / rLs ** 2
+        A, B = 0.5 * tau * pV * jv2, tau * pV * jg
+        z = (1 - np.sqrt(1 - 4 * A * B)) / (2 * A)
+        return [(pV - pL + z * z * jv) / p0, (fw(al, rLs, rL) + fw(np.sqrt(a2), rVs, rV) + z * jv + uV - uL) / 300]
+
+    x = optimize.fsolve(G, [2500.0, 2500.0], xtol=1e-14)
+    s = oracle_mod.interface_solve(EOS, PRM, rL, uL, rV, uV)
+    assert s["p_plus"] == pytest.approx(x[0], rel=1e-10)
+    assert s["p_minus"] == pytest.approx(x[1], rel=1e-10)
+
+
+def test_interface_no_transition_limit(oracle_mod):
+    """z = 0 (tau -> 0) gives [[p]] = [[u]] = 0 and F = (0, p*) - a single scalar
+    equation solved here by bisection."""
+    eos = dict(EOS)
+    eos["tau"] = 1e-20
+    rL, uL, rV, uV = 1000.0, 5.0, 0.02, -3.0
+    s = oracle_mod.interface_solve(eos, PRM, rL, uL, rV, uV)
+    a2, al2, r0, p0, al = EOS["a_v2"], EOS["a_l"] ** 2, EOS["rho0"], EOS["p0"], EOS["a_l"]
+
+    def fw(a, rs, rk):
+        return a * math.log(rs / rk) if rs <= rk else a * (rs - rk) / math.sqrt(rs * rk)
+    h = lambda p: fw(al, r0 + (p - p0) / al2, rL) + fw(math.sqrt(a2), p / a2, rV) + uV - uL
+    p = optimize.brentq(h, 1.0, 1e5, xtol=1e-12, rtol=1e-15)
+    assert abs(s["z"]) < 1e-12
+    assert s["p_minus"] == pytest.approx(p, rel=1e-10)
+    assert s["p_plus"] == pytest.approx(p, rel=1e-10)
+    assert s["F0"] == pytest.approx(0.0, abs=1e-12)
+    assert s["F1"] == pytest.approx(p, rel=1e-10)
+
+
+# ---------------------------------------------------------------------------- creation
+@pytest.mark.parametrize("kind,rl,ul,rr,ur", [
+    (LIQ, 1000.0, -50.0, 1000.0, 50.0), (LIQ, 999.3, -120.0, 1000.8, 60.0),
+    (LIQ, 1002.0, -200.0, 1002.0, 200.0), (VAP, 0.03, 100.0, 0.03, -100.0), (VAP, 0.02, 90.0, 0.025, -40.0)])
+def test_creation_boundaries_are_interface_solutions(oracle_mod, kind, rl, ul, rr, ur):
+    """R18 checked against Appendix A: each created boundary, fed its own star states, is a
+    fixed point of the two-phase interface solver (no outer waves), with the same z, w."""
+    c = oracle_mod.creation_solve(EOS, PRM, kind, rl, ul, rr, ur)
+    uAl = ul - oracle_mod.wave_f(EOS, kind, c["rho_A"], rl)
+    uAr = ur + oracle_mod.wave_f(EOS, kind, c["rho_A"], rr)
+    left = oracle_mod.interface_solve(EOS, PRM, c["rho_A"], uAl, c["rho_B"], c["u_B"])
+    right = oracle_mod.interface_solve(EOS, PRM, c["rho_B"], c["u_B"], c["rho_A"], uAr)
+    assert left["z"] == pytest.approx(c["z_l"], rel=1e-9)
+    assert right["z"] == pytest.approx(c["z_r"], rel=1e-9)
+    assert left["w"] == pytest.approx(c["w_l"], rel=1e-9, abs=1e-12)
+    assert right["w"] == pytest.approx(c["w_r"], rel=1e-9, abs=1e-12)
+    # exact conservation of the created cell: rho_B (w_r - w_l) = z_r - z_l (R17)
+    assert c["rho_B"] * (c["w_r"] - c["w_l"]) == pytest.approx(c["z_r"] - c["z_l"], rel=1e-12)
+    assert c["w_r"] > c["w_l"]
+
+
+def test_creation_symmetric_data(oracle_mod):
+    c = oracle_mod.creation_solve(EOS, PRM, LIQ, 1000.0, -50.0, 1000.0, 50.0)
+    assert abs(c["u_B"]) < 1e-12
+    assert c["w_l"] == pytest.approx(-c["w_r"], rel=1e-12)
+    assert c["Fl1"] == pytest.approx(c["p_B"], rel=1e-15)  # u_B = 0: momentum flux = p_B
+
+
+# ---------------------------------------------------------------------------- time stepping
+def _sim(oracle_mod, rho, mom, xl=0.0, xr=1.0, params=None, cap_slack=16):
+    N = len(rho)
+    s = oracle_mod.Sim(EOS, params or PRM, 1, N, N + cap_slack, xl, xr)
+    R = np.zeros((1, N + cap_slack))
+    Mo = np.zeros((1, N + cap_slack))
+    R[0, :N] = rho
+    Mo[0, :N] = mom
+    s.set_state(R, Mo)
+    return s
+
+
+def test_constant_state_preserved_bitwise(oracle_mod):
+    for r, u in ((1000.3, 0.0), (1000.3, 17.0), (0.021, -40.0)):
+        s = _sim(oracle_mod, np.full(64, r), np.full(64, r * u))
+        s.step(25)
+        st = s.get_state()
+        assert np.array_equal(st["rho"][0, :64], np.full(64, r))
+        assert np.array_equal(st["mom"][0, :64], np.full(64, r * u))
+
+
+def _totals(st):
+    n = st["n"][0]
+    return (st["h"][0, :n] * st["rho"][0, :n]).sum(), (st["h"][0, :n] * st["mom"][0, :n]).sum()
+
+
+def test_conservation_through_creation_and_dts(oracle_mod):
+    """Sum h U changes only by the boundary fluxes (P:621 'by construction ... preserves
+    conservation'; R17 creation; flux bounding P:601).  C2 data; 60 steps through creation,
+    the DTS regions, merges and splits.  Boundary fluxes are zero-gradient: F(U_end)."""
+    w = W.c2()
+    N = w["N"]
+    s = _sim(oracle_mod, w["rho"][0, :N], w["mom"][0, :N], -0.5, 0.5)
+    for _ in range(60):
+        st0 = s.get_state()
+        n = st0["n"][0]
+        m0, p0_ = _totals(st0)
+        F = []
+        for i in (0, n - 1):
+            r, mo = st0["rho"][0, i], st0["mom"][0, i]
+            F.append(np.array(oracle_mod.hll(EOS, r, mo, r, mo)))
+        stats = s.step(1)
+        st1 = s.get_state()
+        dt = st1["t"][0] - st0["t"][0]
+        m1, p1 = _totals(st1)
+        assert m1 - m0 == pytest.approx(-dt * (F[1][0] - F[0][0]), abs=1e-12 * abs(m0))
+        assert p1 - p0_ == pytest.approx(-dt * (F[1][1] - F[0][1]), abs=1e-11 * abs(F[0][1] * dt) + 1e-9)
+    assert stats["creations"] == 1 and stats["regions"] > 0 and stats["merges"] > 0
+    assert s.member_status()[0] == 0
+
+
+def test_split_equals_explicit_without_tiny_cells(oracle_mod):
+    """Mode degeneracy: with no tiny cell Algorithm 1 is the explicit scheme."""
+    w = W.c1()
+    outs = []
+    for mode in (0, 1):
+        p = dict(PRM)
+        p["mode"] = mode
+        s = oracle_mod.Sim(w["eos"], p, 1, w["N"], w["cap"], 0.0, 1.0)
+        s.set_state(w["rho"], w["mom"])
+        s.run_to(w["t_end"])
+        outs.append(s.get_state())
+    assert np.array_equal(outs[0]["rho"], outs[1]["rho"])
+    assert np.array_equal(outs[0]["mom"], outs[1]["mom"])
+
+
+def test_mirror_symmetry_c2(oracle_mod):
+    w = W.c2()
+    N = w["N"]
+    s = _sim(oracle_mod, w["rho"][0, :N], w["mom"][0, :N], -0.5, 0.5)
+    s.step(80)
+    st = s.get_state()
+    n = st["n"][0]
+    r, m = st["rho"][0, :n], st["mom"][0, :n]
+    np.testing.assert_allclose(r, r[::-1], rtol=1e-12)
+    np.testing.assert_allclose(m, -m[::-1], rtol=1e-10, atol=1e-9 * np.abs(m).max())
+
+
+def test_c1_interface_speed_matches_exact_riemann(oracle_mod):
+    """C1: interface position moves with the exact two-phase w (App. A) and the star pressure
+    plateau next to it converges to the exact p*, error decreasing with N (first order)."""
+    ex = oracle_mod.interface_solve(EOS, PRM, 1000.0, 0.0, 0.02, 0.0)
+    errs = []
+    for N in (100, 400):
+        rho = np.where(np.arange(N) < N // 2, 1000.0, 0.02)
+        s = _sim(oracle_mod, rho, np.zeros(N), 0.0, 1.0)
+        s.run_to(2e-4)
+        x = s.interfaces()[0]["x"]
+        errs.append(abs((x - 0.5) / 2e-4 - ex["w"]))
+    assert errs[1] < errs[0]
+    assert errs[1] < 0.02 * abs(ex["w"])
+
+
+@pytest.mark.parametrize("N", [50, 100, 200, 400])
+def test_single_phase_rarefaction_convergence(oracle_mod, N):
+    """P7 closed form: liquid two-rarefaction Riemann problem (du = 6 m/s below the cavitation
+    onset): L1 error of rho against the exact self-similar fan decreases ~ first order."""
+    r, du, a = 1000.0, 6.0, EOS["a_l"]
+    tend = 2e-4
+    res = {}
+    for n in (N, 2 * N):
+        rho = np.full(n, r)
+        mom = np.where(np.arange(n) < n // 2, -r * du / 2, r * du / 2)
+        s = _sim(oracle_mod, rho, mom, -1.0, 1.0)
+        s.run_to(tend)
+        st = s.get_state()
+        x = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+        rs = r * math.exp(-du / (2 * a))
+        xi = x / tend
+        # left fan: rho = rho_L exp((u_L - xi - a)/a) between u_L - a and u* - a
+        us = 0.0
+        exact = np.full(n, rs)
+        lf = (xi > -du / 2 - a) & (xi < us - a)
+        exact[lf] = r * np.exp((-du / 2 - xi[lf] - a) / a)
+        exact[xi <= -du / 2 - a] = r
+        rf = (xi > us + a) & (xi < du / 2 + a)
+        exact[rf] = r * np.exp((xi[rf] - a - du / 2) / a)
+        exact[xi >= du / 2 + a] = r
+        res[n] = np.abs(st["rho"][0, :n] - exact).sum() * (2.0 / n)
+    assert res[2 * N] < res[N]
