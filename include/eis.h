@@ -1,0 +1,165 @@
+/*
+ * include/eis.h — C ABI of libeis.so, the B200-native (sm_100a, fp64) hot path of
+ * May & Thein, "Explicit-Implicit Domain Splitting for Two Phase Flows with Phase
+ * Transition" (arXiv 2211.00705).  "P:n" cites line n of the paper's LaTeX source
+ * (/root/reference/PAPER.md); "R<k>" cites the readings table of DESIGN.md §3.
+ *
+ * What a call computes: one or more LARGE TIME STEPS of the mixed explicit-implicit scheme
+ * (Algorithm 1) for the 1D isothermal Euler equations with a sharp,
+ * grid-aligned liquid-vapour phase boundary, per member of an ensemble of
+ * independent grids:
+ *   a1-a2  decode + CFL time step  dt = C h_min / S_max        (R5, R6)
+ *   a3     HLL fluxes on same-phase edges
+ *   a4     cavitation / nucleation trigger                      (R7)
+ *   a5     phase-boundary Riemann solve with the kinetic relation (App. A; R2)
+ *   a6     phase creation (four-wave solution)                  (App. B; R17, R18)
+ *   a7     explicit moving-cell update
+ *   a8-a9  tiny cells -> implicit blocks -> dual time stepping
+ *   a10    remesh: insert, merge, split                         (R9, R10)
+ *
+ * Conventions
+ *  - Layout: structure of arrays, member-major, fp64: rho[m*cap + i], mom[m*cap + i] (= rho u),
+ *    width[m*cap + i]; only i < n_cells[m] is live.  cap = eis_grid.cell_capacity.
+ *  - where = EIS_HOST: pointers are host memory (copied with cudaMemcpyAsync on the context's
+ *    stream, then the call synchronises).  where = EIS_DEVICE: device pointers on grid.device,
+ *    accessed stream-ordered on grid.stream (no synchronisation unless stated).
+ *  - Ownership: all buffers passed in are BORROWED for the duration of the call.  The context
+ *    owns every device buffer it allocates; eis_destroy frees them.
+ *  - Errors: every call returns an eis_status.  A call-level error (bad argument, CUDA
+ *    failure) is sticky: later calls return it until eis_set_state succeeds.  Member-level
+ *    numerical failures (Newton non-convergence, DTS cap, spinodal state, capacity) do NOT fail
+ *    the call: that member is frozen and eis_member_status reports the code.
+ *  - Threads: one host thread per context at a time.
+ */
+#ifndef EIS_H
+#define EIS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EIS_OK = 0,
+  EIS_E_ARG = 1,             /* invalid argument                                            */
+  EIS_E_ORDER = 2,           /* step/get before a successful eis_set_state                 */
+  EIS_E_NONPOS_DENSITY = 3,  /* rho <= 0                                                   */
+  EIS_E_SPINODAL = 4,        /* a density in (rho_tilde, rho_min)                  */
+  EIS_E_NEWTON = 5,          /* interface Newton-Armijo did not converge (R14)             */
+  EIS_E_CREATION = 6,        /* creation solve failed or w_r <= w_l                        */
+  EIS_E_DTS_CAP = 7,         /* dual time stepping reached dts_max_iter (P:688 l_max)       */
+  EIS_E_WIDTH = 8,           /* a cell width became <= 0                                   */
+  EIS_E_CAPACITY = 9,        /* cell_capacity or an internal table exceeded                */
+  EIS_E_CUDA = 10,           /* CUDA runtime error (message in eis_last_error)             */
+  EIS_E_NCCL = 11,           /* reserved: NCCL error                                       */
+  EIS_E_UNSUPPORTED = 12     /* tiny cell at a domain end (R26)                            */
+} eis_status;
+
+enum { EIS_HOST = 0, EIS_DEVICE = 1 };
+enum { EIS_MODE_SPLIT = 0 /* Algorithms 1-2 */, EIS_MODE_EXPLICIT = 1 /* global explicit, dt from all cells */ };
+enum { EIS_VAP = 0, EIS_LIQ = 1, EIS_SPIN = 2 };
+
+/* EOS record (immutable per context).  Vapour p = a_v2 rho; liquid
+ * p = p0 + a_l^2 (rho - rho0) (P:1121 corrected, R1). */
+typedef struct {
+  double a_v2;      /* kT0/m, m^2/s^2                                                       */
+  double a_l;       /* liquid sound speed sqrt(K0/rho0), m/s                               */
+  double rho0, p0;  /* saturation liquid density and pressure at T0                        */
+  double tau;       /* kinetic coefficient; <= 0 -> (2 pi)^-1/2 a_v2^-3/2 (R22)   */
+  double p_min;     /* minimum liquid pressure; rho_min = rho0 + (p_min - p0)/a_l^2 */
+  double rho_tilde; /* maximum vapour density; <= 0 -> Maxwell equal area from p_min (R3)  */
+} eis_eos;
+
+/* scheme parameters (P:1127-1135 and DESIGN.md readings) */
+typedef struct {
+  double cfl;                /* C_CFL                                               */
+  double eps_split;          /* split cells wider than eps_split*h_av: 2            */
+  double eps_tiny;           /* merge / tiny below eps_tiny*h_av (R4): 0.5                 */
+  double theta_nb;           /* theta_{k+-1}: 0.9; theta_k = alpha (R12)          */
+  double tol_nb, tol_tiny;   /* DTS stop: 1e-3, 1e-1                             */
+  int64_t dts_max_iter;      /* l_max                                             */
+  double newton_rtol;        /* R14: 1e-13                                                 */
+  double newton_gtol;        /* R14: 1e-12 (scaled residual)                               */
+  int32_t newton_max_iter;   /* R14: 50                                                    */
+  int32_t armijo_max;        /* Armijo halvings (Kelley): 30                       */
+  int32_t mode;              /* EIS_MODE_SPLIT | EIS_MODE_EXPLICIT                         */
+  int32_t reserved;
+} eis_params;
+
+typedef struct {
+  int64_t n_members;      /* independent grids (ensembles C3/C4; 1 for C1/C2)              */
+  int64_t n_cells;        /* initial cells per member N; h_av = (x_right - x_left)/N (R9) */
+  int64_t cell_capacity;  /* >= n_cells: slack for created / split cells                   */
+  double x_left, x_right; /* domain                                                        */
+  int32_t device;         /* CUDA device ordinal                                           */
+  int32_t threads;        /* CTA size per member (0 = automatic)                           */
+  void* stream;           /* cudaStream_t (NULL = legacy default stream)                   */
+} eis_grid;
+
+typedef struct {
+  int64_t member, edge;   /* edge e lies between cells e-1 and e                           */
+  double x;               /* x_left + widths summed left to right (fixed order, no FMA)    */
+  int32_t left_phase, right_phase;
+} eis_interface;
+
+typedef struct {
+  int64_t steps;          /* member steps taken (summed over members)                      */
+  int64_t cell_updates;   /* live cells advanced by one large step (the bench metric unit) */
+  int64_t dts_iters;      /* dual-time iterations ("local iterations")             */
+  int64_t iface_solves;   /* phase-boundary Riemann solves                                 */
+  int64_t creations, splits, merges, regions;
+  double t_min, t_max, dt_min, dt_max;
+} eis_stats;
+
+typedef struct { double rho_min, rho_tilde, p_tilde, tau, a_v; } eis_thresholds;
+
+/* Derived thresholds (R3): host computation, no context needed. */
+eis_status eis_thresholds_of(const eis_eos* eos, eis_thresholds* out);
+
+typedef struct eis_ctx eis_ctx;
+
+/* Create a context on grid->device: validates the records, derives the thresholds, allocates
+ * n_members * cell_capacity fp64 state in device memory.  *out is NULL on error. */
+eis_status eis_create(const eis_eos* eos, const eis_params* params, const eis_grid* grid, eis_ctx** out);
+
+/* Load the state U^0 = (rho, mom) and widths (NULL: uniform h_av) of every member, the live
+ * cell counts (NULL: all n_cells) and the start time t0.  Resets member status and counters,
+ * clears a sticky error.  Tiny flags are derived from the state (R4, R10). */
+eis_status eis_set_state(eis_ctx* ctx, const double* rho, const double* mom, const double* width,
+                         const int64_t* n_cells, int32_t where, double t0);
+
+/* Every non-frozen member takes n_steps large steps (its own dt, R25).  Stream-ordered: with
+ * out == NULL nothing synchronises; with out != NULL the call synchronises and fills the
+ * counters accumulated since eis_set_state. */
+eis_status eis_step(eis_ctx* ctx, int64_t n_steps, eis_stats* out);
+
+/* Every non-frozen member steps until t >= t_end (last dt clipped to t_end - t) or max_steps
+ * steps were taken in this call.  Same synchronisation rule as eis_step. */
+eis_status eis_run_to(eis_ctx* ctx, double t_end, int64_t max_steps, eis_stats* out);
+
+/* Copy the state out: arrays sized n_members*cell_capacity (entries past n_cells[m] are 0;
+ * phase is EIS_VAP/EIS_LIQ/EIS_SPIN per cell, 255 past the end), n_cells[n_members] and
+ * t[n_members].  Any pointer may be NULL.  where = EIS_HOST synchronises. */
+eis_status eis_get_state(eis_ctx* ctx, double* rho, double* mom, double* width, uint8_t* phase,
+                         int64_t* n_cells, double* t, int32_t where);
+
+/* Phase boundaries of the current state, member-major and left to right, into a host array of
+ * `capacity` records; *count gets the total (EIS_E_CAPACITY if it exceeds capacity; out == NULL
+ * is a pure count query). */
+eis_status eis_interfaces(eis_ctx* ctx, eis_interface* out, int64_t capacity, int64_t* count);
+
+/* Per-member status codes (host array of n_members). */
+eis_status eis_member_status(eis_ctx* ctx, int32_t* out);
+
+/* Per-member counters (host array of n_members eis_stats; t_min = t_max = member time). */
+eis_status eis_member_stats(eis_ctx* ctx, eis_stats* out);
+
+/* Last error message of the context (static storage owned by the context). */
+const char* eis_last_error(const eis_ctx* ctx);
+
+void eis_destroy(eis_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,211 @@
+"""paper_2211_00705_b200 — B200-native hot path of May & Thein's explicit-implicit domain
+splitting (arXiv 2211.00705) for 1D isothermal liquid-vapour flow with phase transition.
+
+This module is the thin Python binding of ``libeis.so`` (C ABI in ``include/eis.h``):
+argument marshalling only.  Every step of the method runs in the CUDA kernels of the
+library; there is no CPU fallback.  Importing works without a GPU (the library loads), but
+any context call needs a CUDA device and fails loudly otherwise.
+
+Names follow the C ABI: ``eis_create`` -> :class:`Context`, ``eis_set_state`` ->
+:meth:`Context.set_state`, ``eis_step`` -> :meth:`Context.step`, ``eis_run_to`` ->
+:meth:`Context.run_to`, ``eis_get_state`` -> :meth:`Context.get_state`,
+``eis_interfaces`` -> :meth:`Context.interfaces`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libeis.so")
+
+EIS_HOST, EIS_DEVICE = 0, 1
+MODE_SPLIT, MODE_EXPLICIT = 0, 1
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_ORDER", 3: "E_NONPOS_DENSITY", 4: "E_SPINODAL", 5: "E_NEWTON",
+          6: "E_CREATION", 7: "E_DTS_CAP", 8: "E_WIDTH", 9: "E_CAPACITY", 10: "E_CUDA", 11: "E_NCCL",
+          12: "E_UNSUPPORTED"}
+
+
+class EisError(RuntimeError):
+    pass
+
+
+class Eos(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("a_v2", "a_l", "rho0", "p0", "tau", "p_min", "rho_tilde")]
+
+
+class Params(C.Structure):
+    _fields_ = [("cfl", C.c_double), ("eps_split", C.c_double), ("eps_tiny", C.c_double),
+                ("theta_nb", C.c_double), ("tol_nb", C.c_double), ("tol_tiny", C.c_double),
+                ("dts_max_iter", C.c_int64), ("newton_rtol", C.c_double), ("newton_gtol", C.c_double),
+                ("newton_max_iter", C.c_int32), ("armijo_max", C.c_int32), ("mode", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class Grid(C.Structure):
+    _fields_ = [("n_members", C.c_int64), ("n_cells", C.c_int64), ("cell_capacity", C.c_int64),
+                ("x_left", C.c_double), ("x_right", C.c_double), ("device", C.c_int32),
+                ("threads", C.c_int32), ("stream", C.c_void_p)]
+
+
+class Interface(C.Structure):
+    _fields_ = [("member", C.c_int64), ("edge", C.c_int64), ("x", C.c_double),
+                ("left_phase", C.c_int32), ("right_phase", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("steps", "cell_updates", "dts_iters", "iface_solves",
+                                         "creations", "splits", "merges", "regions")] + \
+               [(n, C.c_double) for n in ("t_min", "t_max", "dt_min", "dt_max")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class Thresholds(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("rho_min", "rho_tilde", "p_tilde", "tau", "a_v")]
+
+
+# exported symbols of libeis.so (checked by tests/test_abi.py against include/eis.h)
+SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
+           "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy")
+
+_lib = None
+
+
+def lib():
+    """Load libeis.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EisError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        P, d, i64, i32, vp = C.POINTER, C.c_double, C.c_int64, C.c_int32, C.c_void_p
+        L.eis_thresholds_of.argtypes = [P(Eos), P(Thresholds)]
+        L.eis_create.argtypes = [P(Eos), P(Params), P(Grid), P(vp)]
+        L.eis_set_state.argtypes = [vp, vp, vp, vp, vp, i32, d]
+        L.eis_step.argtypes = [vp, i64, P(Stats)]
+        L.eis_run_to.argtypes = [vp, d, i64, P(Stats)]
+        L.eis_get_state.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32]
+        L.eis_interfaces.argtypes = [vp, P(Interface), i64, P(i64)]
+        L.eis_member_status.argtypes = [vp, P(i32)]
+        L.eis_member_stats.argtypes = [vp, P(Stats)]
+        L.eis_last_error.argtypes = [vp]
+        L.eis_last_error.restype = C.c_char_p
+        L.eis_destroy.argtypes = [vp]
+        for s in SYMBOLS:
+            if s not in ("eis_last_error", "eis_destroy"):
+                getattr(L, s).restype = C.c_int
+        L.eis_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def make_eos(d: dict) -> Eos:
+    return Eos(*(float(d[k]) for k in ("a_v2", "a_l", "rho0", "p0", "tau", "p_min", "rho_tilde")))
+
+
+def make_params(d: dict) -> Params:
+    return Params(float(d["cfl"]), float(d["eps_split"]), float(d["eps_tiny"]), float(d["theta_nb"]),
+                  float(d["tol_nb"]), float(d["tol_tiny"]), int(d["dts_max_iter"]), float(d["newton_rtol"]),
+                  float(d["newton_gtol"]), int(d["newton_max_iter"]), int(d["armijo_max"]), int(d["mode"]), 0)
+
+
+def eis_thresholds_of(eos: dict) -> dict:
+    t = Thresholds()
+    s = lib().eis_thresholds_of(C.byref(make_eos(eos)), C.byref(t))
+    if s:
+        raise EisError(f"eis_thresholds_of: {STATUS.get(s, s)}")
+    return {n: getattr(t, n) for n, _ in t._fields_}
+
+
+def _ptr(a):
+    """Device (torch) or host (numpy) buffer -> (address, where)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):  # torch tensor
+        return a.data_ptr(), (EIS_DEVICE if a.is_cuda else EIS_HOST)
+    return a.ctypes.data, EIS_HOST
+
+
+class Context:
+    """eis_create / eis_destroy.  ``stream``: a cudaStream_t handle (int) or a torch stream."""
+
+    def __init__(self, eos: dict, params: dict, n_members: int, n_cells: int, capacity: int,
+                 x_left: float, x_right: float, device: int = 0, stream=None, threads: int = 0):
+        if stream is not None and hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        self.M, self.N, self.cap = int(n_members), int(n_cells), int(capacity)
+        self.device = int(device)
+        self._grid = Grid(self.M, self.N, self.cap, float(x_left), float(x_right), self.device, int(threads),
+                          C.c_void_p(stream) if stream else None)
+        self._eos, self._prm = make_eos(eos), make_params(params)
+        self._ctx = C.c_void_p()
+        s = lib().eis_create(C.byref(self._eos), C.byref(self._prm), C.byref(self._grid), C.byref(self._ctx))
+        if s:
+            raise EisError(f"eis_create: {STATUS.get(s, s)}")
+
+    def _check(self, s, what):
+        if s:
+            msg = lib().eis_last_error(self._ctx)
+            raise EisError(f"{what}: {STATUS.get(s, s)} ({msg.decode() if msg else ''})")
+
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx.value:
+            lib().eis_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    __del__ = close
+
+    def set_state(self, rho, mom, width=None, n_cells=None, t0: float = 0.0):
+        """rho, mom (and width): n_members*capacity fp64, host (numpy) or device (torch)."""
+        pr, where = _ptr(rho)
+        pm, w2 = _ptr(mom)
+        pw, w3 = _ptr(width)
+        pn, w4 = _ptr(n_cells)
+        if w2 != where or (w3 is not None and w3 != where) or (w4 is not None and w4 != where):
+            raise EisError("set_state: all buffers must be host or all device")
+        self._check(lib().eis_set_state(self._ctx, pr, pm, pw, pn, where, float(t0)), "eis_set_state")
+
+    def step(self, n_steps: int, stats: bool = False):
+        st = Stats()
+        self._check(lib().eis_step(self._ctx, int(n_steps), C.byref(st) if stats else None), "eis_step")
+        return st.as_dict() if stats else None
+
+    def run_to(self, t_end: float, max_steps: int = 10 ** 9, stats: bool = False):
+        st = Stats()
+        self._check(lib().eis_run_to(self._ctx, float(t_end), int(max_steps), C.byref(st) if stats else None),
+                    "eis_run_to")
+        return st.as_dict() if stats else None
+
+    def get_state(self, out: dict | None = None) -> dict:
+        """Host copy (numpy) unless ``out`` holds device tensors (rho, mom, h, phase, n, t)."""
+        if out is None:
+            out = {"rho": np.zeros((self.M, self.cap)), "mom": np.zeros((self.M, self.cap)),
+                   "h": np.zeros((self.M, self.cap)), "phase": np.zeros((self.M, self.cap), np.uint8),
+                   "n": np.zeros(self.M, np.int64), "t": np.zeros(self.M)}
+        ptrs = [_ptr(out.get(k)) for k in ("rho", "mom", "h", "phase", "n", "t")]
+        where = next(w for _, w in ptrs if w is not None)
+        self._check(lib().eis_get_state(self._ctx, *[p for p, _ in ptrs], where), "eis_get_state")
+        return out
+
+    def interfaces(self) -> list:
+        cnt = C.c_int64()
+        self._check(lib().eis_interfaces(self._ctx, None, 0, C.byref(cnt)), "eis_interfaces")
+        arr = (Interface * max(cnt.value, 1))()
+        self._check(lib().eis_interfaces(self._ctx, arr, cnt.value, C.byref(cnt)), "eis_interfaces")
+        return [{"member": a.member, "edge": a.edge, "x": a.x, "left_phase": a.left_phase,
+                 "right_phase": a.right_phase} for a in arr[:cnt.value]]
+
+    def member_status(self) -> np.ndarray:
+        out = np.zeros(self.M, dtype=np.int32)
+        self._check(lib().eis_member_status(self._ctx, out.ctypes.data_as(C.POINTER(C.c_int32))),
+                    "eis_member_status")
+        return out
+
+    def member_stats(self) -> list:
+        arr = (Stats * self.M)()
+        self._check(lib().eis_member_stats(self._ctx, arr), "eis_member_stats")
+        return [a.as_dict() for a in arr]

@@ -1,0 +1,437 @@
+// eis_api.cu — the C ABI of libeis.so (include/eis.h): contexts, stream-ordered launches of
+// the member-resident kernel, state transfer and reporting kernels.  Host code here only
+// validates, allocates and launches; every step of the method runs in the kernels of
+// eis_resident.cuh / eis_device.cuh.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "eis.h"
+#include "eis_resident.cuh"
+
+using namespace eis;
+
+struct eis_ctx {
+  eis_eos eos_in;
+  eis_params prm_in;
+  eis_grid grid;
+  Eos e;
+  Prm p;
+  cudaStream_t stream;
+  int threads;
+  size_t smem;
+  Members g;
+  double *d_rho, *d_mom, *d_h, *d_t;
+  long long* d_n;
+  int* d_status;
+  MemberStats* d_stats;
+  uint8_t* d_u8;    // scratch: phases for get_state
+  double* d_pack;   // scratch for packed host transfers (3 * M * cap)
+  long long* d_cnt; // scratch: per-member interface counts / offsets
+  eis_interface* d_if;
+  long long if_cap;
+  int state_set;
+  eis_status sticky;
+  char msg[512];
+};
+
+static eis_status fail(eis_ctx* c, eis_status s, const char* fmt, const char* extra = "") {
+  if (c) {
+    snprintf(c->msg, sizeof(c->msg), fmt, extra);
+    if (s == EIS_E_CUDA || s == EIS_E_ARG) c->sticky = s;
+  }
+  return s;
+}
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t err_ = (call);                                                         \
+    if (err_ != cudaSuccess) return fail(c, EIS_E_CUDA, "CUDA error: %s", cudaGetErrorString(err_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Thresholds (R3), host side, once per context.  Maxwell equal area along the path liquid ->
+// spinodal linear in rho -> vapour: Phi(rt) = a_l^2 ln(rho_min/rho0) + s ln(rt/rho_min)
+// + a_v^2 ln(rho_V0/rt) with s = (a_v^2 rt - p_min)/(rt - rho_min).  Solved in x = ln(rt) by
+// a sign-change search outward from rho_V0 followed by regula falsi (Illinois).
+// ------------------------------------------------------------------------------------------
+static double maxwell_phi(double x, double a_v2, double a_l2, double rho0, double p0, double p_min, double rho_min) {
+  const double rt = std::exp(x);
+  const double s = (a_v2 * rt - p_min) / (rt - rho_min);
+  return a_l2 * std::log(rho_min / rho0) + s * std::log(rt / rho_min) + a_v2 * std::log((p0 / a_v2) / rt);
+}
+
+extern "C" eis_status eis_thresholds_of(const eis_eos* in, eis_thresholds* out) {
+  if (!in || !out || !(in->a_v2 > 0) || !(in->a_l > 0) || !(in->rho0 > 0) || !(in->p0 > 0)) return EIS_E_ARG;
+  const double a_l2 = in->a_l * in->a_l;
+  const double rho_min = in->rho0 + (in->p_min - in->p0) / a_l2;
+  if (!(rho_min > 0) || !(in->p_min < in->p0)) return EIS_E_ARG;
+  double rt = in->rho_tilde;
+  if (!(rt > 0)) {
+    const double lo0 = std::log(in->p0 / in->a_v2), hi0 = std::log(rho_min);
+    auto F = [&](double x) { return maxwell_phi(x, in->a_v2, a_l2, in->rho0, in->p0, in->p_min, rho_min); };
+    // walk up from rho_V0 in growing steps until the sign changes
+    double xa = lo0 + 1e-12, fa = F(xa), xb = xa, fb = fa, step = 1e-6;
+    bool found = false;
+    while (xb < hi0) {
+      xb = std::fmin(xa + step, hi0 - 1e-12);
+      fb = F(xb);
+      if ((fa < 0) != (fb < 0)) { found = true; break; }
+      xa = xb; fa = fb; step *= 1.5;
+      if (xb >= hi0 - 1e-12) break;
+    }
+    if (!found) return EIS_E_ARG;
+    int side = 0;
+    for (int it = 0; it < 200; ++it) {
+      double xc = (xa * fb - xb * fa) / (fb - fa);
+      double fc = F(xc);
+      if (fc == 0 || std::fabs(xb - xa) < 1e-15 * std::fabs(xb)) { xa = xb = xc; break; }
+      if ((fc < 0) == (fb < 0)) { xb = xc; fb = fc; if (side == -1) fa *= 0.5; side = -1; }
+      else { xa = xc; fa = fc; if (side == 1) fb *= 0.5; side = 1; }
+    }
+    rt = std::exp(0.5 * (xa + xb));
+  }
+  if (!(rt < rho_min)) return EIS_E_ARG;
+  out->rho_min = rho_min;
+  out->rho_tilde = rt;
+  out->p_tilde = in->a_v2 * rt;
+  out->tau = in->tau > 0 ? in->tau : 1.0 / std::sqrt(2.0 * M_PI) * std::pow(in->a_v2, -1.5);
+  out->a_v = std::sqrt(in->a_v2);
+  return EIS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// small kernels: state fill / validation / packing / reporting
+// ------------------------------------------------------------------------------------------
+__global__ void k_fill(double* a, long long count, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) a[i] = v;
+}
+__global__ void k_fill_ll(long long* a, long long count, long long v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) a[i] = v;
+}
+// one CTA per member: validate the initial state (rho > 0, not spinodal), reset counters
+__global__ void k_validate(const Eos e, Members g, double t0) {
+  __shared__ int bad;
+  const long long m = blockIdx.x;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const long long n = g.n[m];
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    double r = g.rho[m * g.cap + i];
+    if (!(r > 0.0)) atomicMax(&bad, ST_NONPOS);
+    else if (phase_of(e, r) == SPIN) atomicMax(&bad, ST_SPINODAL);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g.status[m] = (n < 3 || n > g.cap) ? ST_CAPACITY : bad;
+    g.t[m] = t0;
+    MemberStats z;
+    memset(&z, 0, sizeof(z));
+    g.stats[m] = z;
+  }
+}
+// copy live cells, zero the rest, phases (255 past the end)
+__global__ void k_pack(const Eos e, Members g, double* rho, double* mom, double* h, uint8_t* ph) {
+  const long long m = blockIdx.x;
+  const long long n = g.n[m];
+  for (long long i = threadIdx.x; i < g.cap; i += blockDim.x) {
+    const long long k = m * g.cap + i;
+    const bool live = i < n;
+    const double r = live ? g.rho[k] : 0.0;
+    if (rho) rho[k] = r;
+    if (mom) mom[k] = live ? g.mom[k] : 0.0;
+    if (h) h[k] = live ? g.h[k] : 0.0;
+    if (ph) ph[k] = live ? (uint8_t)phase_of(e, r) : (uint8_t)255;
+  }
+}
+// interfaces: one thread per member, widths summed left to right (fixed order, one add per cell)
+__global__ void k_iface(const Eos e, Members g, long long M, double x_left, const long long* off,
+                        long long* cnt, eis_interface* out, long long cap_out) {
+  const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const long long n = g.n[m];
+  const double* rho = g.rho + m * g.cap;
+  const double* h = g.h + m * g.cap;
+  long long k = off ? off[m] : 0, c = 0;
+  double x = x_left;
+  int pa = phase_of(e, rho[0]);
+  for (long long i = 0; i < n; ++i) {
+    x = __dadd_rn(x, h[i]);
+    if (i + 1 < n) {
+      const int pb = phase_of(e, rho[i + 1]);
+      if (pa != pb) {
+        if (out && k < cap_out) { out[k].member = m; out[k].edge = i + 1; out[k].x = x; out[k].left_phase = pa; out[k].right_phase = pb; }
+        ++k; ++c;
+      }
+      pa = pb;
+    }
+  }
+  if (cnt) cnt[m] = c;
+}
+
+static unsigned grid_for(long long count) {
+  long long b = (count + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b));
+}
+
+// ------------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------------
+extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, const eis_grid* grid, eis_ctx** out) {
+  if (!out) return EIS_E_ARG;
+  *out = nullptr;
+  if (!eos || !prm || !grid) return EIS_E_ARG;
+  if (grid->n_members < 1 || grid->n_cells < 3 || grid->cell_capacity < grid->n_cells || !(grid->x_right > grid->x_left))
+    return EIS_E_ARG;
+  if (!(prm->cfl > 0) || !(prm->eps_tiny > 0) || !(prm->eps_split > prm->eps_tiny) || !(prm->theta_nb > 0) ||
+      prm->newton_max_iter < 1 || prm->armijo_max < 0 || prm->armijo_max > 31 || prm->dts_max_iter < 1 ||
+      (prm->mode != EIS_MODE_SPLIT && prm->mode != EIS_MODE_EXPLICIT))
+    return EIS_E_ARG;
+  eis_thresholds th;
+  if (eis_thresholds_of(eos, &th) != EIS_OK) return EIS_E_ARG;
+  eis_ctx* c = new eis_ctx();
+  memset(c, 0, sizeof(*c));
+  c->eos_in = *eos;
+  c->prm_in = *prm;
+  c->grid = *grid;
+  c->stream = (cudaStream_t)grid->stream;
+  Eos& e = c->e;
+  e.a_v2 = eos->a_v2; e.a_v = th.a_v; e.a_l = eos->a_l; e.a_l2 = eos->a_l * eos->a_l; e.rho0 = eos->rho0;
+  e.p0 = eos->p0; e.tau = th.tau; e.rho_min = th.rho_min; e.rho_tilde = th.rho_tilde;
+  e.inv_av2 = 1.0 / e.a_v2; e.inv_al2 = 1.0 / e.a_l2; e.inv_p0 = 1.0 / e.p0; e.inv_av = 1.0 / e.a_v; e.inv_rho0 = 1.0 / e.rho0;
+  Prm& p = c->p;
+  p.cfl = prm->cfl; p.eps_split = prm->eps_split; p.eps_tiny = prm->eps_tiny; p.theta_nb = prm->theta_nb;
+  p.tol_nb = prm->tol_nb; p.tol_tiny = prm->tol_tiny; p.newton_rtol = prm->newton_rtol; p.newton_gtol = prm->newton_gtol;
+  p.h_av = (grid->x_right - grid->x_left) / (double)grid->n_cells;  // fixed (R9)
+  p.dts_max_iter = prm->dts_max_iter; p.newton_max_iter = prm->newton_max_iter; p.armijo_max = prm->armijo_max;
+  p.mode = prm->mode;
+
+  const long long M = grid->n_members, cap = grid->cell_capacity;
+  if (cap > 16384) { delete c; return EIS_E_ARG; }
+  // CTA size: about 4 cells per thread, warps limited so the DTS scratch fits in the u array
+  int T = grid->threads;
+  if (T <= 0) {
+    long long want = (grid->n_cells + 3) / 4;
+    T = (int)((want + 31) / 32 * 32);
+    if (T < 64) T = 64;
+    if (T > 1024) T = 1024;
+    if (cap <= 2048 && T > 256) T = 256;
+  }
+  if (T % 32 || T < 32 || T > 1024) { delete c; return EIS_E_ARG; }
+  while ((T / 32) * DTS_SCRATCH > cap + 1 && T > 32) T -= 32;
+  c->threads = T;
+  c->smem = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(cap + 1) + (((size_t)cap + 1 + 15) & ~size_t(15));
+  int dev = grid->device;
+  if (cudaSetDevice(dev) != cudaSuccess) { delete c; return EIS_E_CUDA; }
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if ((int)c->smem > max_optin) { delete c; return EIS_E_CAPACITY; }
+  cudaError_t e1 = cudaFuncSetAttribute(resident_steps<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  cudaError_t e2 = cudaFuncSetAttribute(resident_steps<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) { delete c; return EIS_E_CUDA; }
+  const size_t cells = (size_t)M * cap;
+  bool ok = cudaMalloc(&c->d_rho, cells * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cells * 8) == cudaSuccess &&
+            cudaMalloc(&c->d_h, cells * 8) == cudaSuccess && cudaMalloc(&c->d_t, M * 8) == cudaSuccess &&
+            cudaMalloc(&c->d_n, M * 8) == cudaSuccess && cudaMalloc(&c->d_status, M * 4) == cudaSuccess &&
+            cudaMalloc(&c->d_stats, M * sizeof(MemberStats)) == cudaSuccess &&
+            cudaMalloc(&c->d_cnt, (M + 1) * 8) == cudaSuccess;
+  if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
+  c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
+  c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
+  *out = c;
+  return EIS_OK;
+}
+
+extern "C" void eis_destroy(eis_ctx* c) {
+  if (!c) return;
+  cudaFree(c->d_rho); cudaFree(c->d_mom); cudaFree(c->d_h); cudaFree(c->d_t); cudaFree(c->d_n);
+  cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
+  cudaFree(c->d_if);
+  delete c;
+}
+
+extern "C" const char* eis_last_error(const eis_ctx* c) { return c ? c->msg : "null context"; }
+
+static eis_status ensure_pack(eis_ctx* c) {
+  if (!c->d_pack) {
+    const size_t cells = (size_t)c->grid.n_members * c->grid.cell_capacity;
+    CU(cudaMalloc(&c->d_pack, cells * 3 * 8));
+    CU(cudaMalloc(&c->d_u8, cells));
+  }
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double* mom, const double* width,
+                                    const int64_t* n_cells, int32_t where, double t0) {
+  if (!c) return EIS_E_ARG;
+  if (!rho || !mom || (where != EIS_HOST && where != EIS_DEVICE)) return fail(c, EIS_E_ARG, "set_state: bad argument%s");
+  CU(cudaSetDevice(c->grid.device));
+  const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
+  const size_t bytes = (size_t)M * cap * 8;
+  const cudaMemcpyKind kind = where == EIS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(c->d_rho, rho, bytes, kind, c->stream));
+  CU(cudaMemcpyAsync(c->d_mom, mom, bytes, kind, c->stream));
+  if (width) CU(cudaMemcpyAsync(c->d_h, width, bytes, kind, c->stream));
+  else k_fill<<<grid_for(M * cap), 256, 0, c->stream>>>(c->d_h, M * cap, c->p.h_av);
+  if (n_cells) {
+    if (where == EIS_HOST) {
+      for (long long m = 0; m < M; ++m)
+        if (n_cells[m] < 3 || n_cells[m] > cap) return fail(c, EIS_E_ARG, "set_state: n_cells out of range%s");
+    }
+    CU(cudaMemcpyAsync(c->d_n, n_cells, M * 8, kind, c->stream));
+  } else {
+    k_fill_ll<<<grid_for(M), 256, 0, c->stream>>>(c->d_n, M, c->grid.n_cells);
+  }
+  k_validate<<<(unsigned)M, 128, 0, c->stream>>>(c->e, c->g, t0);
+  CU(cudaGetLastError());
+  if (where == EIS_HOST) CU(cudaStreamSynchronize(c->stream));
+  c->state_set = 1;
+  c->sticky = EIS_OK;
+  c->msg[0] = 0;
+  return EIS_OK;
+}
+
+static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
+  const long long M = c->grid.n_members;
+  std::vector<MemberStats> ms(M);
+  std::vector<double> t(M);
+  CU(cudaMemcpyAsync(ms.data(), c->d_stats, M * sizeof(MemberStats), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(t.data(), c->d_t, M * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  memset(out, 0, sizeof(*out));
+  out->t_min = INFINITY; out->t_max = -INFINITY; out->dt_min = INFINITY; out->dt_max = 0;
+  for (long long m = 0; m < M; ++m) {
+    const MemberStats& s = ms[m];
+    out->steps += s.steps; out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters;
+    out->iface_solves += s.iface_solves; out->creations += s.creations; out->splits += s.splits;
+    out->merges += s.merges; out->regions += s.regions;
+    out->t_min = std::fmin(out->t_min, t[m]); out->t_max = std::fmax(out->t_max, t[m]);
+    if (s.steps) out->dt_min = std::fmin(out->dt_min, s.dt_min);
+    out->dt_max = std::fmax(out->dt_max, s.dt_max);
+  }
+  return EIS_OK;
+}
+
+static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats* out) {
+  if (!c) return EIS_E_ARG;
+  if (c->sticky) return c->sticky;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "step before set_state%s");
+  if (n_steps < 0) return fail(c, EIS_E_ARG, "negative step count%s");
+  CU(cudaSetDevice(c->grid.device));
+  if (n_steps > 0) {
+    const unsigned M = (unsigned)c->grid.n_members;
+    if (c->threads <= 256)
+      resident_steps<256, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else
+      resident_steps<1024, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    CU(cudaGetLastError());
+  }
+  if (out) return collect_stats(c, out);
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_step(eis_ctx* c, int64_t n_steps, eis_stats* out) {
+  return launch(c, n_steps, INFINITY, out);
+}
+
+extern "C" eis_status eis_run_to(eis_ctx* c, double t_end, int64_t max_steps, eis_stats* out) {
+  return launch(c, max_steps, t_end, out);
+}
+
+extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double* width, uint8_t* phase,
+                                    int64_t* n_cells, double* t, int32_t where) {
+  if (!c) return EIS_E_ARG;
+  if (c->sticky) return c->sticky;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "get_state before set_state%s");
+  if (where != EIS_HOST && where != EIS_DEVICE) return fail(c, EIS_E_ARG, "get_state: bad where%s");
+  CU(cudaSetDevice(c->grid.device));
+  const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
+  const size_t cells = (size_t)M * cap;
+  if (where == EIS_DEVICE) {
+    k_pack<<<(unsigned)M, 256, 0, c->stream>>>(c->e, c->g, rho, mom, width, phase);
+    CU(cudaGetLastError());
+    if (n_cells) CU(cudaMemcpyAsync(n_cells, c->d_n, M * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (t) CU(cudaMemcpyAsync(t, c->d_t, M * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return EIS_OK;
+  }
+  eis_status s = ensure_pack(c);
+  if (s) return s;
+  double* pr = c->d_pack;
+  k_pack<<<(unsigned)M, 256, 0, c->stream>>>(c->e, c->g, rho ? pr : nullptr, mom ? pr + cells : nullptr,
+                                             width ? pr + 2 * cells : nullptr, phase ? c->d_u8 : nullptr);
+  CU(cudaGetLastError());
+  if (rho) CU(cudaMemcpyAsync(rho, pr, cells * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (mom) CU(cudaMemcpyAsync(mom, pr + cells, cells * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (width) CU(cudaMemcpyAsync(width, pr + 2 * cells, cells * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (phase) CU(cudaMemcpyAsync(phase, c->d_u8, cells, cudaMemcpyDeviceToHost, c->stream));
+  if (n_cells) CU(cudaMemcpyAsync(n_cells, c->d_n, M * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (t) CU(cudaMemcpyAsync(t, c->d_t, M * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t capacity, int64_t* count) {
+  if (!c || !count) return EIS_E_ARG;
+  if (c->sticky) return c->sticky;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "interfaces before set_state%s");
+  CU(cudaSetDevice(c->grid.device));
+  const long long M = c->grid.n_members;
+  const unsigned nb = (unsigned)((M + 127) / 128);
+  k_iface<<<nb, 128, 0, c->stream>>>(c->e, c->g, M, c->grid.x_left, nullptr, c->d_cnt, nullptr, 0);
+  CU(cudaGetLastError());
+  std::vector<long long> cnt(M), off(M);
+  CU(cudaMemcpyAsync(cnt.data(), c->d_cnt, M * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  long long total = 0;
+  for (long long m = 0; m < M; ++m) { off[m] = total; total += cnt[m]; }
+  *count = total;
+  if (out && capacity > 0 && total > 0) {
+    if (c->if_cap < total) {
+      cudaFree(c->d_if);
+      c->d_if = nullptr;
+      CU(cudaMalloc(&c->d_if, total * sizeof(eis_interface)));
+      c->if_cap = total;
+    }
+    long long* d_off = nullptr;
+    CU(cudaMalloc(&d_off, M * 8));
+    CU(cudaMemcpyAsync(d_off, off.data(), M * 8, cudaMemcpyHostToDevice, c->stream));
+    k_iface<<<nb, 128, 0, c->stream>>>(c->e, c->g, M, c->grid.x_left, d_off, nullptr, c->d_if, total);
+    CU(cudaGetLastError());
+    const long long ncopy = total < capacity ? total : capacity;
+    CU(cudaMemcpyAsync(out, c->d_if, ncopy * sizeof(eis_interface), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_off);
+  }
+  return (out && total > capacity) ? EIS_E_CAPACITY : EIS_OK;
+}
+
+extern "C" eis_status eis_member_status(eis_ctx* c, int32_t* out) {
+  if (!c || !out) return EIS_E_ARG;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "member_status before set_state%s");
+  CU(cudaMemcpyAsync(out, c->d_status, c->grid.n_members * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
+  if (!c || !out) return EIS_E_ARG;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "member_stats before set_state%s");
+  const long long M = c->grid.n_members;
+  std::vector<MemberStats> ms(M);
+  std::vector<double> t(M);
+  CU(cudaMemcpyAsync(ms.data(), c->d_stats, M * sizeof(MemberStats), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(t.data(), c->d_t, M * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (long long m = 0; m < M; ++m) {
+    const MemberStats& s = ms[m];
+    eis_stats& o = out[m];
+    o.steps = s.steps; o.cell_updates = s.cell_updates; o.dts_iters = s.dts_iters; o.iface_solves = s.iface_solves;
+    o.creations = s.creations; o.splits = s.splits; o.merges = s.merges; o.regions = s.regions;
+    o.t_min = o.t_max = t[m]; o.dt_min = s.dt_min; o.dt_max = s.dt_max;
+  }
+  return EIS_OK;
+}

@@ -1,0 +1,334 @@
+// eis_device.cuh — device-side thermodynamics and Riemann solvers (sm_100a, fp64).
+//
+// "P:n" = line n of /root/reference/PAPER.md; "R<k>" = DESIGN.md §3 reading.  Written
+// independently of oracle/ (which uses FD Jacobians, sequential Armijo and the pressure form
+// of the wave functions); this file uses the analytic Jacobian of Eq. (14),
+// half-warp lane-parallel Armijo candidates and the density form of the wave functions (R19).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace eis {
+
+enum : int { VAP = 0, LIQ = 1, SPIN = 2 };
+
+// status codes (values of eis_status)
+enum : int {
+  ST_OK = 0, ST_NONPOS = 3, ST_SPINODAL = 4, ST_NEWTON = 5, ST_CREATION = 6, ST_DTS_CAP = 7,
+  ST_WIDTH = 8, ST_CAPACITY = 9, ST_UNSUPPORTED = 12
+};
+
+// Derived, immutable EOS constants (thresholds per R3).
+struct Eos {
+  double a_v2, a_v, a_l, a_l2, rho0, p0, tau, rho_min, rho_tilde;
+  double inv_av2, inv_al2, inv_p0, inv_av, inv_rho0;
+};
+
+struct Prm {
+  double cfl, eps_split, eps_tiny, theta_nb, tol_nb, tol_tiny, newton_rtol, newton_gtol, h_av;
+  long long dts_max_iter;
+  int newton_max_iter, armijo_max, mode;
+};
+
+__device__ __forceinline__ int phase_of(const Eos& e, double rho) {
+  return rho <= e.rho_tilde ? VAP : (rho >= e.rho_min ? LIQ : SPIN);
+}
+// vapour ideal gas, liquid linear Tait (R1)
+__device__ __forceinline__ double pres(const Eos& e, int ph, double rho) {
+  return ph == VAP ? e.a_v2 * rho : e.p0 + e.a_l2 * (rho - e.rho0);
+}
+__device__ __forceinline__ double sound(const Eos& e, int ph) { return ph == VAP ? e.a_v : e.a_l; }
+
+// Outer-wave function in density form (P:1496-1503 with R19): rarefaction a ln(r*/r_K),
+// shock a (r* - r_K)/sqrt(r* r_K); df/dr* alongside.
+__device__ __forceinline__ void wave_fd(double a, double rs, double rk, double& f, double& df) {
+  if (rs > rk) {
+    double q = sqrt(rs * rk);
+    double iq = 1.0 / q;
+    f = a * (rs - rk) * iq;
+    df = 0.5 * a * (rs + rk) * iq / rs;
+  } else {
+    f = a * log(rs / rk);
+    df = a / rs;
+  }
+}
+__device__ __forceinline__ double wave_f(double a, double rs, double rk) {
+  if (rs > rk) return a * (rs - rk) / sqrt(rs * rk);
+  return a * log(rs / rk);
+}
+
+// HLL flux with Davis bounds.  Same phase, constant sound speed a.
+__device__ __forceinline__ void hll(const Eos& e, int ph, double rl, double ml, double ul, double rr,
+                                    double mr, double ur, double& F0, double& F1) {
+  double a = sound(e, ph);
+  double FL1 = ml * ul + pres(e, ph, rl);
+  double FR1 = mr * ur + pres(e, ph, rr);
+  double SL = fmin(ul, ur) - a, SR = fmax(ul, ur) + a;
+  if (SL >= 0.0) { F0 = ml; F1 = FL1; return; }
+  if (SR <= 0.0) { F0 = mr; F1 = FR1; return; }
+  double inv = 1.0 / (SR - SL), SLSR = SL * SR;
+  F0 = (SR * ml - SL * mr + SLSR * (rr - rl)) * inv;
+  F1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
+}
+
+// Creation trigger, reading R7: liquid edge cavitates iff Phi(rho_min) > 0, vapour edge
+// nucleates iff Phi(rho_tilde) < 0, Phi(r) = f(r; r_L) + f(r; r_R) + du.  Exact pre-filters:
+// ln y >= 1 - 1/y gives Phi_liq(rho_min) <= du - a(1 - rho_min^2/(r_L r_R))... (no trigger when
+// du <= a_l (1 - rho_min^2/(r_L r_R)) for two rarefactions); nucleation needs du < 0.
+__device__ __forceinline__ bool creation_trigger(const Eos& e, int ph, double rl, double ul, double rr, double ur) {
+  double du = ur - ul;
+  if (ph == LIQ) {
+    if (rl >= e.rho_min && rr >= e.rho_min && du <= e.a_l * (1.0 - e.rho_min * e.rho_min / (rl * rr))) return false;
+    return wave_f(e.a_l, e.rho_min, rl) + wave_f(e.a_l, e.rho_min, rr) + du > 0.0;
+  }
+  if (du >= 0.0) return false;
+  return wave_f(e.a_v, e.rho_tilde, rl) + wave_f(e.a_v, e.rho_tilde, rr) + du < 0.0;
+}
+
+// ---------------------------------------------------------------------------------------
+// Nonlinear 2x2 problems: G and the analytic Jacobian.
+// ---------------------------------------------------------------------------------------
+// Kinetic relation z = tau p_V [[g + e_kin]], e_kin interface-relative (R2):
+// A z^2 - z + B = 0 -> z = 2B/(1 + sqrt(1 - 4AB)); since 2Az - 1 = -sqrt(1 - 4AB) for this
+// root, dz/dq = (dA/dq z^2 + dB/dq) / sqrt(1 - 4AB).
+
+// Two-phase interface (App. A, system (13), orientation-general [[x]] = x+ - x-),
+// unknowns x = (p_V*, p_L*).
+struct IfaceProb {
+  double rV, uV, rL, uL;  // outer states by phase
+  double du;              // u_plus - u_minus
+  double sV;              // +1 if the vapour is the plus side, -1 if it is the minus side
+};
+
+__device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, double pV, double pL,
+                                           double G[2], double J[4], double* zout) {
+  if (!(pV > 0.0)) return false;
+  double rVs = pV * e.inv_av2;
+  double rLs = e.rho0 + (pL - e.p0) * e.inv_al2;
+  if (!(rLs > 0.0)) return false;
+  double vV = 1.0 / rVs, vL = 1.0 / rLs;
+  double gV = e.a_v2 * log(pV * e.inv_p0), gL = e.a_l2 * log(rLs * e.inv_rho0);
+  double sV = P.sV, sL = -P.sV;
+  double jp = sV * pV + sL * pL, jv = sV * vV + sL * vL;
+  double jv2 = sV * vV * vV + sL * vL * vL, jg = sV * gV + sL * gL;
+  double tp = e.tau * pV;
+  double A = 0.5 * tp * jv2, B = tp * jg;
+  double disc = 1.0 - 4.0 * A * B;
+  if (!(disc > 0.0)) return false;
+  double sq = sqrt(disc);
+  double z = 2.0 * B / (1.0 + sq);
+  double fV, dfV, fL, dfL;
+  wave_fd(e.a_v, rVs, P.rV, fV, dfV);
+  wave_fd(e.a_l, rLs, P.rL, fL, dfL);
+  G[0] = (jp + z * z * jv) * e.inv_p0;
+  G[1] = (fV + fL + z * jv + P.du) * e.inv_av;
+  if (zout) *zout = z;
+  if (J) {
+    double dvV = -vV * vV * e.inv_av2, dvL = -vL * vL * e.inv_al2;  // dv/dp
+    double dA_V = 0.5 * e.tau * jv2 + tp * sV * vV * dvV;           // d(v^2)/dp = 2 v dv/dp
+    double dA_L = tp * sL * vL * dvL;
+    double dB_V = e.tau * jg + tp * sV * vV;                         // dg/dp = v
+    double dB_L = tp * sL * vL;
+    double isq = 1.0 / sq, z2 = z * z;
+    double zV = (dA_V * z2 + dB_V) * isq, zL = (dA_L * z2 + dB_L) * isq;
+    J[0] = (sV + 2.0 * z * zV * jv + z2 * sV * dvV) * e.inv_p0;
+    J[1] = (sL + 2.0 * z * zL * jv + z2 * sL * dvL) * e.inv_p0;
+    J[2] = (dfV * e.inv_av2 + zV * jv + z * sV * dvV) * e.inv_av;
+    J[3] = (dfL * e.inv_al2 + zL * jv + z * sL * dvL) * e.inv_av;
+  }
+  return true;
+}
+
+// Creation (App. B, reading R18): unknowns x = (p_A, p_B); A = outer phase, B = created.
+struct CreateProb {
+  int A;                 // outer phase (LIQ: cavitation, VAP: nucleation)
+  double rl, rr, du;     // outer states' densities and u_r - u_l
+};
+
+__device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, double pA, double pB,
+                                            double G[2], double J[4], double* zout) {
+  const bool cav = (P.A == LIQ);
+  double rA = cav ? e.rho0 + (pA - e.p0) * e.inv_al2 : pA * e.inv_av2;
+  double rB = cav ? pB * e.inv_av2 : e.rho0 + (pB - e.p0) * e.inv_al2;
+  if (!(rA > 0.0) || !(rB > 0.0)) return false;
+  double pV = cav ? pB : pA;
+  if (!(pV > 0.0)) return false;
+  double vA = 1.0 / rA, vB = 1.0 / rB;
+  double gA = cav ? e.a_l2 * log(rA * e.inv_rho0) : e.a_v2 * log(pA * e.inv_p0);
+  double gB = cav ? e.a_v2 * log(pB * e.inv_p0) : e.a_l2 * log(rB * e.inv_rho0);
+  double jv = vA - vB, jv2 = vA * vA - vB * vB, jg = gA - gB;  // right boundary: minus B, plus A
+  double tp = e.tau * pV;
+  double A = 0.5 * tp * jv2, B = tp * jg;
+  double disc = 1.0 - 4.0 * A * B;
+  if (!(disc > 0.0)) return false;
+  double sq = sqrt(disc);
+  double z = 2.0 * B / (1.0 + sq);
+  double aA = cav ? e.a_l : e.a_v;
+  double f1, df1, f2, df2;
+  wave_fd(aA, rA, P.rl, f1, df1);
+  wave_fd(aA, rA, P.rr, f2, df2);
+  G[0] = (pA - pB + z * z * jv) * e.inv_p0;
+  G[1] = (P.du + f1 + f2 + 2.0 * z * jv) * e.inv_av;
+  if (zout) *zout = z;
+  if (J) {
+    double ia2A = cav ? e.inv_al2 : e.inv_av2, ia2B = cav ? e.inv_av2 : e.inv_al2;
+    double dvA = -vA * vA * ia2A, dvB = -vB * vB * ia2B;
+    double dA_A = (cav ? 0.0 : 0.5 * e.tau * jv2) + tp * vA * dvA;
+    double dA_B = (cav ? 0.5 * e.tau * jv2 : 0.0) - tp * vB * dvB;
+    double dB_A = (cav ? 0.0 : e.tau * jg) + tp * vA;
+    double dB_B = (cav ? e.tau * jg : 0.0) - tp * vB;
+    double isq = 1.0 / sq, z2 = z * z;
+    double zA = (dA_A * z2 + dB_A) * isq, zB = (dA_B * z2 + dB_B) * isq;
+    J[0] = (1.0 + 2.0 * z * zA * jv + z2 * dvA) * e.inv_p0;
+    J[1] = (-1.0 + 2.0 * z * zB * jv - z2 * dvB) * e.inv_p0;
+    J[2] = ((df1 + df2) * ia2A + 2.0 * zA * jv + 2.0 * z * dvA) * e.inv_av;
+    J[3] = (2.0 * zB * jv - 2.0 * z * dvB) * e.inv_av;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------------------
+// Newton-Armijo (Kelley) executed by a group of 16 lanes (a half warp):
+// every lane holds the same iterate; Armijo candidates lambda = 2^-k are evaluated in
+// parallel, k = lane (+16 per round), the accepted step is the smallest k satisfying
+// ||G(x + lambda d)||_2 <= (1 - 1e-4 lambda) ||G(x)||_2 (identical to sequential halving).
+// Stop rule R14.  Returns iteration count (>= 0) or -1.
+// ---------------------------------------------------------------------------------------
+template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*)>
+__device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, unsigned mask,
+                         int hl, int base_lane) {
+  double G[2], J[4];
+  if (!EVAL(e, P, x0, x1, G, J, nullptr)) return -1;
+  for (int it = 0; it < p.newton_max_iter; ++it) {
+    double det = J[0] * J[3] - J[1] * J[2];
+    if (!(fabs(det) > 0.0) || !isfinite(det)) return -1;
+    double idet = 1.0 / det;
+    double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
+    double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
+    double n0 = sqrt(G[0] * G[0] + G[1] * G[1]);
+    int acc = -1;
+    double lam_acc = 0.0, xt0 = x0, xt1 = x1;
+    double Gt[2] = {0.0, 0.0}, Jt[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int round = 0; round * 16 <= p.armijo_max; ++round) {
+      int k = round * 16 + hl;
+      double lam = ldexp(1.0, -k);
+      double y0 = x0 + lam * d0, y1 = x1 + lam * d1;
+      double Gy[2], Jy[4];
+      bool ok = false;
+      if (k <= p.armijo_max && EVAL(e, P, y0, y1, Gy, Jy, nullptr))
+        ok = sqrt(Gy[0] * Gy[0] + Gy[1] * Gy[1]) <= (1.0 - 1e-4 * lam) * n0;
+      unsigned b = __ballot_sync(mask, ok) & mask;
+      if (b) {
+        int src = __ffs(b) - 1;  // absolute lane id of the smallest accepted k
+        acc = round * 16 + (src - base_lane);
+        lam_acc = ldexp(1.0, -acc);
+        xt0 = __shfl_sync(mask, y0, src);
+        xt1 = __shfl_sync(mask, y1, src);
+        Gt[0] = __shfl_sync(mask, Gy[0], src);
+        Gt[1] = __shfl_sync(mask, Gy[1], src);
+        for (int q = 0; q < 4; ++q) Jt[q] = __shfl_sync(mask, Jy[q], src);
+        break;
+      }
+    }
+    if (acc < 0) {
+      if (fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol) return it;  // rounding floor
+      return -1;
+    }
+    double s0 = xt0 - x0, s1 = xt1 - x1;
+    (void)lam_acc;
+    x0 = xt0; x1 = xt1;
+    G[0] = Gt[0]; G[1] = Gt[1];
+    for (int q = 0; q < 4; ++q) J[q] = Jt[q];
+    if (fabs(s0) <= p.newton_rtol * fmax(fabs(x0), e.p0) && fabs(s1) <= p.newton_rtol * fmax(fabs(x1), e.p0) &&
+        fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol)
+      return it + 1;
+  }
+  return -1;
+}
+
+// HLLC starting value (Eq. (17)), vapour left / liquid right, mirrored when the
+// liquid is on the left; clamped to [0.01 p0, 4 p0] (R14b).
+__device__ __forceinline__ double hllc_guess(const Eos& e, double rV, double uV, double rL, double uL) {
+  double pV = e.a_v2 * rV, pL = e.p0 + e.a_l2 * (rL - e.rho0);
+  double SL = uL + e.a_l, SV = uV - e.a_v;
+  double w = (pL - pV + rV * uV * (SV - uV) - rL * uL * (SL - uL)) / (rV * (SV - uV) - rL * (SL - uL));
+  double rLs = rL * (SL - uL) / (SL - w);
+  double ps = e.p0 + e.a_l2 * (rLs - e.rho0);
+  return fmin(fmax(ps, 0.01 * e.p0), 4.0 * e.p0);
+}
+
+struct IfaceSol {
+  double F0, F1, w, pV, pL;
+  int iters;  // -1 on failure
+};
+
+// Phase-boundary Riemann solve by a half warp.  (rm, um) minus (left) state, (rp, up) plus.
+// Warm start: if x_init0 > 0 use (x_init0, x_init1) as the first iterate, else HLLC.
+// Outputs F_PB = (-z, -z u_V* + p_V*) (vapour side R17), w = u_V* + z v_V*.
+__device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, double rm, double um, double rp,
+                                                   double up, bool vap_minus, double x_init0, double x_init1,
+                                                   unsigned mask, int hl, int base_lane) {
+  IfaceProb P;
+  if (vap_minus) { P.rV = rm; P.uV = um; P.rL = rp; P.uL = up; P.sV = -1.0; }
+  else { P.rV = rp; P.uV = up; P.rL = rm; P.uL = um; P.sV = 1.0; }
+  P.du = up - um;
+  double x0, x1;
+  if (x_init0 > 0.0) { x0 = x_init0; x1 = x_init1; }
+  else {
+    double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
+    x0 = g; x1 = g;
+  }
+  IfaceSol s;
+  int it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, mask, hl, base_lane);
+  if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
+    double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
+    x0 = g; x1 = g;
+    it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, mask, hl, base_lane);
+  }
+  s.iters = it;
+  double G[2], z = 0.0;
+  if (it < 0 || !iface_eval(e, P, x0, x1, G, nullptr, &z)) { s.iters = -1; s.F0 = s.F1 = s.w = 0.0; s.pV = x0; s.pL = x1; return s; }
+  double rVs = x0 * e.inv_av2;
+  double uVs = vap_minus ? P.uV - wave_f(e.a_v, rVs, P.rV) : P.uV + wave_f(e.a_v, rVs, P.rV);
+  s.w = uVs + z / rVs;
+  s.F0 = -z;
+  s.F1 = -z * uVs + x0;
+  s.pV = x0; s.pL = x1;
+  return s;
+}
+
+struct CreateSol {
+  double Fl0, Fl1, wl, Fr0, Fr1, wr, rB, mB;
+  int iters;
+};
+
+// Phase creation by a half warp (App. B steps (ii)-(v), reading R18), Newton start (p0, p0).
+__device__ __noinline__ CreateSol create_solve_hw(const Eos& e, const Prm& p, int phase_outer, double rl,
+                                                     double ul, double rr, double ur, unsigned mask, int hl,
+                                                     int base_lane) {
+  CreateProb P{phase_outer, rl, rr, ur - ul};
+  double x0 = e.p0, x1 = e.p0;
+  int it = newton_hw<CreateProb, create_eval>(e, p, P, x0, x1, mask, hl, base_lane);
+  CreateSol s;
+  s.iters = it;
+  double G[2], zr = 0.0;
+  if (it < 0 || !create_eval(e, P, x0, x1, G, nullptr, &zr)) { s.iters = -1; return s; }
+  const bool cav = (phase_outer == LIQ);
+  double rA = cav ? e.rho0 + (x0 - e.p0) * e.inv_al2 : x0 * e.inv_av2;
+  double rB = cav ? x1 * e.inv_av2 : e.rho0 + (x1 - e.p0) * e.inv_al2;
+  double aA = cav ? e.a_l : e.a_v;
+  double uAl = ul - wave_f(aA, rA, rl);
+  double vA = 1.0 / rA, vB = 1.0 / rB;
+  double uB = uAl + zr * (vB - vA);
+  double zl = -zr;
+  s.wl = uB + zl * vB;
+  s.wr = uB + zr * vB;
+  s.Fl0 = -zl; s.Fl1 = -zl * uB + x1;
+  s.Fr0 = -zr; s.Fr1 = -zr * uB + x1;
+  s.rB = rB;
+  s.mB = rB * uB;
+  if (!(s.wr > s.wl)) s.iters = -1;
+  return s;
+}
+
+}  // namespace eis
