@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py — fp64 cell-updates/s of the explicit-implicit splitting hot path on B200.
+
+Default workload: BASELINE.json configs[2] (C3), the batched cavitation ensemble — 65,536
+independent 1D grids of N=1024 cells — the largest single-GPU configuration whose metric is
+cell-updates/s (configs[0]/[1] are single ~1e3-cell grids and are parity cases).  One bench
+"step" = one large time step of the whole method for every member.
+The K timed steps start from the seeded initial state (so they include the cavitation step),
+run as ONE launch of the member-resident kernel (eis_step(K)); inputs are resident in HBM
+(1.1 GB, larger than the 126 MB L2) when the timed region starts.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eis|reference] [--workload C3|C4|C1|C2]
+
+Multi-GPU (torchrun): members are sharded contiguously across ranks, no collective in the
+data path (scaling "strong": the ensemble is fixed); timing is the max over ranks.
+--impl reference times the CPU oracle (oracle/) on a bounded member sample (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic fp64 operations per cell-update of the bulk path: decode 5,
+# HLL edge flux + creation pre-filter 36, moving-cell update 15; one division = 1 op.
+FLOP_PER_CELL_UPDATE = 56
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 FMA/clk x 2 x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="eis", choices=["eis", "reference"])
+    ap.add_argument("--workload", default="C3", choices=["C3", "C4", "C1", "C2"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--members", type=int, default=0, help="profiling only: fewer ensemble members")
+    ap.add_argument("--start-steps", type=int, default=0, help="profiling only: untimed steps before the timed launch")
+    return ap.parse_args()
+
+
+def workload(name, members=None):
+    from paper_2211_00705_b200 import workloads as W
+    if name == "C3":
+        return W.c3(members=members) if members is not None else W.c3()
+    if name == "C4":
+        return W.c4(members=members) if members is not None else W.c4()
+    if name == "C1":
+        return W.c1()
+    return W.c2()
+
+
+def total_members(name):
+    return {"C3": 65536, "C4": 16384, "C1": 1, "C2": 1}[name]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        if not self.rows:  # region shorter than one period: one sample right after
+            out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i",
+                                  str(self.device)], capture_output=True, text=True).stdout
+            self.rows = [[s.strip() for s in out.strip().split(",")]] if out.strip() else []
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["fp64_tflops"], "measured DFMA microbenchmark (profiles/fp64_peak.json)"
+    return NOMINAL_FP64_TFLOPS, "nominal 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (no measurement)"
+
+
+def ncu_traffic(workload_name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("workload") == workload_name:
+            return d.get("bytes_per_launch")
+    return None
+
+
+def cpu_sample_size(K, N):
+    return int(min(4096, max(1, round(1.5e8 / (K * N)))))
+
+
+def run_oracle(name, members, steps):
+    from oracle import oracle as O
+    w = workload(name, members)
+    s = O.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"])
+    s.set_state(w["rho"], w["mom"])
+    t0 = time.perf_counter()
+    st = s.step(steps) if "steps" in w else s.run_to(w["t_end"], steps)
+    dt = time.perf_counter() - t0
+    return st, dt
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.workload
+    N = {"C3": 1024, "C4": 4096, "C1": 200, "C2": 1000}[name]
+    S = cpu_sample_size(max(args.steps, 1), N)
+    members = np.arange(S)
+    if args.warmup:
+        run_oracle(name, members[:1], args.warmup)
+    st, dt = run_oracle(name, members, args.steps)
+    v = st["cell_updates"] / dt
+    sample = f"members 0..{S - 1} of {name}, {args.steps} large steps from t=0 (after {args.warmup} warm-up steps on member 0)"
+    print(json.dumps({
+        "impl": "reference", "metric": "fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{name} (CPU oracle sample)", "members": S, "cells_per_member": N},
+        "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00705_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = args.workload
+    Mtot = args.members or total_members(name)
+    lo, hi = rank * Mtot // world, (rank + 1) * Mtot // world
+    w = workload(name, np.arange(lo, hi) if name in ("C3", "C4") else None)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], device=local,
+                    stream=stream)
+    rho_d = torch.from_numpy(w["rho"]).cuda()
+    mom_d = torch.from_numpy(w["mom"]).cuda()
+    t_end = w.get("t_end", float("inf"))
+
+    def advance(k):
+        if t_end == float("inf"):
+            ctx.step(k)
+        else:
+            ctx.run_to(t_end, k)
+
+    # warm-up (untimed), then reset to the initial state
+    ctx.set_state(rho_d, mom_d)
+    advance(args.warmup)
+    torch.cuda.synchronize()
+    ctx.set_state(rho_d, mom_d)
+    cu0 = 0
+    if args.start_steps:
+        advance(args.start_steps)
+        cu0 = ctx.step(0, stats=True)["cell_updates"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    advance(args.steps)  # ONE launch of the member-resident kernel
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = ctx.step(0, stats=True)  # counters of exactly the timed steps (set_state reset them)
+    status = ctx.member_status()
+    nbad = int((status != 0).sum())
+    cu = st["cell_updates"] - cu0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([cu, nbad], device="cuda", dtype=torch.int64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        cu, nbad = int(c[0].item()), int(c[1].item())
+    value = cu / (ms * 1e-3)
+
+    # end to end through the public API with pinned host buffers: set_state(host) + K steps
+    # + get_state(host), one user call sequence per K steps
+    e2e = None
+    if not args.no_e2e:
+        rho_h = torch.from_numpy(w["rho"]).pin_memory()
+        mom_h = torch.from_numpy(w["mom"]).pin_memory()
+        out = {"rho": torch.empty(w["rho"].shape, dtype=torch.float64).pin_memory(),
+               "mom": torch.empty(w["rho"].shape, dtype=torch.float64).pin_memory(),
+               "h": torch.empty(w["rho"].shape, dtype=torch.float64).pin_memory(),
+               "n": torch.empty(w["M"], dtype=torch.int64).pin_memory(),
+               "t": torch.empty(w["M"], dtype=torch.float64).pin_memory()}
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ctx.set_state(rho_h, mom_h)
+        advance(args.steps)
+        ctx.get_state(out)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        cells = w["M"] * w["cap"] * world
+        e2e = {"value": cu / te, "unit": "cell-updates/s",
+               "h2d_bytes_per_step": 2 * 8 * cells / max(args.steps, 1),
+               "d2h_bytes_per_step": (3 * 8 * cells + 16 * w["M"] * world) / max(args.steps, 1),
+               "note": "one set_state(host pinned) + eis_step(K) + get_state(host pinned) sequence; bytes / K"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        S = cpu_sample_size(max(args.steps, 1), w["N"])
+        sts, dts = run_oracle(name, np.arange(S) if name in ("C3", "C4") else None, args.steps)
+        cpu = {"value": sts["cell_updates"] / dts, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"members 0..{S - 1} of {name}, the same {args.steps} large steps from t=0, single thread"}
+
+    peak, peak_src = fp64_peak()
+    achieved = FLOP_PER_CELL_UPDATE * cu / (ms * 1e-3) / world / 1e12  # per GPU
+    if rank == 0:
+        line = {
+            "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64, BASELINE configs recipe)",
+            "config": {"workload": f"{name}: {Mtot} members x {w['N']} cells, cavitation ensemble" if name == "C3"
+                       else f"{name}: {Mtot} members x {w['N']} cells",
+                       "members": Mtot, "cells_per_member": w["N"], "cell_capacity": w["cap"],
+                       "parallelism": f"member-sharded dp{world}", "l2": "inputs (1.1 GB per GPU) larger than L2",
+                       "launches": "one member-resident kernel launch for the K timed steps"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
+                         "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1, "clocks": clk,
+            "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
+                                         "merges", "regions")},
+            "members_not_ok": nbad,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -52,7 +52,8 @@ typedef enum {
   EIS_E_CAPACITY = 9,        /* cell_capacity or an internal table exceeded                */
   EIS_E_CUDA = 10,           /* CUDA runtime error (message in eis_last_error)             */
   EIS_E_NCCL = 11,           /* reserved: NCCL error                                       */
-  EIS_E_UNSUPPORTED = 12     /* tiny cell at a domain end (R26)                            */
+  EIS_E_UNSUPPORTED = 12,    /* tiny cell at a domain end (R26)                            */
+  EIS_E_INTERNAL = 13        /* internal consistency check failed (a bug: please report)   */
 } eis_status;
 
 enum { EIS_HOST = 0, EIS_DEVICE = 1 };

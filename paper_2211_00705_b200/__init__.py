@@ -25,7 +25,7 @@ EIS_HOST, EIS_DEVICE = 0, 1
 MODE_SPLIT, MODE_EXPLICIT = 0, 1
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_ORDER", 3: "E_NONPOS_DENSITY", 4: "E_SPINODAL", 5: "E_NEWTON",
           6: "E_CREATION", 7: "E_DTS_CAP", 8: "E_WIDTH", 9: "E_CAPACITY", 10: "E_CUDA", 11: "E_NCCL",
-          12: "E_UNSUPPORTED"}
+          12: "E_UNSUPPORTED", 13: "E_INTERNAL"}
 
 
 class EisError(RuntimeError):

@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,7 +23,7 @@ struct eis_ctx {
   Eos e;
   Prm p;
   cudaStream_t stream;
-  int threads;
+  int threads, minb;
   size_t smem;
   Members g;
   double *d_rho, *d_mom, *d_h, *d_t;
@@ -206,6 +207,7 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   Prm& p = c->p;
   p.cfl = prm->cfl; p.eps_split = prm->eps_split; p.eps_tiny = prm->eps_tiny; p.theta_nb = prm->theta_nb;
   p.tol_nb = prm->tol_nb; p.tol_tiny = prm->tol_tiny; p.newton_rtol = prm->newton_rtol; p.newton_gtol = prm->newton_gtol;
+  p.newton_stol = std::sqrt(prm->newton_rtol);
   p.h_av = (grid->x_right - grid->x_left) / (double)grid->n_cells;  // fixed (R9)
   p.dts_max_iter = prm->dts_max_iter; p.newton_max_iter = prm->newton_max_iter; p.armijo_max = prm->armijo_max;
   p.mode = prm->mode;
@@ -221,8 +223,7 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
     if (T > 1024) T = 1024;
     if (cap <= 2048 && T > 256) T = 256;
   }
-  if (T % 32 || T < 32 || T > 1024) { delete c; return EIS_E_ARG; }
-  while ((T / 32) * DTS_SCRATCH > cap + 1 && T > 32) T -= 32;
+  if (T % 32 || T < 64 || T > 1024) { delete c; return EIS_E_ARG; }  // >= 1 bulk warp + the solver warp
   c->threads = T;
   c->smem = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(cap + 1) + (((size_t)cap + 1 + 15) & ~size_t(15));
   int dev = grid->device;
@@ -230,9 +231,14 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if ((int)c->smem > max_optin) { delete c; return EIS_E_CAPACITY; }
+  // tuning knob (development): CTAs per SM the 256-thread variant is compiled for (2, 3, 4)
+  c->minb = 4;
+  if (const char* ev = getenv("EIS_RESIDENT_MINB")) { int v = atoi(ev); if (v >= 2 && v <= 4) c->minb = v; }
   cudaError_t e1 = cudaFuncSetAttribute(resident_steps<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  cudaError_t e3 = cudaFuncSetAttribute(resident_steps<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  cudaError_t e4 = cudaFuncSetAttribute(resident_steps<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e2 = cudaFuncSetAttribute(resident_steps<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) { delete c; return EIS_E_CUDA; }
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) { delete c; return EIS_E_CUDA; }
   const size_t cells = (size_t)M * cap;
   bool ok = cudaMalloc(&c->d_rho, cells * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cells * 8) == cudaSuccess &&
             cudaMalloc(&c->d_h, cells * 8) == cudaSuccess && cudaMalloc(&c->d_t, M * 8) == cudaSuccess &&
@@ -324,8 +330,12 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   CU(cudaSetDevice(c->grid.device));
   if (n_steps > 0) {
     const unsigned M = (unsigned)c->grid.n_members;
-    if (c->threads <= 256)
+    if (c->threads <= 256 && c->minb == 4)
       resident_steps<256, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else if (c->threads <= 256 && c->minb == 3)
+      resident_steps<256, 3><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else if (c->threads <= 256)
+      resident_steps<256, 2><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else
       resident_steps<1024, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     CU(cudaGetLastError());

@@ -15,7 +15,7 @@ enum : int { VAP = 0, LIQ = 1, SPIN = 2 };
 // status codes (values of eis_status)
 enum : int {
   ST_OK = 0, ST_NONPOS = 3, ST_SPINODAL = 4, ST_NEWTON = 5, ST_CREATION = 6, ST_DTS_CAP = 7,
-  ST_WIDTH = 8, ST_CAPACITY = 9, ST_UNSUPPORTED = 12
+  ST_WIDTH = 8, ST_CAPACITY = 9, ST_UNSUPPORTED = 12, ST_INTERNAL = 13
 };
 
 // Derived, immutable EOS constants (thresholds per R3).
@@ -25,7 +25,7 @@ struct Eos {
 };
 
 struct Prm {
-  double cfl, eps_split, eps_tiny, theta_nb, tol_nb, tol_tiny, newton_rtol, newton_gtol, h_av;
+  double cfl, eps_split, eps_tiny, theta_nb, tol_nb, tol_tiny, newton_rtol, newton_gtol, newton_stol, h_av;
   long long dts_max_iter;
   int newton_max_iter, armijo_max, mode;
 };
@@ -39,17 +39,27 @@ __device__ __forceinline__ double pres(const Eos& e, int ph, double rho) {
 }
 __device__ __forceinline__ double sound(const Eos& e, int ph) { return ph == VAP ? e.a_v : e.a_l; }
 
+// ln(a/b) for a/b near 1 (liquid densities, |a/b - 1| < 1e-2): 9-term series of ln(1 + x),
+// truncation < 1e-19 relative; otherwise log.  Exact reciprocals use __drcp_rn (correctly rounded,
+// so 1/x bit-for-bit, at half the latency of a division).
+__device__ __forceinline__ double ln_ratio(double a, double b) {
+  const double x = (a - b) * __drcp_rn(b);
+  if (fabs(x) < 1e-2) {
+    return x * (1.0 + x * (-0.5 + x * (1.0 / 3 + x * (-0.25 + x * (0.2 + x * (-1.0 / 6 + x * (1.0 / 7 + x * (-0.125 + x * (1.0 / 9)))))))));
+  }
+  return log(a * __drcp_rn(b));
+}
+
 // Outer-wave function in density form (P:1496-1503 with R19): rarefaction a ln(r*/r_K),
 // shock a (r* - r_K)/sqrt(r* r_K); df/dr* alongside.
 __device__ __forceinline__ void wave_fd(double a, double rs, double rk, double& f, double& df) {
   if (rs > rk) {
-    double q = sqrt(rs * rk);
-    double iq = 1.0 / q;
+    const double iq = rsqrt(rs * rk);
     f = a * (rs - rk) * iq;
-    df = 0.5 * a * (rs + rk) * iq / rs;
+    df = 0.5 * a * (rs + rk) * iq * __drcp_rn(rs);
   } else {
-    f = a * log(rs / rk);
-    df = a / rs;
+    f = a * ln_ratio(rs, rk);
+    df = a * __drcp_rn(rs);
   }
 }
 __device__ __forceinline__ double wave_f(double a, double rs, double rk) {
@@ -93,7 +103,7 @@ __device__ __forceinline__ bool creation_trigger(const Eos& e, int ph, double rl
 // root, dz/dq = (dA/dq z^2 + dB/dq) / sqrt(1 - 4AB).
 
 // Two-phase interface (App. A, system (13), orientation-general [[x]] = x+ - x-),
-// unknowns x = (p_V*, p_L*).
+// unknowns x = (p_V*, p_L*).  aux = (z, f_V).
 struct IfaceProb {
   double rV, uV, rL, uL;  // outer states by phase
   double du;              // u_plus - u_minus
@@ -101,89 +111,88 @@ struct IfaceProb {
 };
 
 __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, double pV, double pL,
-                                           double G[2], double J[4], double* zout) {
+                                           double G[2], double J[4], double aux[2]) {
   if (!(pV > 0.0)) return false;
-  double rVs = pV * e.inv_av2;
-  double rLs = e.rho0 + (pL - e.p0) * e.inv_al2;
+  const double rVs = pV * e.inv_av2;
+  const double rLs = e.rho0 + (pL - e.p0) * e.inv_al2;
   if (!(rLs > 0.0)) return false;
-  double vV = 1.0 / rVs, vL = 1.0 / rLs;
-  double gV = e.a_v2 * log(pV * e.inv_p0), gL = e.a_l2 * log(rLs * e.inv_rho0);
-  double sV = P.sV, sL = -P.sV;
-  double jp = sV * pV + sL * pL, jv = sV * vV + sL * vL;
-  double jv2 = sV * vV * vV + sL * vL * vL, jg = sV * gV + sL * gL;
-  double tp = e.tau * pV;
-  double A = 0.5 * tp * jv2, B = tp * jg;
-  double disc = 1.0 - 4.0 * A * B;
+  const double vV = e.a_v2 * __drcp_rn(pV), vL = __drcp_rn(rLs);
+  const double gV = e.a_v2 * log(pV * e.inv_p0), gL = e.a_l2 * ln_ratio(rLs, e.rho0);
+  const double sV = P.sV, sL = -P.sV;
+  const double jp = sV * pV + sL * pL, jv = sV * vV + sL * vL;
+  const double jv2 = sV * vV * vV + sL * vL * vL, jg = sV * gV + sL * gL;
+  const double tp = e.tau * pV;
+  const double A = 0.5 * tp * jv2, B = tp * jg;
+  const double disc = 1.0 - 4.0 * A * B;
   if (!(disc > 0.0)) return false;
-  double sq = sqrt(disc);
-  double z = 2.0 * B / (1.0 + sq);
+  const double sq = sqrt(disc);
+  const double z = 2.0 * B * __drcp_rn(1.0 + sq);
   double fV, dfV, fL, dfL;
   wave_fd(e.a_v, rVs, P.rV, fV, dfV);
   wave_fd(e.a_l, rLs, P.rL, fL, dfL);
   G[0] = (jp + z * z * jv) * e.inv_p0;
   G[1] = (fV + fL + z * jv + P.du) * e.inv_av;
-  if (zout) *zout = z;
-  if (J) {
-    double dvV = -vV * vV * e.inv_av2, dvL = -vL * vL * e.inv_al2;  // dv/dp
-    double dA_V = 0.5 * e.tau * jv2 + tp * sV * vV * dvV;           // d(v^2)/dp = 2 v dv/dp
-    double dA_L = tp * sL * vL * dvL;
-    double dB_V = e.tau * jg + tp * sV * vV;                         // dg/dp = v
-    double dB_L = tp * sL * vL;
-    double isq = 1.0 / sq, z2 = z * z;
-    double zV = (dA_V * z2 + dB_V) * isq, zL = (dA_L * z2 + dB_L) * isq;
-    J[0] = (sV + 2.0 * z * zV * jv + z2 * sV * dvV) * e.inv_p0;
-    J[1] = (sL + 2.0 * z * zL * jv + z2 * sL * dvL) * e.inv_p0;
-    J[2] = (dfV * e.inv_av2 + zV * jv + z * sV * dvV) * e.inv_av;
-    J[3] = (dfL * e.inv_al2 + zL * jv + z * sL * dvL) * e.inv_av;
-  }
+  aux[0] = z;
+  aux[1] = fV;
+  const double dvV = -vV * vV * e.inv_av2, dvL = -vL * vL * e.inv_al2;  // dv/dp
+  const double dA_V = 0.5 * e.tau * jv2 + tp * sV * vV * dvV;           // d(v^2)/dp = 2 v dv/dp
+  const double dA_L = tp * sL * vL * dvL;
+  const double dB_V = e.tau * jg + tp * sV * vV;                         // dg/dp = v
+  const double dB_L = tp * sL * vL;
+  const double isq = __drcp_rn(sq), z2 = z * z;
+  const double zV = (dA_V * z2 + dB_V) * isq, zL = (dA_L * z2 + dB_L) * isq;
+  J[0] = (sV + 2.0 * z * zV * jv + z2 * sV * dvV) * e.inv_p0;
+  J[1] = (sL + 2.0 * z * zL * jv + z2 * sL * dvL) * e.inv_p0;
+  J[2] = (dfV * e.inv_av2 + zV * jv + z * sV * dvV) * e.inv_av;
+  J[3] = (dfL * e.inv_al2 + zL * jv + z * sL * dvL) * e.inv_av;
   return true;
 }
 
 // Creation (App. B, reading R18): unknowns x = (p_A, p_B); A = outer phase, B = created.
+// aux = (z_r, f(rho_A*; rho_l)).
 struct CreateProb {
   int A;                 // outer phase (LIQ: cavitation, VAP: nucleation)
   double rl, rr, du;     // outer states' densities and u_r - u_l
 };
 
 __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, double pA, double pB,
-                                            double G[2], double J[4], double* zout) {
+                                            double G[2], double J[4], double aux[2]) {
   const bool cav = (P.A == LIQ);
-  double rA = cav ? e.rho0 + (pA - e.p0) * e.inv_al2 : pA * e.inv_av2;
-  double rB = cav ? pB * e.inv_av2 : e.rho0 + (pB - e.p0) * e.inv_al2;
+  const double rA = cav ? e.rho0 + (pA - e.p0) * e.inv_al2 : pA * e.inv_av2;
+  const double rB = cav ? pB * e.inv_av2 : e.rho0 + (pB - e.p0) * e.inv_al2;
   if (!(rA > 0.0) || !(rB > 0.0)) return false;
-  double pV = cav ? pB : pA;
+  const double pV = cav ? pB : pA;
   if (!(pV > 0.0)) return false;
-  double vA = 1.0 / rA, vB = 1.0 / rB;
-  double gA = cav ? e.a_l2 * log(rA * e.inv_rho0) : e.a_v2 * log(pA * e.inv_p0);
-  double gB = cav ? e.a_v2 * log(pB * e.inv_p0) : e.a_l2 * log(rB * e.inv_rho0);
-  double jv = vA - vB, jv2 = vA * vA - vB * vB, jg = gA - gB;  // right boundary: minus B, plus A
-  double tp = e.tau * pV;
-  double A = 0.5 * tp * jv2, B = tp * jg;
-  double disc = 1.0 - 4.0 * A * B;
+  const double vA = __drcp_rn(rA), vB = __drcp_rn(rB);
+  const double gA = cav ? e.a_l2 * ln_ratio(rA, e.rho0) : e.a_v2 * log(pA * e.inv_p0);
+  const double gB = cav ? e.a_v2 * log(pB * e.inv_p0) : e.a_l2 * ln_ratio(rB, e.rho0);
+  const double jv = vA - vB, jv2 = vA * vA - vB * vB, jg = gA - gB;  // right boundary: minus B, plus A
+  const double tp = e.tau * pV;
+  const double A = 0.5 * tp * jv2, B = tp * jg;
+  const double disc = 1.0 - 4.0 * A * B;
   if (!(disc > 0.0)) return false;
-  double sq = sqrt(disc);
-  double z = 2.0 * B / (1.0 + sq);
-  double aA = cav ? e.a_l : e.a_v;
+  const double sq = sqrt(disc);
+  const double z = 2.0 * B * __drcp_rn(1.0 + sq);
+  const double aA = cav ? e.a_l : e.a_v;
   double f1, df1, f2, df2;
   wave_fd(aA, rA, P.rl, f1, df1);
   wave_fd(aA, rA, P.rr, f2, df2);
   G[0] = (pA - pB + z * z * jv) * e.inv_p0;
   G[1] = (P.du + f1 + f2 + 2.0 * z * jv) * e.inv_av;
-  if (zout) *zout = z;
-  if (J) {
-    double ia2A = cav ? e.inv_al2 : e.inv_av2, ia2B = cav ? e.inv_av2 : e.inv_al2;
-    double dvA = -vA * vA * ia2A, dvB = -vB * vB * ia2B;
-    double dA_A = (cav ? 0.0 : 0.5 * e.tau * jv2) + tp * vA * dvA;
-    double dA_B = (cav ? 0.5 * e.tau * jv2 : 0.0) - tp * vB * dvB;
-    double dB_A = (cav ? 0.0 : e.tau * jg) + tp * vA;
-    double dB_B = (cav ? e.tau * jg : 0.0) - tp * vB;
-    double isq = 1.0 / sq, z2 = z * z;
-    double zA = (dA_A * z2 + dB_A) * isq, zB = (dA_B * z2 + dB_B) * isq;
-    J[0] = (1.0 + 2.0 * z * zA * jv + z2 * dvA) * e.inv_p0;
-    J[1] = (-1.0 + 2.0 * z * zB * jv - z2 * dvB) * e.inv_p0;
-    J[2] = ((df1 + df2) * ia2A + 2.0 * zA * jv + 2.0 * z * dvA) * e.inv_av;
-    J[3] = (2.0 * zB * jv - 2.0 * z * dvB) * e.inv_av;
-  }
+  aux[0] = z;
+  aux[1] = f1;
+  const double ia2A = cav ? e.inv_al2 : e.inv_av2, ia2B = cav ? e.inv_av2 : e.inv_al2;
+  const double dvA = -vA * vA * ia2A, dvB = -vB * vB * ia2B;
+  const double dA_A = (cav ? 0.0 : 0.5 * e.tau * jv2) + tp * vA * dvA;
+  const double dA_B = (cav ? 0.5 * e.tau * jv2 : 0.0) - tp * vB * dvB;
+  const double dB_A = (cav ? 0.0 : e.tau * jg) + tp * vA;
+  const double dB_B = (cav ? e.tau * jg : 0.0) - tp * vB;
+  const double isq = __drcp_rn(sq), z2 = z * z;
+  const double zA = (dA_A * z2 + dB_A) * isq, zB = (dA_B * z2 + dB_B) * isq;
+  J[0] = (1.0 + 2.0 * z * zA * jv + z2 * dvA) * e.inv_p0;
+  J[1] = (-1.0 + 2.0 * z * zB * jv - z2 * dvB) * e.inv_p0;
+  J[2] = ((df1 + df2) * ia2A + 2.0 * zA * jv + 2.0 * z * dvA) * e.inv_av;
+  J[3] = (2.0 * zB * jv - 2.0 * z * dvB) * e.inv_av;
   return true;
 }
 
@@ -192,55 +201,57 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
 // every lane holds the same iterate; Armijo candidates lambda = 2^-k are evaluated in
 // parallel, k = lane (+16 per round), the accepted step is the smallest k satisfying
 // ||G(x + lambda d)||_2 <= (1 - 1e-4 lambda) ||G(x)||_2 (identical to sequential halving).
-// Stop rule R14.  Returns iteration count (>= 0) or -1.
+// Each candidate evaluation returns G, the analytic Jacobian (14) and aux, so one
+// evaluation latency per iteration.  Stop (R14c): ||G(x_new)||_inf <= gtol and the accepted
+// step |s_j| <= sqrt(rtol) max(|x_j|, p0) -- with quadratic convergence the new iterate is then
+// within ~rtol of the root (the oracle tests the step against rtol itself, one extra iteration).
+// Returns the iteration count (>= 0) or -1; aux holds the value at the returned iterate.
 // ---------------------------------------------------------------------------------------
 template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*)>
-__device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, unsigned mask,
-                         int hl, int base_lane) {
+__device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, double aux[2],
+                         unsigned mask, int hl, int base_lane) {
   double G[2], J[4];
-  if (!EVAL(e, P, x0, x1, G, J, nullptr)) return -1;
+  if (!EVAL(e, P, x0, x1, G, J, aux)) return -1;
   for (int it = 0; it < p.newton_max_iter; ++it) {
-    double det = J[0] * J[3] - J[1] * J[2];
+    const double det = J[0] * J[3] - J[1] * J[2];
     if (!(fabs(det) > 0.0) || !isfinite(det)) return -1;
-    double idet = 1.0 / det;
-    double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
-    double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
-    double n0 = sqrt(G[0] * G[0] + G[1] * G[1]);
-    int acc = -1;
-    double lam_acc = 0.0, xt0 = x0, xt1 = x1;
-    double Gt[2] = {0.0, 0.0}, Jt[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int round = 0; round * 16 <= p.armijo_max; ++round) {
-      int k = round * 16 + hl;
-      double lam = ldexp(1.0, -k);
-      double y0 = x0 + lam * d0, y1 = x1 + lam * d1;
-      double Gy[2], Jy[4];
-      bool ok = false;
-      if (k <= p.armijo_max && EVAL(e, P, y0, y1, Gy, Jy, nullptr))
-        ok = sqrt(Gy[0] * Gy[0] + Gy[1] * Gy[1]) <= (1.0 - 1e-4 * lam) * n0;
-      unsigned b = __ballot_sync(mask, ok) & mask;
-      if (b) {
-        int src = __ffs(b) - 1;  // absolute lane id of the smallest accepted k
-        acc = round * 16 + (src - base_lane);
-        lam_acc = ldexp(1.0, -acc);
-        xt0 = __shfl_sync(mask, y0, src);
-        xt1 = __shfl_sync(mask, y1, src);
-        Gt[0] = __shfl_sync(mask, Gy[0], src);
-        Gt[1] = __shfl_sync(mask, Gy[1], src);
-        for (int q = 0; q < 4; ++q) Jt[q] = __shfl_sync(mask, Jy[q], src);
-        break;
+    const double idet = __drcp_rn(det);
+    const double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
+    const double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
+    const double n0 = G[0] * G[0] + G[1] * G[1];
+    // the full step first, on every lane alike (no divergence, no shuffles): accepted almost always
+    double y0 = x0 + d0, y1 = x1 + d1, Gy[2], Jy[4], ay[2];
+    const double c1 = 1.0 - 1e-4;
+    bool ok = EVAL(e, P, y0, y1, Gy, Jy, ay) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= c1 * c1 * n0;
+    double s0 = d0, s1 = d1;
+    if (!ok) {  // lane-parallel back-tracking: lane k tries lambda = 2^-(k+1), then 2^-(k+17)
+      int acc = -1;
+      for (int round = 0; round * 16 + 1 <= p.armijo_max && acc < 0; ++round) {
+        const int k = round * 16 + hl + 1;
+        const double lam = __longlong_as_double((long long)(1023 - k) << 52);  // 2^-k
+        y0 = x0 + lam * d0; y1 = x1 + lam * d1;
+        const double cl = 1.0 - 1e-4 * lam;
+        const bool okk = k <= p.armijo_max && EVAL(e, P, y0, y1, Gy, Jy, ay) &&
+                         Gy[0] * Gy[0] + Gy[1] * Gy[1] <= cl * cl * n0;
+        const unsigned b = __ballot_sync(mask, okk) & mask;
+        if (b) {
+          const int src = __ffs(b) - 1;  // the smallest accepted k
+          acc = k;
+          y0 = __shfl_sync(mask, y0, src); y1 = __shfl_sync(mask, y1, src);
+          Gy[0] = __shfl_sync(mask, Gy[0], src); Gy[1] = __shfl_sync(mask, Gy[1], src);
+          for (int q = 0; q < 4; ++q) Jy[q] = __shfl_sync(mask, Jy[q], src);
+          ay[0] = __shfl_sync(mask, ay[0], src); ay[1] = __shfl_sync(mask, ay[1], src);
+        }
       }
+      if (acc < 0) return fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol ? it : -1;  // rounding floor
+      s0 = y0 - x0; s1 = y1 - x1;
     }
-    if (acc < 0) {
-      if (fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol) return it;  // rounding floor
-      return -1;
-    }
-    double s0 = xt0 - x0, s1 = xt1 - x1;
-    (void)lam_acc;
-    x0 = xt0; x1 = xt1;
-    G[0] = Gt[0]; G[1] = Gt[1];
-    for (int q = 0; q < 4; ++q) J[q] = Jt[q];
-    if (fabs(s0) <= p.newton_rtol * fmax(fabs(x0), e.p0) && fabs(s1) <= p.newton_rtol * fmax(fabs(x1), e.p0) &&
-        fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol)
+    x0 = y0; x1 = y1;
+    G[0] = Gy[0]; G[1] = Gy[1];
+    for (int q = 0; q < 4; ++q) J[q] = Jy[q];
+    aux[0] = ay[0]; aux[1] = ay[1];
+    if (fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol && fabs(s0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
+        fabs(s1) <= p.newton_stol * fmax(fabs(x1), e.p0))
       return it + 1;
   }
   return -1;
@@ -266,34 +277,33 @@ struct IfaceSol {
 // Warm start: if x_init0 > 0 use (x_init0, x_init1) as the first iterate, else HLLC.
 // Outputs F_PB = (-z, -z u_V* + p_V*) (vapour side R17), w = u_V* + z v_V*.
 __device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, double rm, double um, double rp,
-                                                   double up, bool vap_minus, double x_init0, double x_init1,
-                                                   unsigned mask, int hl, int base_lane) {
+                                                double up, bool vap_minus, double x_init0, double x_init1,
+                                                unsigned mask, int hl, int base_lane) {
   IfaceProb P;
   if (vap_minus) { P.rV = rm; P.uV = um; P.rL = rp; P.uL = up; P.sV = -1.0; }
   else { P.rV = rp; P.uV = up; P.rL = rm; P.uL = um; P.sV = 1.0; }
   P.du = up - um;
-  double x0, x1;
+  double x0, x1, aux[2];
   if (x_init0 > 0.0) { x0 = x_init0; x1 = x_init1; }
   else {
-    double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
+    const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
+  }
+  int it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+  if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
+    const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
+    x0 = g; x1 = g;
+    it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   }
   IfaceSol s;
-  int it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, mask, hl, base_lane);
-  if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
-    double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
-    x0 = g; x1 = g;
-    it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, mask, hl, base_lane);
-  }
   s.iters = it;
-  double G[2], z = 0.0;
-  if (it < 0 || !iface_eval(e, P, x0, x1, G, nullptr, &z)) { s.iters = -1; s.F0 = s.F1 = s.w = 0.0; s.pV = x0; s.pL = x1; return s; }
-  double rVs = x0 * e.inv_av2;
-  double uVs = vap_minus ? P.uV - wave_f(e.a_v, rVs, P.rV) : P.uV + wave_f(e.a_v, rVs, P.rV);
-  s.w = uVs + z / rVs;
+  s.pV = x0; s.pL = x1;
+  if (it < 0) { s.F0 = s.F1 = s.w = 0.0; return s; }
+  const double z = aux[0], fV = aux[1];
+  const double uVs = vap_minus ? P.uV - fV : P.uV + fV;  // wave relations
+  s.w = uVs + z * e.a_v2 * __drcp_rn(x0);                  // z = -rho_V* (u_V* - w)
   s.F0 = -z;
   s.F1 = -z * uVs + x0;
-  s.pV = x0; s.pL = x1;
   return s;
 }
 
@@ -304,23 +314,22 @@ struct CreateSol {
 
 // Phase creation by a half warp (App. B steps (ii)-(v), reading R18), Newton start (p0, p0).
 __device__ __noinline__ CreateSol create_solve_hw(const Eos& e, const Prm& p, int phase_outer, double rl,
-                                                     double ul, double rr, double ur, unsigned mask, int hl,
-                                                     int base_lane) {
+                                                  double ul, double rr, double ur, unsigned mask, int hl,
+                                                  int base_lane) {
   CreateProb P{phase_outer, rl, rr, ur - ul};
-  double x0 = e.p0, x1 = e.p0;
-  int it = newton_hw<CreateProb, create_eval>(e, p, P, x0, x1, mask, hl, base_lane);
+  double x0 = e.p0, x1 = e.p0, aux[2];
+  const int it = newton_hw<CreateProb, create_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   CreateSol s;
   s.iters = it;
-  double G[2], zr = 0.0;
-  if (it < 0 || !create_eval(e, P, x0, x1, G, nullptr, &zr)) { s.iters = -1; return s; }
+  if (it < 0) return s;
   const bool cav = (phase_outer == LIQ);
-  double rA = cav ? e.rho0 + (x0 - e.p0) * e.inv_al2 : x0 * e.inv_av2;
-  double rB = cav ? x1 * e.inv_av2 : e.rho0 + (x1 - e.p0) * e.inv_al2;
-  double aA = cav ? e.a_l : e.a_v;
-  double uAl = ul - wave_f(aA, rA, rl);
-  double vA = 1.0 / rA, vB = 1.0 / rB;
-  double uB = uAl + zr * (vB - vA);
-  double zl = -zr;
+  const double rA = cav ? e.rho0 + (x0 - e.p0) * e.inv_al2 : x0 * e.inv_av2;
+  const double rB = cav ? x1 * e.inv_av2 : e.rho0 + (x1 - e.p0) * e.inv_al2;
+  const double zr = aux[0];
+  const double uAl = ul - aux[1];  // left outer wave
+  const double vA = __drcp_rn(rA), vB = __drcp_rn(rB);
+  const double uB = uAl + zr * (vB - vA);
+  const double zl = -zr;
   s.wl = uB + zl * vB;
   s.wr = uB + zr * vB;
   s.Fl0 = -zl; s.Fl1 = -zl * uB + x1;

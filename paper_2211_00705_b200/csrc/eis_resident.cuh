@@ -6,39 +6,57 @@
 // dual time stepping (Alg. 2), and written back once.  HBM traffic is paid per call,
 // not per step; inside a step the kernel is bound by the FP64 pipe and shared memory.
 //
-// Per-step passes:
-//   A  decode: phase, u = m/rho, S_max, tiny flags, h_min, implicit blocks, dt   (a1, a2, a8)
-//   B  edges: HLL flux, interface detection, creation trigger                      (a3, a4)
-//   C  special edges: creation acceptance, interface + creation Newton, half-warp  (a5, a6)
-//   D  explicit moving-cell update of all non-block cells                         (a7)
-//   E  dual time stepping, one warp per implicit block                            (a9)
-//   F  remesh: insert, merge, split (block scan + scatter), only when flagged     (a10)
+// Phase boundaries are kept as an ordered list across steps: phases never change during a step
+// (a change is a spinodal error), so boundaries appear only through creation and move only
+// through the remesh; tiny cells (R4, R10) are the cells between two consecutive boundaries, so
+// implicit blocks (R11) follow from the list in O(#boundaries).
+//
+// Warp specialisation inside a step (the serial, latency-bound parts run beside the bulk):
+//   solver warp (the last warp):
+//     S1 tiny cells, implicit blocks, flags, from the boundary list                    (a8)
+//     S2 explicit phase-boundary solves, warm-started from the previous step, half warps (a5)
+//     -- barrier A (dt) --
+//     S4 dual time stepping on every implicit block                                     (a9)
+//     S5 moving-cell update of the cells next to phase boundaries                       (a7)
+//   bulk warps (all others; the solver joins when done), dynamic 32-wide windows:
+//     P1 per edge: u = m/rho, HLL flux (a3), creation trigger (a4), S_max / h_min (a2)
+//     -- barrier A (dt) --
+//     P2 per cell: explicit update of cells with two HLL edges (a7)
+//   -- barrier B --
+//   creations (a6, rare: acceptance R16, half-warp solves, neighbour updates)
+//   remesh (a10): event lists (merge pairs, splits, creations) -> per-cell shift -> scatter
 #pragma once
 #include "eis_device.cuh"
 
 namespace eis {
 
-constexpr int MAXSPEC = 32;  // special edges (interfaces + creations) per member per step
-constexpr int MAXBLK = 16;   // implicit blocks per member per step
+constexpr int MAXIF = 16;    // phase boundaries per member
+constexpr int MAXTRG = 8;    // creation triggers per member per step
+constexpr int MAXBLK = 8;    // implicit blocks per member
 constexpr int MAXB = 8;      // cells per implicit block
-constexpr int DTS_SCRATCH = 64;  // doubles of per-warp DTS scratch (inside the u array)
+constexpr int MAXEV = 16;    // remesh events (merge edges, split cells) per member per step
+constexpr int DTS_SCRATCH = 64;
 
-// per-edge / per-cell flag byte
+// flag byte per index i (cell i and its LEFT edge i share the byte)
 enum : uint8_t {
-  F_PH = 0x03,      // phase of cell i
-  F_TINY = 0x04,    // cell i tiny (pass A) | remesh: merge partner is the left neighbour
-  F_REG = 0x08,     // cell i in an implicit block (pass A) | remesh: partner is the right one
-  F_SPEC = 0x10,    // edge i is special (interface or accepted creation)
-  F_TRIG = 0x20,    // edge i triggered the creation test
-  F_CREATE = 0x40,  // edge i carries an accepted creation
-  F_MERGE = 0x80    // remesh: cells i and i+1 are merged
+  F_TINY = 0x04,    // cell i tiny                      (solver, S1)
+  F_REG = 0x08,     // cell i in an implicit block      (solver, S1)
+  F_SPEC = 0x10,    // edge i: explicit phase boundary  (solver, S1)
+  F_IF = 0x20       // edge i: phase boundary           (boundary list; kernel start / remesh)
 };
 
-struct Spec {
-  double Fl0, Fl1, wl;  // flux / speed seen by the cell LEFT of the edge
-  double Fr0, Fr1, wr;  // ... by the cell RIGHT of the edge (== left for an interface)
-  double rB, mB;        // created cell state
-  int e, kind;          // kind: 1 interface, 2 accepted creation, 3 pending trigger, 0 void
+struct Ifc {            // phase-boundary edge (list ordered by e)
+  double F0, F1, w;     // F_PB and the boundary speed
+  double pV, pL;        // converged star pressures (warm start of the next solve)
+  int e, interior;      // interior: inside an implicit block (solved by DTS)
+};
+struct Trg {            // creation trigger
+  double Fl0, Fl1, wl, Fr0, Fr1, wr, rB, mB;
+  int e, acc;
+};
+struct Grp {            // remesh output replacing cells g0..g1 (merge group, or one split cell)
+  double r, m, h;
+  int g0, g1, split;
 };
 
 struct MemberStats {
@@ -56,13 +74,19 @@ struct Members {  // global (HBM) state, member-major SoA
 };
 
 struct CtaShared {
-  double dt;
-  double red[64];
-  int n, nspec, nblk, status, remesh;
+  double part_s[32], part_h[32];
+  double ws0[MAXIF], ws1[MAXIF];  // warm start by boundary ordinal (previous step)
+  double dts[DTS_SCRATCH];
+  Ifc ifc[MAXIF];
+  Trg trg[MAXTRG];
+  Grp grp[MAXEV];
+  int mev[MAXEV], sev[MAXEV];
+  int blkA[MAXBLK], blkB[MAXBLK];
+  int tc[MAXIF];
+  int nifc, wsn, ntrg, nblk, n, status, remesh, win1, win2, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
-  int blkA[MAXBLK];
-  int warp_sums[33];
-  Spec spec[MAXSPEC];
+  unsigned long long c_dts, c_solves, c_regions;
+  MemberStats st;
 };
 
 __device__ __forceinline__ void set_status(CtaShared& sh, int code) { atomicCAS(&sh.status, 0, code); }
@@ -76,100 +100,138 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
-// look up the special-edge record of edge e (linear search, nspec is tiny)
-__device__ __forceinline__ const Spec* find_spec(const CtaShared& sh, int e) {
-  for (int k = 0; k < sh.nspec; ++k)
-    if (sh.spec[k].e == e && (sh.spec[k].kind == 1 || sh.spec[k].kind == 2)) return &sh.spec[k];
+__device__ __forceinline__ const Ifc* find_ifc(const CtaShared& sh, int e) {
+  for (int k = 0; k < sh.nifc; ++k)
+    if (sh.ifc[k].e == e) return &sh.ifc[k];
   return nullptr;
 }
+__device__ __forceinline__ const Trg* find_trg(const CtaShared& sh, int ntrg, int e) {
+  for (int k = 0; k < ntrg; ++k)
+    if (sh.trg[k].e == e) return &sh.trg[k];
+  return nullptr;
+}
+__device__ __forceinline__ bool created_at(const CtaShared& sh, int ntrg, int e) {
+  const Trg* t = ntrg ? find_trg(sh, ntrg, e) : nullptr;
+  return t && t->acc;
+}
 
-// Block-wide exclusive scan of one int per thread (thread order), returns the prefix and
-// the total through *total.  Uses sh.warp_sums.
-__device__ __forceinline__ int block_excl_scan(CtaShared& sh, int v, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+// tiny / region predicates straight from the shared state (R4, R10, R11); used off the hot
+// path only (creation eligibility, R16)
+__device__ __forceinline__ bool tiny_at(const Eos& e, const Prm& p, const double* rho, const double* h, int n, int i) {
+  if (i < 0 || i >= n) return false;
+  if (!(h[i] < p.eps_tiny * p.h_av)) return false;
+  const int ph = phase_of(e, rho[i]);
+  if (i > 0 && phase_of(e, rho[i - 1]) == ph) return false;
+  if (i < n - 1 && phase_of(e, rho[i + 1]) == ph) return false;
+  return true;
+}
+__device__ __forceinline__ bool region_at(const Eos& e, const Prm& p, const double* rho, const double* h, int n, int i) {
+  return p.mode == 0 && (tiny_at(e, p, rho, h, n, i - 1) || tiny_at(e, p, rho, h, n, i) || tiny_at(e, p, rho, h, n, i + 1));
+}
+
+// moving-cell update: h^{n+1} = h + (wR - wL) dt, U^{n+1} = (h/h^{n+1}) U - (dt/h^{n+1}) dF
+__device__ __forceinline__ int cell_update(double* rho, double* mom, double* h, int i, double FL0, double FL1,
+                                           double wL, double FR0, double FR1, double wR, double dt, const Prm& p,
+                                           int& remesh) {
+  const double hn = h[i];
+  const double hn1 = hn + (wR - wL) * dt;
+  if (!(hn1 > 0.0)) return ST_WIDTH;
+  const double q = hn / hn1, c = dt / hn1;
+  rho[i] = q * rho[i] - c * (FR0 - FL0);
+  mom[i] = q * mom[i] - c * (FR1 - FL1);
+  h[i] = hn1;
+  if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
+  return 0;
+}
+
+// flux and speed of edge `ed` seen from the cell on side `right_cell` (0: the cell left of the
+// edge, 1: the one right of it): accepted creation, explicit phase boundary, or the HLL arrays.
+__device__ __forceinline__ void edge_view(const CtaShared& sh, const uint8_t* fl, const double* F0, const double* F1,
+                                          int ed, int right_cell, double& G0, double& G1, double& w) {
+  if (fl[ed] & F_SPEC) {
+    const Ifc* s = find_ifc(sh, ed);
+    if (s) { G0 = s->F0; G1 = s->F1; w = s->w; return; }
   }
-  if (lane == 31) sh.warp_sums[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int s = lane < nw ? sh.warp_sums[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
+  const int ntrg = sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG;
+  if (ntrg) {
+    const Trg* t = find_trg(sh, ntrg, ed);
+    if (t && t->acc) {
+      if (right_cell) { G0 = t->Fr0; G1 = t->Fr1; w = t->wr; }
+      else { G0 = t->Fl0; G1 = t->Fl1; w = t->wl; }
+      return;
     }
-    if (lane < nw) sh.warp_sums[lane] = s;  // inclusive warp prefix
-    if (lane == 31) sh.warp_sums[32] = s;
   }
-  __syncthreads();
-  int base = warp > 0 ? sh.warp_sums[warp - 1] : 0;
-  *total = sh.warp_sums[32];
-  int r = base + x - v;
-  __syncthreads();
-  return r;
+  G0 = F0[ed]; G1 = F1[ed]; w = 0.0;
+}
+
+// remesh: position shift of old cell i (cells before it: created cells, merge groups, splits)
+__device__ __forceinline__ int remesh_shift(const CtaShared& sh, int ntrg, int i) {
+  int s = 0;
+  for (int k = 0; k < ntrg; ++k)
+    if (sh.trg[k].acc && sh.trg[k].e <= i) s += 1;  // created cell inserted before cell e
+  for (int k = 0; k < sh.ngrp; ++k) {
+    const Grp& g = sh.grp[k];
+    if (g.g1 < i) s += g.split - (g.g1 - g.g0);
+  }
+  return s;
 }
 
 // ------------------------------------------------------------------------------------------
 // Algorithm 2 on one implicit block [a, b] by one warp (
-// R11-R13).  Interior edges are solved by the two half warps in parallel (lane-parallel
-// Armijo), cell updates by lanes 0..K-1, residual (R8) by warp max.
+// R11-R13).  Interior boundaries are solved by the two half warps in parallel, each warm-started
+// from its previous iterate; cell updates by lanes 0..K-1; residual (R8) by warp max.
+// Outer fluxes F_left, F_right are the explicit step's (flux bounding).
 // ------------------------------------------------------------------------------------------
-__device__ __noinline__ void dts_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
-                          const double* F0, const double* F1, const uint8_t* fl, double* sc, int a, int b,
-                          double dt, long long& it_out, long long& solves) {
+__device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
+                                      const double* F0, const double* F1, const uint8_t* fl, int a, int b, double dt,
+                                      long long& it_out, long long& solves, int& remesh) {
   const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   const int K = b - a + 1;
-  double* W0 = sc;                // [MAXB]
-  double* W1 = sc + MAXB;         // [MAXB]
-  double* Fe0 = sc + 2 * MAXB;    // [MAXB+1]
+  double* sc = sh.dts;
+  double* W0 = sc;               // [MAXB]
+  double* W1 = sc + MAXB;        // [MAXB]
+  double* Fe0 = sc + 2 * MAXB;   // [MAXB+1]
   double* Fe1 = Fe0 + MAXB + 1;
   double* we = Fe1 + MAXB + 1;
   double* xs0 = we + MAXB + 1;
   double* xs1 = xs0 + MAXB + 1;
-  // outer fluxes F_left = F_{a-1/2}(U^n), F_right = F_{b+1/2}(U^n): flux bounding
   if (lane == 0) {
-    for (int s = 0; s < 2; ++s) {
-      int ed = s == 0 ? a : b + 1;
-      int j = s == 0 ? 0 : K;
-      const Spec* sp = (fl[ed] & F_SPEC) ? find_spec(sh, ed) : nullptr;
-      if (sp) {
-        Fe0[j] = s == 0 ? sp->Fr0 : sp->Fl0;
-        Fe1[j] = s == 0 ? sp->Fr1 : sp->Fl1;
-        we[j] = s == 0 ? sp->wr : sp->wl;
-      } else {
-        Fe0[j] = F0[ed]; Fe1[j] = F1[ed]; we[j] = 0.0;
-      }
-    }
+    double g0, g1, w;
+    edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
+    Fe0[0] = g0; Fe1[0] = g1; we[0] = w;
+    edge_view(sh, fl, F0, F1, b + 1, 0, g0, g1, w);
+    Fe0[K] = g0; Fe1[K] = g1; we[K] = w;
+  }
+  if (lane >= 1 && lane < K) {  // warm start of interior boundaries from the last step
+    const Ifc* s = find_ifc(sh, a + lane);
+    xs0[lane] = s ? s->pV : -1.0;
+    xs1[lane] = s ? s->pL : -1.0;
   }
   double rn0 = 0, rn1 = 0, hn = 0, r = 0, dtau = 1, w0 = 0, w1 = 0;
   bool tin = false;
   int ph0 = 0;
   if (lane < K) {
+    const uint8_t f = fl[a + lane];
     rn0 = rho[a + lane]; rn1 = mom[a + lane]; hn = h[a + lane];
-    tin = fl[a + lane] & F_TINY;
-    ph0 = fl[a + lane] & F_PH;
-    double theta = tin ? hn / p.h_av : p.theta_nb;  // theta_k = alpha = h_k^n/h_av (R12)
+    tin = f & F_TINY;
+    ph0 = phase_of(e, rn0);
+    const double theta = tin ? hn / p.h_av : p.theta_nb;  // theta_k = alpha = h_k^n / h_av (R12)
     dtau = theta * dt;
     r = dtau / dt;
     w0 = rn0; w1 = rn1;
     W0[lane] = w0; W1[lane] = w1;
   }
-  if (lane <= K) { xs0[lane] = -1.0; xs1[lane] = -1.0; }
   __syncwarp();
   long long l = 0;
   int err = 0;
-  for (int part = 0; part < 2 && !err; ++part) {
-    // part 0: Part 1 iterations; part 1: Part 2 (fluxes at U*, conservative update)
+  for (int part = 0; part < 2 && !err; ++part) {  // part 0: Part 1 iterations; part 1: fluxes at U*
     for (;;) {
-      // (a) interior edges at W^l
-      for (int j0 = 1; j0 < K; j0 += 2) {
-        int j = j0 + half;
+      for (int j0 = 1; j0 < K; j0 += 2) {  // (a) interior edges at W^l, two per round
+        const int j = j0 + half;
         if (j < K) {
-          double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j];
-          int pl = fl[a + j - 1] & F_PH, pr = fl[a + j] & F_PH;
+          const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j];
+          const int pl = phase_of(e, rho[a + j - 1]), pr = phase_of(e, rho[a + j]);  // phases of U^n
           if (pl != pr) {
             IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
             if (hl == 0) {
@@ -185,20 +247,18 @@ __device__ __noinline__ void dts_block(const Eos& e, const Prm& p, CtaShared& sh
       }
       err = __reduce_max_sync(0xffffffffu, err);
       __syncwarp();
-      if (err) break;
-      if (part == 1) break;
-      // (b) relaxed moving-cell update (P:763 form, R13) and residual
-      double res_nb = 0.0, res_t = 0.0;
+      if (err || part == 1) break;
+      double res_nb = 0.0, res_t = 0.0;  // (b) relaxed moving-cell update (R13)
       int bad = 0;
       if (lane < K) {
-        double hl_ = hn + (we[lane + 1] - we[lane]) * dt;
+        const double hl_ = hn + (we[lane + 1] - we[lane]) * dt;
         if (!(hl_ > 0.0)) bad = ST_WIDTH;
-        double q = r / (1.0 + r);
-        double n0 = w0 / (1.0 + r) + q * ((hn / hl_) * rn0 - (dt / hl_) * (Fe0[lane + 1] - Fe0[lane]));
-        double n1 = w1 / (1.0 + r) + q * ((hn / hl_) * rn1 - (dt / hl_) * (Fe1[lane + 1] - Fe1[lane]));
-        double r0 = fabs((1.0 + r) * (n0 - w0) / (dtau * fmax(fabs(w0), 1.0)));
-        double r1 = fabs((1.0 + r) * (n1 - w1) / (dtau * fmax(fabs(w1), 1.0)));
-        double ri = fmax(r0, r1);
+        const double q = r / (1.0 + r);
+        const double n0 = w0 / (1.0 + r) + q * ((hn / hl_) * rn0 - (dt / hl_) * (Fe0[lane + 1] - Fe0[lane]));
+        const double n1 = w1 / (1.0 + r) + q * ((hn / hl_) * rn1 - (dt / hl_) * (Fe1[lane + 1] - Fe1[lane]));
+        const double r0 = fabs((1.0 + r) * (n0 - w0) / (dtau * fmax(fabs(w0), 1.0)));
+        const double r1 = fabs((1.0 + r) * (n1 - w1) / (dtau * fmax(fabs(w1), 1.0)));
+        const double ri = fmax(r0, r1);
         if (tin) res_t = ri; else res_nb = ri;
         w0 = n0; w1 = n1;
         if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
@@ -206,7 +266,6 @@ __device__ __noinline__ void dts_block(const Eos& e, const Prm& p, CtaShared& sh
       res_nb = warp_max(res_nb);
       res_t = warp_max(res_t);
       bad = __reduce_max_sync(0xffffffffu, bad);
-      __syncwarp();
       if (lane < K) { W0[lane] = w0; W1[lane] = w1; }
       __syncwarp();
       ++l;
@@ -216,40 +275,54 @@ __device__ __noinline__ void dts_block(const Eos& e, const Prm& p, CtaShared& sh
     }
   }
   if (!err && lane < K) {  // Part 2 (b): conservative update with F_left, F*, F_right
-    double hn1 = hn + (we[lane + 1] - we[lane]) * dt;
+    const double hn1 = hn + (we[lane + 1] - we[lane]) * dt;
     if (!(hn1 > 0.0)) err = ST_WIDTH;
     else {
       rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
       mom[a + lane] = (hn / hn1) * rn1 - (dt / hn1) * (Fe1[lane + 1] - Fe1[lane]);
       h[a + lane] = hn1;
-      if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) sh.remesh = 1;
+      if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
     }
   }
+  if (lane >= 1 && lane < K && !err) {  // keep the converged boundary states for the next step
+    Ifc* s = const_cast<Ifc*>(find_ifc(sh, a + lane));
+    if (s) { s->pV = xs0[lane]; s->pL = xs1[lane]; }
+  }
   err = __reduce_max_sync(0xffffffffu, err);
-  if (err && lane == 0) set_status(sh, err);
+  __syncwarp();
   it_out = l;
+  return err;
+}
+
+// ------------------------------------------------------------------------------------------
+// Boundary list from a full scan (kernel start only): ordered ballot by the solver warp.
+// ------------------------------------------------------------------------------------------
+__device__ void build_boundary_list(const Eos& e, CtaShared& sh, const double* rho, uint8_t* fl, int n) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int nif = 0;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int i = c0 + lane;
+    const bool isif = i >= 1 && i < n && phase_of(e, rho[i - 1]) != phase_of(e, rho[i]);
+    const unsigned mi = __ballot_sync(0xffffffffu, isif);
+    if (isif) {
+      const int k = nif + __popc(mi & lt_mask);
+      if (k < MAXIF) { sh.ifc[k].e = i; fl[i] |= F_IF; }
+      else set_status(sh, ST_CAPACITY);
+    }
+    nif += __popc(mi);
+  }
+  if (lane == 0) sh.nifc = nif < MAXIF ? nif : MAXIF;
+  __syncwarp();
 }
 
 // ------------------------------------------------------------------------------------------
 // The kernel.  Dynamic shared memory: CtaShared | 6 x (cap+1) doubles | (cap+1) flag bytes.
-// Barrier discipline: sh.status is only READ between two barriers with no write in between
-// (CHECK_STOP), so every thread takes the same branch.
 // ------------------------------------------------------------------------------------------
-#define EIS_CHECK_STOP()                 \
-  {                                      \
-    __syncthreads();                     \
-    const int stop_ = sh.status;         \
-    __syncthreads();                     \
-    if (stop_) break;                    \
-  }
-
-__device__ __forceinline__ void or_flag(uint8_t* fl, int i, uint8_t bits) {
-  atomicOr(reinterpret_cast<unsigned int*>(fl + (i & ~3)), (unsigned)bits << (8 * (i & 3)));
-}
-
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
-resident_steps(const Eos e, const Prm p, Members g, long long n_steps, double t_end) {
+resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Members g,
+               long long n_steps, double t_end) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
   const int C = (int)g.cap;
@@ -257,17 +330,27 @@ resident_steps(const Eos e, const Prm p, Members g, long long n_steps, double t_
   double* rho = arr;
   double* mom = arr + (C + 1);
   double* h = arr + 2 * (C + 1);
-  double* U = arr + 3 * (C + 1);   // velocities (passes A-C) | DTS scratch (E) | remesh output (F)
-  double* F0 = arr + 4 * (C + 1);  // edge fluxes (B-E) | remesh output (F)
-  double* F1 = arr + 5 * (C + 1);
+  double* F0 = arr + 3 * (C + 1);  // edge fluxes (P1-P2) | remesh output
+  double* F1 = arr + 4 * (C + 1);
+  double* X = arr + 5 * (C + 1);   // remesh output
   uint8_t* fl = reinterpret_cast<uint8_t*>(arr + 6 * (C + 1));
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const int SW = nw - 1;  // solver warp
+  const int half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const long long m = blockIdx.x;
   const long long base = m * g.cap;
 
   if (tid == 0) {
     sh.n = (int)g.n[m];
     sh.status = g.status[m];
+    sh.wsn = -1;
+    sh.nblk = 0;
+    sh.ntrg = 0; sh.remesh = 0; sh.win1 = 0; sh.win2 = 0;
+    sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
+    sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0;
+    sh.st = g.stats[m];
   }
   __syncthreads();
   int n = sh.n;
@@ -276,250 +359,340 @@ resident_steps(const Eos e, const Prm p, Members g, long long n_steps, double t_
     mom[i] = g.mom[base + i];
     h[i] = g.h[base + i];
   }
+  for (int i = tid; i <= C; i += T) fl[i] = 0;
   double t = g.t[m];
-  MemberStats st = g.stats[m];  // thread 0's copy is authoritative
-  long long dts_acc = 0, solves_acc = 0, regions_acc = 0;
+  __syncthreads();
+  if (warp == SW) build_boundary_list(e, sh, rho, fl, n);
+  __syncthreads();
 
   for (long long step = 0; step < n_steps; ++step) {
-    EIS_CHECK_STOP();
-    if (!(t < t_end)) break;
-    // ---------------- pass A: decode (a1), S_max, tiny (a8), h_min, dt (a2) ----------------
-    if (tid == 0) { sh.nspec = 0; sh.nblk = 0; sh.remesh = 0; sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0; }
-    double smax = 0.0, hmin = INFINITY;
-    for (int i = tid; i < n; i += T) {
-      double r_ = rho[i], m_ = mom[i];
-      int ph = phase_of(e, r_);
-      if (!(r_ > 0.0)) set_status(sh, ST_NONPOS);
-      else if (ph == SPIN) set_status(sh, ST_SPINODAL);
-      double u = m_ / r_;
-      U[i] = u;
-      smax = fmax(smax, fabs(u) + sound(e, ph));  // S over all cells (R5)
-      fl[i] = (uint8_t)ph;
-    }
-    if (tid == 0) fl[n] = 0;
-    __syncthreads();
-    for (int i = tid; i < n; i += T) {
-      int ph = fl[i] & F_PH;
-      bool same_l = i > 0 && (fl[i - 1] & F_PH) == ph;
-      bool same_r = i < n - 1 && (fl[i + 1] & F_PH) == ph;
-      bool tiny = h[i] < p.eps_tiny * p.h_av && !same_l && !same_r;  // R4, R10
-      if (tiny && p.mode == 0) {
-        fl[i] |= F_TINY;
-        if (i == 0 || i == n - 1) set_status(sh, ST_UNSUPPORTED);  // R26
+    const bool stop = sh.status != 0 || !(t < t_end);
+    __syncthreads();  // every thread has read sh.status before anyone can write it
+    if (stop) break;
+    double s_part = 0.0, h_part = INFINITY;
+
+    if (warp == SW) {
+      // ---------------- S1: tiny cells, implicit blocks, flags (O(#boundaries)) ----------------
+      const int nif = sh.nifc;
+      for (int k = 0; k < sh.nblk; ++k)  // clear last step's block flags
+        for (int c = sh.blkA[k] + lane; c <= sh.blkB[k]; c += 32) fl[c] &= (uint8_t)~(F_TINY | F_REG);
+      for (int k = lane; k < nif; k += 32) fl[sh.ifc[k].e] &= (uint8_t)~F_SPEC;
+      __syncwarp();
+      const bool valid = lane < nif;
+      const int ek = valid ? sh.ifc[lane].e : -10;
+      const int enext = lane + 1 < nif ? sh.ifc[lane + 1].e : -20;
+      // cell ek lies between boundaries ek and ek + 1: tiny if narrower than eps_tiny h_av (R4)
+      const bool tiny = p.mode == 0 && valid && enext == ek + 1 && h[ek] < p.eps_tiny * p.h_av;
+      if (p.mode == 0 && lane == 0 && nif > 0) {  // a tiny cell at a domain end (R26)
+        if (sh.ifc[0].e == 1 && h[0] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
+        if (sh.ifc[nif - 1].e == n - 1 && h[n - 1] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
       }
-      if (p.mode == 1 || !tiny) hmin = fmin(hmin, h[i]);  // h_min over non-tiny cells (R6)
-    }
-    smax = warp_max(smax);
-    hmin = warp_min(hmin);
-    if (lane == 0) { sh.red[warp] = smax; sh.red[32 + warp] = hmin; }
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0, hm = INFINITY;
-      for (int w = 0; w < nw; ++w) { s = fmax(s, sh.red[w]); hm = fmin(hm, sh.red[32 + w]); }
-      double dt = p.cfl * hm / s;
-      if (t + dt > t_end) dt = t_end - t;
-      sh.dt = dt;
-    }
-    if (p.mode == 0) {  // implicit blocks: union of {k-1, k, k+1} (R11)
-      for (int i = tid; i < n; i += T) {
-        bool reg = (fl[i] & F_TINY) || (i > 0 && (fl[i - 1] & F_TINY)) || (i < n - 1 && (fl[i + 1] & F_TINY));
-        if (reg) fl[i] |= F_REG;
+      const unsigned mt = __ballot_sync(0xffffffffu, tiny);
+      const int ntiny = __popc(mt);
+      if (tiny) sh.tc[__popc(mt & lt_mask)] = ek;
+      __syncwarp();
+      // blocks: union of {k-1, k, k+1} over tiny k, overlapping ones merged (R11)
+      const int cj = lane < ntiny ? sh.tc[lane] : 0;
+      const int cprev = lane > 0 && lane < ntiny ? sh.tc[lane - 1] : -100;
+      const int cnext = lane + 1 < ntiny ? sh.tc[lane + 1] : (1 << 29);
+      const bool bstart = lane < ntiny && cprev + 1 < cj - 1;
+      const bool bend = lane < ntiny && cj + 1 < cnext - 1;
+      const unsigned ms = __ballot_sync(0xffffffffu, bstart), me = __ballot_sync(0xffffffffu, bend);
+      const int nblk = __popc(ms);
+      if (nblk > MAXBLK && lane == 0) set_status(sh, ST_CAPACITY);
+      if (bstart && __popc(ms & lt_mask) < MAXBLK) sh.blkA[__popc(ms & lt_mask)] = cj - 1;
+      if (bend && __popc(me & lt_mask) < MAXBLK) sh.blkB[__popc(me & lt_mask)] = cj + 1;
+      __syncwarp();
+      const int nb = nblk < MAXBLK ? nblk : MAXBLK;
+      if (lane == 0) sh.nblk = nb;
+      if (valid) {  // a boundary strictly inside a block is left to Algorithm 2
+        bool interior = false;
+        for (int k = 0; k < nb; ++k) interior |= (sh.blkA[k] < ek && ek <= sh.blkB[k]);
+        sh.ifc[lane].interior = interior;
+        if (!interior) fl[ek] |= F_SPEC;
       }
-    }
-    EIS_CHECK_STOP();
-    const double dt = sh.dt;
-    if (p.mode == 0) {
-      for (int i = tid; i < n; i += T) {
-        if ((fl[i] & F_REG) && (i == 0 || !(fl[i - 1] & F_REG))) {
-          int k = atomicAdd(&sh.nblk, 1);
-          if (k < MAXBLK) sh.blkA[k] = i; else set_status(sh, ST_CAPACITY);
+      __syncwarp();
+      for (int k = 0; k < nb; ++k)
+        for (int c = sh.blkA[k] + lane; c <= sh.blkB[k]; c += 32) fl[c] |= F_REG;
+      __syncwarp();
+      if (tiny) fl[ek] |= F_TINY;
+      const bool warm = (nif == sh.wsn);
+      if (valid) {
+        sh.ifc[lane].pV = warm ? sh.ws0[lane] : -1.0;
+        sh.ifc[lane].pL = warm ? sh.ws1[lane] : -1.0;
+      }
+      __syncwarp();
+      // ---------------- S2: explicit phase-boundary solves (App. A), half warps ----------------
+      for (int k = half; k < nif; k += 2) {
+        Ifc& f = sh.ifc[k];
+        if (f.interior) continue;
+        const int ed = f.e;
+        const double rl = rho[ed - 1], rr = rho[ed];
+        const int pl = phase_of(e, rl), pr = phase_of(e, rr);
+        if (pl == pr || pl == SPIN || pr == SPIN) { if (hl == 0) set_status(sh, pl == pr ? ST_INTERNAL : ST_SPINODAL); continue; }
+        IfaceSol s = iface_solve_hw(e, p, rl, mom[ed - 1] / rl, rr, mom[ed] / rr, pl == VAP, f.pV, f.pL, hmask, hl, half * 16);
+        if (hl == 0) {
+          if (s.iters < 0) set_status(sh, ST_NEWTON);
+          f.F0 = s.F0; f.F1 = s.F1; f.w = s.w; f.pV = s.pV; f.pL = s.pL;
+          atomicAdd(&sh.c_solves, 1ull);
         }
       }
+      __syncwarp();
     }
-    // ---------------- pass B: edge fluxes from U^n (a3), creation trigger (a4) ----------------
-    for (int ed = tid; ed <= n; ed += T) {
-      int L = ed > 0 ? ed - 1 : 0, R = ed < n ? ed : n - 1;  // transmissive ghosts (R15)
-      uint8_t fL = fl[L], fR = fl[R];
-      if (ed > 0 && ed < n && (fL & F_REG) && (fR & F_REG)) continue;  // left to Algorithm 2
-      int pL = fL & F_PH, pR = fR & F_PH;
-      if (pL == pR) {
-        double rl = rho[L], ml = mom[L], ul = U[L], rr = rho[R], mr = mom[R], ur = U[R];
+    // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2); dynamic windows ----------------
+    for (;;) {
+      int wi = 0;
+      if (lane == 0) wi = atomicAdd(&sh.win1, 1);
+      wi = __shfl_sync(0xffffffffu, wi, 0);
+      const int e0 = wi * 32;
+      if (e0 > n) break;
+      const int ed = e0 + lane;
+      const bool active = ed <= n;
+      const int c = ed < n ? ed : n - 1, l = ed > 0 ? ed - 1 : 0;  // transmissive ghosts (R15)
+      const double rc = rho[c], mc = mom[c], rl = rho[l], ml = mom[l];
+      const double uc = mc / rc;
+      double ul = __shfl_up_sync(0xffffffffu, uc, 1);
+      if (lane == 0) ul = ml / rl;
+      const int pc = phase_of(e, rc), pl = phase_of(e, rl);
+      int pr = __shfl_down_sync(0xffffffffu, pc, 1);
+      if (lane == 31 && c + 1 < n) pr = phase_of(e, rho[c + 1]);
+      if (active && ed < n) {
+        if (!(rc > 0.0)) set_status(sh, ST_NONPOS);
+        else if (pc == SPIN) set_status(sh, ST_SPINODAL);
+        s_part = fmax(s_part, fabs(uc) + sound(e, pc));  // S over all cells (R5)
+        const bool tiny = h[c] < p.eps_tiny * p.h_av && !(c > 0 && pl == pc) && !(c + 1 < n && pr == pc);
+        if (p.mode == 1 || !tiny) h_part = fmin(h_part, h[c]);  // h_min over non-tiny cells (R6)
+      }
+      if (active && pl == pc && pc != SPIN) {
         double f0, f1;
-        hll(e, pL, rl, ml, ul, rr, mr, ur, f0, f1);
+        hll(e, pc, rl, ml, ul, rc, mc, uc, f0, f1);
         F0[ed] = f0; F1[ed] = f1;
-        if (ed > 0 && ed < n && !(fL & F_REG) && !(fR & F_REG) && creation_trigger(e, pL, rl, ul, rr, ur)) {
-          int k = atomicAdd(&sh.nspec, 1);
-          if (k < MAXSPEC) { sh.spec[k].e = ed; sh.spec[k].kind = 3; } else set_status(sh, ST_CAPACITY);
-          or_flag(fl, ed, F_TRIG);
+        if (ed > 0 && ed < n && creation_trigger(e, pc, rl, ul, rc, uc) &&
+            !region_at(e, p, rho, h, n, ed - 1) && !region_at(e, p, rho, h, n, ed)) {  // R16
+          const int k = atomicAdd(&sh.ntrg, 1);
+          if (k < MAXTRG) { sh.trg[k].e = ed; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
         }
-      } else {
-        int k = atomicAdd(&sh.nspec, 1);
-        if (k < MAXSPEC) { sh.spec[k].e = ed; sh.spec[k].kind = 1; } else set_status(sh, ST_CAPACITY);
-        or_flag(fl, ed, F_SPEC);
+      } else if (active && ed > 0 && ed < n && pl != pc && !(fl[ed] & F_IF)) {
+        set_status(sh, ST_INTERNAL);  // a phase boundary missing from the list
       }
     }
-    EIS_CHECK_STOP();
-    // ---------------- pass C: creation acceptance (R16), special-edge solves (a5, a6) ----------------
-    const int nspec = sh.nspec;
-    for (int k = tid; k < nspec; k += T) {
-      if (sh.spec[k].kind != 3) continue;
-      int ed = sh.spec[k].e, run = 0;  // leftmost wins: accepted iff an even number of
-      while (ed - run - 1 >= 1 && (fl[ed - run - 1] & F_TRIG)) ++run;  // triggered edges precede it
-      sh.spec[k].kind = (run & 1) ? 0 : 2;
-    }
-    __syncthreads();
-    for (int k = tid; k < nspec; k += T)
-      if (sh.spec[k].kind == 2) or_flag(fl, sh.spec[k].e, F_SPEC | F_CREATE);
-    __syncthreads();
-    {
-      const int half = lane >> 4, hl = lane & 15;
-      const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
-      for (int k = warp * 2 + half; k < nspec; k += nw * 2) {
-        Spec& sp = sh.spec[k];
-        const int kind = sp.kind;
-        if (kind != 1 && kind != 2) continue;
-        const int ed = sp.e, L = ed - 1, R = ed;
-        const double rl = rho[L], ul = U[L], rr = rho[R], ur = U[R];
-        if (kind == 1) {
-          IfaceSol s = iface_solve_hw(e, p, rl, ul, rr, ur, (fl[L] & F_PH) == VAP, -1.0, -1.0, hmask, hl, half * 16);
-          if (hl == 0) {
-            if (s.iters < 0) set_status(sh, ST_NEWTON);
-            sp.Fl0 = sp.Fr0 = s.F0; sp.Fl1 = sp.Fr1 = s.F1; sp.wl = sp.wr = s.w;
-            ++solves_acc;
-          }
-        } else {
-          CreateSol s = create_solve_hw(e, p, fl[L] & F_PH, rl, ul, rr, ur, hmask, hl, half * 16);
-          if (hl == 0) {
-            if (s.iters < 0) set_status(sh, ST_CREATION);
-            sp.Fl0 = s.Fl0; sp.Fl1 = s.Fl1; sp.wl = s.wl;
-            sp.Fr0 = s.Fr0; sp.Fr1 = s.Fr1; sp.wr = s.wr;
-            sp.rB = s.rB; sp.mB = s.mB;
-            atomicAdd(&sh.c_creations, 1);
-            sh.remesh = 1;
-          }
-        }
-      }
-    }
-    EIS_CHECK_STOP();
-    // ---------------- pass D: explicit moving-cell update (a7) ----------------
-    for (int i = tid; i < n; i += T) {
-      const uint8_t f = fl[i];
-      if (f & F_REG) continue;
-      double FL0 = F0[i], FL1 = F1[i], wL = 0.0, FR0 = F0[i + 1], FR1 = F1[i + 1], wR = 0.0;
-      if (f & F_SPEC) {
-        const Spec* s = find_spec(sh, i);
-        if (s) { FL0 = s->Fr0; FL1 = s->Fr1; wL = s->wr; }
-      }
-      if (fl[i + 1] & F_SPEC) {
-        const Spec* s = find_spec(sh, i + 1);
-        if (s) { FR0 = s->Fl0; FR1 = s->Fl1; wR = s->wl; }
-      }
-      const double hn = h[i];
-      const double hn1 = hn + (wR - wL) * dt;
-      if (!(hn1 > 0.0)) { set_status(sh, ST_WIDTH); continue; }
-      const double q = hn / hn1, c = dt / hn1;
-      rho[i] = q * rho[i] - c * (FR0 - FL0);
-      mom[i] = q * mom[i] - c * (FR1 - FL1);
-      h[i] = hn1;
-      if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) sh.remesh = 1;
-    }
-    // ---------------- pass E: dual time stepping (a9), one warp per implicit block ----------------
-    {
-      const int nblk = sh.nblk < MAXBLK ? sh.nblk : MAXBLK;
-      for (int k = warp; k < nblk; k += nw) {
-        const int a = sh.blkA[k];
-        int b = a;
-        while (b + 1 < n && (fl[b + 1] & F_REG)) ++b;
-        if (b - a + 1 > MAXB) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
+    s_part = warp_max(s_part);
+    h_part = warp_min(h_part);
+    if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }
+    __syncthreads();  // ---------------- barrier A ----------------
+    double smax = 0.0, hmin = INFINITY;
+    for (int w = 0; w < nw; ++w) { smax = fmax(smax, sh.part_s[w]); hmin = fmin(hmin, sh.part_h[w]); }
+    double dt = p.cfl * hmin / smax;
+    if (t + dt > t_end) dt = t_end - t;
+    const double dt_hav = dt / p.h_av;
+    const int ntrg = sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG;
+    int remesh = 0;
+
+    if (warp == SW) {
+      // ---------------- S4: dual time stepping on every block (a9) ----------------
+      const int nblk = sh.nblk;
+      for (int k = 0; k < nblk; ++k) {
+        const int a = sh.blkA[k], b = sh.blkB[k];
+        if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
-        dts_block(e, p, sh, rho, mom, h, F0, F1, fl, U + warp * DTS_SCRATCH, a, b, dt, it, sv);
-        if (lane == 0) { dts_acc += it; regions_acc += 1; }
-        if ((lane & 15) == 0) solves_acc += sv;
+        const int err = dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
+        if (err && lane == 0) set_status(sh, err);
+        if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); }
+        if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
       }
+      // ---------------- S5: cells next to explicit phase boundaries (a7) ----------------
+      const int nif = sh.nifc;
+      for (int q = lane; q < 2 * nif; q += 32) {
+        const Ifc& f = sh.ifc[q >> 1];
+        if (f.interior) continue;
+        const int i = (q & 1) ? f.e : f.e - 1;
+        if ((q & 1) == 0 && (fl[i] & F_SPEC)) continue;  // handled as the right cell of edge i
+        if (fl[i] & F_REG) continue;
+        if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;  // creation pass
+        double a0, a1, wa, b0, b1, wb;
+        edge_view(sh, fl, F0, F1, i, 1, a0, a1, wa);
+        edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
+        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, remesh);
+        if (err) set_status(sh, err);
+      }
+      for (int k = lane; k < nif; k += 32) { sh.ws0[k] = sh.ifc[k].pV; sh.ws1[k] = sh.ifc[k].pL; }
+      if (lane == 0) sh.wsn = nif;
+      __syncwarp();
     }
-    EIS_CHECK_STOP();
-    // ---------------- pass F: remesh (a10; R9, R10), only when flagged ----------------
+    // ---------------- P2: explicit update of cells with two HLL edges (a7) ----------------
+    for (;;) {
+      int wi = 0;
+      if (lane == 0) wi = atomicAdd(&sh.win2, 1);
+      wi = __shfl_sync(0xffffffffu, wi, 0);
+      if (wi * 32 >= n) break;
+      const int i = wi * 32 + lane;
+      if (i >= n) continue;
+      if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
+      if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
+      const double hn = h[i];
+      const double cfac = hn == p.h_av ? dt_hav : dt / hn;  // h^{n+1} = h^n, so h^n/h^{n+1} = 1 exactly
+      rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
+      mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
+    }
+    if (remesh) sh.remesh = 1;
+    __syncthreads();  // ---------------- barrier B ----------------
+    // ---------------- creations (a6): acceptance (R16), solves, neighbour updates ----------------
+    if (ntrg) {
+      for (int k = tid; k < ntrg; k += T) {
+        int run = 0;
+        while (find_trg(sh, ntrg, sh.trg[k].e - run - 1)) ++run;  // leftmost wins
+        sh.trg[k].acc = (run & 1) ? 0 : 1;
+      }
+      __syncthreads();
+      for (int k = warp * 2 + half; k < ntrg; k += nw * 2) {
+        Trg& tr = sh.trg[k];
+        if (!tr.acc) continue;
+        const int ed = tr.e;
+        const double rl = rho[ed - 1], rr = rho[ed];  // still U^n: these cells were deferred
+        CreateSol s = create_solve_hw(e, p, phase_of(e, rl), rl, mom[ed - 1] / rl, rr, mom[ed] / rr, hmask, hl, half * 16);
+        if (hl == 0) {
+          if (s.iters < 0) set_status(sh, ST_CREATION);
+          tr.Fl0 = s.Fl0; tr.Fl1 = s.Fl1; tr.wl = s.wl; tr.Fr0 = s.Fr0; tr.Fr1 = s.Fr1; tr.wr = s.wr;
+          tr.rB = s.rB; tr.mB = s.mB;
+          atomicAdd(&sh.c_creations, 1);
+          if ((s.wr - s.wl) * dt > p.eps_split * p.h_av) set_status(sh, ST_UNSUPPORTED);  // never with C <= 1
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < 2 * ntrg; q += T) {
+        const int ed = sh.trg[q >> 1].e;
+        const int i = (q & 1) ? ed : ed - 1;
+        if ((q & 1) == 0 && find_trg(sh, ntrg, i)) continue;  // handled as the right cell of edge i
+        double a0, a1, wa, b0, b1, wb;
+        edge_view(sh, fl, F0, F1, i, 1, a0, a1, wa);
+        edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
+        int rm = 0;
+        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, rm);
+        if (err) set_status(sh, err);
+      }
+      if (tid == 0) sh.remesh = 1;
+      __syncthreads();
+    }
+    {
+      const int stop2 = sh.status;
+      __syncthreads();
+      if (stop2) break;
+    }
+    // ---------------- remesh (a10; R9, R10): events -> shifts -> scatter ----------------
     int n_new = n;
     if (sh.remesh) {
-      for (int i = tid; i < n; i += T) {  // post-update phases; keep the edge bits
-        const int ph = phase_of(e, rho[i]);
-        if (!(rho[i] > 0.0)) set_status(sh, ST_NONPOS);
+      if (tid == 0) { sh.nmev = 0; sh.nsev = 0; sh.ngrp = 0; }
+      __syncthreads();
+      for (int i = tid; i < n; i += T) {
+        const double r_ = rho[i];
+        const int ph = phase_of(e, r_);
+        if (!(r_ > 0.0)) set_status(sh, ST_NONPOS);
         else if (ph == SPIN) set_status(sh, ST_SPINODAL);
-        fl[i] = (uint8_t)((fl[i] & (F_SPEC | F_CREATE)) | ph);
-      }
-      if (tid == 0) fl[n] &= (F_SPEC | F_CREATE);
-      __syncthreads();
-      for (int i = tid; i < n; i += T) {  // merge partner: same-phase neighbour; both -> smaller, ties left
-        uint8_t f = fl[i];
-        if (h[i] < p.eps_tiny * p.h_av) {
-          const int ph = f & F_PH;
-          const bool sl = i > 0 && !(f & F_CREATE) && (fl[i - 1] & F_PH) == ph;
-          const bool sr = i < n - 1 && !(fl[i + 1] & F_CREATE) && (fl[i + 1] & F_PH) == ph;
-          int side = 0;
-          if (sl && sr) side = (h[i + 1] < h[i - 1]) ? 2 : 1;
-          else if (sl) side = 1;
-          else if (sr) side = 2;
-          if (side == 1) fl[i] = f | F_TINY;
-          if (side == 2) fl[i] = f | F_REG;
+        if (h[i] < p.eps_tiny * p.h_av) {  // merge partner: same-phase neighbour; both -> smaller, ties left
+          const bool sl = i > 0 && !created_at(sh, ntrg, i) && phase_of(e, rho[i - 1]) == ph;
+          const bool sr = i < n - 1 && !created_at(sh, ntrg, i + 1) && phase_of(e, rho[i + 1]) == ph;
+          int j = -1;
+          if (sl && sr) j = (h[i + 1] < h[i - 1]) ? i : i - 1;
+          else if (sl) j = i - 1;
+          else if (sr) j = i;
+          if (j >= 0) { const int k = atomicAdd(&sh.nmev, 1); if (k < MAXEV) sh.mev[k] = j; else set_status(sh, ST_CAPACITY); }
+        }
+        if (h[i] > p.eps_split * p.h_av) {
+          const int k = atomicAdd(&sh.nsev, 1);
+          if (k < MAXEV) sh.sev[k] = i; else set_status(sh, ST_CAPACITY);
         }
       }
       __syncthreads();
-      for (int i = tid; i < n - 1; i += T)
-        if ((fl[i] & F_REG) || (fl[i + 1] & F_TINY)) or_flag(fl, i, F_MERGE);
+      if (tid == 0 && sh.status == 0) {  // small serial bookkeeping: groups, splits, new size
+        int nm = sh.nmev, ns = sh.nsev;
+        for (int a = 1; a < nm; ++a) { int v = sh.mev[a], b = a - 1; while (b >= 0 && sh.mev[b] > v) { sh.mev[b + 1] = sh.mev[b]; --b; } sh.mev[b + 1] = v; }
+        for (int a = 1; a < ns; ++a) { int v = sh.sev[a], b = a - 1; while (b >= 0 && sh.sev[b] > v) { sh.sev[b + 1] = sh.sev[b]; --b; } sh.sev[b + 1] = v; }
+        int ng = 0, merges = 0, splits = 0, im = 0, is = 0;
+        // walk merge edges (deduplicated) and split cells in increasing cell order
+        while (im < nm || is < ns) {
+          const int jm = im < nm ? sh.mev[im] : (1 << 29), js = is < ns ? sh.sev[is] : (1 << 29);
+          Grp gr;
+          if (jm <= js) {  // merge group [jm, g1]: consecutive merge edges (R10)
+            int g1 = jm + 1;
+            ++im;
+            while (im < nm && sh.mev[im] <= g1) { if (sh.mev[im] == g1) ++g1; ++im; }
+            double hs = 0.0, s0 = 0.0, s1 = 0.0;
+            for (int k = jm; k <= g1; ++k) { hs += h[k]; s0 += h[k] * rho[k]; s1 += h[k] * mom[k]; }
+            gr.g0 = jm; gr.g1 = g1; gr.h = hs; gr.r = s0 / hs; gr.m = s1 / hs;
+            gr.split = hs > p.eps_split * p.h_av;
+            merges += g1 - jm;
+            while (is < ns && sh.sev[is] <= g1) ++is;  // split candidates inside the group
+          } else {
+            gr.g0 = gr.g1 = js; gr.h = h[js]; gr.r = rho[js]; gr.m = mom[js]; gr.split = 1;
+            ++is;
+          }
+          splits += gr.split;
+          if (ng < MAXEV) sh.grp[ng++] = gr; else set_status(sh, ST_CAPACITY);
+        }
+        sh.ngrp = ng;
+        int ncre = 0;
+        for (int k = 0; k < ntrg; ++k) ncre += sh.trg[k].acc;
+        int nn = n + ncre;
+        for (int k = 0; k < ng; ++k) nn += sh.grp[k].split - (sh.grp[k].g1 - sh.grp[k].g0);
+        if (nn > C) set_status(sh, ST_CAPACITY);
+        sh.n_new = nn;
+        sh.c_merges += merges;
+        sh.c_splits += splits;
+      }
       __syncthreads();
-      int carry = 0;
-      for (int c0 = 0; c0 < n; c0 += T) {  // counts in cell order -> scan -> scatter into (U, F0, F1)
-        const int i = c0 + tid;
-        int cnt = 0;
-        double gr = 0, gm = 0, gh = 0;
-        bool head = false, split = false;
-        if (i < n) {
-          const uint8_t f = fl[i];
-          if (f & F_CREATE) cnt += 1;
-          head = !(i > 0 && (fl[i - 1] & F_MERGE));
-          if (head) {
-            if (!(f & F_MERGE)) { gr = rho[i]; gm = mom[i]; gh = h[i]; }
-            else {  // merge group: h-weighted average summed left to right (R10)
-              double hs = 0.0, s0 = 0.0, s1 = 0.0;
-              int j = i, merged = 0;
-              for (;;) {
-                hs += h[j]; s0 += h[j] * rho[j]; s1 += h[j] * mom[j];
-                if (!(fl[j] & F_MERGE)) break;
-                ++j; ++merged;
-              }
-              gr = s0 / hs; gm = s1 / hs; gh = hs;
-              atomicAdd(&sh.c_merges, merged);
+      if (sh.status == 0 && (sh.ngrp > 0 || sh.c_creations > 0)) {
+        for (int i = tid; i < n; i += T) {  // scatter into (F0, F1, X)
+          int kg = -1;
+          for (int k = 0; k < sh.ngrp; ++k)
+            if (sh.grp[k].g0 <= i && i <= sh.grp[k].g1) kg = k;
+          if (kg >= 0 && sh.grp[kg].g0 != i) continue;  // merged into its group head
+          int pos = i + remesh_shift(sh, ntrg, i);
+          if (created_at(sh, ntrg, i)) {  // created cell, width (w_r - w_l) dt
+            const Trg* tr = find_trg(sh, ntrg, i);
+            F0[pos - 1] = tr->rB; F1[pos - 1] = tr->mB; X[pos - 1] = (tr->wr - tr->wl) * dt;
+          }
+          if (kg >= 0) {
+            const Grp& gr = sh.grp[kg];
+            if (gr.split) {
+              const double hh = 0.5 * gr.h;
+              F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = hh;
+              F0[pos + 1] = gr.r; F1[pos + 1] = gr.m; X[pos + 1] = hh;
+            } else { F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = gr.h; }
+          } else { F0[pos] = rho[i]; F1[pos] = mom[i]; X[pos] = h[i]; }
+        }
+        // boundary list: old boundaries shift with their right cell; each creation adds two
+        __syncthreads();
+        if (tid == 0) {
+          int nif = sh.nifc;
+          for (int k = 0; k < nif; ++k) sh.ifc[k].e += remesh_shift(sh, ntrg, sh.ifc[k].e);
+          for (int k = 0; k < ntrg; ++k) {
+            if (!sh.trg[k].acc) continue;
+            const int pc = sh.trg[k].e + remesh_shift(sh, ntrg, sh.trg[k].e) - 1;  // created cell
+            for (int q = 0; q < 2; ++q) {
+              if (nif >= MAXIF) { set_status(sh, ST_CAPACITY); break; }
+              int b = nif - 1;
+              while (b >= 0 && sh.ifc[b].e > pc + q) { sh.ifc[b + 1] = sh.ifc[b]; --b; }
+              sh.ifc[b + 1].e = pc + q;
+              ++nif;
             }
-            split = gh > p.eps_split * p.h_av;
-            cnt += split ? 2 : 1;
-            if (split) atomicAdd(&sh.c_splits, 1);
           }
+          sh.nifc = nif;
+          if (sh.c_creations) sh.wsn = -1;  // ordinals changed: no warm start next step
+          sh.nblk = 0;                      // flags are rebuilt below
         }
-        int tot = 0;
-        int pos = block_excl_scan(sh, cnt, &tot) + carry;
-        if (i < n) {
-          if (fl[i] & F_CREATE) {
-            const Spec* s = find_spec(sh, i);
-            if (pos < C && s) { U[pos] = s->rB; F0[pos] = s->mB; F1[pos] = (s->wr - s->wl) * dt; }
-            ++pos;
-          }
-          if (head) {
-            if (split) {
-              const double hh = 0.5 * gh;
-              if (pos + 1 < C) { U[pos] = gr; F0[pos] = gm; F1[pos] = hh; U[pos + 1] = gr; F0[pos + 1] = gm; F1[pos + 1] = hh; }
-            } else if (pos < C) { U[pos] = gr; F0[pos] = gm; F1[pos] = gh; }
-          }
-        }
-        carry += tot;
+        n_new = sh.n_new;
+        double* t0 = rho; double* t1 = mom; double* t2 = h;  // (F0, F1, X) become the state
+        rho = F0; mom = F1; h = X;
+        F0 = t0; F1 = t1; X = t2;
+        __syncthreads();
+        for (int i = tid; i <= C; i += T) fl[i] = 0;
+        __syncthreads();
+        for (int k = tid; k < sh.nifc; k += T) fl[sh.ifc[k].e] = F_IF;
       }
-      if (tid == 0 && carry > C) set_status(sh, ST_CAPACITY);
-      n_new = carry;
-      double* t0 = rho; double* t1 = mom; double* t2 = h;  // (U, F0, F1) become the state
-      rho = U; mom = F0; h = F1;
-      U = t0; F0 = t1; F1 = t2;
     }
     __syncthreads();
     if (tid == 0) {
+      MemberStats& st = sh.st;
       st.steps += 1;
       st.cell_updates += n;
       st.creations += sh.c_creations;
@@ -528,9 +701,12 @@ resident_steps(const Eos e, const Prm p, Members g, long long n_steps, double t_
       if (st.steps == 1 || dt < st.dt_min) st.dt_min = dt;
       if (dt > st.dt_max) st.dt_max = dt;
       sh.n = n_new;
+      sh.ntrg = 0; sh.remesh = 0; sh.win1 = 0; sh.win2 = 0;
+      sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
     }
     n = n_new;
     t += dt;
+    __syncthreads();
   }
   // ---------------- write back (one HBM round trip per call) ----------------
   __syncthreads();
@@ -540,28 +716,12 @@ resident_steps(const Eos e, const Prm p, Members g, long long n_steps, double t_
     g.mom[base + i] = mom[i];
     g.h[base + i] = h[i];
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    dts_acc += __shfl_xor_sync(0xffffffffu, dts_acc, o);
-    solves_acc += __shfl_xor_sync(0xffffffffu, solves_acc, o);
-    regions_acc += __shfl_xor_sync(0xffffffffu, regions_acc, o);
-  }
-  long long* red = reinterpret_cast<long long*>(sh.red);  // 64 slots
-  __syncthreads();
-  if (lane == 0) { red[warp] = dts_acc; red[32 + warp] = solves_acc; }
   __syncthreads();
   if (tid == 0) {
-    long long da = 0, sa = 0;
-    for (int w = 0; w < nw; ++w) { da += red[w]; sa += red[32 + w]; }
-    st.dts_iters += da;
-    st.iface_solves += sa;
-  }
-  __syncthreads();
-  if (lane == 0) red[warp] = regions_acc;
-  __syncthreads();
-  if (tid == 0) {
-    long long rr = 0;
-    for (int w = 0; w < nw; ++w) rr += red[w];
-    st.regions += rr;
+    MemberStats st = sh.st;
+    st.dts_iters += (long long)sh.c_dts;
+    st.iface_solves += (long long)sh.c_solves;
+    st.regions += (long long)sh.c_regions;
     g.n[m] = n;
     g.t[m] = t;
     g.status[m] = sh.status;

@@ -88,7 +88,7 @@ def c2(mode: int = MODE_SPLIT, cap_slack: int = 16) -> Workload:
                     cap=N + cap_slack, x_left=-0.5, x_right=0.5, rho=rho, mom=mom, t_end=5e-4)
 
 
-def c3(M: int = 65536, N: int = 1024, members=None, cap_slack: int = 64) -> Workload:
+def c3(M: int = 65536, N: int = 1024, members=None, cap_slack: int = 32) -> Workload:
     """BASELINE configs[2]: per member rho=U[998,1002], |u|=U[20,200], jump x=U[0.3,0.7];
     u = -|u| left of the jump edge, +|u| right of it (expansion -> cavitation)."""
     mem = np.arange(M, dtype=np.uint64) if members is None else np.asarray(members, dtype=np.uint64)
