@@ -81,6 +81,18 @@ __device__ __forceinline__ void hll(const Eos& e, int ph, double rl, double ml, 
   F1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
 }
 
+// HLL with the cell pressures precomputed (the bulk pass shuffles them between lanes).
+__device__ __forceinline__ void hll_p(double a, double rl, double ml, double ul, double pl, double rr, double mr,
+                                      double ur, double pr, double& F0, double& F1) {
+  const double FL1 = ml * ul + pl, FR1 = mr * ur + pr;
+  const double SL = fmin(ul, ur) - a, SR = fmax(ul, ur) + a;
+  if (SL >= 0.0) { F0 = ml; F1 = FL1; return; }
+  if (SR <= 0.0) { F0 = mr; F1 = FR1; return; }
+  const double inv = __drcp_rn(SR - SL), SLSR = SL * SR;
+  F0 = (SR * ml - SL * mr + SLSR * (rr - rl)) * inv;
+  F1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
+}
+
 // Creation trigger, reading R7: liquid edge cavitates iff Phi(rho_min) > 0, vapour edge
 // nucleates iff Phi(rho_tilde) < 0, Phi(r) = f(r; r_L) + f(r; r_R) + du.  Exact pre-filters:
 // ln y >= 1 - 1/y gives Phi_liq(rho_min) <= du - a(1 - rho_min^2/(r_L r_R))... (no trigger when
@@ -88,7 +100,10 @@ __device__ __forceinline__ void hll(const Eos& e, int ph, double rl, double ml, 
 __device__ __forceinline__ bool creation_trigger(const Eos& e, int ph, double rl, double ul, double rr, double ur) {
   double du = ur - ul;
   if (ph == LIQ) {
-    if (rl >= e.rho_min && rr >= e.rho_min && du <= e.a_l * (1.0 - e.rho_min * e.rho_min / (rl * rr))) return false;
+    // pre-filter (exact, ln y <= y - 1): both rarefactions and du <= a_l (1 - rho_min^2/(r_L r_R)),
+    // in product form with a 1e-9 m/s margin so rounding never hides a trigger
+    const double x = rl * rr;
+    if (rl >= e.rho_min && rr >= e.rho_min && du * x <= e.a_l * (x - e.rho_min * e.rho_min) - 1e-9 * x) return false;
     return wave_f(e.a_l, e.rho_min, rl) + wave_f(e.a_l, e.rho_min, rr) + du > 0.0;
   }
   if (du >= 0.0) return false;

@@ -83,7 +83,7 @@ struct CtaShared {
   int mev[MAXEV], sev[MAXEV];
   int blkA[MAXBLK], blkB[MAXBLK];
   int tc[MAXIF];
-  int nifc, wsn, ntrg, nblk, n, status, remesh, win1, win2, nmev, nsev, ngrp, n_new;
+  int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
   unsigned long long c_dts, c_solves, c_regions;
   MemberStats st;
@@ -347,7 +347,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     sh.status = g.status[m];
     sh.wsn = -1;
     sh.nblk = 0;
-    sh.ntrg = 0; sh.remesh = 0; sh.win1 = 0; sh.win2 = 0;
+    sh.ntrg = 0; sh.remesh = 0;
     sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
     sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0;
     sh.st = g.stats[m];
@@ -367,6 +367,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
 
   for (long long step = 0; step < n_steps; ++step) {
     const bool stop = sh.status != 0 || !(t < t_end);
+    const int nbulk = sh.nifc > 0 ? nw - 1 : nw;  // the solver warp joins the bulk when idle
     __syncthreads();  // every thread has read sh.status before anyone can write it
     if (stop) break;
     double s_part = 0.0, h_part = INFINITY;
@@ -439,41 +440,48 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       }
       __syncwarp();
     }
-    // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2); dynamic windows ----------------
-    for (;;) {
-      int wi = 0;
-      if (lane == 0) wi = atomicAdd(&sh.win1, 1);
-      wi = __shfl_sync(0xffffffffu, wi, 0);
-      const int e0 = wi * 32;
-      if (e0 > n) break;
-      const int ed = e0 + lane;
-      const bool active = ed <= n;
-      const int c = ed < n ? ed : n - 1, l = ed > 0 ? ed - 1 : 0;  // transmissive ghosts (R15)
-      const double rc = rho[c], mc = mom[c], rl = rho[l], ml = mom[l];
-      const double uc = mc / rc;
-      double ul = __shfl_up_sync(0xffffffffu, uc, 1);
-      if (lane == 0) ul = ml / rl;
-      const int pc = phase_of(e, rc), pl = phase_of(e, rl);
-      int pr = __shfl_down_sync(0xffffffffu, pc, 1);
-      if (lane == 31 && c + 1 < n) pr = phase_of(e, rho[c + 1]);
-      if (active && ed < n) {
-        if (!(rc > 0.0)) set_status(sh, ST_NONPOS);
-        else if (pc == SPIN) set_status(sh, ST_SPINODAL);
-        s_part = fmax(s_part, fabs(uc) + sound(e, pc));  // S over all cells (R5)
-        const bool tiny = h[c] < p.eps_tiny * p.h_av && !(c > 0 && pl == pc) && !(c + 1 < n && pr == pc);
-        if (p.mode == 1 || !tiny) h_part = fmin(h_part, h[c]);  // h_min over non-tiny cells (R6)
-      }
-      if (active && pl == pc && pc != SPIN) {
-        double f0, f1;
-        hll(e, pc, rl, ml, ul, rc, mc, uc, f0, f1);
-        F0[ed] = f0; F1[ed] = f1;
-        if (ed > 0 && ed < n && creation_trigger(e, pc, rl, ul, rc, uc) &&
-            !region_at(e, p, rho, h, n, ed - 1) && !region_at(e, p, rho, h, n, ed)) {  // R16
-          const int k = atomicAdd(&sh.ntrg, 1);
-          if (k < MAXTRG) { sh.trg[k].e = ed; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
+    // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2) ----------------
+    // window w: lanes hold cells 31w-1 .. 31w+30 (lane 0 is the left halo, transmissive ghosts
+    // at the ends, R15); lane j >= 1 owns cell 31w+j-1 and its LEFT edge.  Each lane divides
+    // once (u = m/rho); the left neighbour's u and p arrive by shuffle.
+    if (warp < nbulk) {
+      const int nwin1 = (n + 31) / 31;  // edges 0..n
+      for (int w = warp; w < nwin1; w += nbulk) {
+        const int cj = 31 * w - 1 + lane;
+        const int cc = cj < 0 ? 0 : (cj >= n ? n - 1 : cj);
+        const int cl = cj - 1 < 0 ? 0 : (cj - 1 >= n ? n - 1 : cj - 1);  // the left lane's cell
+        const double rc = rho[cc], mc = mom[cc];
+        const double uc = mc / rc;
+        const int pc = phase_of(e, rc);
+        const double pcv = pres(e, pc, rc);
+        const double ul = __shfl_up_sync(0xffffffffu, uc, 1);
+        const double plv = __shfl_up_sync(0xffffffffu, pcv, 1);
+        int pr = __shfl_down_sync(0xffffffffu, pc, 1);
+        if (lane == 31) pr = phase_of(e, rho[cj + 1 < n ? cj + 1 : n - 1]);
+        const double rl = rho[cl], ml = mom[cl];
+        const int pl = phase_of(e, rl);
+        if (lane >= 1 && cj < n) {  // cell cj: S_max, h_min partials
+          if (!(rc > 0.0)) set_status(sh, ST_NONPOS);
+          else if (pc == SPIN) set_status(sh, ST_SPINODAL);
+          s_part = fmax(s_part, fabs(uc) + sound(e, pc));  // S over all cells (R5)
+          const double hc = h[cj];
+          const bool tiny = hc < p.eps_tiny * p.h_av && !(cj > 0 && pl == pc) && !(cj + 1 < n && pr == pc);
+          if (p.mode == 1 || !tiny) h_part = fmin(h_part, hc);  // h_min over non-tiny cells (R6)
         }
-      } else if (active && ed > 0 && ed < n && pl != pc && !(fl[ed] & F_IF)) {
-        set_status(sh, ST_INTERNAL);  // a phase boundary missing from the list
+        if (lane >= 1 && cj <= n) {  // edge cj between cells cj-1 and cj
+          if (pl == pc && pc != SPIN) {
+            double f0, f1;
+            hll_p(sound(e, pc), rl, ml, ul, plv, rc, mc, uc, pcv, f0, f1);
+            F0[cj] = f0; F1[cj] = f1;
+            if (cj > 0 && cj < n && creation_trigger(e, pc, rl, ul, rc, uc) &&
+                !region_at(e, p, rho, h, n, cj - 1) && !region_at(e, p, rho, h, n, cj)) {  // R16
+              const int k = atomicAdd(&sh.ntrg, 1);
+              if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
+            }
+          } else if (cj > 0 && cj < n && pl != pc && !(fl[cj] & F_IF)) {
+            set_status(sh, ST_INTERNAL);  // a phase boundary missing from the list
+          }
+        }
       }
     }
     s_part = warp_max(s_part);
@@ -520,19 +528,16 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       __syncwarp();
     }
     // ---------------- P2: explicit update of cells with two HLL edges (a7) ----------------
-    for (;;) {
-      int wi = 0;
-      if (lane == 0) wi = atomicAdd(&sh.win2, 1);
-      wi = __shfl_sync(0xffffffffu, wi, 0);
-      if (wi * 32 >= n) break;
-      const int i = wi * 32 + lane;
-      if (i >= n) continue;
-      if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
-      if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
-      const double hn = h[i];
-      const double cfac = hn == p.h_av ? dt_hav : dt / hn;  // h^{n+1} = h^n, so h^n/h^{n+1} = 1 exactly
-      rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
-      mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
+    if (warp < nbulk) {
+      for (int i = warp * 32 + lane; i - lane < n; i += nbulk * 32) {
+        if (i >= n) continue;
+        if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
+        if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
+        const double hn = h[i];
+        const double cfac = hn == p.h_av ? dt_hav : dt / hn;  // h^{n+1} = h^n, so h^n/h^{n+1} = 1 exactly
+        rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
+        mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
+      }
     }
     if (remesh) sh.remesh = 1;
     __syncthreads();  // ---------------- barrier B ----------------
@@ -701,7 +706,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       if (st.steps == 1 || dt < st.dt_min) st.dt_min = dt;
       if (dt > st.dt_max) st.dt_max = dt;
       sh.n = n_new;
-      sh.ntrg = 0; sh.remesh = 0; sh.win1 = 0; sh.win2 = 0;
+      sh.ntrg = 0; sh.remesh = 0;
       sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
     }
     n = n_new;
