@@ -134,7 +134,7 @@ __device__ __forceinline__ int cell_update(double* rho, double* mom, double* h, 
                                            double wL, double FR0, double FR1, double wR, double dt, const Prm& p,
                                            int& remesh) {
   const double hn = h[i];
-  const double hn1 = hn + (wR - wL) * dt;
+  const double hn1 = __dadd_rn(hn, __dmul_rn(wR - wL, dt));  // no contraction: the oracle's roundings
   if (!(hn1 > 0.0)) return ST_WIDTH;
   const double q = hn / hn1, c = dt / hn1;
   rho[i] = q * rho[i] - c * (FR0 - FL0);
@@ -251,7 +251,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       double res_nb = 0.0, res_t = 0.0;  // (b) relaxed moving-cell update (R13)
       int bad = 0;
       if (lane < K) {
-        const double hl_ = hn + (we[lane + 1] - we[lane]) * dt;
+        const double hl_ = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
         if (!(hl_ > 0.0)) bad = ST_WIDTH;
         const double q = r / (1.0 + r);
         const double n0 = w0 / (1.0 + r) + q * ((hn / hl_) * rn0 - (dt / hl_) * (Fe0[lane + 1] - Fe0[lane]));
@@ -275,7 +275,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
     }
   }
   if (!err && lane < K) {  // Part 2 (b): conservative update with F_left, F*, F_right
-    const double hn1 = hn + (we[lane + 1] - we[lane]) * dt;
+    const double hn1 = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
     if (!(hn1 > 0.0)) err = ST_WIDTH;
     else {
       rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
