@@ -59,6 +59,7 @@ typedef enum {
 enum { EIS_HOST = 0, EIS_DEVICE = 1 };
 enum { EIS_MODE_SPLIT = 0 /* Algorithms 1-2 */, EIS_MODE_EXPLICIT = 1 /* global explicit, dt from all cells */ };
 enum { EIS_VAP = 0, EIS_LIQ = 1, EIS_SPIN = 2 };
+enum { EIS_LAYOUT_AUTO = 0, EIS_LAYOUT_RESIDENT = 1, EIS_LAYOUT_TILED = 2 };
 
 /* EOS record (immutable per context).  Vapour p = a_v2 rho; liquid
  * p = p0 + a_l^2 (rho - rho0) (P:1121 corrected, R1). */
@@ -93,7 +94,11 @@ typedef struct {
   int64_t cell_capacity;  /* >= n_cells: slack for created / split cells                   */
   double x_left, x_right; /* domain                                                        */
   int32_t device;         /* CUDA device ordinal                                           */
-  int32_t threads;        /* CTA size per member (0 = automatic)                           */
+  int32_t threads;        /* CTA size per member / tile (0 = automatic)                    */
+  int32_t layout;         /* EIS_LAYOUT_AUTO | _RESIDENT (grid in shared memory across steps,
+                             ensembles, cell_capacity <= 16384) | _TILED (one huge grid, streamed
+                             through HBM in halo-overlapped tiles each step, n_members == 1)   */
+  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 960)                         */
   void* stream;           /* cudaStream_t (NULL = legacy default stream)                   */
 } eis_grid;
 

@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(HERE, "libeis.so")
 
 EIS_HOST, EIS_DEVICE = 0, 1
 MODE_SPLIT, MODE_EXPLICIT = 0, 1
+LAYOUT_AUTO, LAYOUT_RESIDENT, LAYOUT_TILED = 0, 1, 2
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_ORDER", 3: "E_NONPOS_DENSITY", 4: "E_SPINODAL", 5: "E_NEWTON",
           6: "E_CREATION", 7: "E_DTS_CAP", 8: "E_WIDTH", 9: "E_CAPACITY", 10: "E_CUDA", 11: "E_NCCL",
           12: "E_UNSUPPORTED", 13: "E_INTERNAL"}
@@ -47,7 +48,7 @@ class Params(C.Structure):
 class Grid(C.Structure):
     _fields_ = [("n_members", C.c_int64), ("n_cells", C.c_int64), ("cell_capacity", C.c_int64),
                 ("x_left", C.c_double), ("x_right", C.c_double), ("device", C.c_int32),
-                ("threads", C.c_int32), ("stream", C.c_void_p)]
+                ("threads", C.c_int32), ("layout", C.c_int32), ("tile_cells", C.c_int32), ("stream", C.c_void_p)]
 
 
 class Interface(C.Structure):
@@ -134,13 +135,14 @@ class Context:
     """eis_create / eis_destroy.  ``stream``: a cudaStream_t handle (int) or a torch stream."""
 
     def __init__(self, eos: dict, params: dict, n_members: int, n_cells: int, capacity: int,
-                 x_left: float, x_right: float, device: int = 0, stream=None, threads: int = 0):
+                 x_left: float, x_right: float, device: int = 0, stream=None, threads: int = 0,
+                 layout: int = 0, tile_cells: int = 0):
         if stream is not None and hasattr(stream, "cuda_stream"):
             stream = stream.cuda_stream
         self.M, self.N, self.cap = int(n_members), int(n_cells), int(capacity)
         self.device = int(device)
         self._grid = Grid(self.M, self.N, self.cap, float(x_left), float(x_right), self.device, int(threads),
-                          C.c_void_p(stream) if stream else None)
+                          int(layout), int(tile_cells), C.c_void_p(stream) if stream else None)
         self._eos, self._prm = make_eos(eos), make_params(params)
         self._ctx = C.c_void_p()
         s = lib().eis_create(C.byref(self._eos), C.byref(self._prm), C.byref(self._grid), C.byref(self._ctx))

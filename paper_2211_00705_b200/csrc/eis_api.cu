@@ -13,6 +13,7 @@
 
 #include "eis.h"
 #include "eis_resident.cuh"
+#include "eis_tiled.cuh"
 
 using namespace eis;
 
@@ -36,6 +37,14 @@ struct eis_ctx {
   eis_interface* d_if;
   long long if_cap;
   int state_set;
+  // tiled layout (one huge grid, C5): tile buffers; d_rho/d_mom/d_h stay the contiguous staging
+  int tiled, tile_cells;
+  Tiles tl;
+  double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
+  int *t_cnt[2], *t_ctl;
+  TileStats* t_stats;
+  long long* t_off;
+  int staging_fresh;
   eis_status sticky;
   char msg[512];
 };
@@ -174,9 +183,142 @@ __global__ void k_iface(const Eos e, Members g, long long M, double x_left, cons
   if (cnt) cnt[m] = c;
 }
 
+// contiguous staging (member 0) -> tiles: tile k gets cells [k n / ntiles, (k+1) n / ntiles)
+__global__ void k_to_tiles(Members g, Tiles tl, int cur) {
+  const int k = blockIdx.x;
+  const long long n = g.n[0];
+  const long long lo = (long long)k * n / tl.ntiles, hi = (long long)(k + 1) * n / tl.ntiles;
+  const long long base = (long long)k * tl.capt;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    tl.rho[cur][base + i - lo] = g.rho[i];
+    tl.mom[cur][base + i - lo] = g.mom[i];
+    tl.h[cur][base + i - lo] = g.h[i];
+  }
+  if (threadIdx.x == 0) {
+    tl.cnt[cur][k] = (int)(hi - lo);
+    double* ws = tl.ws + (size_t)k * WS_STRIDE;
+    ws[2 * MAXIF] = -1.0;
+    TileStats z;
+    memset(&z, 0, sizeof(z));
+    tl.tstats[k] = z;
+  }
+}
+// tiles -> contiguous staging, given exclusive offsets
+__global__ void k_from_tiles(Members g, Tiles tl, const long long* off) {
+  const int k = blockIdx.x;
+  const int cur = tl.ctl[0];
+  const int cnt = tl.cnt[cur][k];
+  const long long base = (long long)k * tl.capt, o = off[k];
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    g.rho[o + i] = tl.rho[cur][base + i];
+    g.mom[o + i] = tl.mom[cur][base + i];
+    g.h[o + i] = tl.h[cur][base + i];
+  }
+  if (k == 0 && threadIdx.x == 0) {
+    g.n[0] = off[tl.ntiles];
+    g.t[0] = tl.scal[0];
+    g.status[0] = tl.ctl[1];
+  }
+}
+
 static unsigned grid_for(long long count) {
   long long b = (count + 255) / 256;
   return (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b));
+}
+
+// ------------------------------------------------------------------------------------------
+// tiled layout (one huge grid): allocation, staging <-> tiles
+// ------------------------------------------------------------------------------------------
+static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
+  const eis_grid* grid = &c->grid;
+  const long long cap = grid->cell_capacity;
+  c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 960;
+  if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
+  const int capt = c->tile_cells + 32;
+  long long ntiles = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;
+  if (ntiles < 1) ntiles = 1;
+  if (ntiles > (1 << 30)) { delete c; return EIS_E_ARG; }
+  c->threads = grid->threads > 0 ? grid->threads : 256;
+  if (c->threads != 256) { delete c; return EIS_E_ARG; }
+  const int capg = capt + 2 * HALO + MAXEV;
+  c->smem = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(capg + 1) + (((size_t)capg + 1 + 15) & ~size_t(15));
+  if (cudaSetDevice(grid->device) != cudaSuccess) { delete c; return EIS_E_CUDA; }
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, grid->device);
+  if ((int)c->smem + 1024 > max_optin) { delete c; return EIS_E_CAPACITY; }
+  if (cudaFuncSetAttribute(tiled_step<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
+    delete c; return EIS_E_CUDA;
+  }
+  const size_t tc = (size_t)ntiles * capt;
+  bool ok = cudaMalloc(&c->d_rho, cap * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cap * 8) == cudaSuccess &&
+            cudaMalloc(&c->d_h, cap * 8) == cudaSuccess && cudaMalloc(&c->d_t, 8) == cudaSuccess &&
+            cudaMalloc(&c->d_n, 8) == cudaSuccess && cudaMalloc(&c->d_status, 4) == cudaSuccess &&
+            cudaMalloc(&c->d_stats, sizeof(MemberStats)) == cudaSuccess && cudaMalloc(&c->d_cnt, 16) == cudaSuccess;
+  for (int b = 0; b < 2 && ok; ++b)
+    ok = cudaMalloc(&c->t_rho[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_mom[b], tc * 8) == cudaSuccess &&
+         cudaMalloc(&c->t_h[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_cnt[b], ntiles * 4) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
+       cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
+       cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, 4 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 4 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
+  if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
+  c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
+  c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
+  Tiles& tl = c->tl;
+  for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; }
+  tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
+  tl.ntiles = (int)ntiles; tl.capt = capt;
+  *out = c;
+  return EIS_OK;
+}
+
+__global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
+  tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0;
+  tl.scal[0] = t0; tl.scal[1] = 0.0; tl.scal[2] = 0.0; tl.scal[3] = 0.0;
+}
+
+// tiles -> contiguous staging (member 0), when the staging copy is stale
+static eis_status tiles_to_staging(eis_ctx* c) {
+  if (c->staging_fresh) return EIS_OK;
+  const int nt = c->tl.ntiles;
+  int ctl[4];
+  CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  std::vector<int> cnt(nt);
+  CU(cudaMemcpyAsync(cnt.data(), c->t_cnt[ctl[0]], nt * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  std::vector<long long> off(nt + 1);
+  off[0] = 0;
+  for (int k = 0; k < nt; ++k) off[k + 1] = off[k] + cnt[k];
+  if (off[nt] > c->grid.cell_capacity) return fail(c, EIS_E_CAPACITY, "tiled grid exceeds cell_capacity%s");
+  CU(cudaMemcpyAsync(c->t_off, off.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+  k_from_tiles<<<nt, 256, 0, c->stream>>>(c->g, c->tl, c->t_off);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c->stream));
+  c->staging_fresh = 1;
+  return EIS_OK;
+}
+
+static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
+  const int nt = c->tl.ntiles;
+  std::vector<TileStats> ts(nt);
+  double scal[4];
+  int ctl[4];
+  CU(cudaMemcpyAsync(ts.data(), c->t_stats, nt * sizeof(TileStats), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(scal, c->t_scal, 32, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  memset(out, 0, sizeof(*out));
+  for (const TileStats& s : ts) {
+    out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters; out->iface_solves += s.iface_solves;
+    out->creations += s.creations; out->splits += s.splits; out->merges += s.merges; out->regions += s.regions;
+  }
+  out->steps = ctl[3];
+  out->t_min = out->t_max = scal[0];
+  out->dt_min = scal[2];
+  out->dt_max = scal[3];
+  return EIS_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -213,6 +355,9 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   p.mode = prm->mode;
 
   const long long M = grid->n_members, cap = grid->cell_capacity;
+  c->tiled = grid->layout == EIS_LAYOUT_TILED || (grid->layout == EIS_LAYOUT_AUTO && M == 1 && cap > 16384);
+  if (grid->layout < 0 || grid->layout > 2 || (c->tiled && M != 1)) { delete c; return EIS_E_ARG; }
+  if (c->tiled) return create_tiled(c, out);
   if (cap > 16384) { delete c; return EIS_E_ARG; }
   // CTA size: about 4 cells per thread, warps limited so the DTS scratch fits in the u array
   int T = grid->threads;
@@ -257,6 +402,8 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_rho); cudaFree(c->d_mom); cudaFree(c->d_h); cudaFree(c->d_t); cudaFree(c->d_n);
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
+  for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); }
+  cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   delete c;
 }
 
@@ -294,6 +441,13 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   }
   k_validate<<<(unsigned)M, 128, 0, c->stream>>>(c->e, c->g, t0);
   CU(cudaGetLastError());
+  if (c->tiled) {
+    k_tiles_reset<<<1, 1, 0, c->stream>>>(c->tl, c->d_status, t0);
+    k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0);
+    tiled_init_dt<256><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, INFINITY);
+    CU(cudaGetLastError());
+    c->staging_fresh = 1;
+  }
   if (where == EIS_HOST) CU(cudaStreamSynchronize(c->stream));
   c->state_set = 1;
   c->sticky = EIS_OK;
@@ -328,6 +482,23 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   if (!c->state_set) return fail(c, EIS_E_ORDER, "step before set_state%s");
   if (n_steps < 0) return fail(c, EIS_E_ARG, "negative step count%s");
   CU(cudaSetDevice(c->grid.device));
+  if (c->tiled) {
+    c->staging_fresh = 0;
+    for (long long s = 0; s < n_steps; ++s) {
+      tiled_step<256, 4><<<c->tl.ntiles, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+      if ((s & 63) == 63 && t_end < INFINITY) {  // poll: stop launching once t_end is reached
+        double tt;
+        int ctl[4];
+        CU(cudaMemcpyAsync(&tt, c->t_scal, 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (!(tt < t_end) || ctl[1] != 0) break;
+      }
+    }
+    CU(cudaGetLastError());
+    if (out) return tiled_stats(c, out);
+    return EIS_OK;
+  }
   if (n_steps > 0) {
     const unsigned M = (unsigned)c->grid.n_members;
     if (c->threads <= 256 && c->minb == 4)
@@ -359,6 +530,7 @@ extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double
   if (!c->state_set) return fail(c, EIS_E_ORDER, "get_state before set_state%s");
   if (where != EIS_HOST && where != EIS_DEVICE) return fail(c, EIS_E_ARG, "get_state: bad where%s");
   CU(cudaSetDevice(c->grid.device));
+  if (c->tiled) { eis_status s0 = tiles_to_staging(c); if (s0) return s0; }
   const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
   const size_t cells = (size_t)M * cap;
   if (where == EIS_DEVICE) {
@@ -389,6 +561,7 @@ extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t cap
   if (c->sticky) return c->sticky;
   if (!c->state_set) return fail(c, EIS_E_ORDER, "interfaces before set_state%s");
   CU(cudaSetDevice(c->grid.device));
+  if (c->tiled) { eis_status s0 = tiles_to_staging(c); if (s0) return s0; }
   const long long M = c->grid.n_members;
   const unsigned nb = (unsigned)((M + 127) / 128);
   k_iface<<<nb, 128, 0, c->stream>>>(c->e, c->g, M, c->grid.x_left, nullptr, c->d_cnt, nullptr, 0);
@@ -422,6 +595,11 @@ extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t cap
 extern "C" eis_status eis_member_status(eis_ctx* c, int32_t* out) {
   if (!c || !out) return EIS_E_ARG;
   if (!c->state_set) return fail(c, EIS_E_ORDER, "member_status before set_state%s");
+  if (c->tiled) {
+    CU(cudaMemcpyAsync(out, c->t_ctl + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return EIS_OK;
+  }
   CU(cudaMemcpyAsync(out, c->d_status, c->grid.n_members * 4, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return EIS_OK;
@@ -430,6 +608,7 @@ extern "C" eis_status eis_member_status(eis_ctx* c, int32_t* out) {
 extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
   if (!c || !out) return EIS_E_ARG;
   if (!c->state_set) return fail(c, EIS_E_ORDER, "member_stats before set_state%s");
+  if (c->tiled) return tiled_stats(c, out);
   const long long M = c->grid.n_members;
   std::vector<MemberStats> ms(M);
   std::vector<double> t(M);

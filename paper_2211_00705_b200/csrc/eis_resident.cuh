@@ -85,6 +85,8 @@ struct CtaShared {
   int tc[MAXIF];
   int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
+  int olo, ohi;  // tiles: owned output range after the remesh
+  int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
   unsigned long long c_dts, c_solves, c_regions;
   MemberStats st;
 };
@@ -317,59 +319,49 @@ __device__ void build_boundary_list(const Eos& e, CtaShared& sh, const double* r
 }
 
 // ------------------------------------------------------------------------------------------
-// The kernel.  Dynamic shared memory: CtaShared | 6 x (cap+1) doubles | (cap+1) flag bytes.
+// One large step of one grid held in shared memory (the whole method, a1-a11), shared by the
+// member-resident kernel (ensembles) and the tiled kernel (the single huge grid).  Z restricts
+// error reporting, creation triggers and DTS blocks to the exactly-computed zone of a tile
+// and records which output cells a tile owns after the remesh.  Returns dt, or -1 when the
+// member stopped on an error.  All threads of the CTA call it.
 // ------------------------------------------------------------------------------------------
-template <int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB)
-resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Members g,
-               long long n_steps, double t_end) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
-  const int C = (int)g.cap;
-  double* arr = reinterpret_cast<double*>(smem_raw + ((sizeof(CtaShared) + 15) & ~size_t(15)));
-  double* rho = arr;
-  double* mom = arr + (C + 1);
-  double* h = arr + 2 * (C + 1);
-  double* F0 = arr + 3 * (C + 1);  // edge fluxes (P1-P2) | remesh output
-  double* F1 = arr + 4 * (C + 1);
-  double* X = arr + 5 * (C + 1);   // remesh output
-  uint8_t* fl = reinterpret_cast<uint8_t*>(arr + 6 * (C + 1));
+struct Zone {
+  int zlo, zhi;          // cells [zlo, zhi) are computed exactly (tiles: owned cells +- 2)
+  int own_lo, own_hi;    // owned cells [own_lo, own_hi); owned edges (own_lo, own_hi]
+  double dt_given;       // > 0: this dt (tiles: the global CFL step); else the grid's own CFL dt
+  bool left_real, right_real;  // the smem grid ends are domain ends (transmissive, R15)
+};
+struct Arr {
+  double *rho, *mom, *h, *F0, *F1, *X;
+  uint8_t* fl;
+  int n, C;
+};
+
+__device__ __forceinline__ void zone_status(CtaShared& sh, const Zone& Z, int i, int code) {
+  if (i >= Z.zlo && i < Z.zhi) set_status(sh, code);
+}
+__device__ __forceinline__ void zone_status_e(CtaShared& sh, const Zone& Z, int ed, int code) {
+  if ((ed - 1 >= Z.zlo && ed - 1 < Z.zhi) || (ed >= Z.zlo && ed < Z.zhi)) set_status(sh, code);
+}
+
+__device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShared& sh, Arr& A, double t, double t_end,
+                                            const Zone& Z) {
+  double* rho = A.rho;
+  double* mom = A.mom;
+  double* h = A.h;
+  double* F0 = A.F0;
+  double* F1 = A.F1;
+  double* X = A.X;
+  uint8_t* fl = A.fl;
+  int n = A.n;
+  const int C = A.C;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const int SW = nw - 1;  // solver warp
   const int half = lane >> 4, hl = lane & 15;
   const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const long long m = blockIdx.x;
-  const long long base = m * g.cap;
-
-  if (tid == 0) {
-    sh.n = (int)g.n[m];
-    sh.status = g.status[m];
-    sh.wsn = -1;
-    sh.nblk = 0;
-    sh.ntrg = 0; sh.remesh = 0;
-    sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
-    sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0;
-    sh.st = g.stats[m];
-  }
-  __syncthreads();
-  int n = sh.n;
-  for (int i = tid; i < n; i += T) {
-    rho[i] = g.rho[base + i];
-    mom[i] = g.mom[base + i];
-    h[i] = g.h[base + i];
-  }
-  for (int i = tid; i <= C; i += T) fl[i] = 0;
-  double t = g.t[m];
-  __syncthreads();
-  if (warp == SW) build_boundary_list(e, sh, rho, fl, n);
-  __syncthreads();
-
-  for (long long step = 0; step < n_steps; ++step) {
-    const bool stop = sh.status != 0 || !(t < t_end);
-    const int nbulk = sh.nifc > 0 ? nw - 1 : nw;  // the solver warp joins the bulk when idle
-    __syncthreads();  // every thread has read sh.status before anyone can write it
-    if (stop) break;
+  const int nbulk = sh.nifc > 0 ? nw - 1 : nw;  // the solver warp joins the bulk when idle
+  if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
     double s_part = 0.0, h_part = INFINITY;
 
     if (warp == SW) {
@@ -385,8 +377,8 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       // cell ek lies between boundaries ek and ek + 1: tiny if narrower than eps_tiny h_av (R4)
       const bool tiny = p.mode == 0 && valid && enext == ek + 1 && h[ek] < p.eps_tiny * p.h_av;
       if (p.mode == 0 && lane == 0 && nif > 0) {  // a tiny cell at a domain end (R26)
-        if (sh.ifc[0].e == 1 && h[0] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
-        if (sh.ifc[nif - 1].e == n - 1 && h[n - 1] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
+        if (Z.left_real && sh.ifc[0].e == 1 && h[0] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
+        if (Z.right_real && sh.ifc[nif - 1].e == n - 1 && h[n - 1] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
       }
       const unsigned mt = __ballot_sync(0xffffffffu, tiny);
       const int ntiny = __popc(mt);
@@ -430,12 +422,12 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
         const int ed = f.e;
         const double rl = rho[ed - 1], rr = rho[ed];
         const int pl = phase_of(e, rl), pr = phase_of(e, rr);
-        if (pl == pr || pl == SPIN || pr == SPIN) { if (hl == 0) set_status(sh, pl == pr ? ST_INTERNAL : ST_SPINODAL); continue; }
+        if (pl == pr || pl == SPIN || pr == SPIN) { if (hl == 0) zone_status_e(sh, Z, ed, pl == pr ? ST_INTERNAL : ST_SPINODAL); continue; }
         IfaceSol s = iface_solve_hw(e, p, rl, mom[ed - 1] / rl, rr, mom[ed] / rr, pl == VAP, f.pV, f.pL, hmask, hl, half * 16);
         if (hl == 0) {
-          if (s.iters < 0) set_status(sh, ST_NEWTON);
+          if (s.iters < 0) zone_status_e(sh, Z, ed, ST_NEWTON);
           f.F0 = s.F0; f.F1 = s.F1; f.w = s.w; f.pV = s.pV; f.pL = s.pL;
-          atomicAdd(&sh.c_solves, 1ull);
+          if (Z.own_lo < ed && ed <= Z.own_hi) atomicAdd(&sh.c_solves, 1ull);
         }
       }
       __syncwarp();
@@ -461,8 +453,8 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
         const double rl = rho[cl], ml = mom[cl];
         const int pl = phase_of(e, rl);
         if (lane >= 1 && cj < n) {  // cell cj: S_max, h_min partials
-          if (!(rc > 0.0)) set_status(sh, ST_NONPOS);
-          else if (pc == SPIN) set_status(sh, ST_SPINODAL);
+          if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
+          else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
           s_part = fmax(s_part, fabs(uc) + sound(e, pc));  // S over all cells (R5)
           const double hc = h[cj];
           const bool tiny = hc < p.eps_tiny * p.h_av && !(cj > 0 && pl == pc) && !(cj + 1 < n && pr == pc);
@@ -473,13 +465,13 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
             double f0, f1;
             hll_p(sound(e, pc), rl, ml, ul, plv, rc, mc, uc, pcv, f0, f1);
             F0[cj] = f0; F1[cj] = f1;
-            if (cj > 0 && cj < n && creation_trigger(e, pc, rl, ul, rc, uc) &&
+            if (cj > 0 && cj < n && cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
                 !region_at(e, p, rho, h, n, cj - 1) && !region_at(e, p, rho, h, n, cj)) {  // R16
               const int k = atomicAdd(&sh.ntrg, 1);
               if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
             }
           } else if (cj > 0 && cj < n && pl != pc && !(fl[cj] & F_IF)) {
-            set_status(sh, ST_INTERNAL);  // a phase boundary missing from the list
+            zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
           }
         }
       }
@@ -490,7 +482,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     __syncthreads();  // ---------------- barrier A ----------------
     double smax = 0.0, hmin = INFINITY;
     for (int w = 0; w < nw; ++w) { smax = fmax(smax, sh.part_s[w]); hmin = fmin(hmin, sh.part_h[w]); }
-    double dt = p.cfl * hmin / smax;
+    double dt = Z.dt_given > 0.0 ? Z.dt_given : p.cfl * hmin / smax;  // P:466 (tiles: the global dt)
     if (t + dt > t_end) dt = t_end - t;
     const double dt_hav = dt / p.h_av;
     const int ntrg = sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG;
@@ -501,12 +493,15 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       const int nblk = sh.nblk;
       for (int k = 0; k < nblk; ++k) {
         const int a = sh.blkA[k], b = sh.blkB[k];
+        if (b < Z.zlo || a >= Z.zhi) continue;  // tiles: a block wholly in the halo is not needed
         if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
         const int err = dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
         if (err && lane == 0) set_status(sh, err);
-        if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); }
-        if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
+        if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)
+          if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); }
+          if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
+        }
       }
       // ---------------- S5: cells next to explicit phase boundaries (a7) ----------------
       const int nif = sh.nifc;
@@ -521,7 +516,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
         edge_view(sh, fl, F0, F1, i, 1, a0, a1, wa);
         edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
         const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, remesh);
-        if (err) set_status(sh, err);
+        if (err) zone_status(sh, Z, i, err);
       }
       for (int k = lane; k < nif; k += 32) { sh.ws0[k] = sh.ifc[k].pV; sh.ws1[k] = sh.ifc[k].pL; }
       if (lane == 0) sh.wsn = nif;
@@ -573,7 +568,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
         edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
         int rm = 0;
         const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, rm);
-        if (err) set_status(sh, err);
+        if (err) zone_status(sh, Z, i, err);
       }
       if (tid == 0) sh.remesh = 1;
       __syncthreads();
@@ -581,7 +576,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     {
       const int stop2 = sh.status;
       __syncthreads();
-      if (stop2) break;
+      if (stop2) return -1.0;
     }
     // ---------------- remesh (a10; R9, R10): events -> shifts -> scatter ----------------
     int n_new = n;
@@ -591,8 +586,8 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       for (int i = tid; i < n; i += T) {
         const double r_ = rho[i];
         const int ph = phase_of(e, r_);
-        if (!(r_ > 0.0)) set_status(sh, ST_NONPOS);
-        else if (ph == SPIN) set_status(sh, ST_SPINODAL);
+        if (!(r_ > 0.0)) zone_status(sh, Z, i, ST_NONPOS);
+        else if (ph == SPIN) zone_status(sh, Z, i, ST_SPINODAL);
         if (h[i] < p.eps_tiny * p.h_av) {  // merge partner: same-phase neighbour; both -> smaller, ties left
           const bool sl = i > 0 && !created_at(sh, ntrg, i) && phase_of(e, rho[i - 1]) == ph;
           const bool sr = i < n - 1 && !created_at(sh, ntrg, i + 1) && phase_of(e, rho[i + 1]) == ph;
@@ -645,7 +640,11 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
         sh.c_splits += splits;
       }
       __syncthreads();
+      if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
+      __syncthreads();
       if (sh.status == 0 && (sh.ngrp > 0 || sh.c_creations > 0)) {
+        if (tid == 0) { sh.olo = 1 << 30; sh.ohi = -1; }
+        __syncthreads();
         for (int i = tid; i < n; i += T) {  // scatter into (F0, F1, X)
           int kg = -1;
           for (int k = 0; k < sh.ngrp; ++k)
@@ -655,6 +654,14 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
           if (created_at(sh, ntrg, i)) {  // created cell, width (w_r - w_l) dt
             const Trg* tr = find_trg(sh, ntrg, i);
             F0[pos - 1] = tr->rB; F1[pos - 1] = tr->mB; X[pos - 1] = (tr->wr - tr->wl) * dt;
+            if (Z.own_lo < i && i <= Z.own_hi) {  // owned edge
+              atomicMin(&sh.olo, pos - 1); atomicMax(&sh.ohi, pos); atomicAdd(&sh.o_cre, 1);
+            }
+          }
+          if (Z.own_lo <= i && i < Z.own_hi) {  // owned head: its outputs are owned
+            atomicMin(&sh.olo, pos);
+            atomicMax(&sh.ohi, pos + ((kg >= 0 && sh.grp[kg].split) ? 2 : 1));
+            if (kg >= 0) { atomicAdd(&sh.o_merges, sh.grp[kg].g1 - sh.grp[kg].g0); atomicAdd(&sh.o_splits, sh.grp[kg].split); }
           }
           if (kg >= 0) {
             const Grp& gr = sh.grp[kg];
@@ -700,26 +707,90 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
       MemberStats& st = sh.st;
       st.steps += 1;
       st.cell_updates += n;
-      st.creations += sh.c_creations;
-      st.merges += sh.c_merges;
-      st.splits += sh.c_splits;
+      st.creations += sh.o_cre;
+      st.merges += sh.o_merges;
+      st.splits += sh.o_splits;
       if (st.steps == 1 || dt < st.dt_min) st.dt_min = dt;
       if (dt > st.dt_max) st.dt_max = dt;
       sh.n = n_new;
       sh.ntrg = 0; sh.remesh = 0;
       sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
+      sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
     }
     n = n_new;
-    t += dt;
+    A.rho = rho; A.mom = mom; A.h = h; A.F0 = F0; A.F1 = F1; A.X = X; A.n = n;
     __syncthreads();
+    return dt;
+  }
+
+// ------------------------------------------------------------------------------------------
+// The member-resident kernel.  Dynamic shared memory: CtaShared | 6 x (cap+1) doubles |
+// (cap+1) flag bytes.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ Arr carve(unsigned char* smem_raw, int C) {
+  double* arr = reinterpret_cast<double*>(smem_raw + ((sizeof(CtaShared) + 15) & ~size_t(15)));
+  Arr A;
+  A.rho = arr; A.mom = arr + (C + 1); A.h = arr + 2 * (C + 1);
+  A.F0 = arr + 3 * (C + 1); A.F1 = arr + 4 * (C + 1); A.X = arr + 5 * (C + 1);
+  A.fl = reinterpret_cast<uint8_t*>(arr + 6 * (C + 1));
+  A.C = C;
+  A.n = 0;
+  return A;
+}
+
+__device__ __forceinline__ void reset_counters(CtaShared& sh) {
+  sh.wsn = -1; sh.nblk = 0; sh.ntrg = 0; sh.remesh = 0;
+  sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
+  sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0;
+  sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
+}
+
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Members g,
+               long long n_steps, double t_end) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
+  Arr A = carve(smem_raw, (int)g.cap);
+  const int tid = threadIdx.x, T = blockDim.x, warp = tid >> 5, nw = T >> 5;
+  const long long m = blockIdx.x;
+  const long long base = m * g.cap;
+  if (tid == 0) {
+    sh.n = (int)g.n[m];
+    sh.status = g.status[m];
+    reset_counters(sh);
+    sh.st = g.stats[m];
+  }
+  __syncthreads();
+  A.n = sh.n;
+  for (int i = tid; i < A.n; i += T) {
+    A.rho[i] = g.rho[base + i];
+    A.mom[i] = g.mom[base + i];
+    A.h[i] = g.h[base + i];
+  }
+  for (int i = tid; i <= A.C; i += T) A.fl[i] = 0;
+  double t = g.t[m];
+  __syncthreads();
+  if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, A.n);
+  __syncthreads();
+  Zone Z;
+  Z.zlo = 0; Z.zhi = 1 << 30; Z.own_lo = 0; Z.own_hi = 1 << 30; Z.dt_given = -1.0;
+  Z.left_real = true; Z.right_real = true;
+  for (long long step = 0; step < n_steps; ++step) {
+    const bool stop = sh.status != 0 || !(t < t_end);
+    __syncthreads();  // every thread has read sh.status before anyone can write it
+    if (stop) break;
+    const double dt = step_body(e, p, sh, A, t, t_end, Z);
+    if (dt < 0.0) break;
+    t += dt;
   }
   // ---------------- write back (one HBM round trip per call) ----------------
   __syncthreads();
-  n = sh.n;
+  const int n = sh.n;
   for (int i = tid; i < n; i += T) {
-    g.rho[base + i] = rho[i];
-    g.mom[base + i] = mom[i];
-    g.h[base + i] = h[i];
+    g.rho[base + i] = A.rho[i];
+    g.mom[base + i] = A.mom[i];
+    g.h[base + i] = A.h[i];
   }
   __syncthreads();
   if (tid == 0) {

@@ -130,9 +130,14 @@ def c5_segments(n_cells: int = 1 << 27, seg: int = 4096, first_segment: int = 0,
     return uniform(999.0, 1001.0, 5, 0, 0, s), uniform(-150.0, 150.0, 5, 1, 0, s)
 
 
-def c5(n_cells: int = 1 << 27, seg: int = 4096, h: float = 1e-3) -> Workload:
+def c5(n_cells: int = 1 << 27, seg: int = 4096, h: float = 1e-3, slack: int = 16) -> Workload:
+    """BASELINE configs[4]: one grid of n_cells (default 2^27) on [0, n_cells h], h = 1e-3 m;
+    per 4096-cell segment rho = U[999,1001], v = U[-150,150]; capacity n_cells (1 + 1/slack)."""
     rs, vs = c5_segments(n_cells, seg)
-    rho = np.repeat(rs, seg)[None, :]
-    mom = (np.repeat(rs, seg) * np.repeat(vs, seg))[None, :]
-    return Workload(name="C5", eos=dict(EOS_293K), params=dict(PARAMS), M=1, N=n_cells, cap=n_cells,
+    cap = n_cells + n_cells // slack
+    rho = np.zeros((1, cap))
+    mom = np.zeros((1, cap))
+    rho[0, :n_cells] = np.repeat(rs, seg)
+    mom[0, :n_cells] = np.repeat(rs, seg) * np.repeat(vs, seg)
+    return Workload(name="C5", eos=dict(EOS_293K), params=dict(PARAMS), M=1, N=n_cells, cap=cap,
                     x_left=0.0, x_right=n_cells * h, rho=rho, mom=mom, steps=500)
