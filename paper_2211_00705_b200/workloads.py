@@ -124,7 +124,7 @@ def c4(M: int = 16384, N: int = 4096, members=None, cap_slack: int = 64) -> Work
 
 def c5_segments(n_cells: int = 1 << 27, seg: int = 4096, first_segment: int = 0, n_segments=None):
     """BASELINE configs[4]: per 4096-cell segment s: rho_s=U[999,1001], v_s=U[-150,150]."""
-    total = n_cells // seg
+    total = (n_cells + seg - 1) // seg
     n_segments = total - first_segment if n_segments is None else n_segments
     s = np.arange(first_segment, first_segment + n_segments, dtype=np.uint64)
     return uniform(999.0, 1001.0, 5, 0, 0, s), uniform(-150.0, 150.0, 5, 1, 0, s)
@@ -137,7 +137,7 @@ def c5(n_cells: int = 1 << 27, seg: int = 4096, h: float = 1e-3, slack: int = 16
     cap = n_cells + n_cells // slack
     rho = np.zeros((1, cap))
     mom = np.zeros((1, cap))
-    rho[0, :n_cells] = np.repeat(rs, seg)
-    mom[0, :n_cells] = np.repeat(rs, seg) * np.repeat(vs, seg)
+    rho[0, :n_cells] = np.repeat(rs, seg)[:n_cells]
+    mom[0, :n_cells] = (np.repeat(rs, seg) * np.repeat(vs, seg))[:n_cells]
     return Workload(name="C5", eos=dict(EOS_293K), params=dict(PARAMS), M=1, N=n_cells, cap=cap,
                     x_left=0.0, x_right=n_cells * h, rho=rho, mom=mom, steps=500)
