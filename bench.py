@@ -187,7 +187,7 @@ def main():
     w = workload(name, np.arange(lo, hi) if name in ("C3", "C4") else None)
     stream = torch.cuda.current_stream()
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], device=local,
-                    stream=stream)
+                    stream=stream, threads=int(os.environ.get("EIS_THREADS", "0")))
     rho_d = torch.from_numpy(w["rho"]).cuda()
     mom_d = torch.from_numpy(w["mom"]).cuda()
     t_end = w.get("t_end", float("inf"))

@@ -197,8 +197,11 @@ class Sim:
             raise ValueError(f"eiso_create status {s}")
 
     def __del__(self):
-        if getattr(self, "_ctx", None) and self._ctx.value:
-            lib().eiso_destroy(self._ctx)
+        if getattr(self, "_ctx", None) and self._ctx.value and _lib is not None:
+            try:
+                _lib.eiso_destroy(self._ctx)
+            except Exception:  # interpreter shutdown
+                pass
             self._ctx = C.c_void_p()
 
     def set_state(self, rho, mom, width=None, n_cells=None, t0=0.0):

@@ -155,8 +155,11 @@ class Context:
             raise EisError(f"{what}: {STATUS.get(s, s)} ({msg.decode() if msg else ''})")
 
     def close(self):
-        if getattr(self, "_ctx", None) is not None and self._ctx.value:
-            lib().eis_destroy(self._ctx)
+        if getattr(self, "_ctx", None) is not None and self._ctx.value and _lib is not None:
+            try:
+                _lib.eis_destroy(self._ctx)
+            except Exception:  # interpreter shutdown
+                pass
             self._ctx = C.c_void_p()
 
     __del__ = close

@@ -359,14 +359,12 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   if (grid->layout < 0 || grid->layout > 2 || (c->tiled && M != 1)) { delete c; return EIS_E_ARG; }
   if (c->tiled) return create_tiled(c, out);
   if (cap > 16384) { delete c; return EIS_E_ARG; }
-  // CTA size: about 4 cells per thread, warps limited so the DTS scratch fits in the u array
+  // CTA size: 128 threads (3 bulk warps + the solver warp, 128 registers per thread) up to
+  // 2048 cells; larger members use 1024 threads
   int T = grid->threads;
   if (T <= 0) {
-    long long want = (grid->n_cells + 3) / 4;
-    T = (int)((want + 31) / 32 * 32);
-    if (T < 64) T = 64;
-    if (T > 1024) T = 1024;
-    if (cap <= 2048 && T > 256) T = 256;
+    T = cap <= 2048 ? 128 : 1024;
+    if (grid->n_cells < 128) T = 64;
   }
   if (T % 32 || T < 64 || T > 1024) { delete c; return EIS_E_ARG; }  // >= 1 bulk warp + the solver warp
   c->threads = T;
@@ -383,6 +381,9 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   cudaError_t e3 = cudaFuncSetAttribute(resident_steps<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e4 = cudaFuncSetAttribute(resident_steps<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e2 = cudaFuncSetAttribute(resident_steps<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  if (cudaFuncSetAttribute(resident_steps<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
+    delete c; return EIS_E_CUDA;
+  }
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) { delete c; return EIS_E_CUDA; }
   const size_t cells = (size_t)M * cap;
   bool ok = cudaMalloc(&c->d_rho, cells * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cells * 8) == cudaSuccess &&
@@ -501,7 +502,9 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   }
   if (n_steps > 0) {
     const unsigned M = (unsigned)c->grid.n_members;
-    if (c->threads <= 256 && c->minb == 4)
+    if (c->threads <= 128)
+      resident_steps<128, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else if (c->threads <= 256 && c->minb == 4)
       resident_steps<256, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else if (c->threads <= 256 && c->minb == 3)
       resident_steps<256, 3><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);

@@ -93,6 +93,22 @@ __device__ __forceinline__ void hll_p(double a, double rl, double ml, double ul,
   F1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
 }
 
+// Branch-light HLL for the bulk pass: min/max as compare-selects (finite inputs), the general
+// HLL formula always evaluated, the upwind cases selected afterwards.
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ void hll_fast(double a, double rl, double ml, double ul, double pl, double rr, double mr,
+                                         double ur, double pr, double& F0, double& F1) {
+  const double FL1 = ml * ul + pl, FR1 = mr * ur + pr;
+  const double SL = dmin(ul, ur) - a, SR = dmax(ul, ur) + a;
+  const double inv = __drcp_rn(SR - SL), SLSR = SL * SR;
+  double f0 = (SR * ml - SL * mr + SLSR * (rr - rl)) * inv;
+  double f1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
+  f0 = SL >= 0.0 ? ml : (SR <= 0.0 ? mr : f0);
+  f1 = SL >= 0.0 ? FL1 : (SR <= 0.0 ? FR1 : f1);
+  F0 = f0; F1 = f1;
+}
+
 // Creation trigger, reading R7: liquid edge cavitates iff Phi(rho_min) > 0, vapour edge
 // nucleates iff Phi(rho_tilde) < 0, Phi(r) = f(r; r_L) + f(r; r_R) + du.  Exact pre-filters:
 // ln y >= 1 - 1/y gives Phi_liq(rho_min) <= du - a(1 - rho_min^2/(r_L r_R))... (no trigger when

@@ -93,12 +93,13 @@ struct CtaShared {
 
 __device__ __forceinline__ void set_status(CtaShared& sh, int code) { atomicCAS(&sh.status, 0, code); }
 
+// warp reductions with compare-selects (finite values; a NaN state has already set a status)
 __device__ __forceinline__ double warp_max(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) { const double w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
   return v;
 }
 __device__ __forceinline__ double warp_min(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) { const double w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
   return v;
 }
 
@@ -344,15 +345,126 @@ __device__ __forceinline__ void zone_status_e(CtaShared& sh, const Zone& Z, int 
   if ((ed - 1 >= Z.zlo && ed - 1 < Z.zhi) || (ed >= Z.zlo && ed < Z.zhi)) set_status(sh, code);
 }
 
+// ------------------------------------------------------------------------------------------
+// Bulk pass P1 (own register allocation: the loop invariants stay in registers).
+// window w: lanes hold cells 31w-1 .. 31w+30 (lane 0 is the left halo, transmissive ghosts at
+// the ends, R15); lane j >= 1 owns cell 31w+j-1 and its LEFT edge: HLL flux (a3), creation
+// trigger (a4), S_max / h_min partials (a2).  One reciprocal per lane (u = m/rho); the left
+// neighbour's u and p arrive by shuffle.  Interior windows skip the ghost clamps.
+// ------------------------------------------------------------------------------------------
+__device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
+                                     const double* rho, const double* mom, const double* h, double* F0, double* F1,
+                                     const uint8_t* fl, int n, int warp, int nbulk, double* parts) {
+  const Eos e = e_ref;  // constants into registers once (not a generic load per use)
+  const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
+  const double a_v = e.a_v, a_l = e.a_l, rmin2 = e.rho_min * e.rho_min, inv_rt = 1.0 / e.rho_tilde;
+  const double eps_h = p_ref.eps_tiny * p_ref.h_av;
+  const bool explicit_mode = p_ref.mode == 1;
+  const int lane = threadIdx.x & 31;
+  double s_part = 0.0, h_part = INFINITY;
+  bool bad = false;      // a non-positive or spinodal density somewhere (reported below, rare)
+  bool special = false;  // a trigger candidate or a phase change (handled below, rare)
+  const int nwin1 = (n + 31) / 31;  // edges 0..n
+  for (int w = warp; w < nwin1; w += nbulk) {
+    const int cj = 31 * w - 1 + lane;
+    const bool interior_win = w > 0 && 31 * w + 31 < n;  // cells cj-1 .. cj+1 all exist
+    int cc = cj, cl = cj - 1;
+    if (!interior_win) {
+      cc = cj < 0 ? 0 : (cj >= n ? n - 1 : cj);
+      cl = cj - 1 < 0 ? 0 : (cj - 1 >= n ? n - 1 : cj - 1);
+    }
+    const double rc = rho[cc], mc = mom[cc];
+    const double rl = rho[cl], ml = mom[cl];
+    const double uc = mc * __drcp_rn(rc);
+    const bool vc = rc <= rho_tilde, lc = rc >= rho_min;  // phases
+    const bool vl = rl <= rho_tilde, ll = rl >= rho_min;
+    const double pcv = vc ? a_v2 * rc : p0 + a_l2 * (rc - rho0);
+    const double ul = __shfl_up_sync(0xffffffffu, uc, 1);
+    const double plv = __shfl_up_sync(0xffffffffu, pcv, 1);
+    const unsigned phc = vc ? 1u : (lc ? 2u : 0u), phl = vl ? 1u : (ll ? 2u : 0u);
+    unsigned phr = __shfl_down_sync(0xffffffffu, phc, 1);
+    if (lane == 31) {
+      const double rr = rho[cj + 1 < n ? cj + 1 : n - 1];
+      phr = rr <= rho_tilde ? 1u : (rr >= rho_min ? 2u : 0u);
+    }
+    const double a = vc ? a_v : a_l;
+    const bool own_cell = lane >= 1 && cj < n;
+    if (own_cell) {  // cell cj: S_max, h_min partials
+      bad |= !(rc > 0.0) || phc == 0u;
+      const double su = fabs(uc) + a;
+      s_part = su > s_part ? su : s_part;  // S over all cells (R5)
+      const double hc = h[cj];
+      const bool same_l = cj > 0 && phl == phc, same_r = cj + 1 < n && phr == phc;
+      const bool tiny = hc < eps_h && !same_l && !same_r;
+      const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
+      h_part = hh < h_part ? hh : h_part;  // h_min over non-tiny cells (R6)
+    }
+    if (lane >= 1 && cj <= n && phl == phc && phc != 0u) {  // edge cj between cells cj-1 and cj
+      double f0, f1;
+      hll_fast(a, rl, ml, ul, plv, rc, mc, uc, pcv, f0, f1);
+      F0[cj] = f0; F1[cj] = f1;
+      // creation pre-filters (R7), exact bounds with a 1e-9 m/s margin: liquid, both waves
+      // rarefactions and ln y <= y - 1; vapour, both shocks and sqrt(rt r) <= rt, so
+      // Phi(rt) >= du + a_v (2 - (r_L + r_R)/rt)
+      const double du = uc - ul, x = rl * rc;
+      const bool cand = lc ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x)
+                           : (du < -a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
+      special |= cand && cj > 0 && cj < n;
+    } else if (lane >= 1 && cj > 0 && cj < n && phl != phc) {
+      special |= !(fl[cj] & F_IF);  // a phase change must be a listed boundary
+    }
+  }
+  parts[0] = s_part;
+  parts[1] = h_part;
+  if (__any_sync(0xffffffffu, bad || special)) {  // rare: redo the flagged windows in full
+    for (int w = warp; w < nwin1; w += nbulk) {
+      const int cj = 31 * w - 1 + lane;
+      if (cj < 1 || cj >= n) continue;
+      const double rc = rho[cj], rl = rho[cj - 1];
+      const int pc = phase_of(e, rc), pl = phase_of(e, rl);
+      if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
+      else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
+      if (pl == pc && pc != SPIN) {
+        const double uc = mom[cj] / rc, ul = mom[cj - 1] / rl;
+        if (cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
+            !region_at(e, p_ref, rho, h, n, cj - 1) && !region_at(e, p_ref, rho, h, n, cj)) {  // R16
+          const int k = atomicAdd(&sh.ntrg, 1);
+          if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
+        }
+      } else if (pl != pc && !(fl[cj] & F_IF)) {
+        zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
+      }
+    }
+  }
+}
+
+// Bulk pass P2: explicit update of the cells with two HLL edges (a7); h^{n+1} = h^n there, so
+// h^n/h^{n+1} = 1 exactly and the update is U - (dt/h)(F_R - F_L).
+__device__ __noinline__ void bulk_p2(const Prm& p, const CtaShared& sh, double* rho, double* mom, const double* h,
+                                     const double* F0, const double* F1, const uint8_t* fl, int n, int warp,
+                                     int nbulk, int ntrg, double dt, double dt_hav) {
+  const int lane = threadIdx.x & 31;
+  const double h_av = p.h_av;
+  for (int i = warp * 32 + lane; i - lane < n; i += nbulk * 32) {
+    if (i >= n) continue;
+    if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
+    if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
+    const double hn = h[i];
+    const double cfac = hn == h_av ? dt_hav : dt / hn;
+    rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
+    mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
+  }
+}
+
 __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShared& sh, Arr& A, double t, double t_end,
                                             const Zone& Z) {
-  double* rho = A.rho;
-  double* mom = A.mom;
-  double* h = A.h;
-  double* F0 = A.F0;
-  double* F1 = A.F1;
-  double* X = A.X;
-  uint8_t* fl = A.fl;
+  double* const rho = A.rho;
+  double* const mom = A.mom;
+  double* const h = A.h;
+  double* const F0 = A.F0;
+  double* const F1 = A.F1;
+  double* const X = A.X;
+  uint8_t* const fl = A.fl;
   int n = A.n;
   const int C = A.C;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
@@ -433,55 +545,19 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       __syncwarp();
     }
     // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2) ----------------
-    // window w: lanes hold cells 31w-1 .. 31w+30 (lane 0 is the left halo, transmissive ghosts
-    // at the ends, R15); lane j >= 1 owns cell 31w+j-1 and its LEFT edge.  Each lane divides
-    // once (u = m/rho); the left neighbour's u and p arrive by shuffle.
     if (warp < nbulk) {
-      const int nwin1 = (n + 31) / 31;  // edges 0..n
-      for (int w = warp; w < nwin1; w += nbulk) {
-        const int cj = 31 * w - 1 + lane;
-        const int cc = cj < 0 ? 0 : (cj >= n ? n - 1 : cj);
-        const int cl = cj - 1 < 0 ? 0 : (cj - 1 >= n ? n - 1 : cj - 1);  // the left lane's cell
-        const double rc = rho[cc], mc = mom[cc];
-        const double uc = mc / rc;
-        const int pc = phase_of(e, rc);
-        const double pcv = pres(e, pc, rc);
-        const double ul = __shfl_up_sync(0xffffffffu, uc, 1);
-        const double plv = __shfl_up_sync(0xffffffffu, pcv, 1);
-        int pr = __shfl_down_sync(0xffffffffu, pc, 1);
-        if (lane == 31) pr = phase_of(e, rho[cj + 1 < n ? cj + 1 : n - 1]);
-        const double rl = rho[cl], ml = mom[cl];
-        const int pl = phase_of(e, rl);
-        if (lane >= 1 && cj < n) {  // cell cj: S_max, h_min partials
-          if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
-          else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
-          s_part = fmax(s_part, fabs(uc) + sound(e, pc));  // S over all cells (R5)
-          const double hc = h[cj];
-          const bool tiny = hc < p.eps_tiny * p.h_av && !(cj > 0 && pl == pc) && !(cj + 1 < n && pr == pc);
-          if (p.mode == 1 || !tiny) h_part = fmin(h_part, hc);  // h_min over non-tiny cells (R6)
-        }
-        if (lane >= 1 && cj <= n) {  // edge cj between cells cj-1 and cj
-          if (pl == pc && pc != SPIN) {
-            double f0, f1;
-            hll_p(sound(e, pc), rl, ml, ul, plv, rc, mc, uc, pcv, f0, f1);
-            F0[cj] = f0; F1[cj] = f1;
-            if (cj > 0 && cj < n && cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
-                !region_at(e, p, rho, h, n, cj - 1) && !region_at(e, p, rho, h, n, cj)) {  // R16
-              const int k = atomicAdd(&sh.ntrg, 1);
-              if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
-            }
-          } else if (cj > 0 && cj < n && pl != pc && !(fl[cj] & F_IF)) {
-            zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
-          }
-        }
-      }
+      double parts[2];
+      bulk_p1(e, p, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts);
+      s_part = parts[0];
+      h_part = parts[1];
     }
     s_part = warp_max(s_part);
     h_part = warp_min(h_part);
-    if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }
+    if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }  // folded after barrier A
     __syncthreads();  // ---------------- barrier A ----------------
-    double smax = 0.0, hmin = INFINITY;
-    for (int w = 0; w < nw; ++w) { smax = fmax(smax, sh.part_s[w]); hmin = fmin(hmin, sh.part_h[w]); }
+    // lane-parallel fold of the per-warp partials (every warp computes the same dt)
+    const double smax = warp_max(lane < nw ? sh.part_s[lane] : 0.0);
+    const double hmin = warp_min(lane < nw ? sh.part_h[lane] : INFINITY);
     double dt = Z.dt_given > 0.0 ? Z.dt_given : p.cfl * hmin / smax;  // P:466 (tiles: the global dt)
     if (t + dt > t_end) dt = t_end - t;
     const double dt_hav = dt / p.h_av;
@@ -523,17 +599,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       __syncwarp();
     }
     // ---------------- P2: explicit update of cells with two HLL edges (a7) ----------------
-    if (warp < nbulk) {
-      for (int i = warp * 32 + lane; i - lane < n; i += nbulk * 32) {
-        if (i >= n) continue;
-        if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
-        if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
-        const double hn = h[i];
-        const double cfac = hn == p.h_av ? dt_hav : dt / hn;  // h^{n+1} = h^n, so h^n/h^{n+1} = 1 exactly
-        rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
-        mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
-      }
-    }
+    if (warp < nbulk) bulk_p2(p, sh, rho, mom, h, F0, F1, fl, n, warp, nbulk, ntrg, dt, dt_hav);
     if (remesh) sh.remesh = 1;
     __syncthreads();  // ---------------- barrier B ----------------
     // ---------------- creations (a6): acceptance (R16), solves, neighbour updates ----------------
@@ -693,10 +759,8 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
           sh.nblk = 0;                      // flags are rebuilt below
         }
         n_new = sh.n_new;
-        double* t0 = rho; double* t1 = mom; double* t2 = h;  // (F0, F1, X) become the state
-        rho = F0; mom = F1; h = X;
-        F0 = t0; F1 = t1; X = t2;
         __syncthreads();
+        for (int i = tid; i < n_new; i += T) { rho[i] = F0[i]; mom[i] = F1[i]; h[i] = X[i]; }  // copy back
         for (int i = tid; i <= C; i += T) fl[i] = 0;
         __syncthreads();
         for (int k = tid; k < sh.nifc; k += T) fl[sh.ifc[k].e] = F_IF;
@@ -718,7 +782,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
     }
     n = n_new;
-    A.rho = rho; A.mom = mom; A.h = h; A.F0 = F0; A.F1 = F1; A.X = X; A.n = n;
+    A.n = n;
     __syncthreads();
     return dt;
   }
