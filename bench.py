@@ -9,10 +9,13 @@ The K timed steps start from the seeded initial state (so they include the cavit
 run as ONE launch of the member-resident kernel (eis_step(K)); inputs are resident in HBM
 (1.1 GB, larger than the 126 MB L2) when the timed region starts.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eis|reference] [--workload C3|C4|C1|C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eis|reference] [--workload C3|C4|C1|C2|C5]
 
 Multi-GPU (torchrun): members are sharded contiguously across ranks, no collective in the
 data path (scaling "strong": the ensemble is fixed); timing is the max over ranks.
+--workload C5 (BASELINE configs[4], one 2^27-cell grid, tiled layout, one launch per step) cuts
+the grid into tile-aligned rank slices under torchrun: per step a local launch, a 10-cell halo
+exchange with the neighbour ranks and an all-reduce(MIN) of the CFL pair (paper_2211_00705_b200.decomp).
 --impl reference times the CPU oracle (oracle/) on a bounded member sample (rank 0 only).
 """
 from __future__ import annotations
@@ -34,21 +37,25 @@ sys.path.insert(0, ROOT)
 # Algorithmic fp64 operations per cell-update of the bulk path: decode 5,
 # HLL edge flux + creation pre-filter 36, moving-cell update 15; one division = 1 op.
 FLOP_PER_CELL_UPDATE = 56
+C5_BYTES_PER_CELL_UPDATE = 48  # tiled layout: read rho, mom, h; write rho, mom, h (fp64)
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 FMA/clk x 2 x max clock
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=None, help="default 2000 (C3/C4), 500 (C5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="eis", choices=["eis", "reference"])
-    ap.add_argument("--workload", default="C3", choices=["C3", "C4", "C1", "C2"])
+    ap.add_argument("--workload", default="C3", choices=["C3", "C4", "C1", "C2", "C5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--members", type=int, default=0, help="profiling only: fewer ensemble members")
     ap.add_argument("--start-steps", type=int, default=0, help="profiling only: untimed steps before the timed launch")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 500 if a.workload == "C5" else 2000
+    return a
 
 
 def workload(name, members=None):
@@ -59,6 +66,8 @@ def workload(name, members=None):
         return W.c4(members=members) if members is not None else W.c4()
     if name == "C1":
         return W.c1()
+    if name == "C5":
+        return W.c5(n_cells=members) if members is not None else W.c5()
     return W.c2()
 
 
@@ -132,6 +141,11 @@ def cpu_sample_size(K, N):
     return int(min(4096, max(1, round(1.5e8 / (K * N)))))
 
 
+def c5_cpu_cells(K):
+    """Oracle sample of C5: the first whole 4096-cell segments, ~3e8 cell-updates in total."""
+    return int(max(2, min(256, round(3e8 / (K * 4096))))) * 4096
+
+
 def run_oracle(name, members, steps):
     from oracle import oracle as O
     w = workload(name, members)
@@ -148,19 +162,27 @@ def reference_arm(args):
     if rank != 0:
         return
     name = args.workload
-    N = {"C3": 1024, "C4": 4096, "C1": 200, "C2": 1000}[name]
-    S = cpu_sample_size(max(args.steps, 1), N)
-    members = np.arange(S)
-    if args.warmup:
-        run_oracle(name, members[:1], args.warmup)
-    st, dt = run_oracle(name, members, args.steps)
+    if name == "C5":
+        S = N = c5_cpu_cells(max(args.steps, 1))
+        if args.warmup:
+            run_oracle(name, 4096, args.warmup)
+        st, dt = run_oracle(name, S, args.steps)
+        sample = f"the first {S} cells (whole segments) of the C5 recipe, {args.steps} large steps from t=0"
+    else:
+        N = {"C3": 1024, "C4": 4096, "C1": 200, "C2": 1000}[name]
+        S = cpu_sample_size(max(args.steps, 1), N)
+        members = np.arange(S)
+        if args.warmup:
+            run_oracle(name, members[:1], args.warmup)
+        st, dt = run_oracle(name, members, args.steps)
+        sample = f"members 0..{S - 1} of {name}, {args.steps} large steps from t=0 (after {args.warmup} warm-up steps on member 0)"
     v = st["cell_updates"] / dt
-    sample = f"members 0..{S - 1} of {name}, {args.steps} large steps from t=0 (after {args.warmup} warm-up steps on member 0)"
     print(json.dumps({
         "impl": "reference", "metric": "fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{name} (CPU oracle sample)", "members": S, "cells_per_member": N},
+        "config": ({"workload": "C5 (CPU oracle sample)", "cells": S} if name == "C5" else
+                   {"workload": f"{name} (CPU oracle sample)", "members": S, "cells_per_member": N}),
         "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -182,6 +204,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = args.workload
+    if name == "C5":
+        return main_c5(args, torch, dist, P, world, rank, local)
     Mtot = args.members or total_members(name)
     lo, hi = rank * Mtot // world, (rank + 1) * Mtot // world
     w = workload(name, np.arange(lo, hi) if name in ("C3", "C4") else None)
@@ -289,6 +313,111 @@ def main():
                          "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
                          "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1, "clocks": clk,
+            "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
+                                         "merges", "regions")},
+            "members_not_ok": nbad,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_c5(args, torch, dist, P, world, rank, local):
+    """BASELINE configs[4]: one 2^27-cell grid, tiled layout; world > 1 cuts it into rank slices."""
+    from paper_2211_00705_b200 import workloads as W
+    from paper_2211_00705_b200.decomp import RankGrid
+    n_glob = args.members or (1 << 27)   # --members: profiling only, fewer cells
+    w = W.c5(n_cells=n_glob)
+    stream = torch.cuda.current_stream()
+    rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
+                  stream=stream)
+    rho_l = np.zeros(rg.cap)
+    mom_l = np.zeros(rg.cap)
+    rho_l[:rg.n] = w["rho"][0, rg.c0:rg.c1]
+    mom_l[:rg.n] = w["mom"][0, rg.c0:rg.c1]
+    del w
+    rho_d = torch.from_numpy(rho_l).cuda()
+    mom_d = torch.from_numpy(mom_l).cuda()
+    rg.set_state(rho_d, mom_d)
+    rg.step(args.warmup)
+    torch.cuda.synchronize()
+    rg.set_state(rho_d, mom_d)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    rg.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = rg.ctx.step(0, stats=True) if world == 1 else rg.ctx.member_stats()[0]
+    nbad = int(rg.ctx.member_status()[0] != 0)
+    cu = st["cell_updates"]
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([cu, nbad, st["creations"]], device="cuda", dtype=torch.int64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        cu, nbad = int(c[0].item()), int(c[1].item())
+    value = cu / (ms * 1e-3)
+
+    e2e = None
+    if not args.no_e2e:
+        rho_h = torch.from_numpy(rho_l).pin_memory()
+        mom_h = torch.from_numpy(mom_l).pin_memory()
+        out = {k: torch.empty(rg.cap, dtype=torch.float64).pin_memory() for k in ("rho", "mom", "h")}
+        out["n"] = torch.empty(1, dtype=torch.int64).pin_memory()
+        out["t"] = torch.empty(1, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        rg.set_state(rho_h, mom_h)
+        rg.step(args.steps)
+        rg.ctx.get_state(out)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": cu / te, "unit": "cell-updates/s",
+               "h2d_bytes_per_step": 2 * 8 * rg.cap * world / max(args.steps, 1),
+               "d2h_bytes_per_step": (3 * 8 * rg.cap + 16) * world / max(args.steps, 1),
+               "note": "one set_state(host pinned) + K steps + get_state(host pinned) per rank; bytes / K"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        S = c5_cpu_cells(max(args.steps, 1))
+        sts, dts = run_oracle("C5", S, args.steps)
+        cpu = {"value": sts["cell_updates"] / dts, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"the first {S} cells (whole segments) of C5, the same {args.steps} large steps, single thread"}
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
+    achieved = C5_BYTES_PER_CELL_UPDATE * cu / (ms * 1e-3) / world / 1e9  # per GPU
+    if rank == 0:
+        line = {
+            "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64, BASELINE configs[4] recipe)",
+            "config": {"workload": f"C5: one grid of {n_glob} cells, 4096-cell random segments",
+                       "cells": n_glob, "parallelism": f"tile-aligned grid slices x{world}, halo exchange + CFL min",
+                       "l2": "state (2 GB) larger than L2", "launches": "one tiled-step launch per step"
+                       + (" + step_finish + NCCL halo/all-reduce" if world > 1 else "")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "kernel": "eis::tiled_step",
+                         "bytes_per_cell_update": C5_BYTES_PER_CELL_UPDATE,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * (1 if world == 1 else 2), "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
             "members_not_ok": nbad,

@@ -93,12 +93,18 @@ typedef struct {
   int64_t n_cells;        /* initial cells per member N; h_av = (x_right - x_left)/N (R9) */
   int64_t cell_capacity;  /* >= n_cells: slack for created / split cells                   */
   double x_left, x_right; /* domain                                                        */
+  double h_av;            /* 0: (x_right - x_left)/n_cells; > 0: this value (a slice of a grid
+                             cut over ranks keeps the whole grid's h_av bit for bit)          */
   int32_t device;         /* CUDA device ordinal                                           */
   int32_t threads;        /* CTA size per member / tile (0 = automatic)                    */
   int32_t layout;         /* EIS_LAYOUT_AUTO | _RESIDENT (grid in shared memory across steps,
                              ensembles, cell_capacity <= 16384) | _TILED (one huge grid, streamed
                              through HBM in halo-overlapped tiles each step, n_members == 1)   */
-  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 960)                         */
+  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 960); tiles are fixed-size from
+                             the left, the last one takes the remainder                      */
+  int32_t nbr_left;       /* tiled rank mode: 1 if this grid is the right part of a grid cut
+                             over ranks (its left halo arrives through the exchange buffer)  */
+  int32_t nbr_right;      /* ... 1 if a rank continues the grid on the right                   */
   void* stream;           /* cudaStream_t (NULL = legacy default stream)                   */
 } eis_grid;
 
@@ -159,6 +165,28 @@ eis_status eis_member_status(eis_ctx* ctx, int32_t* out);
 
 /* Per-member counters (host array of n_members eis_stats; t_min = t_max = member time). */
 eis_status eis_member_stats(eis_ctx* ctx, eis_stats* out);
+
+/* ---- rank mode: one tiled grid cut over ranks (BASELINE configs[4] on 2-8 GPUs) ----------
+ * Each rank owns a contiguous, tile-aligned slice.  Per step the caller runs
+ *   eis_step_local   -> (exchange: send_left -> left rank's recv_right, send_right -> right
+ *                       rank's recv_left; min-allreduce of the 2-double CFL pair)
+ *   eis_step_finish(after_step = 1)
+ * and after eis_set_state: exchange, then eis_step_finish(after_step = 0) (initial dt).
+ * Exchange buffer: EIS_XB_DOUBLES doubles of device memory owned by the caller, borrowed for
+ * the context's lifetime: records of EIS_HALO cells (rho[EIS_HALO], mom[..], h[..], count)
+ * at offsets EIS_XB_SEND_LEFT, _SEND_RIGHT, _RECV_LEFT, _RECV_RIGHT, then the pair
+ * (-S_max, h_min) at EIS_XB_DT.  Min-reduction of the pair gives the global CFL dt. */
+#define EIS_HALO 10
+#define EIS_XB_REC (3 * EIS_HALO + 1)
+#define EIS_XB_SEND_LEFT 0
+#define EIS_XB_SEND_RIGHT EIS_XB_REC
+#define EIS_XB_RECV_LEFT (2 * EIS_XB_REC)
+#define EIS_XB_RECV_RIGHT (3 * EIS_XB_REC)
+#define EIS_XB_DT (4 * EIS_XB_REC)
+#define EIS_XB_DOUBLES (4 * EIS_XB_REC + 2)
+eis_status eis_set_exchange_buffer(eis_ctx* ctx, double* dev_xbuf);
+eis_status eis_step_local(eis_ctx* ctx, double t_end);
+eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
 
 /* Last error message of the context (static storage owned by the context). */
 const char* eis_last_error(const eis_ctx* ctx);

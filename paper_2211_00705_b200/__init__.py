@@ -47,8 +47,9 @@ class Params(C.Structure):
 
 class Grid(C.Structure):
     _fields_ = [("n_members", C.c_int64), ("n_cells", C.c_int64), ("cell_capacity", C.c_int64),
-                ("x_left", C.c_double), ("x_right", C.c_double), ("device", C.c_int32),
-                ("threads", C.c_int32), ("layout", C.c_int32), ("tile_cells", C.c_int32), ("stream", C.c_void_p)]
+                ("x_left", C.c_double), ("x_right", C.c_double), ("h_av", C.c_double), ("device", C.c_int32),
+                ("threads", C.c_int32), ("layout", C.c_int32), ("tile_cells", C.c_int32),
+                ("nbr_left", C.c_int32), ("nbr_right", C.c_int32), ("stream", C.c_void_p)]
 
 
 class Interface(C.Structure):
@@ -71,7 +72,14 @@ class Thresholds(C.Structure):
 
 # exported symbols of libeis.so (checked by tests/test_abi.py against include/eis.h)
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
-           "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy")
+           "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
+           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish")
+# exchange-buffer layout (include/eis.h EIS_XB_*)
+HALO = 10
+XB_REC = 3 * HALO + 1
+XB_SEND_LEFT, XB_SEND_RIGHT, XB_RECV_LEFT, XB_RECV_RIGHT = 0, XB_REC, 2 * XB_REC, 3 * XB_REC
+XB_DT = 4 * XB_REC
+XB_DOUBLES = 4 * XB_REC + 2
 
 _lib = None
 
@@ -96,6 +104,9 @@ def lib():
         L.eis_last_error.argtypes = [vp]
         L.eis_last_error.restype = C.c_char_p
         L.eis_destroy.argtypes = [vp]
+        L.eis_set_exchange_buffer.argtypes = [vp, vp]
+        L.eis_step_local.argtypes = [vp, d]
+        L.eis_step_finish.argtypes = [vp, d, i32]
         for s in SYMBOLS:
             if s not in ("eis_last_error", "eis_destroy"):
                 getattr(L, s).restype = C.c_int
@@ -136,13 +147,15 @@ class Context:
 
     def __init__(self, eos: dict, params: dict, n_members: int, n_cells: int, capacity: int,
                  x_left: float, x_right: float, device: int = 0, stream=None, threads: int = 0,
-                 layout: int = 0, tile_cells: int = 0):
+                 layout: int = 0, tile_cells: int = 0, nbr_left: bool = False, nbr_right: bool = False,
+                 h_av: float = 0.0):
         if stream is not None and hasattr(stream, "cuda_stream"):
             stream = stream.cuda_stream
         self.M, self.N, self.cap = int(n_members), int(n_cells), int(capacity)
         self.device = int(device)
-        self._grid = Grid(self.M, self.N, self.cap, float(x_left), float(x_right), self.device, int(threads),
-                          int(layout), int(tile_cells), C.c_void_p(stream) if stream else None)
+        self._grid = Grid(self.M, self.N, self.cap, float(x_left), float(x_right), float(h_av), self.device, int(threads),
+                          int(layout), int(tile_cells), int(bool(nbr_left)), int(bool(nbr_right)),
+                          C.c_void_p(stream) if stream else None)
         self._eos, self._prm = make_eos(eos), make_params(params)
         self._ctx = C.c_void_p()
         s = lib().eis_create(C.byref(self._eos), C.byref(self._prm), C.byref(self._grid), C.byref(self._ctx))
@@ -209,6 +222,18 @@ class Context:
         self._check(lib().eis_member_status(self._ctx, out.ctypes.data_as(C.POINTER(C.c_int32))),
                     "eis_member_status")
         return out
+
+    # ---- rank mode (tiled grid cut over ranks) ------------------------------------------
+    def set_exchange_buffer(self, xbuf):
+        """xbuf: a device tensor of XB_DOUBLES float64 owned by the caller (kept alive by it)."""
+        self._xbuf = xbuf
+        self._check(lib().eis_set_exchange_buffer(self._ctx, xbuf.data_ptr()), "eis_set_exchange_buffer")
+
+    def step_local(self, t_end: float = float("inf")):
+        self._check(lib().eis_step_local(self._ctx, float(t_end)), "eis_step_local")
+
+    def step_finish(self, t_end: float = float("inf"), after_step: bool = True):
+        self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
 
     def member_stats(self) -> list:
         arr = (Stats * self.M)()

@@ -184,10 +184,12 @@ __global__ void k_iface(const Eos e, Members g, long long M, double x_left, cons
 }
 
 // contiguous staging (member 0) -> tiles: tile k gets cells [k n / ntiles, (k+1) n / ntiles)
-__global__ void k_to_tiles(Members g, Tiles tl, int cur) {
+__global__ void k_to_tiles(Members g, Tiles tl, int cur, int tile_cells) {
   const int k = blockIdx.x;
   const long long n = g.n[0];
-  const long long lo = (long long)k * n / tl.ntiles, hi = (long long)(k + 1) * n / tl.ntiles;
+  // fixed-size tiles, the last one takes the remainder: any tile-aligned split of a grid over
+  // ranks therefore reproduces the single-grid tiling exactly
+  const long long lo = (long long)k * tile_cells, hi = k == tl.ntiles - 1 ? n : lo + tile_cells;
   const long long base = (long long)k * tl.capt;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     tl.rho[cur][base + i - lo] = g.rho[i];
@@ -236,6 +238,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
   const int capt = c->tile_cells + 32;
   long long ntiles = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;
+  if (ntiles > 1 && grid->n_cells - (ntiles - 1) * c->tile_cells < HALO) --ntiles;  // tiny remainder joins the last tile
   if (ntiles < 1) ntiles = 1;
   if (ntiles > (1 << 30)) { delete c; return EIS_E_ARG; }
   c->threads = grid->threads > 0 ? grid->threads : 256;
@@ -260,7 +263,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
        cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
-       cudaMalloc(&c->t_scal, 4 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 4 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 4 * 4) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
@@ -269,6 +272,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; }
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
   tl.ntiles = (int)ntiles; tl.capt = capt;
+  tl.xbuf = nullptr;
+  tl.nbr_left = grid->nbr_left != 0; tl.nbr_right = grid->nbr_right != 0;
   *out = c;
   return EIS_OK;
 }
@@ -350,7 +355,7 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   p.cfl = prm->cfl; p.eps_split = prm->eps_split; p.eps_tiny = prm->eps_tiny; p.theta_nb = prm->theta_nb;
   p.tol_nb = prm->tol_nb; p.tol_tiny = prm->tol_tiny; p.newton_rtol = prm->newton_rtol; p.newton_gtol = prm->newton_gtol;
   p.newton_stol = std::sqrt(prm->newton_rtol);
-  p.h_av = (grid->x_right - grid->x_left) / (double)grid->n_cells;  // fixed (R9)
+  p.h_av = grid->h_av > 0 ? grid->h_av : (grid->x_right - grid->x_left) / (double)grid->n_cells;  // fixed (R9)
   p.dts_max_iter = prm->dts_max_iter; p.newton_max_iter = prm->newton_max_iter; p.armijo_max = prm->armijo_max;
   p.mode = prm->mode;
 
@@ -444,7 +449,15 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   CU(cudaGetLastError());
   if (c->tiled) {
     k_tiles_reset<<<1, 1, 0, c->stream>>>(c->tl, c->d_status, t0);
-    k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0);
+    if ((c->tl.nbr_left || c->tl.nbr_right) && !c->tl.xbuf)
+      return fail(c, EIS_E_ORDER, "rank mode: eis_set_exchange_buffer before eis_set_state%s");
+    {
+      long long nn = c->grid.n_cells;
+      if (n_cells && where == EIS_HOST) nn = n_cells[0];
+      const long long lo_last = (long long)(c->tl.ntiles - 1) * c->tile_cells;
+      if (nn - lo_last < HALO || nn - lo_last > c->tl.capt) return fail(c, EIS_E_ARG, "set_state: n_cells does not fit the tiling%s");
+    }
+    k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0, c->tile_cells);
     tiled_init_dt<256><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, INFINITY);
     CU(cudaGetLastError());
     c->staging_fresh = 1;
@@ -625,5 +638,34 @@ extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
     o.creations = s.creations; o.splits = s.splits; o.merges = s.merges; o.regions = s.regions;
     o.t_min = o.t_max = t[m]; o.dt_min = s.dt_min; o.dt_max = s.dt_max;
   }
+  return EIS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// rank mode (one tiled grid decomposed over ranks): exchange buffer + split step
+// ------------------------------------------------------------------------------------------
+extern "C" eis_status eis_set_exchange_buffer(eis_ctx* c, double* xbuf) {
+  if (!c || !c->tiled || !xbuf) return EIS_E_ARG;
+  c->tl.xbuf = xbuf;
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_step_local(eis_ctx* c, double t_end) {
+  if (!c || !c->tiled || !c->tl.xbuf) return EIS_E_ARG;
+  if (c->sticky) return c->sticky;
+  if (!c->state_set) return fail(c, EIS_E_ORDER, "step before set_state%s");
+  CU(cudaSetDevice(c->grid.device));
+  c->staging_fresh = 0;
+  tiled_step<256, 4><<<c->tl.ntiles, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+  CU(cudaGetLastError());
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_step_finish(eis_ctx* c, double t_end, int32_t after_step) {
+  if (!c || !c->tiled || !c->tl.xbuf) return EIS_E_ARG;
+  if (c->sticky) return c->sticky;
+  CU(cudaSetDevice(c->grid.device));
+  tiled_finish<<<1, 1, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
+  CU(cudaGetLastError());
   return EIS_OK;
 }

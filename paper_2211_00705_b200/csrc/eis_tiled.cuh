@@ -30,8 +30,16 @@ struct Tiles {
   TileStats* tstats;
   double* scal;                    // [0] t  [1] dt of the next step  [2] dt_min  [3] dt_max
   int* ctl;                        // [0] cur  [1] status  [2] done-counter  [3] steps
-  int ntiles, capt;
+  double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
+  int ntiles, capt, nbr_left, nbr_right;
 };
+
+// Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
+// HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
+constexpr int XB_REC = 3 * HALO + 1;
+constexpr int XB_SEND_LEFT = 0, XB_SEND_RIGHT = XB_REC, XB_RECV_LEFT = 2 * XB_REC, XB_RECV_RIGHT = 3 * XB_REC;
+constexpr int XB_DT = 4 * XB_REC;
+constexpr int XB_DOUBLES = 4 * XB_REC + 2;
 
 constexpr int WS_STRIDE = 2 * MAXIF + 1;
 
@@ -72,6 +80,13 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, double dt_used,
   __syncthreads();
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
+    if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
+      tl.xbuf[XB_DT] = -s;
+      tl.xbuf[XB_DT + 1] = hm;
+      tl.scal[4] = dt_used;
+      __threadfence();
+      return;
+    }
     const double t_new = tl.scal[0] + dt_used;
     double dt = p.cfl * hm / s;
     if (t_new + dt > t_end) dt = t_end - t_new;
@@ -102,8 +117,9 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   const int in = cur, out = 1 - cur;
   const long long base = (long long)k * tl.capt;
   const int cnt = tl.cnt[in][k];
-  const int nL = k > 0 ? min(HALO, tl.cnt[in][k - 1]) : 0;
-  const int nR = k < tl.ntiles - 1 ? min(HALO, tl.cnt[in][k + 1]) : 0;
+  const bool xl = (k == 0 && tl.nbr_left), xr = (k == tl.ntiles - 1 && tl.nbr_right);  // halo from a rank
+  const int nL = k > 0 ? min(HALO, tl.cnt[in][k - 1]) : (xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
+  const int nR = k < tl.ntiles - 1 ? min(HALO, tl.cnt[in][k + 1]) : (xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
   if (tid == 0) {
     sh.status = 0;
     reset_counters(sh);
@@ -117,6 +133,18 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     const long long bl = base - tl.capt, br = base + tl.capt;
     const int cl = k > 0 ? tl.cnt[in][k - 1] : 0;
     for (int i = tid; i < n; i += T) {
+      if (xl && i < nL) {  // left halo received from the left rank (its last cells)
+        const double* rb = tl.xbuf + XB_RECV_LEFT;
+        const int j = HALO - nL + i;
+        A.rho[i] = rb[j]; A.mom[i] = rb[HALO + j]; A.h[i] = rb[2 * HALO + j];
+        continue;
+      }
+      if (xr && i >= nL + cnt) {  // right halo received from the right rank (its first cells)
+        const double* rb = tl.xbuf + XB_RECV_RIGHT;
+        const int j = i - nL - cnt;
+        A.rho[i] = rb[j]; A.mom[i] = rb[HALO + j]; A.h[i] = rb[2 * HALO + j];
+        continue;
+      }
       long long g;
       if (i < nL) g = bl + (cl - nL + i);
       else if (i < nL + cnt) g = base + (i - nL);
@@ -135,7 +163,7 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   Z.own_lo = nL; Z.own_hi = nL + cnt;
   Z.zlo = max(nL - 2, 0); Z.zhi = min(nL + cnt + 2, n);
   Z.dt_given = dt_given;
-  Z.left_real = (k == 0); Z.right_real = (k == tl.ntiles - 1);
+  Z.left_real = (k == 0 && !tl.nbr_left); Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
   // ---------------- owned output, partials of the next dt, side tables ----------------
   __syncthreads();
@@ -149,6 +177,19 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
       tl.rho[out][ob + i] = A.rho[olo + i];
       tl.mom[out][ob + i] = A.mom[olo + i];
       tl.h[out][ob + i] = A.h[olo + i];
+    }
+    if (xl) {  // my first HALO owned cells go to the left rank (its right halo)
+      double* sb = tl.xbuf + XB_SEND_LEFT;
+      for (int i = tid; i < HALO; i += T) { sb[i] = A.rho[olo + i]; sb[HALO + i] = A.mom[olo + i]; sb[2 * HALO + i] = A.h[olo + i]; }
+      if (tid == 0) sb[3 * HALO] = HALO;
+    }
+    if (xr) {  // my last HALO owned cells go to the right rank (its left halo)
+      double* sb = tl.xbuf + XB_SEND_RIGHT;
+      for (int i = tid; i < HALO; i += T) {
+        const int j = ohi - HALO + i;
+        sb[i] = A.rho[j]; sb[HALO + i] = A.mom[j]; sb[2 * HALO + i] = A.h[j];
+      }
+      if (tid == 0) sb[3 * HALO] = HALO;
     }
     double s, hm;
     cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, Z.left_real, Z.right_real, s, hm);
@@ -235,12 +276,57 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     __syncthreads();
     if (tid == 0) {
       for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
-      double dt = p.cfl * hm / s;
-      if (tl.scal[0] + dt > t_end) dt = t_end - tl.scal[0];
-      tl.scal[1] = dt;
+      if (tl.xbuf) {
+        tl.xbuf[XB_DT] = -s;
+        tl.xbuf[XB_DT + 1] = hm;
+      } else {
+        double dt = p.cfl * hm / s;
+        if (tl.scal[0] + dt > t_end) dt = t_end - tl.scal[0];
+        tl.scal[1] = dt;
+      }
       tl.ctl[2] = 0;
     }
   }
+  if (tl.xbuf && (k == 0 || k == tl.ntiles - 1)) {  // initial halos for the first exchange
+    const int cur2 = tl.ctl[0];
+    if (k == 0 && tl.nbr_left) {
+      double* sb = tl.xbuf + XB_SEND_LEFT;
+      for (int i = tid; i < HALO; i += blockDim.x) {
+        sb[i] = tl.rho[cur2][base + i]; sb[HALO + i] = tl.mom[cur2][base + i]; sb[2 * HALO + i] = tl.h[cur2][base + i];
+      }
+      if (tid == 0) sb[3 * HALO] = HALO;
+    }
+    if (k == tl.ntiles - 1 && tl.nbr_right) {
+      double* sb = tl.xbuf + XB_SEND_RIGHT;
+      for (int i = tid; i < HALO; i += blockDim.x) {
+        const long long j = base + cnt - HALO + i;
+        sb[i] = tl.rho[cur2][j]; sb[HALO + i] = tl.mom[cur2][j]; sb[2 * HALO + i] = tl.h[cur2][j];
+      }
+      if (tid == 0) sb[3 * HALO] = HALO;
+    }
+  }
+}
+
+// rank mode, after the exchange: dt from the min-reduced pair; after a step also advance t and
+// flip the buffers (what the last CTA does in single-rank mode)
+__global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constant__ Tiles tl, double t_end, int after_step) {
+  if (tl.ctl[1] != 0) return;
+  const double S = -tl.xbuf[XB_DT], hm = tl.xbuf[XB_DT + 1];
+  double t_new = tl.scal[0];
+  if (after_step) {
+    if (!(t_new < t_end)) return;  // the step was a no-op
+    const double dt_used = tl.scal[4];
+    t_new += dt_used;
+    if (tl.ctl[3] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
+    if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
+    tl.ctl[0] = 1 - tl.ctl[0];
+    tl.ctl[3] += 1;
+    tl.ctl[2] = 0;
+  }
+  double dt = p.cfl * hm / S;
+  if (t_new + dt > t_end) dt = t_end - t_new;
+  tl.scal[0] = t_new;
+  tl.scal[1] = dt;
 }
 
 }  // namespace eis

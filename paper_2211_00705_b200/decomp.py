@@ -1,0 +1,149 @@
+"""One tiled grid cut over ranks (BASELINE configs[4] on several GPUs): tile-aligned slices, a
+per-step halo exchange with the neighbour ranks and a min-reduction of the CFL pair.
+
+Plumbing only: every step of the method runs in libeis kernels; this module
+moves 10-cell halo records between ranks with torch.distributed (NCCL on GPUs, gloo on CPU)
+and folds the (-S_max, h_min) pairs with an all-reduce(MIN).  Slices are whole tiles, so a
+P-rank run computes exactly what the 1-rank run computes (min/max are exact, halos copy bits).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import (HALO, LAYOUT_TILED, XB_DOUBLES, XB_DT, XB_REC, XB_RECV_LEFT, XB_RECV_RIGHT,
+               XB_SEND_LEFT, XB_SEND_RIGHT, Context)
+
+
+def tile_count(n: int, tile: int) -> int:
+    """Tiles of the library's fixed-size tiling (the last takes the remainder, >= HALO cells)."""
+    nt = max(1, math.ceil(n / tile))
+    if nt > 1 and n - (nt - 1) * tile < HALO:
+        nt -= 1
+    return nt
+
+
+def rank_slice(n: int, tile: int, rank: int, world: int) -> tuple[int, int]:
+    """Cells [c0, c1) of rank `rank`: a contiguous, balanced range of whole tiles."""
+    T = tile_count(n, tile)
+    if T < world:
+        raise ValueError(f"{T} tiles cannot be split over {world} ranks")
+    t0, t1 = rank * T // world, (rank + 1) * T // world
+    return t0 * tile, (n if rank == world - 1 else t1 * tile)
+
+
+def exchange_halos(xbuf: torch.Tensor, rank: int, world: int, group=None) -> None:
+    """send_left -> left rank's recv_right, send_right -> right rank's recv_left, then
+    all-reduce(MIN) of the CFL pair.  Works for CUDA (NCCL) and CPU (gloo) tensors."""
+    import torch.distributed as dist
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, xbuf[XB_SEND_LEFT:XB_SEND_LEFT + XB_REC], rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, xbuf[XB_RECV_LEFT:XB_RECV_LEFT + XB_REC], rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, xbuf[XB_SEND_RIGHT:XB_SEND_RIGHT + XB_REC], rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, xbuf[XB_RECV_RIGHT:XB_RECV_RIGHT + XB_REC], rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if world > 1:
+        dist.all_reduce(xbuf[XB_DT:XB_DT + 2], op=dist.ReduceOp.MIN, group=group)
+
+
+class RankGrid:
+    """This rank's slice of one tiled grid.  For world == 1 it is a plain tiled context."""
+
+    def __init__(self, eos: dict, params: dict, n_global: int, x_left: float, x_right: float, rank: int,
+                 world: int, tile: int = 960, device: int = 0, stream=None, group=None, slack: int = 16):
+        self.rank, self.world, self.group = rank, world, group
+        self.c0, self.c1 = rank_slice(n_global, tile, rank, world)
+        self.n = self.c1 - self.c0
+        self.h_av = (x_right - x_left) / n_global
+        self.cap = self.n + self.n // slack + tile
+        self.ctx = Context(eos, params, 1, self.n, self.cap, x_left + self.c0 * self.h_av,
+                           x_left + self.c1 * self.h_av, device=device, stream=stream, layout=LAYOUT_TILED,
+                           tile_cells=tile, nbr_left=rank > 0, nbr_right=rank < world - 1, h_av=self.h_av)
+        self.xbuf = None
+        if world > 1:
+            self.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
+            self.ctx.set_exchange_buffer(self.xbuf)
+
+    def exchange(self):
+        exchange_halos(self.xbuf, self.rank, self.world, self.group)
+
+    def set_state(self, rho_local, mom_local, t_end: float = float("inf")):
+        """rho/mom: this rank's cells [c0, c1) (padded to cap), device or host buffers."""
+        self.ctx.set_state(rho_local, mom_local)
+        if self.world > 1:
+            self.exchange()
+            self.ctx.step_finish(t_end, after_step=False)
+
+    def step(self, n_steps: int, t_end: float = float("inf")):
+        if self.world == 1:
+            return self.ctx.step(n_steps) if t_end == float("inf") else self.ctx.run_to(t_end, n_steps)
+        for _ in range(n_steps):
+            self.ctx.step_local(t_end)
+            self.exchange()
+            self.ctx.step_finish(t_end, after_step=True)
+
+
+class VirtualRanks:
+    """P rank slices of one grid on ONE device, exchanged by device copies (no NCCL, no kernel
+    waits on another): exercises the rank-mode library path against the 1-rank run."""
+
+    def __init__(self, eos, params, n_global, x_left, x_right, world, tile=960, device=0, stream=None):
+        self.parts = []
+        for r in range(world):
+            g = RankGrid.__new__(RankGrid)
+            g.rank, g.world, g.group = r, world, None
+            g.c0, g.c1 = rank_slice(n_global, tile, r, world)
+            g.n = g.c1 - g.c0
+            g.h_av = (x_right - x_left) / n_global
+            g.cap = g.n + g.n // 16 + tile
+            g.ctx = Context(eos, params, 1, g.n, g.cap, x_left + g.c0 * g.h_av, x_left + g.c1 * g.h_av,
+                            device=device, stream=stream, layout=LAYOUT_TILED, tile_cells=tile,
+                            nbr_left=r > 0, nbr_right=r < world - 1, h_av=g.h_av)
+            g.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
+            g.ctx.set_exchange_buffer(g.xbuf)
+            self.parts.append(g)
+
+    def _exchange(self):
+        P = self.parts
+        for r, g in enumerate(P):
+            if r > 0:
+                g.xbuf[XB_RECV_LEFT:XB_RECV_LEFT + XB_REC].copy_(P[r - 1].xbuf[XB_SEND_RIGHT:XB_SEND_RIGHT + XB_REC])
+            if r < len(P) - 1:
+                g.xbuf[XB_RECV_RIGHT:XB_RECV_RIGHT + XB_REC].copy_(P[r + 1].xbuf[XB_SEND_LEFT:XB_SEND_LEFT + XB_REC])
+        pair = torch.stack([g.xbuf[XB_DT:XB_DT + 2] for g in P]).amin(dim=0)
+        for g in P:
+            g.xbuf[XB_DT:XB_DT + 2].copy_(pair)
+
+    def set_state(self, rho_global, mom_global, t_end=float("inf")):
+        """rho/mom: the whole grid as 1-D device tensors."""
+        for g in self.parts:
+            r = torch.zeros(g.cap, dtype=torch.float64, device=rho_global.device)
+            m = torch.zeros_like(r)
+            r[:g.n] = rho_global[g.c0:g.c1]
+            m[:g.n] = mom_global[g.c0:g.c1]
+            g.ctx.set_state(r, m)
+        self._exchange()
+        for g in self.parts:
+            g.ctx.step_finish(t_end, after_step=False)
+
+    def step(self, n_steps, t_end=float("inf")):
+        for _ in range(n_steps):
+            for g in self.parts:
+                g.ctx.step_local(t_end)
+            self._exchange()
+            for g in self.parts:
+                g.ctx.step_finish(t_end, after_step=True)
+
+    def get_state(self):
+        outs = [g.ctx.get_state() for g in self.parts]
+        import numpy as np
+        rho = np.concatenate([o["rho"][0, :int(o["n"][0])] for o in outs])
+        mom = np.concatenate([o["mom"][0, :int(o["n"][0])] for o in outs])
+        h = np.concatenate([o["h"][0, :int(o["n"][0])] for o in outs])
+        return {"rho": rho, "mom": mom, "h": h, "t": [float(o["t"][0]) for o in outs],
+                "status": [int(g.ctx.member_status()[0]) for g in self.parts]}
