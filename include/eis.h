@@ -121,6 +121,7 @@ typedef struct {
   int64_t iface_solves;   /* phase-boundary Riemann solves                                 */
   int64_t creations, splits, merges, regions;
   double t_min, t_max, dt_min, dt_max;
+  int64_t dts_iter_max;   /* most dual-time iterations one implicit block took in one step */
 } eis_stats;
 
 typedef struct { double rho_min, rho_tilde, p_tilde, tau, a_v; } eis_thresholds;
@@ -187,6 +188,12 @@ eis_status eis_member_stats(eis_ctx* ctx, eis_stats* out);
 eis_status eis_set_exchange_buffer(eis_ctx* ctx, double* dev_xbuf);
 eis_status eis_step_local(eis_ctx* ctx, double t_end);
 eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
+
+/* Tiled-layout diagnostics (EIS_E_ARG for a member-resident context): the number of tiles and
+ * the tile-steps since eis_set_state that took the full step (a phase boundary, a creation
+ * candidate or a remesh event in the tile or its halo) rather than the single-phase fast path.
+ * Reads device counters (synchronises the stream). */
+eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps);
 
 /* Last error message of the context (static storage owned by the context). */
 const char* eis_last_error(const eis_ctx* ctx);

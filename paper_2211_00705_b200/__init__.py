@@ -60,7 +60,8 @@ class Interface(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("steps", "cell_updates", "dts_iters", "iface_solves",
                                          "creations", "splits", "merges", "regions")] + \
-               [(n, C.c_double) for n in ("t_min", "t_max", "dt_min", "dt_max")]
+               [(n, C.c_double) for n in ("t_min", "t_max", "dt_min", "dt_max")] + \
+               [("dts_iter_max", C.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -73,7 +74,7 @@ class Thresholds(C.Structure):
 # exported symbols of libeis.so (checked by tests/test_abi.py against include/eis.h)
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
-           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish")
+           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
 XB_REC = 3 * HALO + 1
@@ -101,6 +102,7 @@ def lib():
         L.eis_interfaces.argtypes = [vp, P(Interface), i64, P(i64)]
         L.eis_member_status.argtypes = [vp, P(i32)]
         L.eis_member_stats.argtypes = [vp, P(Stats)]
+        L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64)]
         L.eis_last_error.argtypes = [vp]
         L.eis_last_error.restype = C.c_char_p
         L.eis_destroy.argtypes = [vp]
@@ -234,6 +236,11 @@ class Context:
 
     def step_finish(self, t_end: float = float("inf"), after_step: bool = True):
         self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
+
+    def tile_info(self) -> dict:
+        nt, full = C.c_int64(), C.c_int64()
+        self._check(lib().eis_tile_info(self._ctx, C.byref(nt), C.byref(full)), "eis_tile_info")
+        return {"n_tiles": nt.value, "full_tile_steps": full.value}
 
     def member_stats(self) -> list:
         arr = (Stats * self.M)()

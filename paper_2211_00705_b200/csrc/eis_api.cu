@@ -4,6 +4,7 @@
 // eis_resident.cuh / eis_device.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 using namespace eis;
 
 struct eis_ctx {
+  long long tile_full_steps = 0;
   eis_eos eos_in;
   eis_params prm_in;
   eis_grid grid;
@@ -41,7 +43,9 @@ struct eis_ctx {
   int tiled, tile_cells;
   Tiles tl;
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
-  int *t_cnt[2], *t_ctl;
+  int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow;
+  double* t_part2;
+  int slow_grid;
   TileStats* t_stats;
   long long* t_off;
   int staging_fresh;
@@ -198,6 +202,7 @@ __global__ void k_to_tiles(Members g, Tiles tl, int cur, int tile_cells) {
   }
   if (threadIdx.x == 0) {
     tl.cnt[cur][k] = (int)(hi - lo);
+    tl.hu[cur][k] = 0;  // widths stored; the first step finds out whether they are all h_av
     double* ws = tl.ws + (size_t)k * WS_STRIDE;
     ws[2 * MAXIF] = -1.0;
     TileStats z;
@@ -206,15 +211,16 @@ __global__ void k_to_tiles(Members g, Tiles tl, int cur, int tile_cells) {
   }
 }
 // tiles -> contiguous staging, given exclusive offsets
-__global__ void k_from_tiles(Members g, Tiles tl, const long long* off) {
+__global__ void k_from_tiles(Members g, Tiles tl, const long long* off, double h_av) {
   const int k = blockIdx.x;
   const int cur = tl.ctl[0];
   const int cnt = tl.cnt[cur][k];
+  const bool hu = tl.hu[cur][k] != 0;
   const long long base = (long long)k * tl.capt, o = off[k];
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     g.rho[o + i] = tl.rho[cur][base + i];
     g.mom[o + i] = tl.mom[cur][base + i];
-    g.h[o + i] = tl.h[cur][base + i];
+    g.h[o + i] = hu ? h_av : tl.h[cur][base + i];
   }
   if (k == 0 && threadIdx.x == 0) {
     g.n[0] = off[tl.ntiles];
@@ -236,22 +242,26 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   const long long cap = grid->cell_capacity;
   c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 960;
   if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
-  const int capt = c->tile_cells + 32;
+  const int capt = c->tile_cells + 32 + (c->tile_cells & 1);  // even: 16-byte aligned tile rows
   long long ntiles = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;
   if (ntiles > 1 && grid->n_cells - (ntiles - 1) * c->tile_cells < HALO) --ntiles;  // tiny remainder joins the last tile
   if (ntiles < 1) ntiles = 1;
   if (ntiles > (1 << 30)) { delete c; return EIS_E_ARG; }
   c->threads = grid->threads > 0 ? grid->threads : 256;
   if (c->threads != 256) { delete c; return EIS_E_ARG; }
-  const int capg = capt + 2 * HALO + MAXEV;
+  const int capg = capt + 2 * HALO + MAXEV + 1;  // as tiled_step
   c->smem = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(capg + 1) + (((size_t)capg + 1 + 15) & ~size_t(15));
   if (cudaSetDevice(grid->device) != cudaSuccess) { delete c; return EIS_E_CUDA; }
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, grid->device);
   if ((int)c->smem + 1024 > max_optin) { delete c; return EIS_E_CAPACITY; }
-  if (cudaFuncSetAttribute(tiled_step<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
+  if (cudaFuncSetAttribute(tiled_slow<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
+  int nsm = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
+  c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
   const size_t tc = (size_t)ntiles * capt;
   bool ok = cudaMalloc(&c->d_rho, cap * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cap * 8) == cudaSuccess &&
             cudaMalloc(&c->d_h, cap * 8) == cudaSuccess && cudaMalloc(&c->d_t, 8) == cudaSuccess &&
@@ -259,17 +269,21 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
             cudaMalloc(&c->d_stats, sizeof(MemberStats)) == cudaSuccess && cudaMalloc(&c->d_cnt, 16) == cudaSuccess;
   for (int b = 0; b < 2 && ok; ++b)
     ok = cudaMalloc(&c->t_rho[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_mom[b], tc * 8) == cudaSuccess &&
-         cudaMalloc(&c->t_h[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_cnt[b], ntiles * 4) == cudaSuccess;
+         cudaMalloc(&c->t_h[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_cnt[b], ntiles * 4) == cudaSuccess &&
+         cudaMalloc(&c->t_hu[b], ntiles * 4) == cudaSuccess;
   ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
        cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
-       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 4 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 8 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
   Tiles& tl = c->tl;
-  for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; }
+  for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
+  tl.slow = c->t_slow; tl.part2 = c->t_part2;
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
   tl.ntiles = (int)ntiles; tl.capt = capt;
   tl.xbuf = nullptr;
@@ -279,7 +293,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 }
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
-  tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0;
+  tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
   tl.scal[0] = t0; tl.scal[1] = 0.0; tl.scal[2] = 0.0; tl.scal[3] = 0.0;
 }
 
@@ -298,7 +312,7 @@ static eis_status tiles_to_staging(eis_ctx* c) {
   for (int k = 0; k < nt; ++k) off[k + 1] = off[k] + cnt[k];
   if (off[nt] > c->grid.cell_capacity) return fail(c, EIS_E_CAPACITY, "tiled grid exceeds cell_capacity%s");
   CU(cudaMemcpyAsync(c->t_off, off.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, c->stream));
-  k_from_tiles<<<nt, 256, 0, c->stream>>>(c->g, c->tl, c->t_off);
+  k_from_tiles<<<nt, 256, 0, c->stream>>>(c->g, c->tl, c->t_off, c->p.h_av);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
   c->staging_fresh = 1;
@@ -315,10 +329,14 @@ static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
   CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   memset(out, 0, sizeof(*out));
+  long long full = 0;
   for (const TileStats& s : ts) {
     out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters; out->iface_solves += s.iface_solves;
     out->creations += s.creations; out->splits += s.splits; out->merges += s.merges; out->regions += s.regions;
+    out->dts_iter_max = std::max(out->dts_iter_max, (int64_t)s.dts_max);
+    full += s.full_steps;
   }
+  c->tile_full_steps = full;
   out->steps = ctl[3];
   out->t_min = out->t_max = scal[0];
   out->dt_min = scal[2];
@@ -408,9 +426,21 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_rho); cudaFree(c->d_mom); cudaFree(c->d_h); cudaFree(c->d_t); cudaFree(c->d_n);
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
-  for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); }
+  for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
+  cudaFree(c->t_slow); cudaFree(c->t_part2);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   delete c;
+}
+
+extern "C" eis_status eis_tile_info(eis_ctx* c, int64_t* n_tiles, int64_t* full_tile_steps) {
+  if (!c || !n_tiles || !full_tile_steps) return EIS_E_ARG;
+  if (!c->tiled) return fail(c, EIS_E_ARG, "eis_tile_info: not a tiled context%s");
+  eis_stats st;
+  const eis_status s = tiled_stats(c, &st);
+  if (s) return s;
+  *n_tiles = c->tl.ntiles;
+  *full_tile_steps = c->tile_full_steps;
+  return EIS_OK;
 }
 
 extern "C" const char* eis_last_error(const eis_ctx* c) { return c ? c->msg : "null context"; }
@@ -483,11 +513,19 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
     out->steps += s.steps; out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters;
     out->iface_solves += s.iface_solves; out->creations += s.creations; out->splits += s.splits;
     out->merges += s.merges; out->regions += s.regions;
+    out->dts_iter_max = std::max(out->dts_iter_max, (int64_t)s.dts_max);
     out->t_min = std::fmin(out->t_min, t[m]); out->t_max = std::fmax(out->t_max, t[m]);
     if (s.steps) out->dt_min = std::fmin(out->dt_min, s.dt_min);
     out->dt_max = std::fmax(out->dt_max, s.dt_max);
   }
   return EIS_OK;
+}
+
+// one large step of the tiled grid: the streaming pass over every tile, then the full step of
+// the listed tiles (and, by its last CTA, the next dt)
+static void tiled_launch(eis_ctx* c, double t_end) {
+  tiled_fast<256, 4><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
 }
 
 static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats* out) {
@@ -499,7 +537,7 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   if (c->tiled) {
     c->staging_fresh = 0;
     for (long long s = 0; s < n_steps; ++s) {
-      tiled_step<256, 4><<<c->tl.ntiles, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+      tiled_launch(c, t_end);
       if ((s & 63) == 63 && t_end < INFINITY) {  // poll: stop launching once t_end is reached
         double tt;
         int ctl[4];
@@ -636,7 +674,7 @@ extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
     eis_stats& o = out[m];
     o.steps = s.steps; o.cell_updates = s.cell_updates; o.dts_iters = s.dts_iters; o.iface_solves = s.iface_solves;
     o.creations = s.creations; o.splits = s.splits; o.merges = s.merges; o.regions = s.regions;
-    o.t_min = o.t_max = t[m]; o.dt_min = s.dt_min; o.dt_max = s.dt_max;
+    o.t_min = o.t_max = t[m]; o.dt_min = s.dt_min; o.dt_max = s.dt_max; o.dts_iter_max = s.dts_max;
   }
   return EIS_OK;
 }
@@ -656,7 +694,7 @@ extern "C" eis_status eis_step_local(eis_ctx* c, double t_end) {
   if (!c->state_set) return fail(c, EIS_E_ORDER, "step before set_state%s");
   CU(cudaSetDevice(c->grid.device));
   c->staging_fresh = 0;
-  tiled_step<256, 4><<<c->tl.ntiles, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_launch(c, t_end);
   CU(cudaGetLastError());
   return EIS_OK;
 }

@@ -97,11 +97,22 @@ __device__ __forceinline__ void hll_p(double a, double rl, double ml, double ul,
 // HLL formula always evaluated, the upwind cases selected afterwards.
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+// Reciprocal for the bulk passes: the hardware seed (rcp.approx.ftz.f64, ~2^-23 relative)
+// and one cubic refinement r (1 + e + e^2), e = 1 - x r, relative error ~e^3 before rounding,
+// so within an ulp of the correctly rounded value; 4 instructions, deterministic.  Arguments
+// are positive normal numbers (densities, HLL speed spans) wherever the result is kept.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
 __device__ __forceinline__ void hll_fast(double a, double rl, double ml, double ul, double pl, double rr, double mr,
                                          double ur, double pr, double& F0, double& F1) {
   const double FL1 = ml * ul + pl, FR1 = mr * ur + pr;
   const double SL = dmin(ul, ur) - a, SR = dmax(ul, ur) + a;
-  const double inv = __drcp_rn(SR - SL), SLSR = SL * SR;
+  const double inv = rcp_fast(SR - SL), SLSR = SL * SR;
   double f0 = (SR * ml - SL * mr + SLSR * (rr - rl)) * inv;
   double f1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
   f0 = SL >= 0.0 ? ml : (SR <= 0.0 ? mr : f0);

@@ -62,6 +62,7 @@ struct Grp {            // remesh output replacing cells g0..g1 (merge group, or
 struct MemberStats {
   long long steps, cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
   double dt_min, dt_max;
+  long long dts_max;
 };
 
 struct Members {  // global (HBM) state, member-major SoA
@@ -86,8 +87,9 @@ struct CtaShared {
   int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
   int olo, ohi;  // tiles: owned output range after the remesh
+  int fbits;     // tiles: phase bits of the smem grid (fast-path test)
   int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
-  unsigned long long c_dts, c_solves, c_regions;
+  unsigned long long c_dts, c_solves, c_regions, c_dtsmax;
   MemberStats st;
 };
 
@@ -375,7 +377,7 @@ __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShar
     }
     const double rc = rho[cc], mc = mom[cc];
     const double rl = rho[cl], ml = mom[cl];
-    const double uc = mc * __drcp_rn(rc);
+    const double uc = mc * rcp_fast(rc);
     const bool vc = rc <= rho_tilde, lc = rc >= rho_min;  // phases
     const bool vl = rl <= rho_tilde, ll = rl >= rho_min;
     const double pcv = vc ? a_v2 * rc : p0 + a_l2 * (rc - rho0);
@@ -575,7 +577,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         const int err = dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
         if (err && lane == 0) set_status(sh, err);
         if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)
-          if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); }
+          if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); atomicMax(&sh.c_dtsmax, (unsigned long long)it); }
           if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
         }
       }
@@ -805,7 +807,7 @@ __device__ __forceinline__ Arr carve(unsigned char* smem_raw, int C) {
 __device__ __forceinline__ void reset_counters(CtaShared& sh) {
   sh.wsn = -1; sh.nblk = 0; sh.ntrg = 0; sh.remesh = 0;
   sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
-  sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0;
+  sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0; sh.c_dtsmax = 0;
   sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
 }
 
@@ -862,6 +864,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     st.dts_iters += (long long)sh.c_dts;
     st.iface_solves += (long long)sh.c_solves;
     st.regions += (long long)sh.c_regions;
+    if ((long long)sh.c_dtsmax > st.dts_max) st.dts_max = (long long)sh.c_dtsmax;
     g.n[m] = n;
     g.t[m] = t;
     g.status[m] = sh.status;

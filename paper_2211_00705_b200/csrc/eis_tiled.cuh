@@ -1,16 +1,20 @@
-// eis_tiled.cuh — the tiled streaming kernel for one huge grid (BASELINE configs[4], C5).
+// eis_tiled.cuh — the tiled streaming kernels for one huge grid (BASELINE configs[4], C5).
 //
 // The grid is cut into tiles of about TILE cells, each stored with slack (capt cells) so that
-// creations and splits insert locally.  One launch = one large step of the whole grid: every
-// CTA loads its tile plus H halo cells from each neighbour tile (ping-pong buffers: step n
-// reads buffer cur, writes 1-cur), runs the same step body as the member-resident kernel with
-// the global dt, and writes back the cells it owns after the remesh.  The halo is computed
-// redundantly by both neighbours with identical inputs and code, so every decision at a tile
-// boundary (boundary solves, creations, DTS blocks, merges) is taken identically on both sides;
-// ownership rules: a created cell at a tile boundary and a merge group headed left of it belong
-// to the left tile.  The CTA also reduces S_max / h_min of its new cells; the last CTA to finish
-// folds all tiles into the next step's dt (CFL, R5/R6), so a step costs one launch and one
-// read + one write of the state (24 B + 24 B per cell).
+// creations and splits insert locally; ping-pong buffers (step n reads buffer cur, writes
+// 1-cur).  A step is two launches:
+//   tiled_fast (one CTA per tile, no shared-memory staging, high occupancy): streams the tile
+//     plus HALO cells of each neighbour through registers in warp windows and, when the tile is
+//     plain (one phase over tile + halos, no creation candidate), completes its step: HLL
+//     fluxes (a3), update (a7), the next step's CFL partials (a2).  Otherwise it appends the
+//     tile to the work list.  Widths are not stored for tiles whose widths are all h_av.
+//   tiled_slow (persistent CTAs, dynamic work list): runs the member-resident step body (the
+//     whole method, a1-a11) on each listed tile held in shared memory, then the last CTA folds
+//     the CFL partials into the next dt (R5/R6).
+// The halo is computed redundantly by both neighbours with identical inputs and code, so every
+// decision at a tile boundary (boundary solves, creations, DTS blocks, merges) is taken
+// identically on both sides; ownership: a created cell at a tile boundary and a merge group
+// headed left of it belong to the left tile.
 #pragma once
 #include "eis_resident.cuh"
 
@@ -20,19 +24,24 @@ constexpr int HALO = 10;  // halo cells per side: >= MAXB + 2 keeps every needed
 
 struct TileStats {
   long long cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
+  long long dts_max, full_steps;  // full_steps: steps this tile took the full (not the fast) path
 };
 
 struct Tiles {
   double *rho[2], *mom[2], *h[2];  // ntiles x capt, ping-pong
   int* cnt[2];                     // live cells per tile
+  int* hu[2];                      // per tile: 1 = every width is h_av (widths not stored)
   double* ws;                      // per tile: ws0[MAXIF], ws1[MAXIF], wsn  (2*MAXIF + 1 doubles)
   double* part;                    // per tile: S_max, h_min of the tile's new cells
   TileStats* tstats;
   double* scal;                    // [0] t  [1] dt of the next step  [2] dt_min  [3] dt_max
   int* ctl;                        // [0] cur  [1] status  [2] done-counter  [3] steps
   double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
+  int* slow;                       // work list of tiles needing the full step (this step)
+  double* part2;                   // per tiled_slow CTA: S_max, h_min
   int ntiles, capt, nbr_left, nbr_right;
 };
+// ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] work-list length  [5] next job
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -51,7 +60,7 @@ __device__ __forceinline__ void cfl_partials(const Eos& e, const Prm& p, const d
   for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
     const double r = rho[i];
     const int ph = phase_of(e, r);
-    s = fmax(s, fabs(mom[i] / r) + sound(e, ph));
+    s = fmax(s, fabs(mom[i] * rcp_fast(r)) + sound(e, ph));  // u as in bulk_p1 / tiled_fast
     bool tiny = false;
     if (p.mode == 0 && h[i] < p.eps_tiny * p.h_av) {
       const bool same_l = (i > 0) ? phase_of(e, rho[i - 1]) == ph : false;
@@ -65,14 +74,14 @@ __device__ __forceinline__ void cfl_partials(const Eos& e, const Prm& p, const d
   h_out = warp_min(hm);
 }
 
-// Last CTA of a step: fold the per-tile partials into the next dt, advance t.
-__device__ void tiles_finish_step(const Prm& p, const Tiles& tl, double dt_used, double t_end) {
+// Last CTA of a step: fold the per-CTA partials into the next dt, advance t.
+__device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, double dt_used, double t_end) {
   __shared__ double rs[32], rh[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double s = 0.0, hm = INFINITY;
-  for (int k = tid; k < tl.ntiles; k += blockDim.x) {
-    s = fmax(s, tl.part[2 * k]);
-    hm = fmin(hm, tl.part[2 * k + 1]);
+  for (int k = tid; k < nparts; k += blockDim.x) {
+    s = fmax(s, tl.part2[2 * k]);
+    hm = fmin(hm, tl.part2[2 * k + 1]);
   }
   s = warp_max(s);
   hm = warp_min(hm);
@@ -80,6 +89,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, double dt_used,
   __syncthreads();
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
     if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
       tl.xbuf[XB_DT] = -s;
       tl.xbuf[XB_DT + 1] = hm;
@@ -96,30 +106,187 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, double dt_used,
     if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
     tl.ctl[0] = 1 - tl.ctl[0];
     tl.ctl[3] += 1;
-    tl.ctl[2] = 0;
     __threadfence();
+  }
+}
+
+// Geometry of tile k in the step reading buffer `in`: own cells and up to HALO halo cells per
+// side (from the neighbour tiles, or from the exchange buffer at a rank boundary), seen as one
+// virtual array [0, n) = left halo | own | right halo.
+struct TGeo {
+  long long base, bl, br;
+  int k, in, out, cnt, cl, nL, nR, n;
+  bool xl, xr, hu_in;
+};
+__device__ __forceinline__ TGeo tile_geo(const Tiles& tl, int k, int cur) {
+  TGeo g;
+  g.k = k; g.in = cur; g.out = 1 - cur;
+  g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
+  g.cnt = tl.cnt[cur][k];
+  g.hu_in = tl.hu[cur][k] != 0;
+  g.xl = (k == 0 && tl.nbr_left); g.xr = (k == tl.ntiles - 1 && tl.nbr_right);
+  g.cl = k > 0 ? tl.cnt[cur][k - 1] : 0;
+  g.nL = k > 0 ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
+  g.nR = k < tl.ntiles - 1 ? min(HALO, tl.cnt[cur][k + 1]) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
+  g.n = g.nL + g.cnt + g.nR;
+  return g;
+}
+// address of virtual cell i's density (the momentum is at +mo, in the same array family)
+__device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, int i, long long& mo) {
+  if (i < g.nL) {
+    if (g.xl) { mo = HALO; return tl.xbuf + XB_RECV_LEFT + HALO - g.nL + i; }
+    mo = tl.mom[g.in] - tl.rho[g.in];
+    return tl.rho[g.in] + g.bl + g.cl - g.nL + i;
+  }
+  if (i >= g.nL + g.cnt && g.xr) { mo = HALO; return tl.xbuf + XB_RECV_RIGHT + (i - g.nL - g.cnt); }
+  mo = tl.mom[g.in] - tl.rho[g.in];
+  return tl.rho[g.in] + (i < g.nL + g.cnt ? g.base + (i - g.nL) : g.br + (i - g.nL - g.cnt));
+}
+
+// ------------------------------------------------------------------------------------------
+// tiled_fast: one CTA per tile.  Warp windows of 32 lanes over virtual cells s-1 .. s+30 (lane
+// 0 is the left neighbour; ghosts clamp at the grid ends, R15): u = m/rho and p (a1), the HLL
+// flux of edge s-1+lane on lanes 1..31 (a3), the creation pre-filter (a4, R7), the right flux
+// by shuffle and the update of cells s .. s+29 (a7) written to the output tile with the
+// next step's CFL partials (a2) -- the same expressions as step_body's bulk passes, so a plain
+// tile's result is the full step's bit for bit.  Windows are loaded in batches of FB (all
+// loads in flight before the arithmetic).  Outputs of a tile that turns out not plain are
+// overwritten by tiled_slow.
+// ------------------------------------------------------------------------------------------
+constexpr int FB = 4;
+
+template <int MAXT, int MINB, bool HU>
+__device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
+  __shared__ double ps[32], ph[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int k = g.k, n = g.n, own_lo = g.nL, own_hi = g.nL + g.cnt;
+  const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
+  const double a_v = e.a_v, a_l = e.a_l, rmin2 = rho_min * rho_min, inv_rt = 1.0 / rho_tilde;
+  const double h_av = p.h_av, dt_hav = dt / h_av;
+  // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
+  const double* const rin = tl.rho[g.in];
+  const long long mo_t = tl.mom[g.in] - rin;
+  const double* const segL = g.xl ? tl.xbuf + XB_RECV_LEFT + HALO - g.nL : rin + g.bl + g.cl - g.nL;
+  const long long moL = g.xl ? HALO : mo_t;
+  const double* const segO = rin + g.base - g.nL;
+  const double* const segR = g.xr ? tl.xbuf + XB_RECV_RIGHT - own_hi : rin + g.br - own_hi;
+  const long long moR = g.xr ? HALO : mo_t;
+  double* const orho = tl.rho[g.out] + g.base - own_lo;  // indexed by the virtual cell
+  double* const omom = tl.mom[g.out] + g.base - own_lo;
+  double* const oh = tl.h[g.out] + g.base - own_lo;
+  const double* const ih = tl.h[g.in] + g.base - own_lo;
+  int bits = 0;          // 1 vapour, 2 liquid, 4 spinodal / non-positive
+  bool cand = false;     // a creation candidate (R7 pre-filter) at some edge
+  bool unif = true;      // output widths all h_av
+  double snum = 0.0, sden = 1.0;  // max |m|/rho of the new cells, by cross-multiplication
+  double h_part = HU ? h_av : INFINITY;
+  const int nwin = (n + 29) / 30;
+  for (int w0 = warp; w0 < nwin; w0 += nw * FB) {
+    double rr[FB], mm[FB];
+#pragma unroll
+    for (int b = 0; b < FB; ++b) {  // all loads of the batch first
+      const int c = 30 * (w0 + nw * b) - 1 + lane;
+      const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
+      const double* pr = cc < own_lo ? segL : (cc < own_hi ? segO : segR);
+      const long long mo = cc < own_lo ? moL : (cc < own_hi ? mo_t : moR);
+      rr[b] = 1.0; mm[b] = 0.0;
+      if (w0 + nw * b < nwin) { rr[b] = pr[cc]; mm[b] = pr[cc + mo]; }
+    }
+#pragma unroll
+    for (int b = 0; b < FB; ++b) {
+      if (w0 + nw * b >= nwin) break;  // warp-uniform
+      const int c = 30 * (w0 + nw * b) - 1 + lane;
+      const double rc = rr[b], mc = mm[b];
+      const double uc = mc * rcp_fast(rc);
+      const bool vc = rc <= rho_tilde, lc = rc >= rho_min;
+      const double pc = vc ? a_v2 * rc : p0 + a_l2 * (rc - rho0);
+      const double a = vc ? a_v : a_l;
+      // lanes beyond the grid hold clamped copies of real cells: the bits are those of [0, n)
+      bits |= (vc ? 1 : (lc ? 2 : 4)) | (rc > 0.0 ? 0 : 4);
+      const double rl = __shfl_up_sync(0xffffffffu, rc, 1), ml = __shfl_up_sync(0xffffffffu, mc, 1);
+      const double ul = __shfl_up_sync(0xffffffffu, uc, 1), pl = __shfl_up_sync(0xffffffffu, pc, 1);
+      double f0, f1;  // edge c (between c-1 and c)
+      hll_fast(a, rl, ml, ul, pl, rc, mc, uc, pc, f0, f1);
+      {  // creation pre-filters (R7) as bulk_p1; at ghost / duplicate edges du = 0: no candidate
+        const double du = uc - ul, x = rl * rc;
+        cand |= lc ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
+      }
+      const double g0 = __shfl_down_sync(0xffffffffu, f0, 1), g1 = __shfl_down_sync(0xffffffffu, f1, 1);
+      if (lane >= 1 && lane <= 30 && c >= own_lo && c < own_hi) {  // P2, h^{n+1} = h^n
+        double cfac = dt_hav, hn = h_av;
+        if (!HU) { hn = ih[c]; if (hn != h_av) cfac = dt / hn; }
+        const double r1 = rc - cfac * (g0 - f0);
+        const double m1 = mc - cfac * (g1 - f1);
+        orho[c] = r1;
+        omom[c] = m1;
+        if (!HU) { oh[c] = hn; unif &= hn == h_av; h_part = fmin(h_part, hn); }
+        const double am = fabs(m1);
+        if (am * sden > snum * r1) { snum = am; sden = r1; }
+      }
+    }
+  }
+  // S_max of this lane's new cells: |m| rcp(rho) + a, as cfl_partials (one phase: a uniform)
+  const double sl = snum * rcp_fast(sden);
+  const double s_lane = warp_max(sl);
+  const double h_lane = HU ? h_av : warp_min(h_part);
+  if (lane == 0) { ps[warp] = s_lane; ph[warp] = h_lane; }
+  const int any_v = __syncthreads_or(bits & 1), any_l = __syncthreads_or(bits & 2);
+  const int any_bad = __syncthreads_or((bits & 4) || cand);
+  if (!HU) unif = __syncthreads_and(unif);
+  const bool fast = !any_bad && !(any_v && any_l);
+  if (fast && (g.xl || g.xr)) {  // rank mode: send records of the first / last HALO owned cells
+    for (int q = tid; q < 2 * HALO; q += blockDim.x) {
+      const bool left = q < HALO;
+      if (left ? !g.xl : !g.xr) continue;
+      const int c = left ? own_lo + q : own_hi - 2 * HALO + q;
+      double* sb = tl.xbuf + (left ? XB_SEND_LEFT : XB_SEND_RIGHT) + (left ? q : q - HALO);
+      sb[0] = orho[c]; sb[HALO] = omom[c]; sb[2 * HALO] = HU ? h_av : oh[c];
+    }
+  }
+  if (tid == 0) {
+    if (fast) {
+      double s = 0.0, hm = INFINITY;
+      for (int w = 0; w < nw; ++w) { s = fmax(s, ps[w]); hm = fmin(hm, ph[w]); }
+      tl.part[2 * k] = s + (any_v ? a_v : a_l);
+      tl.part[2 * k + 1] = hm;
+      tl.cnt[g.out][k] = g.cnt;
+      tl.hu[g.out][k] = unif ? 1 : 0;
+      tl.ws[(size_t)k * WS_STRIDE + 2 * MAXIF] = 0.0;  // no boundary: no warm start
+      tl.tstats[k].cell_updates += g.cnt;
+      if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
+      if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
+    } else {
+      tl.part[2 * k] = 0.0;  // neutral: tiled_slow folds this tile's own partials
+      tl.part[2 * k + 1] = INFINITY;
+      tl.slow[atomicAdd(&tl.ctl[4], 1)] = k;
+    }
   }
 }
 
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
-tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
+tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
-  const int capg = tl.capt + 2 * HALO + MAXEV;
-  Arr A = carve(smem_raw, capg);
-  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const int k = blockIdx.x;
-  const int cur = tl.ctl[0];
-  const double t = tl.scal[0], dt_given = tl.scal[1];
+  const double t = tl.scal[0];
   if (tl.ctl[1] != 0 || !(t < t_end)) return;  // uniform across the grid: nothing to do
-  const int in = cur, out = 1 - cur;
-  const long long base = (long long)k * tl.capt;
-  const int cnt = tl.cnt[in][k];
-  const bool xl = (k == 0 && tl.nbr_left), xr = (k == tl.ntiles - 1 && tl.nbr_right);  // halo from a rank
-  const int nL = k > 0 ? min(HALO, tl.cnt[in][k - 1]) : (xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
-  const int nR = k < tl.ntiles - 1 ? min(HALO, tl.cnt[in][k + 1]) : (xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
+  double dt = tl.scal[1];
+  if (t + dt > t_end) dt = t_end - t;  // as step_body
+  const TGeo g = tile_geo(tl, blockIdx.x, tl.ctl[0]);
+  if (g.hu_in) tiled_fast_body<MAXT, MINB, true>(e, p, tl, g, dt);
+  else tiled_fast_body<MAXT, MINB, false>(e, p, tl, g, dt);
+}
+
+// ------------------------------------------------------------------------------------------
+// The full step of tile k (shared memory): load tile + halos, step_body, owned output after
+// the remesh, CFL partials, warm-start table, stats.  Returns (via s_out/h_out on thread 0)
+// the tile's partials; a status is raised on tl.ctl[1].
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capg,
+                                          int k, double t, double t_end, double dt_given, double& s_out,
+                                          double& h_out) {
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const TGeo g = tile_geo(tl, k, tl.ctl[0]);
+  const int n = g.n, nL = g.nL, cnt = g.cnt;
   if (tid == 0) {
     sh.status = 0;
     reset_counters(sh);
@@ -128,33 +295,19 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
-  const int n = nL + cnt + nR;
-  {  // load: left halo | own | right halo (coalesced)
-    const long long bl = base - tl.capt, br = base + tl.capt;
-    const int cl = k > 0 ? tl.cnt[in][k - 1] : 0;
-    for (int i = tid; i < n; i += T) {
-      if (xl && i < nL) {  // left halo received from the left rank (its last cells)
-        const double* rb = tl.xbuf + XB_RECV_LEFT;
-        const int j = HALO - nL + i;
-        A.rho[i] = rb[j]; A.mom[i] = rb[HALO + j]; A.h[i] = rb[2 * HALO + j];
-        continue;
-      }
-      if (xr && i >= nL + cnt) {  // right halo received from the right rank (its first cells)
-        const double* rb = tl.xbuf + XB_RECV_RIGHT;
-        const int j = i - nL - cnt;
-        A.rho[i] = rb[j]; A.mom[i] = rb[HALO + j]; A.h[i] = rb[2 * HALO + j];
-        continue;
-      }
-      long long g;
-      if (i < nL) g = bl + (cl - nL + i);
-      else if (i < nL + cnt) g = base + (i - nL);
-      else g = br + (i - nL - cnt);
-      A.rho[i] = tl.rho[in][g];
-      A.mom[i] = tl.mom[in][g];
-      A.h[i] = tl.h[in][g];
-    }
-    for (int i = tid; i <= capg; i += T) A.fl[i] = 0;
+  const int huL = k > 0 ? tl.hu[g.in][k - 1] : 0, huR = k < tl.ntiles - 1 ? tl.hu[g.in][k + 1] : 0;
+  for (int i = tid; i < n; i += T) {
+    long long mo;
+    const double* pr = vcell(tl, g, i, mo);
+    A.rho[i] = pr[0];
+    A.mom[i] = pr[mo];
+    double hh;
+    if (i < nL) hh = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + i]);
+    else if (i < nL + cnt) hh = g.hu_in ? p.h_av : tl.h[g.in][g.base + i - nL];
+    else hh = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + i - nL - cnt]);
+    A.h[i] = hh;
   }
+  for (int i = tid; i <= capg; i += T) A.fl[i] = 0;
   A.n = n;
   __syncthreads();
   if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, n);
@@ -165,25 +318,28 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   Z.dt_given = dt_given;
   Z.left_real = (k == 0 && !tl.nbr_left); Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
-  // ---------------- owned output, partials of the next dt, side tables ----------------
   __syncthreads();
   const int olo = sh.olo, ohi = sh.ohi;
   const int nout = ohi - olo;
   int st = sh.status;
   if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.ntiles > 1 ? HALO : 3))) st = ST_CAPACITY;
+  bool unif = true;
   if (dt >= 0.0 && st == 0) {
-    const long long ob = base;
+    bool u = true;  // widths all h_av?  then they are not stored
+    for (int i = olo + tid; i < ohi; i += T) u &= A.h[i] == p.h_av;
+    unif = __syncthreads_and(u);
+    const long long ob = g.base;
     for (int i = tid; i < nout; i += T) {
-      tl.rho[out][ob + i] = A.rho[olo + i];
-      tl.mom[out][ob + i] = A.mom[olo + i];
-      tl.h[out][ob + i] = A.h[olo + i];
+      tl.rho[g.out][ob + i] = A.rho[olo + i];
+      tl.mom[g.out][ob + i] = A.mom[olo + i];
+      if (!unif) tl.h[g.out][ob + i] = A.h[olo + i];
     }
-    if (xl) {  // my first HALO owned cells go to the left rank (its right halo)
+    if (g.xl) {  // my first HALO owned cells go to the left rank (its right halo)
       double* sb = tl.xbuf + XB_SEND_LEFT;
       for (int i = tid; i < HALO; i += T) { sb[i] = A.rho[olo + i]; sb[HALO + i] = A.mom[olo + i]; sb[2 * HALO + i] = A.h[olo + i]; }
       if (tid == 0) sb[3 * HALO] = HALO;
     }
-    if (xr) {  // my last HALO owned cells go to the right rank (its left halo)
+    if (g.xr) {  // my last HALO owned cells go to the right rank (its left halo)
       double* sb = tl.xbuf + XB_SEND_RIGHT;
       for (int i = tid; i < HALO; i += T) {
         const int j = ohi - HALO + i;
@@ -192,18 +348,19 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
       if (tid == 0) sb[3 * HALO] = HALO;
     }
     double s, hm;
-    cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, Z.left_real, Z.right_real, s, hm);
+    cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, false, false, s, hm);
     if (lane == 0) { sh.part_s[warp] = s; sh.part_h[warp] = hm; }
   }
   __syncthreads();
   if (tid == 0) {
+    s_out = 0.0; h_out = INFINITY;
     if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
     if (dt >= 0.0 && st == 0) {
-      double s = 0.0, hm = INFINITY;
-      for (int w = 0; w < nw; ++w) { s = fmax(s, sh.part_s[w]); hm = fmin(hm, sh.part_h[w]); }
-      tl.part[2 * k] = s;
-      tl.part[2 * k + 1] = hm;
-      tl.cnt[out][k] = nout;
+      for (int w = 0; w < nw; ++w) { s_out = fmax(s_out, sh.part_s[w]); h_out = fmin(h_out, sh.part_h[w]); }
+      tl.part[2 * k] = s_out;
+      tl.part[2 * k + 1] = h_out;
+      tl.cnt[g.out][k] = nout;
+      tl.hu[g.out][k] = unif ? 1 : 0;
       double* ws = tl.ws + (size_t)k * WS_STRIDE;
       for (int q = 0; q < MAXIF; ++q) { ws[q] = sh.ws0[q]; ws[MAXIF + q] = sh.ws1[q]; }
       ws[2 * MAXIF] = (double)sh.wsn;
@@ -212,18 +369,69 @@ tiled_step(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
       ts.dts_iters += (long long)sh.c_dts;
       ts.iface_solves += (long long)sh.c_solves;
       ts.regions += (long long)sh.c_regions;
+      if ((long long)sh.c_dtsmax > ts.dts_max) ts.dts_max = (long long)sh.c_dtsmax;
+      ts.full_steps += 1;
       ts.creations += sh.st.creations;  // owned events only (step_body)
       ts.splits += sh.st.splits;
       ts.merges += sh.st.merges;
     }
-    __threadfence();
-    sh.remesh = atomicAdd(&tl.ctl[2], 1) == tl.ntiles - 1;  // reuse as "I am the last CTA"
   }
   __syncthreads();
-  if (sh.remesh) {
+}
+
+// ------------------------------------------------------------------------------------------
+// tiled_slow: persistent CTAs take listed tiles one at a time (dynamic: DTS-heavy tiles vary a
+// lot), fold the fast tiles' partials in strides, and the last CTA finishes the step.
+// ------------------------------------------------------------------------------------------
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
+           double t_end) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
+  const int capg = tl.capt + 2 * HALO + MAXEV + 1;  // even array stride (16-byte aligned rows)
+  Arr A = carve(smem_raw, capg);
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const double t = tl.scal[0], dt_given = tl.scal[1];
+  if (tl.ctl[1] != 0 || !(t < t_end)) return;  // uniform across the grid: nothing to do
+  double dt = dt_given;
+  if (t + dt > t_end) dt = t_end - t;
+  // fast tiles' partials (slow tiles hold neutral values here)
+  double s = 0.0, hm = INFINITY;
+  for (int q = blockIdx.x * T + tid; q < tl.ntiles; q += gridDim.x * T) {
+    s = fmax(s, tl.part[2 * q]);
+    hm = fmin(hm, tl.part[2 * q + 1]);
+  }
+  s = warp_max(s);
+  hm = warp_min(hm);
+  if (lane == 0) { sh.part_s[warp] = s; sh.part_h[warp] = hm; }
+  __syncthreads();
+  double cta_s = 0.0, cta_h = INFINITY;  // thread 0
+  if (tid == 0)
+    for (int w = 0; w < nw; ++w) { cta_s = fmax(cta_s, sh.part_s[w]); cta_h = fmin(cta_h, sh.part_h[w]); }
+  const int njobs = tl.ctl[4];
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) sh.n_new = atomicAdd(&tl.ctl[5], 1);
+    __syncthreads();
+    const int j = sh.n_new;
+    if (j >= njobs) break;
+    double sk = 0.0, hk = INFINITY;
+    tile_full(e, p, tl, sh, A, capg, tl.slow[j], t, t_end, dt_given, sk, hk);
+    if (tid == 0) { cta_s = fmax(cta_s, sk); cta_h = fmin(cta_h, hk); }
+  }
+  __shared__ int last;
+  if (tid == 0) {
+    tl.part2[2 * blockIdx.x] = cta_s;
+    tl.part2[2 * blockIdx.x + 1] = cta_h;
     __threadfence();
-    if (tl.ctl[1] == 0) tiles_finish_step(p, tl, dt, t_end);
-    else if (tid == 0) tl.ctl[2] = 0;
+    last = atomicAdd(&tl.ctl[2], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (tl.ctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
+    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; }
   }
 }
 
@@ -243,15 +451,16 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     const long long g = base + i;
     const double r = tl.rho[cur][g];
     const int ph = phase_of(e, r);
-    s = fmax(s, fabs(tl.mom[cur][g] / r) + sound(e, ph));
+    s = fmax(s, fabs(tl.mom[cur][g] * rcp_fast(r)) + sound(e, ph));
     bool tiny = false;
-    if (p.mode == 0 && tl.h[cur][g] < p.eps_tiny * p.h_av) {  // neighbours may live in the next tiles
+    const double hg = tl.hu[cur][k] ? p.h_av : tl.h[cur][g];
+    if (p.mode == 0 && hg < p.eps_tiny * p.h_av) {  // neighbours may live in the next tiles
       const double rl = i > 0 ? tl.rho[cur][g - 1] : (k > 0 ? tl.rho[cur][base - tl.capt + tl.cnt[cur][k - 1] - 1] : -1.0);
       const double rr = i < cnt - 1 ? tl.rho[cur][g + 1] : (k < tl.ntiles - 1 ? tl.rho[cur][base + tl.capt] : -1.0);
       const bool same_l = rl > 0.0 && phase_of(e, rl) == ph, same_r = rr > 0.0 && phase_of(e, rr) == ph;
       tiny = !same_l && !same_r;
     }
-    if (!tiny) hm = fmin(hm, tl.h[cur][g]);
+    if (!tiny) hm = fmin(hm, hg);
   }
   s = warp_max(s);
   hm = warp_min(hm);
@@ -292,7 +501,8 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     if (k == 0 && tl.nbr_left) {
       double* sb = tl.xbuf + XB_SEND_LEFT;
       for (int i = tid; i < HALO; i += blockDim.x) {
-        sb[i] = tl.rho[cur2][base + i]; sb[HALO + i] = tl.mom[cur2][base + i]; sb[2 * HALO + i] = tl.h[cur2][base + i];
+        sb[i] = tl.rho[cur2][base + i]; sb[HALO + i] = tl.mom[cur2][base + i];
+        sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][base + i];
       }
       if (tid == 0) sb[3 * HALO] = HALO;
     }
@@ -300,7 +510,7 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
       double* sb = tl.xbuf + XB_SEND_RIGHT;
       for (int i = tid; i < HALO; i += blockDim.x) {
         const long long j = base + cnt - HALO + i;
-        sb[i] = tl.rho[cur2][j]; sb[HALO + i] = tl.mom[cur2][j]; sb[2 * HALO + i] = tl.h[cur2][j];
+        sb[i] = tl.rho[cur2][j]; sb[HALO + i] = tl.mom[cur2][j]; sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][j];
       }
       if (tid == 0) sb[3 * HALO] = HALO;
     }
@@ -321,8 +531,8 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
     if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
     tl.ctl[0] = 1 - tl.ctl[0];
     tl.ctl[3] += 1;
-    tl.ctl[2] = 0;
   }
+  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
   double dt = p.cfl * hm / S;
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;
