@@ -100,7 +100,7 @@ typedef struct {
   int32_t layout;         /* EIS_LAYOUT_AUTO | _RESIDENT (grid in shared memory across steps,
                              ensembles, cell_capacity <= 16384) | _TILED (one huge grid, streamed
                              through HBM in halo-overlapped tiles each step, n_members == 1)   */
-  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 960); tiles are fixed-size from
+  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 940); tiles are fixed-size from
                              the left, the last one takes the remainder                      */
   int32_t nbr_left;       /* tiled rank mode: 1 if this grid is the right part of a grid cut
                              over ranks (its left halo arrives through the exchange buffer)  */

@@ -43,9 +43,10 @@ struct eis_ctx {
   int tiled, tile_cells;
   Tiles tl;
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
-  int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow;
+  int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow, *t_wlist;
   double* t_part2;
-  int slow_grid;
+  int slow_grid, win_grid;
+  size_t smem_win;
   TileStats* t_stats;
   long long* t_off;
   int staging_fresh;
@@ -240,7 +241,7 @@ static unsigned grid_for(long long count) {
 static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   const eis_grid* grid = &c->grid;
   const long long cap = grid->cell_capacity;
-  c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 960;
+  c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 940;
   if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
   const int capt = c->tile_cells + 32 + (c->tile_cells & 1);  // even: 16-byte aligned tile rows
   long long ntiles = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;
@@ -258,10 +259,16 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (cudaFuncSetAttribute(tiled_slow<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
-  int nsm = 0, per_sm = 0;
+  c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
+  if (cudaFuncSetAttribute(tiled_win<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+    delete c; return EIS_E_CUDA;
+  }
+  int nsm = 0, per_sm = 0, per_sm_w = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<128, 8>, 128, c->smem_win);
   c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
+  c->win_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm_w, 1));
   const size_t tc = (size_t)ntiles * capt;
   bool ok = cudaMalloc(&c->d_rho, cap * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cap * 8) == cudaSuccess &&
             cudaMalloc(&c->d_h, cap * 8) == cudaSuccess && cudaMalloc(&c->d_t, 8) == cudaSuccess &&
@@ -276,6 +283,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
        cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 8 * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_wlist, (size_t)ntiles * 12) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
@@ -283,7 +291,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
   Tiles& tl = c->tl;
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
-  tl.slow = c->t_slow; tl.part2 = c->t_part2;
+  tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
   tl.ntiles = (int)ntiles; tl.capt = capt;
   tl.xbuf = nullptr;
@@ -294,6 +302,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
   tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
+  tl.ctl[6] = 0; tl.ctl[7] = 0;
   tl.scal[0] = t0; tl.scal[1] = 0.0; tl.scal[2] = 0.0; tl.scal[3] = 0.0;
 }
 
@@ -427,7 +436,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
-  cudaFree(c->t_slow); cudaFree(c->t_part2);
+  cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   delete c;
 }
@@ -524,7 +533,8 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
 // one large step of the tiled grid: the streaming pass over every tile, then the full step of
 // the listed tiles (and, by its last CTA, the next dt)
 static void tiled_launch(eis_ctx* c, double t_end) {
-  tiled_fast<256, 4><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_win<128, 8><<<c->win_grid, 128, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
 }
 

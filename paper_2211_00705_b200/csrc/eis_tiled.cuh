@@ -37,11 +37,13 @@ struct Tiles {
   double* scal;                    // [0] t  [1] dt of the next step  [2] dt_min  [3] dt_max
   int* ctl;                        // [0] cur  [1] status  [2] done-counter  [3] steps
   double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
-  int* slow;                       // work list of tiles needing the full step (this step)
+  int* slow;                       // work list of tiles needing the full step of the whole tile
+  int* wlist;                      // work list of (tile, window begin, window end): full step of a window
   double* part2;                   // per tiled_slow CTA: S_max, h_min
   int ntiles, capt, nbr_left, nbr_right;
 };
-// ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] work-list length  [5] next job
+// ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] tile-list length  [5] next tile job
+//      [6] window-list length  [7] next window job
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -89,7 +91,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
   __syncthreads();
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0;
     if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
       tl.xbuf[XB_DT] = -s;
       tl.xbuf[XB_DT + 1] = hm;
@@ -131,6 +133,26 @@ __device__ __forceinline__ TGeo tile_geo(const Tiles& tl, int k, int cur) {
   g.n = g.nL + g.cnt + g.nR;
   return g;
 }
+// the same, with the tile metadata of both buffers loaded before `cur` is known (one
+// dependent global round trip fewer at the start of every tile)
+__device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
+  const bool hasl = k > 0, hasr = k < tl.ntiles - 1;
+  const int c0 = tl.cnt[0][k], c1 = tl.cnt[1][k], h0 = tl.hu[0][k], h1 = tl.hu[1][k];
+  const int l0 = hasl ? tl.cnt[0][k - 1] : 0, l1 = hasl ? tl.cnt[1][k - 1] : 0;
+  const int r0 = hasr ? tl.cnt[0][k + 1] : 0, r1 = hasr ? tl.cnt[1][k + 1] : 0;
+  const int cur = tl.ctl[0];
+  TGeo g;
+  g.k = k; g.in = cur; g.out = 1 - cur;
+  g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
+  g.cnt = cur ? c1 : c0;
+  g.hu_in = (cur ? h1 : h0) != 0;
+  g.xl = (k == 0 && tl.nbr_left); g.xr = (k == tl.ntiles - 1 && tl.nbr_right);
+  g.cl = cur ? l1 : l0;
+  g.nL = hasl ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
+  g.nR = hasr ? min(HALO, cur ? r1 : r0) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
+  g.n = g.nL + g.cnt + g.nR;
+  return g;
+}
 // address of virtual cell i's density (the momentum is at +mo, in the same array family)
 __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, int i, long long& mo) {
   if (i < g.nL) {
@@ -153,16 +175,69 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 // loads in flight before the arithmetic).  Outputs of a tile that turns out not plain are
 // overwritten by tiled_slow.
 // ------------------------------------------------------------------------------------------
-constexpr int FB = 4;
+constexpr int FB = 4;  // windows per warp per batch (tile 940 + 2 x 10 halo = 32 windows = 8 warps x 4)
 
-template <int MAXT, int MINB, bool HU>
+// one window batch of one warp after its loads: the arithmetic, specialised by the phase the
+// warp's first cell has (LIQ) and by uniform widths (HU).  A cell of another phase (or spinodal,
+// or non-positive) and the right cell of a creation-candidate edge are "special": their index
+// range [slo, shi] decides between the fast result and a full step of a window around them.
+template <bool HU, bool LIQ>
+__device__ __forceinline__ void fast_windows(const Eos& e, const double (&rr)[FB], const double (&mm)[FB], int w0, int nw,
+                                             int nwin, int n, int own_lo, int own_hi, double dt, double dt_hav,
+                                             double h_av, const double* ih, double* orho, double* omom, double* oh,
+                                             int& slo, int& shi, bool& unif, double& snum, double& sden,
+                                             double& h_part) {
+  const int lane = threadIdx.x & 31;
+  const double a = LIQ ? e.a_l : e.a_v;
+  const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
+  const double rmin2 = rho_min * rho_min, inv_rt = 1.0 / rho_tilde;
+#pragma unroll
+  for (int b = 0; b < FB; ++b) {
+    if (w0 + nw * b >= nwin) break;  // warp-uniform
+    const int c = 30 * (w0 + nw * b) - 1 + lane;
+    const double rc = rr[b], mc = mm[b];
+    const double uc = mc * rcp_fast(rc);
+    // lanes beyond the grid hold clamped copies of real cells: every cell of [0, n) is checked
+    bool sp = LIQ ? !(rc >= rho_min) : !(rc <= rho_tilde && rc > 0.0);
+    const double pc = LIQ ? p0 + a_l2 * (rc - rho0) : a_v2 * rc;
+    const double rl = __shfl_up_sync(0xffffffffu, rc, 1), ml = __shfl_up_sync(0xffffffffu, mc, 1);
+    const double ul = __shfl_up_sync(0xffffffffu, uc, 1), pl = __shfl_up_sync(0xffffffffu, pc, 1);
+    double f0, f1;  // edge c (between c-1 and c)
+    hll_fast(a, rl, ml, ul, pl, rc, mc, uc, pc, f0, f1);
+    {  // creation pre-filters (R7) as bulk_p1; at ghost / duplicate edges du = 0: no candidate
+      const double du = uc - ul, x = rl * rc;
+      sp |= LIQ ? !(du * x <= e.a_l * (x - rmin2) - 1e-9 * x) : (du < -e.a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
+    }
+    if (sp) {
+      const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
+      slo = min(slo, cc);
+      shi = max(shi, cc);
+    }
+    const double g0 = __shfl_down_sync(0xffffffffu, f0, 1), g1 = __shfl_down_sync(0xffffffffu, f1, 1);
+    if (lane >= 1 && lane <= 30 && c >= own_lo && c < own_hi) {  // P2, h^{n+1} = h^n
+      double cfac = dt_hav, hn = h_av;
+      if (!HU) { hn = ih[c]; if (hn != h_av) cfac = dt / hn; }
+      const double r1 = rc - cfac * (g0 - f0);
+      const double m1 = mc - cfac * (g1 - f1);
+      orho[c] = r1;
+      omom[c] = m1;
+      if (!HU) { oh[c] = hn; unif &= hn == h_av; h_part = fmin(h_part, hn); }
+      const double am = fabs(m1);
+      if (am * sden > snum * r1) { snum = am; sden = r1; }
+    }
+  }
+}
+
+constexpr int WMAX = 256;  // owned cells of a full-step window (larger: the whole tile)
+
+template <bool HU>
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
   __shared__ double ps[32], ph[32];
+  __shared__ int fl_or, s_lo, s_hi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int k = g.k, n = g.n, own_lo = g.nL, own_hi = g.nL + g.cnt;
-  const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
-  const double a_v = e.a_v, a_l = e.a_l, rmin2 = rho_min * rho_min, inv_rt = 1.0 / rho_tilde;
   const double h_av = p.h_av, dt_hav = dt / h_av;
+  if (tid == 0) { fl_or = 0; s_lo = 1 << 30; s_hi = -1; }
   // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
   const double* const rin = tl.rho[g.in];
   const long long mo_t = tl.mom[g.in] - rin;
@@ -175,9 +250,9 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   double* const omom = tl.mom[g.out] + g.base - own_lo;
   double* const oh = tl.h[g.out] + g.base - own_lo;
   const double* const ih = tl.h[g.in] + g.base - own_lo;
-  int bits = 0;          // 1 vapour, 2 liquid, 4 spinodal / non-positive
-  bool cand = false;     // a creation candidate (R7 pre-filter) at some edge
+  int slo = 1 << 30, shi = -1;  // special cells (see fast_windows)
   bool unif = true;      // output widths all h_av
+  int phases = 0;        // 1 vapour, 2 liquid: the warps' specialisations
   double snum = 0.0, sden = 1.0;  // max |m|/rho of the new cells, by cross-multiplication
   double h_part = HU ? h_av : INFINITY;
   const int nwin = (n + 29) / 30;
@@ -185,55 +260,45 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     double rr[FB], mm[FB];
 #pragma unroll
     for (int b = 0; b < FB; ++b) {  // all loads of the batch first
-      const int c = 30 * (w0 + nw * b) - 1 + lane;
-      const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
-      const double* pr = cc < own_lo ? segL : (cc < own_hi ? segO : segR);
-      const long long mo = cc < own_lo ? moL : (cc < own_hi ? mo_t : moR);
+      const int wi = w0 + nw * b;
+      const int c = 30 * wi - 1 + lane;
       rr[b] = 1.0; mm[b] = 0.0;
-      if (w0 + nw * b < nwin) { rr[b] = pr[cc]; mm[b] = pr[cc + mo]; }
-    }
-#pragma unroll
-    for (int b = 0; b < FB; ++b) {
-      if (w0 + nw * b >= nwin) break;  // warp-uniform
-      const int c = 30 * (w0 + nw * b) - 1 + lane;
-      const double rc = rr[b], mc = mm[b];
-      const double uc = mc * rcp_fast(rc);
-      const bool vc = rc <= rho_tilde, lc = rc >= rho_min;
-      const double pc = vc ? a_v2 * rc : p0 + a_l2 * (rc - rho0);
-      const double a = vc ? a_v : a_l;
-      // lanes beyond the grid hold clamped copies of real cells: the bits are those of [0, n)
-      bits |= (vc ? 1 : (lc ? 2 : 4)) | (rc > 0.0 ? 0 : 4);
-      const double rl = __shfl_up_sync(0xffffffffu, rc, 1), ml = __shfl_up_sync(0xffffffffu, mc, 1);
-      const double ul = __shfl_up_sync(0xffffffffu, uc, 1), pl = __shfl_up_sync(0xffffffffu, pc, 1);
-      double f0, f1;  // edge c (between c-1 and c)
-      hll_fast(a, rl, ml, ul, pl, rc, mc, uc, pc, f0, f1);
-      {  // creation pre-filters (R7) as bulk_p1; at ghost / duplicate edges du = 0: no candidate
-        const double du = uc - ul, x = rl * rc;
-        cand |= lc ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
-      }
-      const double g0 = __shfl_down_sync(0xffffffffu, f0, 1), g1 = __shfl_down_sync(0xffffffffu, f1, 1);
-      if (lane >= 1 && lane <= 30 && c >= own_lo && c < own_hi) {  // P2, h^{n+1} = h^n
-        double cfac = dt_hav, hn = h_av;
-        if (!HU) { hn = ih[c]; if (hn != h_av) cfac = dt / hn; }
-        const double r1 = rc - cfac * (g0 - f0);
-        const double m1 = mc - cfac * (g1 - f1);
-        orho[c] = r1;
-        omom[c] = m1;
-        if (!HU) { oh[c] = hn; unif &= hn == h_av; h_part = fmin(h_part, hn); }
-        const double am = fabs(m1);
-        if (am * sden > snum * r1) { snum = am; sden = r1; }
+      if (wi < nwin) {
+        if (30 * wi - 1 >= own_lo && 30 * wi + 30 < own_hi) {  // interior window (warp-uniform)
+          rr[b] = segO[c]; mm[b] = segO[c + mo_t];
+        } else {
+          const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
+          const double* pr = cc < own_lo ? segL : (cc < own_hi ? segO : segR);
+          const long long mo = cc < own_lo ? moL : (cc < own_hi ? mo_t : moR);
+          rr[b] = pr[cc]; mm[b] = pr[cc + mo];
+        }
       }
     }
+    const bool liq = __shfl_sync(0xffffffffu, rr[0], 1) >= e.rho_min;  // warp-uniform choice
+    phases |= liq ? 2 : 1;
+    if (liq) fast_windows<HU, true>(e, rr, mm, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                    slo, shi, unif, snum, sden, h_part);
+    else fast_windows<HU, false>(e, rr, mm, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                 slo, shi, unif, snum, sden, h_part);
   }
-  // S_max of this lane's new cells: |m| rcp(rho) + a, as cfl_partials (one phase: a uniform)
-  const double sl = snum * rcp_fast(sden);
-  const double s_lane = warp_max(sl);
+  // S_max of this lane's new cells: |m| rcp(rho) (+ a below, as cfl_partials; one phase)
+  const double s_lane = warp_max(snum * rcp_fast(sden));
   const double h_lane = HU ? h_av : warp_min(h_part);
-  if (lane == 0) { ps[warp] = s_lane; ph[warp] = h_lane; }
-  const int any_v = __syncthreads_or(bits & 1), any_l = __syncthreads_or(bits & 2);
-  const int any_bad = __syncthreads_or((bits & 4) || cand);
-  if (!HU) unif = __syncthreads_and(unif);
-  const bool fast = !any_bad && !(any_v && any_l);
+  const int flags = (__all_sync(0xffffffffu, unif) ? 0 : 8) | phases;
+  slo = __reduce_min_sync(0xffffffffu, slo);
+  shi = __reduce_max_sync(0xffffffffu, shi);
+  if (lane == 0) {
+    ps[warp] = s_lane; ph[warp] = h_lane;
+    if (flags) atomicOr(&fl_or, flags);
+    if (shi >= 0) { atomicMin(&s_lo, slo); atomicMax(&s_hi, shi); }
+  }
+  __syncthreads();
+  const int f = fl_or;
+  // owned cells within HALO (+1 for the edge) of a special cell need the full step: window [wa, wb)
+  const int wa = max(own_lo, s_lo - 1 - HALO), wb = min(own_hi, s_hi + 2 + HALO);
+  const bool mixed = (f & 3) == 3;
+  const bool fast = !mixed && wa >= wb;
+  unif = !(f & 8);
   if (fast && (g.xl || g.xr)) {  // rank mode: send records of the first / last HALO owned cells
     for (int q = tid; q < 2 * HALO; q += blockDim.x) {
       const bool left = q < HALO;
@@ -247,7 +312,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     if (fast) {
       double s = 0.0, hm = INFINITY;
       for (int w = 0; w < nw; ++w) { s = fmax(s, ps[w]); hm = fmin(hm, ph[w]); }
-      tl.part[2 * k] = s + (any_v ? a_v : a_l);
+      tl.part[2 * k] = s + ((f & 3) == 1 ? e.a_v : e.a_l);
       tl.part[2 * k + 1] = hm;
       tl.cnt[g.out][k] = g.cnt;
       tl.hu[g.out][k] = unif ? 1 : 0;
@@ -256,9 +321,14 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
       if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
     } else {
-      tl.part[2 * k] = 0.0;  // neutral: tiled_slow folds this tile's own partials
+      tl.part[2 * k] = 0.0;  // neutral: the full-step kernels fold this tile's own partials
       tl.part[2 * k + 1] = INFINITY;
-      tl.slow[atomicAdd(&tl.ctl[4], 1)] = k;
+      if (!mixed && wb - wa <= WMAX) {  // a window of the tile
+        const int j = atomicAdd(&tl.ctl[6], 1);
+        tl.wlist[3 * j] = k; tl.wlist[3 * j + 1] = wa; tl.wlist[3 * j + 2] = wb;
+      } else {
+        tl.slow[atomicAdd(&tl.ctl[4], 1)] = k;
+      }
     }
   }
 }
@@ -267,13 +337,13 @@ template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
+  const TGeo g = tile_geo_spec(tl, blockIdx.x);
   const double t = tl.scal[0];
   if (tl.ctl[1] != 0 || !(t < t_end)) return;  // uniform across the grid: nothing to do
   double dt = tl.scal[1];
   if (t + dt > t_end) dt = t_end - t;  // as step_body
-  const TGeo g = tile_geo(tl, blockIdx.x, tl.ctl[0]);
-  if (g.hu_in) tiled_fast_body<MAXT, MINB, true>(e, p, tl, g, dt);
-  else tiled_fast_body<MAXT, MINB, false>(e, p, tl, g, dt);
+  if (g.hu_in) tiled_fast_body<true>(e, p, tl, g, dt);
+  else tiled_fast_body<false>(e, p, tl, g, dt);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -380,6 +450,184 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
 }
 
 // ------------------------------------------------------------------------------------------
+// The full step of a window [wa, wb) of tile k's owned cells (virtual indices) that holds every
+// special cell of the tile with a margin of HALO: step_body on the window plus HALO cells each
+// side (shared memory), then the tile's output is assembled in place: the fast results left of
+// the window stay, the window's remeshed cells follow, the fast results right of it shift by
+// the change in cell count.  Cells outside the window are plain (one phase, both edges HLL, no
+// block, creation or remesh event within HALO cells), so their fast results are step_body's.
+// ------------------------------------------------------------------------------------------
+constexpr int WCAP = WMAX + 2 * HALO + MAXEV + MAXTRG + 2;  // window grid capacity (even)
+
+// move out[s, e) to out[s + d, e + d) (block-wide, chunked; overlapping ranges are safe)
+__device__ __forceinline__ void shift_cells(double* a0, double* a1, double* a2, int s, int e, int d) {
+  if (d == 0 || s >= e) return;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int nch = (e - s + T - 1) / T;
+  for (int q = 0; q < nch; ++q) {
+    const int lo = d > 0 ? max(s, e - (q + 1) * T) : s + q * T;
+    const int hi = d > 0 ? e - q * T : min(e, s + (q + 1) * T);
+    const int i = lo + tid;
+    double v0 = 0, v1 = 0, v2 = 0;
+    if (i < hi) { v0 = a0[i]; v1 = a1[i]; if (a2) v2 = a2[i]; }
+    __syncthreads();
+    if (i < hi) { a0[i + d] = v0; a1[i + d] = v1; if (a2) a2[i + d] = v2; }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
+                                            int k, int wa, int wb, double t, double t_end, double dt_given) {
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const TGeo g = tile_geo(tl, k, tl.ctl[0]);
+  const int nL = g.nL, cnt = g.cnt;
+  const int s0 = max(0, wa - HALO), s1 = min(g.n, wb + HALO), n = s1 - s0;
+  if (tid == 0) {
+    sh.status = 0;
+    reset_counters(sh);
+    memset(&sh.st, 0, sizeof(sh.st));
+    const double* ws = tl.ws + (size_t)k * WS_STRIDE;
+    sh.wsn = (int)ws[2 * MAXIF];
+    for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
+  }
+  const int huL = k > 0 ? tl.hu[g.in][k - 1] : 0, huR = k < tl.ntiles - 1 ? tl.hu[g.in][k + 1] : 0;
+  for (int i = tid; i < n; i += T) {
+    const int v = s0 + i;
+    long long mo;
+    const double* pr = vcell(tl, g, v, mo);
+    A.rho[i] = pr[0];
+    A.mom[i] = pr[mo];
+    double hh;
+    if (v < nL) hh = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + v]);
+    else if (v < nL + cnt) hh = g.hu_in ? p.h_av : tl.h[g.in][g.base + v - nL];
+    else hh = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + v - nL - cnt]);
+    A.h[i] = hh;
+  }
+  for (int i = tid; i <= capw; i += T) A.fl[i] = 0;
+  A.n = n;
+  __syncthreads();
+  if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, n);
+  __syncthreads();
+  Zone Z;
+  Z.own_lo = wa - s0; Z.own_hi = wb - s0;
+  Z.zlo = max(Z.own_lo - 2, 0); Z.zhi = min(Z.own_hi + 2, n);
+  Z.dt_given = dt_given;
+  Z.left_real = (k == 0 && !tl.nbr_left && s0 == 0);
+  Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right && s1 == g.n);
+  const double dt = step_body(e, p, sh, A, t, t_end, Z);
+  __syncthreads();
+  const int olo = sh.olo, ohi = sh.ohi;
+  const int nw_out = ohi - olo;
+  const int d = nw_out - (wb - wa);
+  const int nout = cnt + d;
+  int st = sh.status;
+  if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.ntiles > 1 ? HALO : 3))) st = ST_CAPACITY;
+  __syncthreads();
+  double s_th = 0.0, h_th = INFINITY;
+  bool unif = true;
+  if (dt >= 0.0 && st == 0) {
+    double* const orho = tl.rho[g.out] + g.base;
+    double* const omom = tl.mom[g.out] + g.base;
+    double* const oh = tl.h[g.out] + g.base;
+    const int pa = wa - nL;  // output position of the window's first cell
+    shift_cells(orho, omom, g.hu_in ? nullptr : oh, wb - nL, cnt, d);  // fast cells right of it
+    bool uw = true;
+    for (int i = olo + tid; i < ohi; i += T) uw &= A.h[i] == p.h_av;
+    const bool unif_w = __syncthreads_and(uw);
+    bool uf = true;  // fast cells' widths (stored unless the input tile was uniform)
+    if (!g.hu_in)
+      for (int q = tid; q < nout; q += T)
+        if (q < pa || q >= pa + nw_out) uf &= oh[q] == p.h_av;
+    unif = __syncthreads_and(uf) && unif_w;
+    for (int i = tid; i < nw_out; i += T) {
+      orho[pa + i] = A.rho[olo + i];
+      omom[pa + i] = A.mom[olo + i];
+      if (!unif) oh[pa + i] = A.h[olo + i];
+    }
+    if (!unif && g.hu_in)
+      for (int q = tid; q < nout; q += T)
+        if (q < pa || q >= pa + nw_out) oh[q] = p.h_av;
+    // CFL partials: the window's cells (tiny test inside the window grid) ...
+    double s, hm;
+    cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, false, false, s, hm);
+    s_th = s; h_th = hm;
+    // ... and the fast cells (plain: never tiny), from the output
+    double sf = 0.0, hf = INFINITY;
+    for (int q = tid; q < nout; q += T) {
+      if (q >= pa && q < pa + nw_out) continue;
+      const double r = orho[q];
+      sf = fmax(sf, fabs(omom[q] * rcp_fast(r)) + sound(e, phase_of(e, r)));
+      hf = fmin(hf, g.hu_in ? p.h_av : oh[q]);
+    }
+    s_th = fmax(s_th, warp_max(sf));
+    h_th = fmin(h_th, warp_min(hf));
+    __syncthreads();
+    if (g.xl || g.xr) {  // rank mode: send records of the first / last HALO output cells
+      for (int q = tid; q < 2 * HALO; q += T) {
+        const bool left = q < HALO;
+        if (left ? !g.xl : !g.xr) continue;
+        const int c = left ? q : nout - 2 * HALO + q;
+        double* sb = tl.xbuf + (left ? XB_SEND_LEFT : XB_SEND_RIGHT) + (left ? q : q - HALO);
+        sb[0] = orho[c]; sb[HALO] = omom[c]; sb[2 * HALO] = unif ? p.h_av : oh[c];
+      }
+      if (tid == 0) {
+        if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
+        if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
+      }
+    }
+  }
+  if (lane == 0) { sh.part_s[warp] = s_th; sh.part_h[warp] = h_th; }
+  __syncthreads();
+  if (tid == 0) {
+    if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
+    if (dt >= 0.0 && st == 0) {
+      double so = 0.0, ho = INFINITY;
+      for (int w = 0; w < nw; ++w) { so = fmax(so, sh.part_s[w]); ho = fmin(ho, sh.part_h[w]); }
+      tl.part[2 * k] = so;
+      tl.part[2 * k + 1] = ho;
+      tl.cnt[g.out][k] = nout;
+      tl.hu[g.out][k] = unif ? 1 : 0;
+      double* ws = tl.ws + (size_t)k * WS_STRIDE;
+      for (int q = 0; q < MAXIF; ++q) { ws[q] = sh.ws0[q]; ws[MAXIF + q] = sh.ws1[q]; }
+      ws[2 * MAXIF] = (double)sh.wsn;
+      TileStats& ts = tl.tstats[k];
+      ts.cell_updates += cnt;
+      ts.dts_iters += (long long)sh.c_dts;
+      ts.iface_solves += (long long)sh.c_solves;
+      ts.regions += (long long)sh.c_regions;
+      if ((long long)sh.c_dtsmax > ts.dts_max) ts.dts_max = (long long)sh.c_dtsmax;
+      ts.full_steps += 1;
+      ts.creations += sh.st.creations;
+      ts.splits += sh.st.splits;
+      ts.merges += sh.st.merges;
+    }
+  }
+  __syncthreads();
+}
+
+// tiled_win: persistent CTAs over the window list (launched between tiled_fast and tiled_slow)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
+          double t_end) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
+  Arr A = carve(smem_raw, WCAP);
+  const int tid = threadIdx.x;
+  const double t = tl.scal[0], dt_given = tl.scal[1];
+  if (tl.ctl[1] != 0 || !(t < t_end)) return;
+  const int njobs = tl.ctl[6];
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) sh.n_new = atomicAdd(&tl.ctl[7], 1);
+    __syncthreads();
+    const int j = sh.n_new;
+    if (j >= njobs) break;
+    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[3 * j], tl.wlist[3 * j + 1], tl.wlist[3 * j + 2], t, t_end, dt_given);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // tiled_slow: persistent CTAs take listed tiles one at a time (dynamic: DTS-heavy tiles vary a
 // lot), fold the fast tiles' partials in strides, and the last CTA finishes the step.
 // ------------------------------------------------------------------------------------------
@@ -431,7 +679,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (last) {
     __threadfence();
     if (tl.ctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
-    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; }
+    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; }
   }
 }
 
@@ -532,7 +780,7 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
     tl.ctl[0] = 1 - tl.ctl[0];
     tl.ctl[3] += 1;
   }
-  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
+  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0;
   double dt = p.cfl * hm / S;
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;

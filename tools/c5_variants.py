@@ -10,7 +10,7 @@ from paper_2211_00705_b200 import workloads as W
 var = sys.argv[1] if len(sys.argv) > 1 else "recipe"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 27
-tile = int(os.environ.get("TILE", "960"))
+tile = int(os.environ.get("TILE", "940"))
 w = W.c5(n_cells=n)
 if var == "uniform":
     w["rho"][0, :n] = 1000.0
