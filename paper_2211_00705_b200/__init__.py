@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libeis.so")
+LIB_PATH = os.environ.get("EIS_LIB") or os.path.join(HERE, "libeis.so")  # EIS_LIB: a variant build (tools)
 
 EIS_HOST, EIS_DEVICE = 0, 1
 MODE_SPLIT, MODE_EXPLICIT = 0, 1
@@ -102,7 +102,7 @@ def lib():
         L.eis_interfaces.argtypes = [vp, P(Interface), i64, P(i64)]
         L.eis_member_status.argtypes = [vp, P(i32)]
         L.eis_member_stats.argtypes = [vp, P(Stats)]
-        L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64)]
+        L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.eis_last_error.argtypes = [vp]
         L.eis_last_error.restype = C.c_char_p
         L.eis_destroy.argtypes = [vp]
@@ -238,9 +238,9 @@ class Context:
         self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
 
     def tile_info(self) -> dict:
-        nt, full = C.c_int64(), C.c_int64()
-        self._check(lib().eis_tile_info(self._ctx, C.byref(nt), C.byref(full)), "eis_tile_info")
-        return {"n_tiles": nt.value, "full_tile_steps": full.value}
+        nt, full, win = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().eis_tile_info(self._ctx, C.byref(nt), C.byref(full), C.byref(win)), "eis_tile_info")
+        return {"n_tiles": nt.value, "full_tile_steps": full.value, "window_steps": win.value}
 
     def member_stats(self) -> list:
         arr = (Stats * self.M)()

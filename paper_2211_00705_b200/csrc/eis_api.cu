@@ -19,7 +19,7 @@
 using namespace eis;
 
 struct eis_ctx {
-  long long tile_full_steps = 0;
+  long long tile_full_steps = 0, tile_win_steps = 0;
   eis_eos eos_in;
   eis_params prm_in;
   eis_grid grid;
@@ -260,13 +260,13 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     delete c; return EIS_E_CUDA;
   }
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
-  if (cudaFuncSetAttribute(tiled_win<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+  if (cudaFuncSetAttribute(tiled_win<64, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   int nsm = 0, per_sm = 0, per_sm_w = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<128, 8>, 128, c->smem_win);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<64, 16>, 64, c->smem_win);
   c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
   c->win_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm_w, 1));
   const size_t tc = (size_t)ntiles * capt;
@@ -338,14 +338,16 @@ static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
   CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   memset(out, 0, sizeof(*out));
-  long long full = 0;
+  long long full = 0, win = 0;
   for (const TileStats& s : ts) {
     out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters; out->iface_solves += s.iface_solves;
     out->creations += s.creations; out->splits += s.splits; out->merges += s.merges; out->regions += s.regions;
     out->dts_iter_max = std::max(out->dts_iter_max, (int64_t)s.dts_max);
     full += s.full_steps;
+    win += s.win_steps;
   }
   c->tile_full_steps = full;
+  c->tile_win_steps = win;
   out->steps = ctl[3];
   out->t_min = out->t_max = scal[0];
   out->dt_min = scal[2];
@@ -441,14 +443,15 @@ extern "C" void eis_destroy(eis_ctx* c) {
   delete c;
 }
 
-extern "C" eis_status eis_tile_info(eis_ctx* c, int64_t* n_tiles, int64_t* full_tile_steps) {
-  if (!c || !n_tiles || !full_tile_steps) return EIS_E_ARG;
+extern "C" eis_status eis_tile_info(eis_ctx* c, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps) {
+  if (!c || !n_tiles || !full_tile_steps || !window_steps) return EIS_E_ARG;
   if (!c->tiled) return fail(c, EIS_E_ARG, "eis_tile_info: not a tiled context%s");
   eis_stats st;
   const eis_status s = tiled_stats(c, &st);
   if (s) return s;
   *n_tiles = c->tl.ntiles;
   *full_tile_steps = c->tile_full_steps;
+  *window_steps = c->tile_win_steps;
   return EIS_OK;
 }
 
@@ -534,7 +537,7 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
 // the listed tiles (and, by its last CTA, the next dt)
 static void tiled_launch(eis_ctx* c, double t_end) {
   tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
-  tiled_win<128, 8><<<c->win_grid, 128, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_win<64, 16><<<c->win_grid, 64, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
 }
 

@@ -24,7 +24,7 @@ constexpr int HALO = 10;  // halo cells per side: >= MAXB + 2 keeps every needed
 
 struct TileStats {
   long long cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
-  long long dts_max, full_steps;  // full_steps: steps this tile took the full (not the fast) path
+  long long dts_max, full_steps, win_steps;  // steps this tile took the whole-tile / window full step
 };
 
 struct Tiles {
@@ -175,7 +175,10 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 // loads in flight before the arithmetic).  Outputs of a tile that turns out not plain are
 // overwritten by tiled_slow.
 // ------------------------------------------------------------------------------------------
-constexpr int FB = 4;  // windows per warp per batch (tile 940 + 2 x 10 halo = 32 windows = 8 warps x 4)
+#ifndef EIS_FB
+#define EIS_FB 3
+#endif
+constexpr int FB = EIS_FB;  // windows per warp per batch (measured: 3 best of 2, 3, 4, 8 at 128 threads)
 
 // one window batch of one warp after its loads: the arithmetic, specialised by the phase the
 // warp's first cell has (LIQ) and by uniform widths (HU).  A cell of another phase (or spinodal,
@@ -228,7 +231,7 @@ __device__ __forceinline__ void fast_windows(const Eos& e, const double (&rr)[FB
   }
 }
 
-constexpr int WMAX = 256;  // owned cells of a full-step window (larger: the whole tile)
+constexpr int WMAX = 160;  // owned cells of a full-step window (larger: the whole tile)
 
 template <bool HU>
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
@@ -274,7 +277,12 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
         }
       }
     }
-    const bool liq = __shfl_sync(0xffffffffu, rr[0], 1) >= e.rho_min;  // warp-uniform choice
+    // specialisation: liquid if the batch (windows spread over the tile) has a liquid cell;
+    // warps that differ make the tile take the whole-tile full step
+    bool anyl = false;
+#pragma unroll
+    for (int b = 0; b < FB; ++b) anyl |= w0 + nw * b < nwin && rr[b] >= e.rho_min;
+    const bool liq = __any_sync(0xffffffffu, anyl);
     phases |= liq ? 2 : 1;
     if (liq) fast_windows<HU, true>(e, rr, mm, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
                                     slo, shi, unif, snum, sden, h_part);
@@ -596,7 +604,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
       ts.iface_solves += (long long)sh.c_solves;
       ts.regions += (long long)sh.c_regions;
       if ((long long)sh.c_dtsmax > ts.dts_max) ts.dts_max = (long long)sh.c_dtsmax;
-      ts.full_steps += 1;
+      ts.win_steps += 1;
       ts.creations += sh.st.creations;
       ts.splits += sh.st.splits;
       ts.merges += sh.st.merges;
