@@ -1,21 +1,23 @@
 #!/usr/bin/env python
 """bench.py — fp64 cell-updates/s of the explicit-implicit splitting hot path on B200.
 
-Default workload: BASELINE.json configs[2] (C3), the batched cavitation ensemble — 65,536
-independent 1D grids of N=1024 cells — the largest single-GPU configuration whose metric is
-cell-updates/s (configs[0]/[1] are single ~1e3-cell grids and are parity cases).  One bench
-"step" = one large time step of the whole method for every member.
-The K timed steps start from the seeded initial state (so they include the cavitation step),
-run as ONE launch of the member-resident kernel (eis_step(K)); inputs are resident in HBM
-(1.1 GB, larger than the 126 MB L2) when the timed region starts.
+Default workload: BASELINE.json configs[4] (C5), one 2^27-cell grid with 4096-cell random
+segments (~14.5k cavitation bubbles), 500 large steps: the largest single-GPU configuration and
+the one the metric's 1/2/4/8-GPU scaling is quoted on (domain decomposition).  One bench
+"step" = one large time step of the whole method over the whole
+grid: the tiled fast pass, the window / whole-tile full steps, the next dt.  The K timed steps
+start from the seeded initial state (so they include the creation step); the state (2 GB) is
+resident in HBM and larger than the 126 MB L2.
+
+--workload C3: BASELINE configs[2], the batched cavitation ensemble (65,536 grids of N=1024,
+2000 steps) as ONE launch of the member-resident kernel (eis_step(K)); C4 likewise.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eis|reference] [--workload C3|C4|C1|C2|C5]
 
-Multi-GPU (torchrun): members are sharded contiguously across ranks, no collective in the
-data path (scaling "strong": the ensemble is fixed); timing is the max over ranks.
---workload C5 (BASELINE configs[4], one 2^27-cell grid, tiled layout, one launch per step) cuts
-the grid into tile-aligned rank slices under torchrun: per step a local launch, a 10-cell halo
-exchange with the neighbour ranks and an all-reduce(MIN) of the CFL pair (paper_2211_00705_b200.decomp).
+Multi-GPU (torchrun): C5 cuts the grid into tile-aligned rank slices: per step the local
+kernels, a 10-cell halo exchange with the neighbour ranks and an all-reduce(MIN) of the CFL pair
+(paper_2211_00705_b200.decomp); C3/C4 shard members contiguously with no collective in the data
+path.  Scaling "strong" (the problem is fixed); timing is the max over ranks.
 --impl reference times the CPU oracle (oracle/) on a bounded member sample (rank 0 only).
 """
 from __future__ import annotations
@@ -37,7 +39,8 @@ sys.path.insert(0, ROOT)
 # Algorithmic fp64 operations per cell-update of the bulk path: decode 5,
 # HLL edge flux + creation pre-filter 36, moving-cell update 15; one division = 1 op.
 FLOP_PER_CELL_UPDATE = 56
-C5_BYTES_PER_CELL_UPDATE = 48  # tiled layout: read rho, mom, h; write rho, mom, h (fp64)
+C5_BYTES_PER_CELL_UPDATE = 32  # the fast pass: read rho, mom; write rho, mom (fp64; widths of
+                                # tiles whose widths are all h_av are neither read nor written)
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 FMA/clk x 2 x max clock
 
 
@@ -47,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=None, help="default 2000 (C3/C4), 500 (C5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="eis", choices=["eis", "reference"])
-    ap.add_argument("--workload", default="C3", choices=["C3", "C4", "C1", "C2", "C5"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C3", "C4", "C1", "C2"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--members", type=int, default=0, help="profiling only: fewer ensemble members")
@@ -131,8 +134,8 @@ def fp64_peak():
 def ncu_traffic(workload_name):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        if d.get("workload") == workload_name:
+        d = json.load(open(p)).get(workload_name)
+        if d:
             return d.get("bytes_per_launch")
     return None
 
@@ -142,8 +145,9 @@ def cpu_sample_size(K, N):
 
 
 def c5_cpu_cells(K):
-    """Oracle sample of C5: the first whole 4096-cell segments, ~3e8 cell-updates in total."""
-    return int(max(2, min(256, round(3e8 / (K * 4096))))) * 4096
+    """Oracle sample of C5: the first whole 4096-cell segments, ~6e7 cell-updates in total
+    (10-30 s of one host core)."""
+    return int(max(2, min(256, round(6e7 / (K * 4096))))) * 4096
 
 
 def run_oracle(name, members, steps):
@@ -237,6 +241,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.set_timing(True)  # CUDA events around the kernel on the library's (this) stream
     torch.cuda.synchronize()
     e0.record(stream)
     advance(args.steps)  # ONE launch of the member-resident kernel
@@ -246,6 +251,8 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    kt = ctx.get_timing()
+    ctx.set_timing(False)
     st = ctx.step(0, stats=True)  # counters of exactly the timed steps (set_state reset them)
     status = ctx.member_status()
     nbad = int((status != 0).sum())
@@ -297,7 +304,9 @@ def main():
                "sample": f"members 0..{S - 1} of {name}, the same {args.steps} large steps from t=0, single thread"}
 
     peak, peak_src = fp64_peak()
-    achieved = FLOP_PER_CELL_UPDATE * cu / (ms * 1e-3) / world / 1e12  # per GPU
+    cu_local = st["cell_updates"] - cu0 if world == 1 else None
+    kms = kt["resident_ms"] if kt["resident_ms"] > 0 else ms
+    achieved = FLOP_PER_CELL_UPDATE * (cu / world if cu_local is None else cu_local) / (kms * 1e-3) / 1e12  # per GPU
     if rank == 0:
         line = {
             "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
@@ -311,6 +320,7 @@ def main():
                        "launches": "one member-resident kernel launch for the K timed steps"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
+                         "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                          "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1, "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
@@ -348,6 +358,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rg.ctx.set_timing(True)  # CUDA events around each kernel on the library's (this) stream
     torch.cuda.synchronize()
     e0.record(stream)
     rg.step(args.steps)
@@ -357,7 +368,10 @@ def main_c5(args, torch, dist, P, world, rank, local):
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    kt = rg.ctx.get_timing()
+    rg.ctx.set_timing(False)
     st = rg.ctx.step(0, stats=True) if world == 1 else rg.ctx.member_stats()[0]
+    cu_local = st["cell_updates"]
     nbad = int(rg.ctx.member_status()[0] != 0)
     cu = st["cell_updates"]
     if world > 1:
@@ -402,7 +416,9 @@ def main_c5(args, torch, dist, P, world, rank, local):
                "sample": f"the first {S} cells (whole segments) of C5, the same {args.steps} large steps, single thread"}
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
-    achieved = C5_BYTES_PER_CELL_UPDATE * cu / (ms * 1e-3) / world / 1e9  # per GPU
+    # dominant kernel: the fast pass streams every cell of this rank's grid once per step
+    achieved = C5_BYTES_PER_CELL_UPDATE * cu_local / (kt["fast_ms"] * 1e-3) / 1e9
+    step_bw = C5_BYTES_PER_CELL_UPDATE * cu / (ms * 1e-3) / world / 1e9
     if rank == 0:
         line = {
             "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
@@ -411,13 +427,19 @@ def main_c5(args, torch, dist, P, world, rank, local):
             "data": "synthetic (seeded SplitMix64, BASELINE configs[4] recipe)",
             "config": {"workload": f"C5: one grid of {n_glob} cells, 4096-cell random segments",
                        "cells": n_glob, "parallelism": f"tile-aligned grid slices x{world}, halo exchange + CFL min",
-                       "l2": "state (2 GB) larger than L2", "launches": "one tiled-step launch per step"
-                       + (" + step_finish + NCCL halo/all-reduce" if world > 1 else "")},
+                       "l2": "state (2 GB) larger than L2",
+                       "launches": "per step: tiled_fast + tiled_win + tiled_slow"
+                       + (" + NCCL halo exchange / all-reduce + tiled_finish" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "kernel": "eis::tiled_step",
+                         "traffic": ncu_traffic("C5"), "kernel": "eis::tiled_fast",
                          "bytes_per_cell_update": C5_BYTES_PER_CELL_UPDATE,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * (1 if world == 1 else 2), "clocks": clk,
+                         "kernel_ms_per_step": kt["fast_ms"] / max(args.steps, 1),
+                         "kernel_share_of_step": kt["fast_ms"] / ms,
+                         "window_ms_per_step": kt["window_ms"] / max(args.steps, 1),
+                         "tile_ms_per_step": kt["tile_ms"] / max(args.steps, 1),
+                         "whole_step_gbs": step_bw, "whole_step_frac": step_bw / hbm,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * (3 if world == 1 else 4), "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
             "members_not_ok": nbad,

@@ -195,6 +195,14 @@ eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
  * candidates), rather than only the single-phase fast path.  Synchronises the stream. */
 eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps);
 
+/* Kernel timing (measurement support): with timing enabled, every step launch records CUDA
+ * events on the context's stream around each kernel (a few microseconds per step).
+ * eis_get_timing synchronises the stream and returns the summed milliseconds since
+ * eis_set_timing: ms[0] tiled fast pass, ms[1] tiled window full steps, ms[2] tiled whole-tile
+ * full steps + next dt, ms[3] member-resident kernel; *launches = recorded launch groups. */
+eis_status eis_set_timing(eis_ctx* ctx, int32_t enable);
+eis_status eis_get_timing(eis_ctx* ctx, double* ms /* [4] */, int64_t* launches);
+
 /* Last error message of the context (static storage owned by the context). */
 const char* eis_last_error(const eis_ctx* ctx);
 

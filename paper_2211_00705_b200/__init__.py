@@ -74,7 +74,8 @@ class Thresholds(C.Structure):
 # exported symbols of libeis.so (checked by tests/test_abi.py against include/eis.h)
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
-           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info")
+           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info", "eis_set_timing",
+           "eis_get_timing")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
 XB_REC = 3 * HALO + 1
@@ -103,6 +104,8 @@ def lib():
         L.eis_member_status.argtypes = [vp, P(i32)]
         L.eis_member_stats.argtypes = [vp, P(Stats)]
         L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+        L.eis_set_timing.argtypes = [vp, C.c_int32]
+        L.eis_get_timing.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         L.eis_last_error.argtypes = [vp]
         L.eis_last_error.restype = C.c_char_p
         L.eis_destroy.argtypes = [vp]
@@ -236,6 +239,15 @@ class Context:
 
     def step_finish(self, t_end: float = float("inf"), after_step: bool = True):
         self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
+
+    def set_timing(self, enable: bool = True):
+        self._check(lib().eis_set_timing(self._ctx, int(bool(enable))), "eis_set_timing")
+
+    def get_timing(self) -> dict:
+        ms = (C.c_double * 4)()
+        n = C.c_int64()
+        self._check(lib().eis_get_timing(self._ctx, ms, C.byref(n)), "eis_get_timing")
+        return {"fast_ms": ms[0], "window_ms": ms[1], "tile_ms": ms[2], "resident_ms": ms[3], "launches": n.value}
 
     def tile_info(self) -> dict:
         nt, full, win = C.c_int64(), C.c_int64(), C.c_int64()

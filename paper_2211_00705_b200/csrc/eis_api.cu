@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +21,11 @@ using namespace eis;
 
 struct eis_ctx {
   long long tile_full_steps = 0, tile_win_steps = 0;
+  // kernel timing (eis_set_timing): events around each step kernel, summed on request
+  int timing = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::array<int, 5>> ev_marks;  // per recorded launch group: event indices + kind
+  size_t ev_used = 0;
   eis_eos eos_in;
   eis_params prm_in;
   eis_grid grid;
@@ -129,24 +135,34 @@ __global__ void k_fill_ll(long long* a, long long count, long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) a[i] = v;
 }
 // one CTA per member: validate the initial state (rho > 0, not spinodal), reset counters
+// member status from the initial state (status zeroed before): grid (members, chunks of a
+// member's cells), so one huge grid is checked by many CTAs
+constexpr int VALIDATE_CHUNK = 8192;
 __global__ void k_validate(const Eos e, Members g, double t0) {
   __shared__ int bad;
   const long long m = blockIdx.x;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   const long long n = g.n[m];
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-    double r = g.rho[m * g.cap + i];
-    if (!(r > 0.0)) atomicMax(&bad, ST_NONPOS);
-    else if (phase_of(e, r) == SPIN) atomicMax(&bad, ST_SPINODAL);
+  for (long long lo = (long long)blockIdx.y * VALIDATE_CHUNK; lo < n; lo += (long long)gridDim.y * VALIDATE_CHUNK) {
+    const long long hi = min(n, lo + VALIDATE_CHUNK);
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      double r = g.rho[m * g.cap + i];
+      if (!(r > 0.0)) atomicMax(&bad, ST_NONPOS);
+      else if (phase_of(e, r) == SPIN) atomicMax(&bad, ST_SPINODAL);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    g.status[m] = (n < 3 || n > g.cap) ? ST_CAPACITY : bad;
-    g.t[m] = t0;
-    MemberStats z;
-    memset(&z, 0, sizeof(z));
-    g.stats[m] = z;
+    int st = bad;
+    if (blockIdx.y == 0) {
+      if (n < 3 || n > g.cap) st = ST_CAPACITY;
+      g.t[m] = t0;
+      MemberStats z;
+      memset(&z, 0, sizeof(z));
+      g.stats[m] = z;
+    }
+    if (st) atomicMax(&g.status[m], st);
   }
 }
 // copy live cells, zero the rest, phases (255 past the end)
@@ -440,7 +456,36 @@ extern "C" void eis_destroy(eis_ctx* c) {
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
+  for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   delete c;
+}
+
+extern "C" eis_status eis_set_timing(eis_ctx* c, int32_t enable) {
+  if (!c) return EIS_E_ARG;
+  c->timing = enable != 0;
+  c->ev_marks.clear();
+  c->ev_used = 0;
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_get_timing(eis_ctx* c, double* ms, int64_t* launches) {
+  if (!c || !ms || !launches) return EIS_E_ARG;
+  CU(cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < 4; ++q) ms[q] = 0.0;
+  *launches = (int64_t)c->ev_marks.size();
+  for (const auto& m : c->ev_marks) {
+    float t = 0.f;
+    if (m[4] == 0) {  // resident: one kernel
+      CU(cudaEventElapsedTime(&t, c->ev_pool[m[0]], c->ev_pool[m[1]]));
+      ms[3] += t;
+      continue;
+    }
+    for (int q = 0; q < 3; ++q) {
+      CU(cudaEventElapsedTime(&t, c->ev_pool[m[q]], c->ev_pool[m[q + 1]]));
+      ms[q] += t;
+    }
+  }
+  return EIS_OK;
 }
 
 extern "C" eis_status eis_tile_info(eis_ctx* c, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps) {
@@ -487,7 +532,11 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   } else {
     k_fill_ll<<<grid_for(M), 256, 0, c->stream>>>(c->d_n, M, c->grid.n_cells);
   }
-  k_validate<<<(unsigned)M, 128, 0, c->stream>>>(c->e, c->g, t0);
+  CU(cudaMemsetAsync(c->d_status, 0, (size_t)M * 4, c->stream));
+  {
+    const long long ny = std::min<long long>(65535, (c->grid.cell_capacity + VALIDATE_CHUNK - 1) / VALIDATE_CHUNK);
+    k_validate<<<dim3((unsigned)M, (unsigned)std::max<long long>(ny, 1)), 256, 0, c->stream>>>(c->e, c->g, t0);
+  }
   CU(cudaGetLastError());
   if (c->tiled) {
     k_tiles_reset<<<1, 1, 0, c->stream>>>(c->tl, c->d_status, t0);
@@ -535,10 +584,26 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
 
 // one large step of the tiled grid: the streaming pass over every tile, then the full step of
 // the listed tiles (and, by its last CTA, the next dt)
+static int timing_event(eis_ctx* c) {  // an event from the pool, recorded on the stream
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return -1;
+    c->ev_pool.push_back(ev);
+  }
+  const int i = (int)c->ev_used++;
+  cudaEventRecord(c->ev_pool[i], c->stream);
+  return i;
+}
+
 static void tiled_launch(eis_ctx* c, double t_end) {
+  std::array<int, 5> m{-1, -1, -1, -1, 1};
+  if (c->timing) m[0] = timing_event(c);
   tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->timing) m[1] = timing_event(c);
   tiled_win<64, 16><<<c->win_grid, 64, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->timing) { m[3] = timing_event(c); c->ev_marks.push_back(m); }
 }
 
 static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats* out) {
@@ -566,6 +631,8 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   }
   if (n_steps > 0) {
     const unsigned M = (unsigned)c->grid.n_members;
+    std::array<int, 5> m{-1, -1, -1, -1, 0};
+    if (c->timing) m[0] = timing_event(c);
     if (c->threads <= 128)
       resident_steps<128, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else if (c->threads <= 256 && c->minb == 4)
@@ -576,6 +643,7 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
       resident_steps<256, 2><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else
       resident_steps<1024, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    if (c->timing) { m[1] = timing_event(c); c->ev_marks.push_back(m); }
     CU(cudaGetLastError());
   }
   if (out) return collect_stats(c, out);
