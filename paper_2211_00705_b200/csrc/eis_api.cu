@@ -308,6 +308,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   Tiles& tl = c->tl;
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
   tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
+  tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
+  if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
   tl.ntiles = (int)ntiles; tl.capt = capt;
   tl.xbuf = nullptr;

@@ -41,6 +41,7 @@ struct Tiles {
   int* wlist;                      // work list of (tile, window begin, window end): full step of a window
   double* part2;                   // per tiled_slow CTA: S_max, h_min
   int ntiles, capt, nbr_left, nbr_right;
+  int wmax;                        // largest window (owned cells) of a window full step (<= WMAX)
 };
 // ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] tile-list length  [5] next tile job
 //      [6] window-list length  [7] next window job
@@ -331,7 +332,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     } else {
       tl.part[2 * k] = 0.0;  // neutral: the full-step kernels fold this tile's own partials
       tl.part[2 * k + 1] = INFINITY;
-      if (!mixed && wb - wa <= WMAX) {  // a window of the tile
+      if (!mixed && wb - wa <= tl.wmax) {  // a window of the tile
         const int j = atomicAdd(&tl.ctl[6], 1);
         tl.wlist[3 * j] = k; tl.wlist[3 * j + 1] = wa; tl.wlist[3 * j + 2] = wb;
       } else {

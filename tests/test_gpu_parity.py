@@ -380,3 +380,36 @@ def test_c5_virtual_ranks_bitwise(P, world):
     np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
     np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
     np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
+
+
+@pytest.mark.parametrize("n,steps", [(40 * 940 + 517, 200)])
+def test_c5_window_path_matches_whole_tile_path(P, oracle_mod, n, steps, monkeypatch):
+    """The windowed full step (tiled_win: step body on <= 160 owned cells around a tile's special
+    cells, output assembled in place) against the whole-tile full step (tiled_slow) and the
+    oracle: same events, states within Newton-tolerance rounding (warm starts may differ)."""
+    w = W.c5(n_cells=n)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)
+    out = {}
+    for wmax in ("160", "0"):
+        monkeypatch.setenv("EIS_TILED_WMAX", wmax)
+        ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                        stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
+        ctx.set_state(rho, mom)
+        st = ctx.step(steps, stats=True)
+        info = ctx.tile_info()
+        g = ctx.get_state()
+        g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["mstats"] = [st]
+        out[wmax] = (g, st, info)
+    (gw, sw, iw), (gf, sf, inf_) = out["160"], out["0"]
+    assert iw["window_steps"] > 0 and iw["full_tile_steps"] == 0
+    assert inf_["window_steps"] == 0 and inf_["full_tile_steps"] > 0
+    for k in ("creations", "splits", "merges", "regions", "cell_updates"):
+        assert sw[k] == sf[k], k
+    nn = int(gw["n"][0])
+    assert nn == int(gf["n"][0])
+    np.testing.assert_allclose(gw["rho"][0, :nn], gf["rho"][0, :nn], rtol=1e-11)
+    np.testing.assert_allclose(gw["mom"][0, :nn], gf["mom"][0, :nn], rtol=1e-9, atol=1e-6)
+    np.testing.assert_allclose(gw["h"][0, :nn], gf["h"][0, :nn], rtol=1e-11)
+    o = oracle_run(oracle_mod, w, steps=steps)
+    assert_parity(gw, o, h_av(w))
