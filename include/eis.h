@@ -195,6 +195,12 @@ eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
  * candidates), rather than only the single-phase fast path.  Synchronises the stream. */
 eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps);
 
+/* Window diagnostics (tiled layout, context created with the environment variable
+ * EIS_WINDOW_DEBUG set): per window full step of the last step, 5 int64 each -- SM clock cycles,
+ * dual-time iterations, window owned cells, phase boundaries in the window grid, start clock.
+ * *count = windows of the last step; out may be NULL (count query). */
+eis_status eis_window_diag(eis_ctx* ctx, int64_t* out, int64_t capacity, int64_t* count);
+
 /* Kernel timing (measurement support): with timing enabled, every step launch records CUDA
  * events on the context's stream around each kernel (a few microseconds per step).
  * eis_get_timing synchronises the stream and returns the summed milliseconds since

@@ -75,7 +75,7 @@ class Thresholds(C.Structure):
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
            "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info", "eis_set_timing",
-           "eis_get_timing")
+           "eis_get_timing", "eis_window_diag")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
 XB_REC = 3 * HALO + 1
@@ -104,6 +104,7 @@ def lib():
         L.eis_member_status.argtypes = [vp, P(i32)]
         L.eis_member_stats.argtypes = [vp, P(Stats)]
         L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+        L.eis_window_diag.argtypes = [vp, P(C.c_int64), C.c_int64, P(C.c_int64)]
         L.eis_set_timing.argtypes = [vp, C.c_int32]
         L.eis_get_timing.argtypes = [vp, P(C.c_double), P(C.c_int64)]
         L.eis_last_error.argtypes = [vp]
@@ -239,6 +240,15 @@ class Context:
 
     def step_finish(self, t_end: float = float("inf"), after_step: bool = True):
         self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
+
+    def window_diag(self):
+        """(count, 5) int64 array: cycles, DTS iterations, window cells, boundaries, start clock."""
+        n = C.c_int64()
+        self._check(lib().eis_window_diag(self._ctx, None, 0, C.byref(n)), "eis_window_diag")
+        out = np.zeros((max(n.value, 1), 5), dtype=np.int64)
+        self._check(lib().eis_window_diag(self._ctx, out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)),
+                    "eis_window_diag")
+        return out[:n.value]
 
     def set_timing(self, enable: bool = True):
         self._check(lib().eis_set_timing(self._ctx, int(bool(enable))), "eis_set_timing")

@@ -50,6 +50,7 @@ struct eis_ctx {
   Tiles tl;
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow, *t_wlist;
+  long long* t_wdbg = nullptr;
   double* t_part2;
   int slow_grid, win_grid;
   size_t smem_win;
@@ -297,7 +298,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
        cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
-       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 8 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
        cudaMalloc(&c->t_wlist, (size_t)ntiles * 12) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
@@ -308,6 +309,11 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   Tiles& tl = c->tl;
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
   tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
+  tl.wdbg = nullptr;
+  if (getenv("EIS_WINDOW_DEBUG")) {
+    if (cudaMalloc(&c->t_wdbg, (size_t)ntiles * 5 * 8) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
+    tl.wdbg = c->t_wdbg;
+  }
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
   if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
@@ -412,10 +418,11 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   if (c->tiled) return create_tiled(c, out);
   if (cap > 16384) { delete c; return EIS_E_ARG; }
   // CTA size: 128 threads (3 bulk warps + the solver warp, 128 registers per thread) up to
-  // 2048 cells; larger members use 1024 threads
+  // 2048 cells; larger members 512 threads (128 registers: the solver code does not spill;
+  // measured on C4 against 256 and 1024 threads)
   int T = grid->threads;
   if (T <= 0) {
-    T = cap <= 2048 ? 128 : 1024;
+    T = cap <= 2048 ? 128 : 512;
     if (grid->n_cells < 128) T = 64;
   }
   if (T % 32 || T < 64 || T > 1024) { delete c; return EIS_E_ARG; }  // >= 1 bulk warp + the solver warp
@@ -426,11 +433,11 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if ((int)c->smem > max_optin) { delete c; return EIS_E_CAPACITY; }
-  // tuning knob (development): CTAs per SM the 256-thread variant is compiled for (2, 3, 4)
+  // tuning knob (development): CTAs per SM the 256-thread variant is compiled for (2 or 4)
   c->minb = 4;
-  if (const char* ev = getenv("EIS_RESIDENT_MINB")) { int v = atoi(ev); if (v >= 2 && v <= 4) c->minb = v; }
+  if (const char* ev = getenv("EIS_RESIDENT_MINB")) { int v = atoi(ev); if (v == 2 || v == 4) c->minb = v; }
   cudaError_t e1 = cudaFuncSetAttribute(resident_steps<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
-  cudaError_t e3 = cudaFuncSetAttribute(resident_steps<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  cudaError_t e3 = cudaFuncSetAttribute(resident_steps<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e4 = cudaFuncSetAttribute(resident_steps<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e2 = cudaFuncSetAttribute(resident_steps<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   if (cudaFuncSetAttribute(resident_steps<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
@@ -456,7 +463,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
-  cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist);
+  cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   delete c;
@@ -486,6 +493,21 @@ extern "C" eis_status eis_get_timing(eis_ctx* c, double* ms, int64_t* launches) 
       CU(cudaEventElapsedTime(&t, c->ev_pool[m[q]], c->ev_pool[m[q + 1]]));
       ms[q] += t;
     }
+  }
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_window_diag(eis_ctx* c, int64_t* out, int64_t capacity, int64_t* count) {
+  if (!c || !count) return EIS_E_ARG;
+  if (!c->tiled || !c->t_wdbg) return fail(c, EIS_E_ARG, "eis_window_diag: tiled context created with EIS_WINDOW_DEBUG set%s");
+  int ctl[9];
+  CU(cudaMemcpyAsync(ctl, c->t_ctl, sizeof(ctl), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  *count = ctl[8];
+  if (out && capacity > 0) {
+    const long long n = std::min<long long>(capacity, ctl[8]);
+    CU(cudaMemcpyAsync(out, c->t_wdbg, (size_t)n * 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
   }
   return EIS_OK;
 }
@@ -639,10 +661,10 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
       resident_steps<128, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else if (c->threads <= 256 && c->minb == 4)
       resident_steps<256, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
-    else if (c->threads <= 256 && c->minb == 3)
-      resident_steps<256, 3><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else if (c->threads <= 256)
       resident_steps<256, 2><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else if (c->threads <= 512)
+      resident_steps<512, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else
       resident_steps<1024, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     if (c->timing) { m[1] = timing_event(c); c->ev_marks.push_back(m); }

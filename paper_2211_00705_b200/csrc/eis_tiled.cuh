@@ -40,11 +40,13 @@ struct Tiles {
   int* slow;                       // work list of tiles needing the full step of the whole tile
   int* wlist;                      // work list of (tile, window begin, window end): full step of a window
   double* part2;                   // per tiled_slow CTA: S_max, h_min
+  long long* wdbg;                 // diagnostics (EIS_WINDOW_DEBUG): per window job of the last step
+                                   // {cycles, dts iterations, window cells, boundaries, start clock}
   int ntiles, capt, nbr_left, nbr_right;
   int wmax;                        // largest window (owned cells) of a window full step (<= WMAX)
 };
 // ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] tile-list length  [5] next tile job
-//      [6] window-list length  [7] next window job
+//      [6] window-list length  [7] next window job  [8] window jobs of the last step
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -92,6 +94,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
   __syncthreads();
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
+    tl.ctl[8] = tl.ctl[6];  // window jobs of this step (diagnostics)
     tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0;
     if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
       tl.xbuf[XB_DT] = -s;
@@ -468,20 +471,43 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
 // ------------------------------------------------------------------------------------------
 constexpr int WCAP = WMAX + 2 * HALO + MAXEV + MAXTRG + 2;  // window grid capacity (even)
 
-// move out[s, e) to out[s + d, e + d) (block-wide, chunked; overlapping ranges are safe)
-__device__ __forceinline__ void shift_cells(double* a0, double* a1, double* a2, int s, int e, int d) {
-  if (d == 0 || s >= e) return;
-  const int T = blockDim.x, tid = threadIdx.x;
-  const int nch = (e - s + T - 1) / T;
+// Fast cells of a window tile: out[s, e) moves to out[s + d, e + d) (d = 0: stays), and their
+// CFL partials (plain cells: |m| rcp(rho) + a, never tiny) and width uniformity are folded on
+// the way.  Block-wide, chunks of FP_U x blockDim cells with all loads in flight; chunks run
+// against the direction of the move, so overlapping ranges are safe.
+constexpr int FP_U = 4;
+__device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, double* omom, double* oh, double h_av,
+                                               int s, int en, int d, double& sf, double& hf, bool& uf) {
+  if (s >= en) return;
+  const int T = blockDim.x, tid = threadIdx.x, CH = FP_U * T;
+  const int nch = (en - s + CH - 1) / CH;
   for (int q = 0; q < nch; ++q) {
-    const int lo = d > 0 ? max(s, e - (q + 1) * T) : s + q * T;
-    const int hi = d > 0 ? e - q * T : min(e, s + (q + 1) * T);
-    const int i = lo + tid;
-    double v0 = 0, v1 = 0, v2 = 0;
-    if (i < hi) { v0 = a0[i]; v1 = a1[i]; if (a2) v2 = a2[i]; }
-    __syncthreads();
-    if (i < hi) { a0[i + d] = v0; a1[i + d] = v1; if (a2) a2[i + d] = v2; }
-    __syncthreads();
+    const int lo = d > 0 ? max(s, en - (q + 1) * CH) : s + q * CH;
+    const int hi = d > 0 ? en - q * CH : min(en, s + (q + 1) * CH);
+    double r[FP_U], m[FP_U], h[FP_U];
+#pragma unroll
+    for (int u = 0; u < FP_U; ++u) {
+      const int i = lo + tid + u * T;
+      r[u] = 1.0; m[u] = 0.0; h[u] = h_av;
+      if (i < hi) { r[u] = orho[i]; m[u] = omom[i]; if (oh) h[u] = oh[i]; }
+    }
+#pragma unroll
+    for (int u = 0; u < FP_U; ++u) {
+      if (lo + tid + u * T < hi) {
+        sf = fmax(sf, fabs(m[u] * rcp_fast(r[u])) + sound(e, phase_of(e, r[u])));
+        hf = fmin(hf, h[u]);
+        uf &= h[u] == h_av;
+      }
+    }
+    if (d != 0) {
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < FP_U; ++u) {
+        const int i = lo + tid + u * T;
+        if (i < hi) { orho[i + d] = r[u]; omom[i + d] = m[u]; if (oh) oh[i + d] = h[u]; }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -539,15 +565,14 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     double* const omom = tl.mom[g.out] + g.base;
     double* const oh = tl.h[g.out] + g.base;
     const int pa = wa - nL;  // output position of the window's first cell
-    shift_cells(orho, omom, g.hu_in ? nullptr : oh, wb - nL, cnt, d);  // fast cells right of it
+    // fast cells: left of the window (stay), right of it (shift by d); partials, uniformity
+    double sf = 0.0, hf = INFINITY;
+    bool uf = true;
+    fast_part_pass(e, orho, omom, g.hu_in ? nullptr : oh, p.h_av, 0, pa, 0, sf, hf, uf);
+    fast_part_pass(e, orho, omom, g.hu_in ? nullptr : oh, p.h_av, wb - nL, cnt, d, sf, hf, uf);
     bool uw = true;
     for (int i = olo + tid; i < ohi; i += T) uw &= A.h[i] == p.h_av;
-    const bool unif_w = __syncthreads_and(uw);
-    bool uf = true;  // fast cells' widths (stored unless the input tile was uniform)
-    if (!g.hu_in)
-      for (int q = tid; q < nout; q += T)
-        if (q < pa || q >= pa + nw_out) uf &= oh[q] == p.h_av;
-    unif = __syncthreads_and(uf) && unif_w;
+    unif = __syncthreads_and(uw && uf);
     for (int i = tid; i < nw_out; i += T) {
       orho[pa + i] = A.rho[olo + i];
       omom[pa + i] = A.mom[olo + i];
@@ -556,20 +581,11 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     if (!unif && g.hu_in)
       for (int q = tid; q < nout; q += T)
         if (q < pa || q >= pa + nw_out) oh[q] = p.h_av;
-    // CFL partials: the window's cells (tiny test inside the window grid) ...
+    // CFL partials: the window's cells (tiny test inside the window grid) and the fast cells
     double s, hm;
     cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, false, false, s, hm);
-    s_th = s; h_th = hm;
-    // ... and the fast cells (plain: never tiny), from the output
-    double sf = 0.0, hf = INFINITY;
-    for (int q = tid; q < nout; q += T) {
-      if (q >= pa && q < pa + nw_out) continue;
-      const double r = orho[q];
-      sf = fmax(sf, fabs(omom[q] * rcp_fast(r)) + sound(e, phase_of(e, r)));
-      hf = fmin(hf, g.hu_in ? p.h_av : oh[q]);
-    }
-    s_th = fmax(s_th, warp_max(sf));
-    h_th = fmin(h_th, warp_min(hf));
+    s_th = fmax(s, warp_max(sf));
+    h_th = fmin(hm, warp_min(hf));
     __syncthreads();
     if (g.xl || g.xr) {  // rank mode: send records of the first / last HALO output cells
       for (int q = tid; q < 2 * HALO; q += T) {
@@ -632,7 +648,13 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
     __syncthreads();
     const int j = sh.n_new;
     if (j >= njobs) break;
+    const long long c0 = clock64();
     tile_window(e, p, tl, sh, A, WCAP, tl.wlist[3 * j], tl.wlist[3 * j + 1], tl.wlist[3 * j + 2], t, t_end, dt_given);
+    if (tl.wdbg && tid == 0) {
+      long long* d = tl.wdbg + 5 * (long long)j;
+      d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[3 * j + 2] - tl.wlist[3 * j + 1];
+      d[3] = sh.nifc; d[4] = c0;
+    }
   }
 }
 
