@@ -196,8 +196,10 @@ eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
 eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps);
 
 /* Window diagnostics (tiled layout, context created with the environment variable
- * EIS_WINDOW_DEBUG set): per window full step of the last step, 5 int64 each -- SM clock cycles,
- * dual-time iterations, window owned cells, phase boundaries in the window grid, start clock.
+ * EIS_WINDOW_DEBUG set): per window full step of the last step, 11 int64 each -- SM clock cycles,
+ * dual-time iterations, window owned cells, phase boundaries in the window grid, start clock,
+ * then 6 phase durations (load, to barrier A, to barrier B, creations, remesh, assembly; zero
+ * unless the library was built with -DEIS_PHASE_CLOCK).
  * *count = windows of the last step; out may be NULL (count query). */
 eis_status eis_window_diag(eis_ctx* ctx, int64_t* out, int64_t capacity, int64_t* count);
 

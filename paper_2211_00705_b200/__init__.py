@@ -242,10 +242,10 @@ class Context:
         self._check(lib().eis_step_finish(self._ctx, float(t_end), int(bool(after_step))), "eis_step_finish")
 
     def window_diag(self):
-        """(count, 5) int64 array: cycles, DTS iterations, window cells, boundaries, start clock."""
+        """(count, 11) int64: cycles, DTS iterations, window cells, boundaries, start clock, 6 phases."""
         n = C.c_int64()
         self._check(lib().eis_window_diag(self._ctx, None, 0, C.byref(n)), "eis_window_diag")
-        out = np.zeros((max(n.value, 1), 5), dtype=np.int64)
+        out = np.zeros((max(n.value, 1), 11), dtype=np.int64)
         self._check(lib().eis_window_diag(self._ctx, out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)),
                     "eis_window_diag")
         return out[:n.value]

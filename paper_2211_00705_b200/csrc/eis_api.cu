@@ -311,7 +311,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
   tl.wdbg = nullptr;
   if (getenv("EIS_WINDOW_DEBUG")) {
-    if (cudaMalloc(&c->t_wdbg, (size_t)ntiles * 5 * 8) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
+    if (cudaMalloc(&c->t_wdbg, (size_t)ntiles * WDBG_FIELDS * 8) != cudaSuccess ||
+        cudaMemset(c->t_wdbg, 0, (size_t)ntiles * WDBG_FIELDS * 8) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
     tl.wdbg = c->t_wdbg;
   }
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
@@ -506,7 +507,7 @@ extern "C" eis_status eis_window_diag(eis_ctx* c, int64_t* out, int64_t capacity
   *count = ctl[8];
   if (out && capacity > 0) {
     const long long n = std::min<long long>(capacity, ctl[8]);
-    CU(cudaMemcpyAsync(out, c->t_wdbg, (size_t)n * 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(out, c->t_wdbg, (size_t)n * WDBG_FIELDS * 8, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
   }
   return EIS_OK;

@@ -91,7 +91,15 @@ struct CtaShared {
   int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
   unsigned long long c_dts, c_solves, c_regions, c_dtsmax;
   MemberStats st;
+#ifdef EIS_PHASE_CLOCK
+  long long tclk[10];  // development: clock64 at phase boundaries of the last step (thread 0)
+#endif
 };
+#ifdef EIS_PHASE_CLOCK
+#define EIS_TCLK(i) do { if (threadIdx.x == 0) sh.tclk[i] = clock64(); } while (0)
+#else
+#define EIS_TCLK(i) do { } while (0)
+#endif
 
 __device__ __forceinline__ void set_status(CtaShared& sh, int code) { atomicCAS(&sh.status, 0, code); }
 
@@ -557,6 +565,10 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     h_part = warp_min(h_part);
     if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }  // folded after barrier A
     __syncthreads();  // ---------------- barrier A ----------------
+    EIS_TCLK(1);
+#ifdef EIS_PHASE_CLOCK
+    if (threadIdx.x == 32) sh.tclk[9] = clock64();
+#endif
     // lane-parallel fold of the per-warp partials (every warp computes the same dt)
     const double smax = warp_max(lane < nw ? sh.part_s[lane] : 0.0);
     const double hmin = warp_min(lane < nw ? sh.part_h[lane] : INFINITY);
@@ -568,6 +580,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
 
     if (warp == SW) {
       // ---------------- S4: dual time stepping on every block (a9) ----------------
+#ifdef EIS_PHASE_CLOCK
+      if (lane == 0) sh.tclk[6] = clock64();
+#endif
       const int nblk = sh.nblk;
       for (int k = 0; k < nblk; ++k) {
         const int a = sh.blkA[k], b = sh.blkB[k];
@@ -581,6 +596,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
           if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
         }
       }
+#ifdef EIS_PHASE_CLOCK
+      if (lane == 0) sh.tclk[7] = clock64();
+#endif
       // ---------------- S5: cells next to explicit phase boundaries (a7) ----------------
       const int nif = sh.nifc;
       for (int q = lane; q < 2 * nif; q += 32) {
@@ -604,6 +622,10 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     if (warp < nbulk) bulk_p2(p, sh, rho, mom, h, F0, F1, fl, n, warp, nbulk, ntrg, dt, dt_hav);
     if (remesh) sh.remesh = 1;
     __syncthreads();  // ---------------- barrier B ----------------
+    EIS_TCLK(2);
+#ifdef EIS_PHASE_CLOCK
+    if (threadIdx.x == 32) sh.tclk[8] = clock64();
+#endif
     // ---------------- creations (a6): acceptance (R16), solves, neighbour updates ----------------
     if (ntrg) {
       for (int k = tid; k < ntrg; k += T) {
@@ -642,6 +664,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       __syncthreads();
     }
     {
+      EIS_TCLK(3);
       const int stop2 = sh.status;
       __syncthreads();
       if (stop2) return -1.0;
@@ -770,6 +793,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     }
     __syncthreads();
     if (tid == 0) {
+      EIS_TCLK(4);
       MemberStats& st = sh.st;
       st.steps += 1;
       st.cell_updates += n;

@@ -41,7 +41,8 @@ struct Tiles {
   int* wlist;                      // work list of (tile, window begin, window end): full step of a window
   double* part2;                   // per tiled_slow CTA: S_max, h_min
   long long* wdbg;                 // diagnostics (EIS_WINDOW_DEBUG): per window job of the last step
-                                   // {cycles, dts iterations, window cells, boundaries, start clock}
+                                   // {cycles, dts iterations, window cells, boundaries, start clock,
+                                   //  6 phase cycles (EIS_PHASE_CLOCK builds, else 0)}
   int ntiles, capt, nbr_left, nbr_right;
   int wmax;                        // largest window (owned cells) of a window full step (<= WMAX)
 };
@@ -50,6 +51,7 @@ struct Tiles {
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
+constexpr int WDBG_FIELDS = 11;
 constexpr int XB_REC = 3 * HALO + 1;
 constexpr int XB_SEND_LEFT = 0, XB_SEND_RIGHT = XB_REC, XB_RECV_LEFT = 2 * XB_REC, XB_RECV_RIGHT = 3 * XB_REC;
 constexpr int XB_DT = 4 * XB_REC;
@@ -543,6 +545,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   __syncthreads();
   if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, n);
   __syncthreads();
+  EIS_TCLK(0);
   Zone Z;
   Z.own_lo = wa - s0; Z.own_hi = wb - s0;
   Z.zlo = max(Z.own_lo - 2, 0); Z.zhi = min(Z.own_hi + 2, n);
@@ -603,6 +606,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   }
   if (lane == 0) { sh.part_s[warp] = s_th; sh.part_h[warp] = h_th; }
   __syncthreads();
+  EIS_TCLK(5);
   if (tid == 0) {
     if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
     if (dt >= 0.0 && st == 0) {
@@ -651,9 +655,18 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
     const long long c0 = clock64();
     tile_window(e, p, tl, sh, A, WCAP, tl.wlist[3 * j], tl.wlist[3 * j + 1], tl.wlist[3 * j + 2], t, t_end, dt_given);
     if (tl.wdbg && tid == 0) {
-      long long* d = tl.wdbg + 5 * (long long)j;
+      long long* d = tl.wdbg + WDBG_FIELDS * (long long)j;
       d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[3 * j + 2] - tl.wlist[3 * j + 1];
       d[3] = sh.nifc; d[4] = c0;
+#ifdef EIS_PHASE_CLOCK
+      // phases: load+list | P1,S1,S2 to barrier A | to barrier B | creations | remesh,stats | assembly
+      long long* q = d + 5;
+      q[0] = sh.tclk[0] - c0;
+      for (int i = 1; i < 6; ++i) q[i] = sh.tclk[i] - sh.tclk[i - 1];
+      q[3] = sh.tclk[7] - sh.tclk[6];  // (replaces "creations": the solver warp's S4, DTS)
+      q[4] = sh.tclk[8] - sh.tclk[2];  // (replaces: thread 32 vs thread 0 leaving barrier B)
+      q[5] = sh.tclk[9] - sh.tclk[1];  // (replaces: thread 32 vs thread 0 leaving barrier A)
+#endif
     }
   }
 }
