@@ -172,30 +172,33 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 }
 
 // ------------------------------------------------------------------------------------------
-// tiled_fast: one CTA per tile.  Warp windows of 32 lanes over virtual cells s-1 .. s+30 (lane
-// 0 is the left neighbour; ghosts clamp at the grid ends, R15): u = m/rho and p (a1), the HLL
-// flux of edge s-1+lane on lanes 1..31 (a3), the creation pre-filter (a4, R7), the right flux
-// by shuffle and the update of cells s .. s+29 (a7) written to the output tile with the
-// next step's CFL partials (a2) -- the same expressions as step_body's bulk passes, so a plain
-// tile's result is the full step's bit for bit.  Windows are loaded in batches of FB (all
-// loads in flight before the arithmetic).  Outputs of a tile that turns out not plain are
-// overwritten by tiled_slow.
+// tiled_fast: one CTA per tile.  Warp windows of 64 virtual cells s-2 .. s+61, two per lane
+// (c0 = s-2+2l, c1 = c0+1; ghosts clamp at the grid ends, R15): u = m/rho and p (a1), the HLL
+// fluxes of the lane's left edge (c0; the left state by shuffle from the previous lane) and of
+// its internal edge (c1) (a3), the creation pre-filter on both (a4, R7), the right flux of c1
+// by shuffle and the updates of the pairs of lanes 1..30, cells s .. s+59 (a7; lanes 0
+// and 31 are halo, so every store is an aligned 16-byte pair) written to the output tile with
+// the next step's CFL partials (a2) -- the same expressions as step_body's bulk passes, so a
+// plain tile's result is the full step's bit for bit.  Interior windows load and store cell
+// pairs as 16-byte vectors.  Windows are loaded in batches of FB (all loads in flight before
+// the arithmetic).  Outputs of a tile that turns out not plain are overwritten by the full step.
 // ------------------------------------------------------------------------------------------
 #ifndef EIS_FB
-#define EIS_FB 3
+#define EIS_FB 2
 #endif
-constexpr int FB = EIS_FB;  // windows per warp per batch (measured: 3 best of 2, 3, 4, 8 at 128 threads)
+constexpr int FB = EIS_FB;  // windows per warp per batch
+constexpr int FW = 60;      // cells updated per window: the pairs of lanes 1..30
 
-// one window batch of one warp after its loads: the arithmetic, specialised by the phase the
-// warp's first cell has (LIQ) and by uniform widths (HU).  A cell of another phase (or spinodal,
-// or non-positive) and the right cell of a creation-candidate edge are "special": their index
-// range [slo, shi] decides between the fast result and a full step of a window around them.
+// one window batch of one warp after its loads: the arithmetic, specialised by the phase (LIQ)
+// and by uniform widths (HU).  A cell of another phase (or spinodal, or non-positive) and the
+// right cell of a creation-candidate edge are "special": their index range [slo, shi] decides
+// between the fast result and a full step of a window around them.
 template <bool HU, bool LIQ>
-__device__ __forceinline__ void fast_windows(const Eos& e, const double (&rr)[FB], const double (&mm)[FB], int w0, int nw,
-                                             int nwin, int n, int own_lo, int own_hi, double dt, double dt_hav,
-                                             double h_av, const double* ih, double* orho, double* omom, double* oh,
-                                             int& slo, int& shi, bool& unif, double& snum, double& sden,
-                                             double& h_part) {
+__device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB], const double2 (&mv)[FB], int w0,
+                                           int nw, int nwin, int n, int own_lo, int own_hi, double dt, double dt_hav,
+                                           double h_av, const double* ih, double* orho, double* omom, double* oh,
+                                           int& slo, int& shi, bool& unif, double& snum, double& sden,
+                                           double& h_part) {
   const int lane = threadIdx.x & 31;
   const double a = LIQ ? e.a_l : e.a_v;
   const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
@@ -203,36 +206,58 @@ __device__ __forceinline__ void fast_windows(const Eos& e, const double (&rr)[FB
 #pragma unroll
   for (int b = 0; b < FB; ++b) {
     if (w0 + nw * b >= nwin) break;  // warp-uniform
-    const int c = 30 * (w0 + nw * b) - 1 + lane;
-    const double rc = rr[b], mc = mm[b];
-    const double uc = mc * rcp_fast(rc);
+    const int c0 = FW * (w0 + nw * b) - 2 + 2 * lane, c1 = c0 + 1;
+    const double r0 = rv[b].x, r1 = rv[b].y, m0 = mv[b].x, m1 = mv[b].y;
+    const double u0 = m0 * rcp_fast(r0), u1 = m1 * rcp_fast(r1);
     // lanes beyond the grid hold clamped copies of real cells: every cell of [0, n) is checked
-    bool sp = LIQ ? !(rc >= rho_min) : !(rc <= rho_tilde && rc > 0.0);
-    const double pc = LIQ ? p0 + a_l2 * (rc - rho0) : a_v2 * rc;
-    const double rl = __shfl_up_sync(0xffffffffu, rc, 1), ml = __shfl_up_sync(0xffffffffu, mc, 1);
-    const double ul = __shfl_up_sync(0xffffffffu, uc, 1), pl = __shfl_up_sync(0xffffffffu, pc, 1);
-    double f0, f1;  // edge c (between c-1 and c)
-    hll_fast(a, rl, ml, ul, pl, rc, mc, uc, pc, f0, f1);
-    {  // creation pre-filters (R7) as bulk_p1; at ghost / duplicate edges du = 0: no candidate
-      const double du = uc - ul, x = rl * rc;
-      sp |= LIQ ? !(du * x <= e.a_l * (x - rmin2) - 1e-9 * x) : (du < -e.a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
+    const bool sp0 = LIQ ? !(r0 >= rho_min) : !(r0 <= rho_tilde && r0 > 0.0);
+    bool sp1 = LIQ ? !(r1 >= rho_min) : !(r1 <= rho_tilde && r1 > 0.0);
+    const double q0 = LIQ ? p0 + a_l2 * (r0 - rho0) : a_v2 * r0;
+    const double q1 = LIQ ? p0 + a_l2 * (r1 - rho0) : a_v2 * r1;
+    const double rl = __shfl_up_sync(0xffffffffu, r1, 1), ml = __shfl_up_sync(0xffffffffu, m1, 1);
+    const double ul = __shfl_up_sync(0xffffffffu, u1, 1), pl = __shfl_up_sync(0xffffffffu, q1, 1);
+    double fl0, fl1, fi0, fi1;  // edge c0 (left of c0), edge c1 (between c0 and c1)
+    hll_fast(a, rl, ml, ul, pl, r0, m0, u0, q0, fl0, fl1);
+    hll_fast(a, r0, m0, u0, q0, r1, m1, u1, q1, fi0, fi1);
+    bool cl;  // creation pre-filters (R7) as bulk_p1; ghost / duplicate edges have du = 0
+    {
+      const double du = u0 - ul, x = rl * r0;
+      cl = lane > 0 && (LIQ ? !(du * x <= e.a_l * (x - rmin2) - 1e-9 * x) : (du < -e.a_v * (2.0 - (rl + r0) * inv_rt) + 1e-9));
     }
-    if (sp) {
-      const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
-      slo = min(slo, cc);
-      shi = max(shi, cc);
+    {
+      const double du = u1 - u0, x = r0 * r1;
+      sp1 |= LIQ ? !(du * x <= e.a_l * (x - rmin2) - 1e-9 * x) : (du < -e.a_v * (2.0 - (r0 + r1) * inv_rt) + 1e-9);
     }
-    const double g0 = __shfl_down_sync(0xffffffffu, f0, 1), g1 = __shfl_down_sync(0xffffffffu, f1, 1);
-    if (lane >= 1 && lane <= 30 && c >= own_lo && c < own_hi) {  // P2, h^{n+1} = h^n
-      double cfac = dt_hav, hn = h_av;
-      if (!HU) { hn = ih[c]; if (hn != h_av) cfac = dt / hn; }
-      const double r1 = rc - cfac * (g0 - f0);
-      const double m1 = mc - cfac * (g1 - f1);
-      orho[c] = r1;
-      omom[c] = m1;
-      if (!HU) { oh[c] = hn; unif &= hn == h_av; h_part = fmin(h_part, hn); }
-      const double am = fabs(m1);
-      if (am * sden > snum * r1) { snum = am; sden = r1; }
+    if (sp0 || cl) { const int cc = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0); slo = min(slo, cc); shi = max(shi, cc); }
+    if (sp1) { const int cc = c1 < 0 ? 0 : (c1 >= n ? n - 1 : c1); slo = min(slo, cc); shi = max(shi, cc); }
+    const double fr0 = __shfl_down_sync(0xffffffffu, fl0, 1), fr1 = __shfl_down_sync(0xffffffffu, fl1, 1);
+    // P2, h^{n+1} = h^n: the pair of lanes 1..30 (own_lo is even, so both or neither
+    // cell of a pair are own except the last cell of a tile with an odd end)
+    const bool inner = lane >= 1 && lane <= 30;
+    const bool up0 = inner && c0 >= own_lo && c0 < own_hi;
+    const bool up1 = inner && c1 >= own_lo && c1 < own_hi;
+    double ca = dt_hav, cb = dt_hav, ha = h_av, hb = h_av;
+    if (!HU) {
+      if (up0) { ha = ih[c0]; if (ha != h_av) ca = dt / ha; }
+      if (up1) { hb = ih[c1]; if (hb != h_av) cb = dt / hb; }
+    }
+    const double n0 = r0 - ca * (fi0 - fl0), k0 = m0 - ca * (fi1 - fl1);
+    const double n1 = r1 - cb * (fr0 - fi0), k1 = m1 - cb * (fr1 - fi1);
+    if (up0 && up1) {  // c0 even: 16-byte aligned pair in the output tile
+      *reinterpret_cast<double2*>(orho + c0) = make_double2(n0, n1);
+      *reinterpret_cast<double2*>(omom + c0) = make_double2(k0, k1);
+    } else if (up0) {
+      orho[c0] = n0; omom[c0] = k0;
+    }
+    if (up0) {
+      if (!HU) { oh[c0] = ha; unif &= ha == h_av; h_part = fmin(h_part, ha); }
+      const double am = fabs(k0);
+      if (am * sden > snum * n0) { snum = am; sden = n0; }
+    }
+    if (up1) {
+      if (!HU) { oh[c1] = hb; unif &= hb == h_av; h_part = fmin(h_part, hb); }
+      const double am = fabs(k1);
+      if (am * sden > snum * n1) { snum = am; sden = n1; }
     }
   }
 }
@@ -264,22 +289,26 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   int phases = 0;        // 1 vapour, 2 liquid: the warps' specialisations
   double snum = 0.0, sden = 1.0;  // max |m|/rho of the new cells, by cross-multiplication
   double h_part = HU ? h_av : INFINITY;
-  const int nwin = (n + 29) / 30;
+  const int nwin = (n + FW - 1) / FW;  // windows update cells [0, 60 nwin)
   for (int w0 = warp; w0 < nwin; w0 += nw * FB) {
-    double rr[FB], mm[FB];
+    double2 rv[FB], mv[FB];
 #pragma unroll
     for (int b = 0; b < FB; ++b) {  // all loads of the batch first
       const int wi = w0 + nw * b;
-      const int c = 30 * wi - 1 + lane;
-      rr[b] = 1.0; mm[b] = 0.0;
+      const int c0 = FW * wi - 2 + 2 * lane;
+      rv[b] = make_double2(1.0, 1.0); mv[b] = make_double2(0.0, 0.0);
       if (wi < nwin) {
-        if (30 * wi - 1 >= own_lo && 30 * wi + 30 < own_hi) {  // interior window (warp-uniform)
-          rr[b] = segO[c]; mm[b] = segO[c + mo_t];
+        if (FW * wi - 2 >= own_lo && FW * wi + 62 <= own_hi) {  // interior window: aligned pairs
+          rv[b] = *reinterpret_cast<const double2*>(segO + c0);
+          mv[b] = *reinterpret_cast<const double2*>(segO + c0 + mo_t);
         } else {
-          const int cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
-          const double* pr = cc < own_lo ? segL : (cc < own_hi ? segO : segR);
-          const long long mo = cc < own_lo ? moL : (cc < own_hi ? mo_t : moR);
-          rr[b] = pr[cc]; mm[b] = pr[cc + mo];
+          const int ca = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0), cb = c0 + 1 < 0 ? 0 : (c0 + 1 >= n ? n - 1 : c0 + 1);
+          const double* pa = ca < own_lo ? segL : (ca < own_hi ? segO : segR);
+          const long long ma = ca < own_lo ? moL : (ca < own_hi ? mo_t : moR);
+          const double* pb = cb < own_lo ? segL : (cb < own_hi ? segO : segR);
+          const long long mb = cb < own_lo ? moL : (cb < own_hi ? mo_t : moR);
+          rv[b] = make_double2(pa[ca], pb[cb]);
+          mv[b] = make_double2(pa[ca + ma], pb[cb + mb]);
         }
       }
     }
@@ -287,13 +316,13 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     // warps that differ make the tile take the whole-tile full step
     bool anyl = false;
 #pragma unroll
-    for (int b = 0; b < FB; ++b) anyl |= w0 + nw * b < nwin && rr[b] >= e.rho_min;
+    for (int b = 0; b < FB; ++b) anyl |= w0 + nw * b < nwin && (rv[b].x >= e.rho_min || rv[b].y >= e.rho_min);
     const bool liq = __any_sync(0xffffffffu, anyl);
     phases |= liq ? 2 : 1;
-    if (liq) fast_windows<HU, true>(e, rr, mm, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
-                                    slo, shi, unif, snum, sden, h_part);
-    else fast_windows<HU, false>(e, rr, mm, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
-                                 slo, shi, unif, snum, sden, h_part);
+    if (liq) fast_pairs<HU, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                  slo, shi, unif, snum, sden, h_part);
+    else fast_pairs<HU, false>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                               slo, shi, unif, snum, sden, h_part);
   }
   // S_max of this lane's new cells: |m| rcp(rho) (+ a below, as cfl_partials; one phase)
   const double s_lane = warp_max(snum * rcp_fast(sden));
