@@ -277,13 +277,13 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     delete c; return EIS_E_CUDA;
   }
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
-  if (cudaFuncSetAttribute(tiled_win<64, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+  if (cudaFuncSetAttribute(tiled_win<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   int nsm = 0, per_sm = 0, per_sm_w = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<64, 16>, 64, c->smem_win);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<32, 16>, 32, c->smem_win);
   c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
   c->win_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm_w, 1));
   const size_t tc = (size_t)ntiles * capt;
@@ -625,7 +625,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   if (c->timing) m[0] = timing_event(c);
   tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[1] = timing_event(c);
-  tiled_win<64, 16><<<c->win_grid, 64, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_win<32, 16><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) { m[3] = timing_event(c); c->ev_marks.push_back(m); }

@@ -482,7 +482,8 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
   const int half = lane >> 4, hl = lane & 15;
   const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int nbulk = sh.nifc > 0 ? nw - 1 : nw;  // the solver warp joins the bulk when idle
+  // the solver warp joins the bulk when idle; a one-warp CTA (tiled windows) does all in order
+  const int nbulk = (sh.nifc > 0 && nw > 1) ? nw - 1 : nw;
   if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
     double s_part = 0.0, h_part = INFINITY;
 

@@ -16,7 +16,7 @@ for target in [int(a) for a in (sys.argv[1:] or ["1", "2", "5", "40", "200", "50
     ctx.set_timing(True); ctx.step(1); done += 1
     kt = ctx.get_timing(); ctx.set_timing(False)
     d = ctx.window_diag()
-    cyc, it, wc, nb, t0 = d.T
+    cyc, it, wc, nb, t0 = d[:, :5].T
     span = (t0 + cyc).max() - t0.min()
     q = np.percentile(cyc, [50, 90, 99, 100])
     print(f"step {done}: windows {len(d)} fast {kt['fast_ms']:.3f} ms win {kt['window_ms']:.3f} ms slow {kt['tile_ms']:.3f} ms | "
