@@ -306,6 +306,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
+  c->g.dbg = nullptr;
   Tiles& tl = c->tl;
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
   tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
@@ -453,6 +454,12 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
             cudaMalloc(&c->d_cnt, (M + 1) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
+  c->g.dbg = nullptr;
+#ifdef EIS_PHASE_CLOCK
+  if (cudaMalloc(&c->g.dbg, (size_t)M * 64) != cudaSuccess || cudaMemset(c->g.dbg, 0, (size_t)M * 64) != cudaSuccess) {
+    eis_destroy(c); return EIS_E_CUDA;
+  }
+#endif
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
   *out = c;
   return EIS_OK;
@@ -463,6 +470,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_rho); cudaFree(c->d_mom); cudaFree(c->d_h); cudaFree(c->d_t); cudaFree(c->d_n);
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
+  if (!c->tiled) cudaFree(c->g.dbg);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
@@ -587,6 +595,18 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
 
 static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
   const long long M = c->grid.n_members;
+#ifdef EIS_PHASE_CLOCK
+  if (c->g.dbg) {  // development: mean cycles per step (all members)
+    std::vector<long long> d((size_t)M * 8);
+    CU(cudaMemcpyAsync(d.data(), c->g.dbg, (size_t)M * 64, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    double acc[7] = {0};
+    for (long long m = 0; m < M; ++m) for (int i = 0; i < 7; ++i) acc[i] += (double)d[8 * m + i];
+    const double ns = acc[6] > 0 ? acc[6] : 1;
+    fprintf(stderr, "[phase] steps %.0f | cycles/step from start: solver@A %.0f warp0@A %.0f solver@B %.0f warp0@B %.0f end %.0f | S4 %.0f\n",
+            acc[6], acc[0] / ns, acc[1] / ns, acc[2] / ns, acc[3] / ns, acc[4] / ns, acc[5] / ns);
+  }
+#endif
   std::vector<MemberStats> ms(M);
   std::vector<double> t(M);
   CU(cudaMemcpyAsync(ms.data(), c->d_stats, M * sizeof(MemberStats), cudaMemcpyDeviceToHost, c->stream));

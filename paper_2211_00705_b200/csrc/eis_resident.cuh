@@ -72,6 +72,7 @@ struct Members {  // global (HBM) state, member-major SoA
   int* status;
   MemberStats* stats;
   long long cap;
+  long long* dbg;  // development (-DEIS_PHASE_CLOCK): per member summed phase clocks, else null
 };
 
 struct CtaShared {
@@ -95,10 +96,15 @@ struct CtaShared {
   long long tclk[10];  // development: clock64 at phase boundaries of the last step (thread 0)
 #endif
 };
+// development probes (-DEIS_PHASE_CLOCK): clock64 at step start (0), arrivals of the solver
+// warp (1, 3) and of warp 0 (2, 4) at barriers A and B, step end (5), S4 start/end (6, 7).
+// (Reads right after a barrier may issue before the barrier completes, so arrivals are used.)
 #ifdef EIS_PHASE_CLOCK
 #define EIS_TCLK(i) do { if (threadIdx.x == 0) sh.tclk[i] = clock64(); } while (0)
+#define EIS_ARRIVE(i) do { if ((threadIdx.x & 31) == 0) { if (warp == SW) sh.tclk[i] = clock64(); if (warp == 0) sh.tclk[(i) + 1] = clock64(); } } while (0)
 #else
 #define EIS_TCLK(i) do { } while (0)
+#define EIS_ARRIVE(i) do { } while (0)
 #endif
 
 __device__ __forceinline__ void set_status(CtaShared& sh, int code) { atomicCAS(&sh.status, 0, code); }
@@ -357,14 +363,16 @@ __device__ __forceinline__ void zone_status_e(CtaShared& sh, const Zone& Z, int 
 
 // ------------------------------------------------------------------------------------------
 // Bulk pass P1 (own register allocation: the loop invariants stay in registers).
-// window w: lanes hold cells 31w-1 .. 31w+30 (lane 0 is the left halo, transmissive ghosts at
-// the ends, R15); lane j >= 1 owns cell 31w+j-1 and its LEFT edge: HLL flux (a3), creation
-// trigger (a4), S_max / h_min partials (a2).  One reciprocal per lane (u = m/rho); the left
-// neighbour's u and p arrive by shuffle.  Interior windows skip the ghost clamps.
+// window w: 64 cells, two per lane, c0 = 62w-2+2l and c1 = c0+1 (lane 0 is the left halo,
+// transmissive ghosts at the ends, R15); lane l >= 1 owns c0, c1, the LEFT edge of c0 and the
+// edge between c0 and c1: HLL flux (a3), creation trigger (a4), S_max / h_min partials (a2).
+// One reciprocal per cell (u = m/rho); the left neighbour's state arrives by shuffle.
+// Interior windows skip the ghost clamps.  Flagged cells are re-checked in full (rare).
 // ------------------------------------------------------------------------------------------
 __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
-                                     const double* rho, const double* mom, const double* h, double* F0, double* F1,
-                                     const uint8_t* fl, int n, int warp, int nbulk, double* parts) {
+                                     const double* __restrict__ rho, const double* __restrict__ mom,
+                                     const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
+                                     const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
   const Eos e = e_ref;  // constants into registers once (not a generic load per use)
   const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
   const double a_v = e.a_v, a_l = e.a_l, rmin2 = e.rho_min * e.rho_min, inv_rt = 1.0 / e.rho_tilde;
@@ -374,75 +382,102 @@ __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShar
   double s_part = 0.0, h_part = INFINITY;
   bool bad = false;      // a non-positive or spinodal density somewhere (reported below, rare)
   bool special = false;  // a trigger candidate or a phase change (handled below, rare)
-  const int nwin1 = (n + 31) / 31;  // edges 0..n
-  for (int w = warp; w < nwin1; w += nbulk) {
-    const int cj = 31 * w - 1 + lane;
-    const bool interior_win = w > 0 && 31 * w + 31 < n;  // cells cj-1 .. cj+1 all exist
-    int cc = cj, cl = cj - 1;
+  // main pass: windows of 64 cells, two per lane (c0 = 62w-2+2l, c1 = c0+1); lanes >= 1 own
+  // c0, c1, the left edge of c0 (left state by shuffle) and the internal edge c1
+  const int nwp = (n + 62) / 62;  // edges 0..n
+  for (int w = warp; w < nwp; w += nbulk) {
+    const int c0 = 62 * w - 2 + 2 * lane, c1 = c0 + 1;
+    const bool interior_win = w > 0 && 62 * w + 62 < n;  // c0 .. c1 + 1 all exist
+    int i0 = c0, i1 = c1;
     if (!interior_win) {
-      cc = cj < 0 ? 0 : (cj >= n ? n - 1 : cj);
-      cl = cj - 1 < 0 ? 0 : (cj - 1 >= n ? n - 1 : cj - 1);
+      i0 = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0);
+      i1 = c1 < 0 ? 0 : (c1 >= n ? n - 1 : c1);
     }
-    const double rc = rho[cc], mc = mom[cc];
-    const double rl = rho[cl], ml = mom[cl];
-    const double uc = mc * rcp_fast(rc);
-    const bool vc = rc <= rho_tilde, lc = rc >= rho_min;  // phases
-    const bool vl = rl <= rho_tilde, ll = rl >= rho_min;
-    const double pcv = vc ? a_v2 * rc : p0 + a_l2 * (rc - rho0);
-    const double ul = __shfl_up_sync(0xffffffffu, uc, 1);
-    const double plv = __shfl_up_sync(0xffffffffu, pcv, 1);
-    const unsigned phc = vc ? 1u : (lc ? 2u : 0u), phl = vl ? 1u : (ll ? 2u : 0u);
-    unsigned phr = __shfl_down_sync(0xffffffffu, phc, 1);
+    const double r0 = rho[i0], m0 = mom[i0], r1 = rho[i1], m1 = mom[i1];
+    const double u0 = m0 * rcp_fast(r0), u1 = m1 * rcp_fast(r1);
+    const bool v0 = r0 <= rho_tilde, l0 = r0 >= rho_min, v1 = r1 <= rho_tilde, l1 = r1 >= rho_min;
+    const unsigned ph0 = v0 ? 1u : (l0 ? 2u : 0u), ph1 = v1 ? 1u : (l1 ? 2u : 0u);
+    const double q0 = v0 ? a_v2 * r0 : p0 + a_l2 * (r0 - rho0);
+    const double q1 = v1 ? a_v2 * r1 : p0 + a_l2 * (r1 - rho0);
+    const double a0 = v0 ? a_v : a_l, a1 = v1 ? a_v : a_l;
+    const double rl = __shfl_up_sync(0xffffffffu, r1, 1), ml = __shfl_up_sync(0xffffffffu, m1, 1);
+    const double ul = __shfl_up_sync(0xffffffffu, u1, 1), pl = __shfl_up_sync(0xffffffffu, q1, 1);
+    const unsigned phl = __shfl_up_sync(0xffffffffu, ph1, 1);
+    unsigned phr = __shfl_down_sync(0xffffffffu, ph0, 1);
     if (lane == 31) {
-      const double rr = rho[cj + 1 < n ? cj + 1 : n - 1];
+      const double rr = rho[c1 + 1 < n ? c1 + 1 : n - 1];
       phr = rr <= rho_tilde ? 1u : (rr >= rho_min ? 2u : 0u);
     }
-    const double a = vc ? a_v : a_l;
-    const bool own_cell = lane >= 1 && cj < n;
-    if (own_cell) {  // cell cj: S_max, h_min partials
-      bad |= !(rc > 0.0) || phc == 0u;
-      const double su = fabs(uc) + a;
-      s_part = su > s_part ? su : s_part;  // S over all cells (R5)
-      const double hc = h[cj];
-      const bool same_l = cj > 0 && phl == phc, same_r = cj + 1 < n && phr == phc;
-      const bool tiny = hc < eps_h && !same_l && !same_r;
-      const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
-      h_part = hh < h_part ? hh : h_part;  // h_min over non-tiny cells (R6)
-    }
-    if (lane >= 1 && cj <= n && phl == phc && phc != 0u) {  // edge cj between cells cj-1 and cj
-      double f0, f1;
-      hll_fast(a, rl, ml, ul, plv, rc, mc, uc, pcv, f0, f1);
-      F0[cj] = f0; F1[cj] = f1;
+    if (lane >= 1) {
+      if (c0 < n) {  // cell c0: S_max, h_min partials
+        bad |= !(r0 > 0.0) || ph0 == 0u;
+        const double su = fabs(u0) + a0;
+        s_part = su > s_part ? su : s_part;  // S over all cells (R5)
+        const double hc = h[c0];
+        const bool same_l = c0 > 0 && phl == ph0, same_r = c0 + 1 < n && ph1 == ph0;
+        const bool tiny = hc < eps_h && !same_l && !same_r;
+        const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
+        h_part = hh < h_part ? hh : h_part;  // h_min over non-tiny cells (R6)
+      }
+      if (c1 < n) {  // cell c1
+        bad |= !(r1 > 0.0) || ph1 == 0u;
+        const double su = fabs(u1) + a1;
+        s_part = su > s_part ? su : s_part;
+        const double hc = h[c1];
+        const bool same_l = ph0 == ph1, same_r = c1 + 1 < n && phr == ph1;
+        const bool tiny = hc < eps_h && !same_l && !same_r;
+        const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
+        h_part = hh < h_part ? hh : h_part;
+      }
       // creation pre-filters (R7), exact bounds with a 1e-9 m/s margin: liquid, both waves
       // rarefactions and ln y <= y - 1; vapour, both shocks and sqrt(rt r) <= rt, so
       // Phi(rt) >= du + a_v (2 - (r_L + r_R)/rt)
-      const double du = uc - ul, x = rl * rc;
-      const bool cand = lc ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x)
-                           : (du < -a_v * (2.0 - (rl + rc) * inv_rt) + 1e-9);
-      special |= cand && cj > 0 && cj < n;
-    } else if (lane >= 1 && cj > 0 && cj < n && phl != phc) {
-      special |= !(fl[cj] & F_IF);  // a phase change must be a listed boundary
+      if (c0 <= n && phl == ph0 && ph0 != 0u) {  // edge c0 between cells c0-1 and c0
+        double f0, f1;
+        hll_fast(a0, rl, ml, ul, pl, r0, m0, u0, q0, f0, f1);
+        F0[c0] = f0; F1[c0] = f1;
+        const double du = u0 - ul, x = rl * r0;
+        const bool cand = l0 ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (rl + r0) * inv_rt) + 1e-9);
+        special |= cand && c0 > 0 && c0 < n;
+      } else if (c0 > 0 && c0 < n && phl != ph0) {
+        special |= !(fl[c0] & F_IF);  // a phase change must be a listed boundary
+      }
+      if (c1 <= n && ph0 == ph1 && ph1 != 0u) {  // edge c1 between cells c0 and c1
+        double f0, f1;
+        hll_fast(a1, r0, m0, u0, q0, r1, m1, u1, q1, f0, f1);
+        F0[c1] = f0; F1[c1] = f1;
+        const double du = u1 - u0, x = r0 * r1;
+        const bool cand = l1 ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (r0 + r1) * inv_rt) + 1e-9);
+        special |= cand && c1 < n;
+      } else if (c1 < n && ph0 != ph1) {
+        special |= !(fl[c1] & F_IF);
+      }
     }
   }
   parts[0] = s_part;
   parts[1] = h_part;
-  if (__any_sync(0xffffffffu, bad || special)) {  // rare: redo the flagged windows in full
-    for (int w = warp; w < nwin1; w += nbulk) {
-      const int cj = 31 * w - 1 + lane;
-      if (cj < 1 || cj >= n) continue;
-      const double rc = rho[cj], rl = rho[cj - 1];
-      const int pc = phase_of(e, rc), pl = phase_of(e, rl);
-      if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
-      else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
-      if (pl == pc && pc != SPIN) {
-        const double uc = mom[cj] / rc, ul = mom[cj - 1] / rl;
-        if (cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
-            !region_at(e, p_ref, rho, h, n, cj - 1) && !region_at(e, p_ref, rho, h, n, cj)) {  // R16
-          const int k = atomicAdd(&sh.ntrg, 1);
-          if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
+  if (__any_sync(0xffffffffu, bad || special)) {  // rare: redo this warp's cells and edges in full
+    for (int w = warp; w < nwp; w += nbulk) {
+      for (int q = 0; q < 2; ++q) {
+        const int cj = 62 * w - 2 + 2 * lane + q;
+        if (lane < 1 || cj >= n) continue;
+        const double rc = rho[cj];
+        const int pc = phase_of(e, rc);
+        if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
+        else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
+        if (cj < 1) continue;
+        const double rl = rho[cj - 1];
+        const int pl = phase_of(e, rl);
+        if (pl == pc && pc != SPIN) {
+          const double uc = mom[cj] / rc, ul = mom[cj - 1] / rl;
+          if (cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
+              !region_at(e, p_ref, rho, h, n, cj - 1) && !region_at(e, p_ref, rho, h, n, cj)) {  // R16
+            const int k = atomicAdd(&sh.ntrg, 1);
+            if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
+          }
+        } else if (pl != pc && !(fl[cj] & F_IF)) {
+          zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
         }
-      } else if (pl != pc && !(fl[cj] & F_IF)) {
-        zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
       }
     }
   }
@@ -450,19 +485,32 @@ __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShar
 
 // Bulk pass P2: explicit update of the cells with two HLL edges (a7); h^{n+1} = h^n there, so
 // h^n/h^{n+1} = 1 exactly and the update is U - (dt/h)(F_R - F_L).
-__device__ __noinline__ void bulk_p2(const Prm& p, const CtaShared& sh, double* rho, double* mom, const double* h,
-                                     const double* F0, const double* F1, const uint8_t* fl, int n, int warp,
+__device__ __noinline__ void bulk_p2(const Prm& p, const CtaShared& sh, double* __restrict__ rho, double* __restrict__ mom,
+                                     const double* __restrict__ h, const double* __restrict__ F0,
+                                     const double* __restrict__ F1, const uint8_t* __restrict__ fl, int n, int warp,
                                      int nbulk, int ntrg, double dt, double dt_hav) {
+  constexpr int U = 4;  // cells per lane per round, all loads first (shared-memory latency)
   const int lane = threadIdx.x & 31;
   const double h_av = p.h_av;
-  for (int i = warp * 32 + lane; i - lane < n; i += nbulk * 32) {
-    if (i >= n) continue;
-    if ((fl[i] & (F_REG | F_SPEC)) || (fl[i + 1] & F_SPEC)) continue;
-    if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
-    const double hn = h[i];
-    const double cfac = hn == h_av ? dt_hav : dt / hn;
-    rho[i] = rho[i] - cfac * (F0[i + 1] - F0[i]);
-    mom[i] = mom[i] - cfac * (F1[i + 1] - F1[i]);
+  for (int i0 = warp * 32 * U; i0 < n; i0 += nbulk * 32 * U) {
+    double r[U], m[U], hn[U], a0[U], b0[U], a1[U], b1[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * 32 + lane, j = i < n ? i : 0;
+      ok[u] = i < n && !((fl[j] & (F_REG | F_SPEC)) || (fl[j + 1] & F_SPEC));
+      r[u] = rho[j]; m[u] = mom[j]; hn[u] = h[j];
+      a0[u] = F0[j]; b0[u] = F0[j + 1]; a1[u] = F1[j]; b1[u] = F1[j + 1];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * 32 + lane;
+      if (!ok[u]) continue;
+      if (ntrg && (find_trg(sh, ntrg, i) || find_trg(sh, ntrg, i + 1))) continue;
+      const double cfac = hn[u] == h_av ? dt_hav : dt / hn[u];
+      rho[i] = r[u] - cfac * (b0[u] - a0[u]);
+      mom[i] = m[u] - cfac * (b1[u] - a1[u]);
+    }
   }
 }
 
@@ -485,6 +533,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
   // the solver warp joins the bulk when idle; a one-warp CTA (tiled windows) does all in order
   const int nbulk = (sh.nifc > 0 && nw > 1) ? nw - 1 : nw;
   if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
+  EIS_TCLK(0);
     double s_part = 0.0, h_part = INFINITY;
 
     if (warp == SW) {
@@ -565,11 +614,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     s_part = warp_max(s_part);
     h_part = warp_min(h_part);
     if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }  // folded after barrier A
+    EIS_ARRIVE(1);
     __syncthreads();  // ---------------- barrier A ----------------
-    EIS_TCLK(1);
-#ifdef EIS_PHASE_CLOCK
-    if (threadIdx.x == 32) sh.tclk[9] = clock64();
-#endif
+
     // lane-parallel fold of the per-warp partials (every warp computes the same dt)
     const double smax = warp_max(lane < nw ? sh.part_s[lane] : 0.0);
     const double hmin = warp_min(lane < nw ? sh.part_h[lane] : INFINITY);
@@ -622,11 +669,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     // ---------------- P2: explicit update of cells with two HLL edges (a7) ----------------
     if (warp < nbulk) bulk_p2(p, sh, rho, mom, h, F0, F1, fl, n, warp, nbulk, ntrg, dt, dt_hav);
     if (remesh) sh.remesh = 1;
+    EIS_ARRIVE(3);
     __syncthreads();  // ---------------- barrier B ----------------
-    EIS_TCLK(2);
-#ifdef EIS_PHASE_CLOCK
-    if (threadIdx.x == 32) sh.tclk[8] = clock64();
-#endif
+
     // ---------------- creations (a6): acceptance (R16), solves, neighbour updates ----------------
     if (ntrg) {
       for (int k = tid; k < ntrg; k += T) {
@@ -665,7 +710,6 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       __syncthreads();
     }
     {
-      EIS_TCLK(3);
       const int stop2 = sh.status;
       __syncthreads();
       if (stop2) return -1.0;
@@ -794,7 +838,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     }
     __syncthreads();
     if (tid == 0) {
-      EIS_TCLK(4);
+      EIS_TCLK(5);
       MemberStats& st = sh.st;
       st.steps += 1;
       st.cell_updates += n;
@@ -872,6 +916,14 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     __syncthreads();  // every thread has read sh.status before anyone can write it
     if (stop) break;
     const double dt = step_body(e, p, sh, A, t, t_end, Z);
+#ifdef EIS_PHASE_CLOCK
+    if (g.dbg && tid == 0) {
+      long long* d = g.dbg + 8 * m;
+      for (int i = 1; i <= 5; ++i) d[i - 1] += sh.tclk[i] - sh.tclk[0];
+      d[5] += sh.tclk[7] - sh.tclk[6];
+      d[6] += 1;
+    }
+#endif
     if (dt < 0.0) break;
     t += dt;
   }

@@ -635,7 +635,6 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   }
   if (lane == 0) { sh.part_s[warp] = s_th; sh.part_h[warp] = h_th; }
   __syncthreads();
-  EIS_TCLK(5);
   if (tid == 0) {
     if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
     if (dt >= 0.0 && st == 0) {
@@ -688,13 +687,14 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[3 * j + 2] - tl.wlist[3 * j + 1];
       d[3] = sh.nifc; d[4] = c0;
 #ifdef EIS_PHASE_CLOCK
-      // phases: load+list | P1,S1,S2 to barrier A | to barrier B | creations | remesh,stats | assembly
+      // phases: load+list | to arrival at A | arrival A -> arrival B | S4 (DTS) | B -> step end | assembly
       long long* q = d + 5;
       q[0] = sh.tclk[0] - c0;
-      for (int i = 1; i < 6; ++i) q[i] = sh.tclk[i] - sh.tclk[i - 1];
-      q[3] = sh.tclk[7] - sh.tclk[6];  // (replaces "creations": the solver warp's S4, DTS)
-      q[4] = sh.tclk[8] - sh.tclk[2];  // (replaces: thread 32 vs thread 0 leaving barrier B)
-      q[5] = sh.tclk[9] - sh.tclk[1];  // (replaces: thread 32 vs thread 0 leaving barrier A)
+      q[1] = sh.tclk[1] - sh.tclk[0];
+      q[2] = sh.tclk[3] - sh.tclk[1];
+      q[3] = sh.tclk[7] - sh.tclk[6];
+      q[4] = sh.tclk[5] - sh.tclk[3];
+      q[5] = clock64() - sh.tclk[5];
 #endif
     }
   }

@@ -19,7 +19,7 @@ for target in [int(a) for a in (sys.argv[1:] or ["1", "40", "200"])]:
     d = ctx.window_diag()
     n = len(d)
     ph = d[:, 5:11]
-    names = ["load+list", "S1S2|P1->A", "S4S5|P2->B", "S4 (DTS) only", "dB(t32-t0)", "dA(t32-t0)"]
+    names = ["load+list", "start->A", "A->B", "S4 (DTS)", "B->end", "assembly"]
     print(f"step {done}: windows {n}, total p50 {np.percentile(d[:, 0], 50):.0f}, dts mean {d[:, 1].mean():.1f}")
     for i, nm in enumerate(names):
         print(f"   {nm:14s} mean {ph[:, i].mean():9.0f}  p50 {np.percentile(ph[:, i], 50):9.0f}  p90 {np.percentile(ph[:, i], 90):9.0f}")
