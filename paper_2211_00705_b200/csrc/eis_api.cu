@@ -51,7 +51,7 @@ struct eis_ctx {
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow, *t_wlist;
   long long* t_wdbg = nullptr;
-  double* t_part2;
+  double *t_part2, *t_partf;
   int slow_grid, win_grid;
   size_t smem_win;
   TileStats* t_stats;
@@ -301,6 +301,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
        cudaMalloc(&c->t_wlist, (size_t)ntiles * 12) == cudaSuccess &&
+       cudaMalloc(&c->t_partf, (size_t)ntiles * 24) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
@@ -309,7 +310,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->g.dbg = nullptr;
   Tiles& tl = c->tl;
   for (int b = 0; b < 2; ++b) { tl.rho[b] = c->t_rho[b]; tl.mom[b] = c->t_mom[b]; tl.h[b] = c->t_h[b]; tl.cnt[b] = c->t_cnt[b]; tl.hu[b] = c->t_hu[b]; }
-  tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist;
+  tl.slow = c->t_slow; tl.part2 = c->t_part2; tl.wlist = c->t_wlist; tl.partf = c->t_partf;
   tl.wdbg = nullptr;
   if (getenv("EIS_WINDOW_DEBUG")) {
     if (cudaMalloc(&c->t_wdbg, (size_t)ntiles * WDBG_FIELDS * 8) != cudaSuccess ||
@@ -472,7 +473,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_if);
   if (!c->tiled) cudaFree(c->g.dbg);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
-  cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg);
+  cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   delete c;

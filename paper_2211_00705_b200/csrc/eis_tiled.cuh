@@ -39,6 +39,7 @@ struct Tiles {
   double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
   int* slow;                       // work list of tiles needing the full step of the whole tile
   int* wlist;                      // work list of (tile, window begin, window end): full step of a window
+  double* partf;                   // per window tile: S_max, h_min, all-h_av of its fast cells
   double* part2;                   // per tiled_slow CTA: S_max, h_min
   long long* wdbg;                 // diagnostics (EIS_WINDOW_DEBUG): per window job of the last step
                                    // {cycles, dts iterations, window cells, boundaries, start clock,
@@ -341,7 +342,30 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   const int wa = max(own_lo, s_lo - 1 - HALO), wb = min(own_hi, s_hi + 2 + HALO);
   const bool mixed = (f & 3) == 3;
   const bool fast = !mixed && wa >= wb;
+  const bool window = !fast && !mixed && wb - wa <= tl.wmax;
   unif = !(f & 8);
+  if (window) {  // partials and width uniformity of the fast cells (outside [wa, wb)), from the
+                 // output just written (the window full step only moves them): as cfl_partials
+    double sf = 0.0, hf = INFINITY;
+    bool uf = true;
+    for (int c = own_lo + tid; c < own_hi; c += blockDim.x) {
+      if (c >= wa && c < wb) continue;
+      const double r = orho[c], hh = HU ? h_av : oh[c];
+      sf = fmax(sf, fabs(omom[c] * rcp_fast(r)) + sound(e, phase_of(e, r)));
+      hf = fmin(hf, hh);
+      uf &= hh == h_av;
+    }
+    sf = warp_max(sf);
+    hf = warp_min(hf);
+    uf = __all_sync(0xffffffffu, uf);
+    if (lane == 0) { ps[warp] = sf; ph[warp] = hf; if (!uf) atomicOr(&fl_or, 16); }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0, hm = INFINITY;
+      for (int w = 0; w < nw; ++w) { s = fmax(s, ps[w]); hm = fmin(hm, ph[w]); }
+      tl.partf[3 * k] = s; tl.partf[3 * k + 1] = hm; tl.partf[3 * k + 2] = (fl_or & 16) ? 0.0 : 1.0;
+    }
+  }
   if (fast && (g.xl || g.xr)) {  // rank mode: send records of the first / last HALO owned cells
     for (int q = tid; q < 2 * HALO; q += blockDim.x) {
       const bool left = q < HALO;
@@ -366,7 +390,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     } else {
       tl.part[2 * k] = 0.0;  // neutral: the full-step kernels fold this tile's own partials
       tl.part[2 * k + 1] = INFINITY;
-      if (!mixed && wb - wa <= tl.wmax) {  // a window of the tile
+      if (window) {  // a window of the tile
         const int j = atomicAdd(&tl.ctl[6], 1);
         tl.wlist[3 * j] = k; tl.wlist[3 * j + 1] = wa; tl.wlist[3 * j + 2] = wb;
       } else {
@@ -597,11 +621,12 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     double* const omom = tl.mom[g.out] + g.base;
     double* const oh = tl.h[g.out] + g.base;
     const int pa = wa - nL;  // output position of the window's first cell
-    // fast cells: left of the window (stay), right of it (shift by d); partials, uniformity
+    // fast cells: left of the window stay, right of it shift by d; their partials and width
+    // uniformity were folded by tiled_fast (tl.partf)
     double sf = 0.0, hf = INFINITY;
     bool uf = true;
-    fast_part_pass(e, orho, omom, g.hu_in ? nullptr : oh, p.h_av, 0, pa, 0, sf, hf, uf);
-    fast_part_pass(e, orho, omom, g.hu_in ? nullptr : oh, p.h_av, wb - nL, cnt, d, sf, hf, uf);
+    if (d != 0) fast_part_pass(e, orho, omom, g.hu_in ? nullptr : oh, p.h_av, wb - nL, cnt, d, sf, hf, uf);
+    sf = tl.partf[3 * k]; hf = tl.partf[3 * k + 1]; uf = tl.partf[3 * k + 2] != 0.0;
     bool uw = true;
     for (int i = olo + tid; i < ohi; i += T) uw &= A.h[i] == p.h_av;
     unif = __syncthreads_and(uw && uf);
@@ -616,8 +641,8 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     // CFL partials: the window's cells (tiny test inside the window grid) and the fast cells
     double s, hm;
     cfl_partials(e, p, A.rho, A.mom, A.h, A.n, olo, ohi, false, false, s, hm);
-    s_th = fmax(s, warp_max(sf));
-    h_th = fmin(hm, warp_min(hf));
+    s_th = fmax(s, sf);
+    h_th = fmin(hm, hf);
     __syncthreads();
     if (g.xl || g.xr) {  // rank mode: send records of the first / last HALO output cells
       for (int q = tid; q < 2 * HALO; q += T) {
