@@ -413,3 +413,36 @@ def test_c5_window_path_matches_whole_tile_path(P, oracle_mod, n, steps, monkeyp
     np.testing.assert_allclose(gw["h"][0, :nn], gf["h"][0, :nn], rtol=1e-11)
     o = oracle_run(oracle_mod, w, steps=steps)
     assert_parity(gw, o, h_av(w))
+
+
+def test_c5_tiled_run_to_and_virtual_ranks(P, oracle_mod):
+    """run_to on the tiled layout: the last step is clipped to t_end exactly (R5 with run_to),
+    against the oracle's run_to; the rank-sliced run (P = 2, t_end passed to every step) lands
+    on the same state bit for bit."""
+    from paper_2211_00705_b200.decomp import VirtualRanks
+    n = 30 * 940 + 311
+    w = W.c5(n_cells=n)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
+    ctx.set_state(rho, mom)
+    t40 = ctx.step(40, stats=True)["t_max"]
+    t41 = ctx.step(1, stats=True)["t_max"]
+    t_end = 0.5 * (t40 + t41)  # inside step 41: step 41 is clipped
+    ctx.set_state(rho, mom)
+    st = ctx.run_to(t_end, stats=True)
+    assert st["steps"] == 41 and st["t_max"] == t_end
+    g = ctx.get_state()
+    g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["mstats"] = [st]
+    o = oracle_run(oracle_mod, w, t_end=t_end)
+    assert_parity(g, o, h_av(w))
+    vr = VirtualRanks(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], 2,
+                      stream=torch.cuda.current_stream())
+    vr.set_state(rho[:w["N"]], mom[:w["N"]], t_end=t_end)
+    vr.step(45, t_end=t_end)  # steps after t_end are no-ops
+    v = vr.get_state()
+    n1 = int(g["n"][0])
+    assert all(t == t_end for t in v["t"])
+    np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
+    np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
