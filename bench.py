@@ -340,6 +340,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     w = W.c5(n_cells=n_glob)
     stream = torch.cuda.current_stream()
     rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
+                  tile=int(os.environ.get("EIS_TILE", "940")),
                   stream=stream)
     rho_l = np.zeros(rg.cap)
     mom_l = np.zeros(rg.cap)

@@ -593,6 +593,99 @@ out:
   return st;
 }
 
+/* Explicit time-accurate local time stepping (LTS) on an implicit block [a, b]: the paper's
+ * comparison method, the reduced Mueller-Stiriba scheme of the disabled passage
+ * P:1068-1091, readings R29-R31.  The tiny cells of the block advance with 2^n0 sub-steps of
+ * dtau = dt / 2^n0, n0 the smallest integer with dtau <= C_CFL h_T / S_max (h_T the smallest
+ * tiny width at t^n, S_max the step's, R29; P:1077 footnote); the other block cells stay at U^n
+ * meanwhile.  Each sub-step nu: fluxes F^nu and boundary speeds w^nu at the block's
+ * interior edges next to a tiny cell from the current states, then the moving small-cell update
+ * (P:1079-1081): h^{nu+1} = h^nu + (w_R - w_L) dtau, W^{nu+1} = (h^nu/h^{nu+1}) W^nu -
+ * (dtau/h^{nu+1})(F_R - F_L).  The non-tiny block cells then take the large step with the time
+ * averages Fbar = sum_nu (dtau/dt) F^nu and wbar = sum_nu (dtau/dt) w^nu at the edges they share
+ * with tiny cells (R30) and the U^n fluxes elsewhere, which balances mass, momentum
+ * and width exactly.  *iters_out = number of sub-steps ("local iterations"). */
+static int lts_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t* E, double dt, double Smax,
+                     double* rho_new, double* mom_new, double* h_new, int64_t* iters_out, int64_t* nsolves) {
+  int64_t base = m * c->cap;
+  const double* rho = c->rho + base;
+  const double* mom = c->mom + base;
+  const double* h = c->h + base;
+  const uint8_t* tiny = c->tiny + base;
+  int64_t K = b - a + 1;
+  double* W0 = (double*)malloc(sizeof(double) * 10 * (K + 1));
+  double *W1 = W0 + (K + 1), *hw = W1 + (K + 1);
+  double *F0 = hw + (K + 1), *F1 = F0 + (K + 1), *w = F1 + (K + 1);     /* edges a .. b+1 -> 0..K */
+  double *Fb0 = w + (K + 1), *Fb1 = Fb0 + (K + 1), *wb = Fb1 + (K + 1);
+  int* sub = (int*)malloc(sizeof(int) * (K + 1)); /* edge j next to a tiny cell */
+  int* ph0 = (int*)malloc(sizeof(int) * (K + 1));
+  int st = 0;
+  double hT = INFINITY;
+  for (int64_t i = 0; i < K; ++i) {
+    W0[i] = rho[a + i]; W1[i] = mom[a + i]; hw[i] = h[a + i];
+    ph0[i] = phase_of(&c->e, rho[a + i]);
+    if (tiny[a + i] && h[a + i] < hT) hT = h[a + i];
+  }
+  /* R29: dtau = dt / 2^n0 <= C_CFL h_T / S_max */
+  double dtau = dt;
+  int n0 = 0;
+  while (dtau > c->prm.cfl * hT / Smax) { dtau *= 0.5; if (++n0 > 62) { st = EISO_E_DTS_CAP; goto out; } }
+  const int64_t ns = (int64_t)1 << n0;
+  const double f = dtau / dt; /* 2^-n0, exact */
+  /* outer edges: the explicit step's U^n fluxes (flux bounding); interior edges not next
+   * to a tiny cell: U^n fluxes, constant during the sub-steps */
+  F0[0] = E[a].F0; F1[0] = E[a].F1; w[0] = E[a].w;
+  F0[K] = E[b + 1].F0; F1[K] = E[b + 1].F1; w[K] = E[b + 1].w;
+  sub[0] = sub[K] = 0;
+  for (int64_t j = 1; j < K; ++j) {
+    sub[j] = tiny[a + j - 1] || tiny[a + j];
+    Fb0[j] = Fb1[j] = wb[j] = 0.0;
+    if (!sub[j]) {
+      int kind;
+      st = edge_flux(c, rho[a + j - 1], mom[a + j - 1], rho[a + j], mom[a + j], &F0[j], &F1[j], &w[j], &kind, nsolves);
+      if (st) goto out;
+    }
+  }
+  for (int64_t nu = 0; nu < ns; ++nu) {
+    for (int64_t j = 1; j < K; ++j) { /* fluxes at the current sub-step states */
+      if (!sub[j]) continue;
+      int kind;
+      st = edge_flux(c, W0[j - 1], W1[j - 1], W0[j], W1[j], &F0[j], &F1[j], &w[j], &kind, nsolves);
+      if (st) goto out;
+    }
+    for (int64_t i = 0; i < K; ++i) { /* small-cell updates */
+      if (!tiny[a + i]) continue;
+      double hn = hw[i] + (w[i + 1] - w[i]) * dtau;
+      if (!(hn > 0.0)) { st = EISO_E_WIDTH; goto out; }
+      W0[i] = (hw[i] / hn) * W0[i] - (dtau / hn) * (F0[i + 1] - F0[i]);
+      W1[i] = (hw[i] / hn) * W1[i] - (dtau / hn) * (F1[i + 1] - F1[i]);
+      hw[i] = hn;
+      if (!(W0[i] > 0.0) || phase_of(&c->e, W0[i]) != ph0[i]) { st = EISO_E_SPINODAL; goto out; }
+    }
+    for (int64_t j = 1; j < K; ++j) { /* time averages for the large cells (R30) */
+      if (!sub[j]) continue;
+      Fb0[j] += f * F0[j]; Fb1[j] += f * F1[j]; wb[j] += f * w[j];
+    }
+  }
+  for (int64_t i = 0; i < K; ++i) {
+    if (tiny[a + i]) { rho_new[a + i] = W0[i]; mom_new[a + i] = W1[i]; h_new[a + i] = hw[i]; continue; }
+    const double FL0 = sub[i] ? Fb0[i] : F0[i], FL1 = sub[i] ? Fb1[i] : F1[i], wL = sub[i] ? wb[i] : w[i];
+    const double FR0 = sub[i + 1] ? Fb0[i + 1] : F0[i + 1], FR1 = sub[i + 1] ? Fb1[i + 1] : F1[i + 1];
+    const double wR = sub[i + 1] ? wb[i + 1] : w[i + 1];
+    double hn = h[a + i] + (wR - wL) * dt;
+    if (!(hn > 0.0)) { st = EISO_E_WIDTH; goto out; }
+    h_new[a + i] = hn;
+    rho_new[a + i] = (h[a + i] / hn) * rho[a + i] - (dt / hn) * (FR0 - FL0);
+    mom_new[a + i] = (h[a + i] / hn) * mom[a + i] - (dt / hn) * (FR1 - FL1);
+  }
+  *iters_out = ns;
+out:
+  free(W0);
+  free(sub);
+  free(ph0);
+  return st;
+}
+
 /* One large time step of one member: Algorithm 1 extended by the moving mesh
  * (§2.3, §3.4) and phase creation (App. B).  Order of sub-steps: DESIGN.md
  * §2. */
@@ -632,8 +725,9 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
   double dt = P->cfl * hmin / Smax;
   if (c->t[m] + dt > t_end) dt = t_end - c->t[m]; /* last step clipped (run_to) */
 
-  /* 2. implicit regions {k-1, k, k+1} around tiny cells, overlapping ones merged */
-  if (P->mode == EISO_MODE_SPLIT) {
+  /* 2. implicit regions {k-1, k, k+1} around tiny cells, overlapping ones merged
+   *    (SPLIT: dual time stepping; LTS: local time stepping of the tiny cells) */
+  if (P->mode != EISO_MODE_EXPLICIT) {
     for (int64_t k = 0; k < n; ++k) {
       if (!tiny[k]) continue;
       if (k == 0 || k == n - 1) { st = EISO_E_UNSUPPORTED; goto out; }
@@ -689,13 +783,16 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     mom_new[i] = (h[i] / hn) * mom[i] - (dt / hn) * (FR1 - FL1);
   }
 
-  /* 6. Algorithm 2 on every implicit block (Alg. 1 Step 2) */
+  /* 6. Algorithm 2 on every implicit block (Alg. 1 Step 2), or local time stepping (LTS mode) */
   for (int64_t i = 0; i < n;) {
     if (!inreg[i]) { ++i; continue; }
     int64_t a = i;
     while (i < n && inreg[i]) ++i;
     int64_t b = i - 1, it = 0;
-    st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
+    if (P->mode == EISO_MODE_LTS)
+      st = lts_block(c, m, a, b, E, dt, Smax, rho_new, mom_new, h_new, &it, &S->iface_solves);
+    else
+      st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
     if (st) goto out;
     S->dts_iters += it;
     S->regions++;

@@ -289,13 +289,20 @@ def _totals(st):
     return (st["h"][0, :n] * st["rho"][0, :n]).sum(), (st["h"][0, :n] * st["mom"][0, :n]).sum()
 
 
-def test_conservation_through_creation_and_dts(oracle_mod):
+@pytest.mark.parametrize("mode", [0, 2])
+def test_conservation_through_creation_and_dts(oracle_mod, mode):
     """Sum h U changes only by the boundary fluxes (P:621 'by construction ... preserves
     conservation'; R17 creation; flux bounding P:601).  C2 data; 60 steps through creation,
-    the DTS regions, merges and splits.  Boundary fluxes are zero-gradient: F(U_end)."""
+    the DTS regions (mode 0) or the local time stepping with time-averaged neighbour fluxes
+    (mode 2, R30), merges and splits.  Boundary fluxes are zero-gradient: F(U_end)."""
     w = W.c2()
     N = w["N"]
-    s = _sim(oracle_mod, w["rho"][0, :N], w["mom"][0, :N], -0.5, 0.5)
+    prm = dict(PRM)
+    prm["mode"] = mode
+    s = oracle_mod.Sim(EOS, prm, 1, N, N + 64, -0.5, 0.5)
+    rho = np.zeros((1, N + 64)); mom = np.zeros((1, N + 64))
+    rho[0, :N] = w["rho"][0, :N]; mom[0, :N] = w["mom"][0, :N]
+    s.set_state(rho, mom)
     for _ in range(60):
         st0 = s.get_state()
         n = st0["n"][0]
@@ -314,7 +321,73 @@ def test_conservation_through_creation_and_dts(oracle_mod):
     assert s.member_status()[0] == 0
 
 
-def test_split_equals_explicit_without_tiny_cells(oracle_mod):
+def _e2_run(oracle_mod, mode, t_end=5e-4, steps=None):
+    from conftest import eos_363K, read_golden
+    eos = eos_363K()
+    g = read_golden("cavitation_363K.txt")
+    N, cap = 400, 416
+    r = eos["rho0"] + (g["p_init"] - eos["p0"]) / eos["a_l"] ** 2
+    prm = dict(PRM)
+    prm["cfl"] = 0.5
+    prm["mode"] = mode
+    s = oracle_mod.Sim(eos, prm, 1, N, cap, -2.0, 2.0)
+    rho = np.zeros((1, cap)); mom = np.zeros((1, cap))
+    rho[0, :N] = r
+    mom[0, :N // 2] = -r * g["u_init"]
+    mom[0, N // 2:N] = r * g["u_init"]
+    s.set_state(rho, mom)
+    st = s.run_to(t_end) if steps is None else s.step(steps)
+    return g, eos, s, st
+
+
+def test_lts_mode_cavitation_e2(oracle_mod):
+    """Local time stepping (LTS, mode 2, readings R29-R31) on the paper's cavitation
+    test: the same 166 large steps (the large step does not depend on how the tiny
+    cell is advanced), the bubble kinematics of the DTS run (both follow the same
+    boundary speeds), widths summing to the domain length (R30 balances the width), and more
+    local iterations than DTS (P:1324 prints 1941 LTS vs 355 DTS; here 2893 vs 335)."""
+    g, eos, s, st = _e2_run(oracle_mod, 2)
+    g0, _, s0, st0 = _e2_run(oracle_mod, 0)
+    assert s.member_status()[0] == 0
+    assert st["steps"] == int(g["large_steps"]) == st0["steps"]
+    xs = [i["x"] for i in s.interfaces()]
+    x0 = [i["x"] for i in s0.interfaces()]
+    assert xs[1] - xs[0] == pytest.approx(g["bubble_width_t_end"], rel=1e-5)
+    assert xs[1] - xs[0] == pytest.approx(x0[1] - x0[0], rel=1e-9)
+    o = s.get_state()
+    n = int(o["n"][0])
+    assert o["h"][0, :n].sum() == pytest.approx(4.0, rel=1e-13)
+    assert st["dts_iters"] > 3 * st0["dts_iters"]
+
+
+def test_lts_substeps_follow_the_fine_cfl(oracle_mod):
+    """R29: every LTS region takes 2^n0 sub-steps with n0 the smallest integer such that
+    dt / 2^n0 <= C_CFL h_T / S_max; checked on the first step after the bubble is created
+    (E2: one tiny cell, its width and S_max from the state at the start of the step)."""
+    from conftest import eos_363K
+    eos = eos_363K()
+    g, eos, s, st1 = _e2_run(oracle_mod, 2, steps=1)  # step 1: the creation
+    assert st1["steps"] == 1 and st1["creations"] == 1
+    th = oracle_mod.thresholds(eos)
+    for _ in range(3):
+        o = s.get_state()
+        n = int(o["n"][0])
+        rho, mom, h = o["rho"][0, :n], o["mom"][0, :n], o["h"][0, :n]
+        vap = rho <= th["rho_tilde"]
+        a = np.where(vap, th["a_v"], eos["a_l"])
+        S = np.max(np.abs(mom / rho) + a)
+        h_av = 4.0 / 400
+        tiny = [i for i in range(1, n - 1) if h[i] < 0.5 * h_av and vap[i] != vap[i - 1] and vap[i] != vap[i + 1]]
+        assert len(tiny) == 1
+        hmin = np.min(np.delete(h, tiny))
+        dt = 0.5 * hmin / S
+        n0 = 0
+        while dt / 2 ** n0 > 0.5 * h[tiny[0]] / S:
+            n0 += 1
+        before = s.member_stats(0)["dts_iters"]
+        s.step(1)
+        assert s.member_stats(0)["dts_iters"] - before == 2 ** n0
+
     """Mode degeneracy (SPEC S:592): with no tiny cell Algorithm 1 is the explicit scheme."""
     w = W.c1()
     outs = []
