@@ -57,7 +57,13 @@ typedef enum {
 } eis_status;
 
 enum { EIS_HOST = 0, EIS_DEVICE = 1 };
-enum { EIS_MODE_SPLIT = 0 /* Algorithms 1-2 */, EIS_MODE_EXPLICIT = 1 /* global explicit, dt from all cells */ };
+enum {
+  EIS_MODE_SPLIT = 0,    /* Algorithms 1-2: dual time stepping on the tiny cells' neighbourhoods        */
+  EIS_MODE_EXPLICIT = 1, /* global explicit, dt from all cells                                          */
+  EIS_MODE_LTS = 2       /* explicit local time stepping of the tiny cells (the paper's comparison method,
+                            P:472-482; readings R29-R31); stats count its sub-steps as
+                            dts_iters ("local iterations")                                               */
+};
 enum { EIS_VAP = 0, EIS_LIQ = 1, EIS_SPIN = 2 };
 enum { EIS_LAYOUT_AUTO = 0, EIS_LAYOUT_RESIDENT = 1, EIS_LAYOUT_TILED = 2 };
 
@@ -84,7 +90,7 @@ typedef struct {
   double newton_gtol;        /* R14: 1e-12 (scaled residual)                               */
   int32_t newton_max_iter;   /* R14: 50                                                    */
   int32_t armijo_max;        /* Armijo halvings (Kelley): 30                       */
-  int32_t mode;              /* EIS_MODE_SPLIT | EIS_MODE_EXPLICIT                         */
+  int32_t mode;              /* EIS_MODE_SPLIT | EIS_MODE_EXPLICIT | EIS_MODE_LTS          */
   int32_t reserved;
 } eis_params;
 

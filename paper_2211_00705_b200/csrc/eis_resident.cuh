@@ -145,7 +145,7 @@ __device__ __forceinline__ bool tiny_at(const Eos& e, const Prm& p, const double
   return true;
 }
 __device__ __forceinline__ bool region_at(const Eos& e, const Prm& p, const double* rho, const double* h, int n, int i) {
-  return p.mode == 0 && (tiny_at(e, p, rho, h, n, i - 1) || tiny_at(e, p, rho, h, n, i) || tiny_at(e, p, rho, h, n, i + 1));
+  return p.mode != 1 && (tiny_at(e, p, rho, h, n, i - 1) || tiny_at(e, p, rho, h, n, i) || tiny_at(e, p, rho, h, n, i + 1));
 }
 
 // moving-cell update: h^{n+1} = h + (wR - wL) dt, U^{n+1} = (h/h^{n+1}) U - (dt/h^{n+1}) dF
@@ -314,6 +314,154 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
 }
 
 // ------------------------------------------------------------------------------------------
+// Explicit local time stepping (mode LTS, the paper's comparison method, the
+// disabled passage P:1068-1091, readings R29-R31) on one implicit block [a, b] by one warp: the
+// tiny cells advance with 2^n0 sub-steps of dtau = dt / 2^n0 (dtau <= C_CFL h_T / S_max, R29),
+// the other block cells stay at U^n meanwhile; fluxes at the edges next to a tiny cell from the
+// current sub-step states (the two half warps solve two boundaries at a time, warm-started from
+// the previous sub-step), moving small-cell update, time averages of the fluxes
+// and boundary speeds for the large cells (R30), which then take the large step.  The same
+// order of operations and accumulation as the oracle's lts_block.
+// ------------------------------------------------------------------------------------------
+__device__ __noinline__ int lts_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
+                                      const double* F0, const double* F1, const uint8_t* fl, int a, int b, double dt,
+                                      double smax, long long& it_out, long long& solves, int& remesh) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const int K = b - a + 1;
+  double* sc = sh.dts;
+  double* W0 = sc;               // [MAXB] sub-step states (tiny cells) / U^n (others)
+  double* W1 = sc + MAXB;        // [MAXB]
+  double* Fe0 = sc + 2 * MAXB;   // [MAXB+1] current edge fluxes
+  double* Fe1 = Fe0 + MAXB + 1;
+  double* we = Fe1 + MAXB + 1;
+  double* xs0 = we + MAXB + 1;   // warm starts of the boundary solves
+  double* xs1 = xs0 + MAXB + 1;
+  double fb0 = 0.0, fb1 = 0.0, wbar = 0.0;  // lane j: averages at edge j (R30)
+  if (lane == 0) {
+    double g0, g1, w;
+    edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
+    Fe0[0] = g0; Fe1[0] = g1; we[0] = w;
+    edge_view(sh, fl, F0, F1, b + 1, 0, g0, g1, w);
+    Fe0[K] = g0; Fe1[K] = g1; we[K] = w;
+  }
+  if (lane >= 1 && lane < K) {
+    const Ifc* s = find_ifc(sh, a + lane);
+    xs0[lane] = s ? s->pV : -1.0;
+    xs1[lane] = s ? s->pL : -1.0;
+  }
+  double rn0 = 0, rn1 = 0, hn = 0, w0 = 0, w1 = 0, hw = 0;
+  bool tin = false;
+  int ph0 = 0;
+  if (lane < K) {
+    const uint8_t f = fl[a + lane];
+    rn0 = rho[a + lane]; rn1 = mom[a + lane]; hn = h[a + lane];
+    tin = f & F_TINY;
+    ph0 = phase_of(e, rn0);
+    w0 = rn0; w1 = rn1; hw = hn;
+    W0[lane] = w0; W1[lane] = w1;
+  }
+  // R29: dtau = dt / 2^n0 <= C_CFL h_T / S_max
+  const double hT = warp_min(lane < K && tin ? hn : INFINITY);
+  double dtau = dt;
+  int n0 = 0;
+  while (dtau > p.cfl * hT / smax && n0 <= 62) { dtau *= 0.5; ++n0; }
+  if (n0 > 62) { it_out = 0; return ST_DTS_CAP; }
+  const long long ns = 1ll << n0;
+  const double f = dtau / dt;
+  // edge j (1 <= j < K) is sub-stepped iff next to a tiny cell; the others keep the U^n flux
+  const unsigned tmask = __ballot_sync(0xffffffffu, lane < K && tin);
+  auto sub_edge = [&](int j) { return j >= 1 && j < K && (((tmask >> (j - 1)) & 1u) || ((tmask >> j) & 1u)); };
+  __syncwarp();
+  int err = 0;
+  for (int j0 = 1; j0 < K; j0 += 2) {  // constant interior fluxes (U^n) of edges not next to a tiny cell
+    const int j = j0 + half;
+    if (j < K && !sub_edge(j)) {
+      const double rl = rho[a + j - 1], ml = mom[a + j - 1], rr = rho[a + j], mr = mom[a + j];
+      const int pl = phase_of(e, rl), pr = phase_of(e, rr);
+      if (pl != pr) {
+        IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
+        if (hl == 0) {
+          if (s.iters < 0) err = ST_NEWTON;
+          Fe0[j] = s.F0; Fe1[j] = s.F1; we[j] = s.w;
+          ++solves;
+        }
+      } else if (hl == 0) {
+        hll(e, pl, rl, ml, ml / rl, rr, mr, mr / rr, Fe0[j], Fe1[j]);
+        we[j] = 0.0;
+      }
+    }
+  }
+  err = __reduce_max_sync(0xffffffffu, err);
+  __syncwarp();
+  long long nu = 0;
+  for (; nu < ns && !err; ++nu) {
+    for (int j0 = 1; j0 < K; j0 += 2) {  // fluxes at the current sub-step states
+      const int j = j0 + half;
+      if (j < K && sub_edge(j)) {
+        const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j];
+        const int pl = phase_of(e, rho[a + j - 1]), pr = phase_of(e, rho[a + j]);  // phases of U^n
+        if (pl != pr) {
+          IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
+          if (hl == 0) {
+            if (s.iters < 0) err = ST_NEWTON;
+            Fe0[j] = s.F0; Fe1[j] = s.F1; we[j] = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
+            ++solves;
+          }
+        } else if (hl == 0) {
+          hll(e, pl, rl, ml, ml / rl, rr, mr, mr / rr, Fe0[j], Fe1[j]);
+          we[j] = 0.0;
+        }
+      }
+    }
+    err = __reduce_max_sync(0xffffffffu, err);
+    __syncwarp();
+    if (err) break;
+    int bad = 0;
+    if (lane < K && tin) {  // small-cell update
+      const double hn1 = __dadd_rn(hw, __dmul_rn(we[lane + 1] - we[lane], dtau));
+      if (!(hn1 > 0.0)) bad = ST_WIDTH;
+      w0 = (hw / hn1) * w0 - (dtau / hn1) * (Fe0[lane + 1] - Fe0[lane]);
+      w1 = (hw / hn1) * w1 - (dtau / hn1) * (Fe1[lane + 1] - Fe1[lane]);
+      hw = hn1;
+      if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
+    }
+    if (sub_edge(lane)) { fb0 += f * Fe0[lane]; fb1 += f * Fe1[lane]; wbar += f * we[lane]; }  // R30
+    bad = __reduce_max_sync(0xffffffffu, bad);
+    __syncwarp();
+    if (lane < K && tin) { W0[lane] = w0; W1[lane] = w1; }
+    __syncwarp();
+    if (bad) { err = bad; break; }
+  }
+  // large step of the non-tiny block cells with the averaged fluxes at their sub-stepped edges
+  if (sub_edge(lane)) { Fe0[lane] = fb0; Fe1[lane] = fb1; we[lane] = wbar; }
+  __syncwarp();
+  if (!err && lane < K) {
+    if (tin) {
+      rho[a + lane] = w0; mom[a + lane] = w1; h[a + lane] = hw;
+      if (hw < p.eps_tiny * p.h_av || hw > p.eps_split * p.h_av) remesh = 1;
+    } else {
+      const double hn1 = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
+      if (!(hn1 > 0.0)) err = ST_WIDTH;
+      else {
+        rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
+        mom[a + lane] = (hn / hn1) * rn1 - (dt / hn1) * (Fe1[lane + 1] - Fe1[lane]);
+        h[a + lane] = hn1;
+        if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
+      }
+    }
+  }
+  if (lane >= 1 && lane < K && !err) {  // keep the last boundary states for the next step
+    Ifc* s = const_cast<Ifc*>(find_ifc(sh, a + lane));
+    if (s) { s->pV = xs0[lane]; s->pL = xs1[lane]; }
+  }
+  err = __reduce_max_sync(0xffffffffu, err);
+  __syncwarp();
+  it_out = nu;
+  return err;
+}
+
+// ------------------------------------------------------------------------------------------
 // Boundary list from a full scan (kernel start only): ordered ballot by the solver warp.
 // ------------------------------------------------------------------------------------------
 __device__ void build_boundary_list(const Eos& e, CtaShared& sh, const double* rho, uint8_t* fl, int n) {
@@ -346,6 +494,7 @@ struct Zone {
   int zlo, zhi;          // cells [zlo, zhi) are computed exactly (tiles: owned cells +- 2)
   int own_lo, own_hi;    // owned cells [own_lo, own_hi); owned edges (own_lo, own_hi]
   double dt_given;       // > 0: this dt (tiles: the global CFL step); else the grid's own CFL dt
+  double s_given;        // > 0: the S_max of that step (tiles, LTS mode); else the grid's own
   bool left_real, right_real;  // the smem grid ends are domain ends (transmissive, R15)
 };
 struct Arr {
@@ -547,8 +696,8 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       const int ek = valid ? sh.ifc[lane].e : -10;
       const int enext = lane + 1 < nif ? sh.ifc[lane + 1].e : -20;
       // cell ek lies between boundaries ek and ek + 1: tiny if narrower than eps_tiny h_av (R4)
-      const bool tiny = p.mode == 0 && valid && enext == ek + 1 && h[ek] < p.eps_tiny * p.h_av;
-      if (p.mode == 0 && lane == 0 && nif > 0) {  // a tiny cell at a domain end (R26)
+      const bool tiny = p.mode != 1 && valid && enext == ek + 1 && h[ek] < p.eps_tiny * p.h_av;
+      if (p.mode != 1 && lane == 0 && nif > 0) {  // a tiny cell at a domain end (R26)
         if (Z.left_real && sh.ifc[0].e == 1 && h[0] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
         if (Z.right_real && sh.ifc[nif - 1].e == n - 1 && h[n - 1] < p.eps_tiny * p.h_av) set_status(sh, ST_UNSUPPORTED);
       }
@@ -621,6 +770,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     const double smax = warp_max(lane < nw ? sh.part_s[lane] : 0.0);
     const double hmin = warp_min(lane < nw ? sh.part_h[lane] : INFINITY);
     double dt = Z.dt_given > 0.0 ? Z.dt_given : p.cfl * hmin / smax;  // P:466 (tiles: the global dt)
+    const double smax_step = Z.s_given > 0.0 ? Z.s_given : smax;       // LTS fine-level CFL (R29)
     if (t + dt > t_end) dt = t_end - t;
     const double dt_hav = dt / p.h_av;
     const int ntrg = sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG;
@@ -637,7 +787,8 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         if (b < Z.zlo || a >= Z.zhi) continue;  // tiles: a block wholly in the halo is not needed
         if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
-        const int err = dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
+        const int err = p.mode == 2 ? lts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, smax_step, it, sv, remesh)
+                                    : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
         if (err && lane == 0) set_status(sh, err);
         if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)
           if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); atomicMax(&sh.c_dtsmax, (unsigned long long)it); }
@@ -909,7 +1060,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
   if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, A.n);
   __syncthreads();
   Zone Z;
-  Z.zlo = 0; Z.zhi = 1 << 30; Z.own_lo = 0; Z.own_hi = 1 << 30; Z.dt_given = -1.0;
+  Z.zlo = 0; Z.zhi = 1 << 30; Z.own_lo = 0; Z.own_hi = 1 << 30; Z.dt_given = -1.0; Z.s_given = -1.0;
   Z.left_real = true; Z.right_real = true;
   for (long long step = 0; step < n_steps; ++step) {
     const bool stop = sh.status != 0 || !(t < t_end);

@@ -70,7 +70,7 @@ __device__ __forceinline__ void cfl_partials(const Eos& e, const Prm& p, const d
     const int ph = phase_of(e, r);
     s = fmax(s, fabs(mom[i] * rcp_fast(r)) + sound(e, ph));  // u as in bulk_p1 / tiled_fast
     bool tiny = false;
-    if (p.mode == 0 && h[i] < p.eps_tiny * p.h_av) {
+    if (p.mode != 1 && h[i] < p.eps_tiny * p.h_av) {
       const bool same_l = (i > 0) ? phase_of(e, rho[i - 1]) == ph : false;
       const bool same_r = (i < n - 1) ? phase_of(e, rho[i + 1]) == ph : false;
       tiny = !same_l && !same_r;
@@ -111,6 +111,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
     if (t_new + dt > t_end) dt = t_end - t_new;
     tl.scal[0] = t_new;
     tl.scal[1] = dt;
+    tl.scal[5] = s;  // S_max of the next step (LTS fine-level CFL, R29)
     if (tl.ctl[3] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
     if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
     tl.ctl[0] = 1 - tl.ctl[0];
@@ -453,6 +454,7 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
   Z.own_lo = nL; Z.own_hi = nL + cnt;
   Z.zlo = max(nL - 2, 0); Z.zhi = min(nL + cnt + 2, n);
   Z.dt_given = dt_given;
+  Z.s_given = tl.scal[5];
   Z.left_real = (k == 0 && !tl.nbr_left); Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
   __syncthreads();
@@ -603,6 +605,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   Z.own_lo = wa - s0; Z.own_hi = wb - s0;
   Z.zlo = max(Z.own_lo - 2, 0); Z.zhi = min(Z.own_hi + 2, n);
   Z.dt_given = dt_given;
+  Z.s_given = tl.scal[5];
   Z.left_real = (k == 0 && !tl.nbr_left && s0 == 0);
   Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right && s1 == g.n);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
@@ -800,7 +803,7 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     s = fmax(s, fabs(tl.mom[cur][g] * rcp_fast(r)) + sound(e, ph));
     bool tiny = false;
     const double hg = tl.hu[cur][k] ? p.h_av : tl.h[cur][g];
-    if (p.mode == 0 && hg < p.eps_tiny * p.h_av) {  // neighbours may live in the next tiles
+    if (p.mode != 1 && hg < p.eps_tiny * p.h_av) {  // neighbours may live in the next tiles
       const double rl = i > 0 ? tl.rho[cur][g - 1] : (k > 0 ? tl.rho[cur][base - tl.capt + tl.cnt[cur][k - 1] - 1] : -1.0);
       const double rr = i < cnt - 1 ? tl.rho[cur][g + 1] : (k < tl.ntiles - 1 ? tl.rho[cur][base + tl.capt] : -1.0);
       const bool same_l = rl > 0.0 && phase_of(e, rl) == ph, same_r = rr > 0.0 && phase_of(e, rr) == ph;
@@ -838,6 +841,7 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
         double dt = p.cfl * hm / s;
         if (tl.scal[0] + dt > t_end) dt = t_end - tl.scal[0];
         tl.scal[1] = dt;
+        tl.scal[5] = s;
       }
       tl.ctl[2] = 0;
     }
@@ -883,6 +887,7 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;
   tl.scal[1] = dt;
+  tl.scal[5] = S;
 }
 
 }  // namespace eis

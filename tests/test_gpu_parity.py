@@ -481,3 +481,65 @@ def test_c5_tiled_run_to_and_virtual_ranks(P, oracle_mod):
     assert all(t == t_end for t in v["t"])
     np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
     np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
+
+
+# ------------------------------------------------------------------------------ LTS mode
+def _e2_workload(mode):
+    eos = eos_363K()
+    g_ = read_golden("cavitation_363K.txt")
+    N, cap = 400, 416
+    r = eos["rho0"] + (g_["p_init"] - eos["p0"]) / eos["a_l"] ** 2
+    prm = dict(W.PARAMS)
+    prm["cfl"] = 0.5
+    prm["mode"] = mode
+    rho = np.zeros((1, cap)); mom = np.zeros((1, cap))
+    rho[0, :N] = r
+    mom[0, :N // 2] = -r * g_["u_init"]
+    mom[0, N // 2:N] = r * g_["u_init"]
+    return g_, dict(eos=eos, params=prm, M=1, N=N, cap=cap, x_left=-2.0, x_right=2.0, rho=rho, mom=mom, t_end=5e-4)
+
+
+def test_lts_mode_e2_against_oracle(P, oracle_mod):
+    """Explicit local time stepping (EIS_MODE_LTS; readings R29-R31) on the paper's cavitation
+    test: same large steps and the same number of sub-steps as the oracle (2^n0 per region from
+    the fine-level CFL), state within the parity tolerance, the paper's bubble width."""
+    g_, w = _e2_workload(2)
+    g, _ = gpu_run(P, w, t_end=w["t_end"])
+    o = oracle_run(oracle_mod, w, t_end=w["t_end"])
+    assert g["status"][0] == 0
+    assert g["stats"]["steps"] == o["stats"]["steps"] == int(g_["large_steps"])
+    assert g["stats"]["dts_iters"] == o["stats"]["dts_iters"]
+    assert_parity(g, o, h_av(w))
+    xs = [i["x"] for i in g["ifc"]]
+    assert xs[1] - xs[0] == pytest.approx(g_["bubble_width_t_end"], rel=1e-5)
+
+
+def test_lts_mode_c2_and_c3_against_oracle(P, oracle_mod):
+    """LTS on the C2 cavitation problem and on C3 members (resident kernel), against the oracle."""
+    w = W.c2()
+    w["params"] = dict(w["params"]); w["params"]["mode"] = 2
+    g, _ = gpu_run(P, w, t_end=w["t_end"])
+    o = oracle_run(oracle_mod, w, t_end=w["t_end"])
+    assert g["stats"]["dts_iters"] == o["stats"]["dts_iters"] > 0
+    assert_parity(g, o, h_av(w))
+    w = W.c3(members=np.arange(6))
+    w["params"] = dict(w["params"]); w["params"]["mode"] = 2
+    g, _ = gpu_run(P, w, steps=200)
+    o = oracle_run(oracle_mod, w, steps=200)
+    assert_parity(g, o, h_av(w))
+
+
+def test_lts_mode_c5_tiled_against_oracle(P, oracle_mod):
+    """LTS through the tiled layout (window full steps take the step's global S_max, R29)."""
+    w = W.c5(n_cells=30 * 940 + 311)
+    w["params"] = dict(w["params"]); w["params"]["mode"] = 2
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
+    ctx.set_state(torch.tensor(w["rho"], device="cuda"), torch.tensor(w["mom"], device="cuda"))
+    st = ctx.step(150, stats=True)
+    g = ctx.get_state()
+    g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["mstats"] = [st]
+    o = oracle_run(oracle_mod, w, steps=150)
+    assert st["creations"] >= 1 and st["dts_iters"] > 0
+    assert st["dts_iters"] == o["stats"]["dts_iters"]
+    assert_parity(g, o, h_av(w))
