@@ -167,10 +167,11 @@ __global__ void k_validate(const Eos e, Members g, double t0) {
   }
 }
 // copy live cells, zero the rest, phases (255 past the end)
+// grid (members, chunks of a member's cells) as k_validate, so one huge grid packs on many CTAs
 __global__ void k_pack(const Eos e, Members g, double* rho, double* mom, double* h, uint8_t* ph) {
   const long long m = blockIdx.x;
   const long long n = g.n[m];
-  for (long long i = threadIdx.x; i < g.cap; i += blockDim.x) {
+  for (long long i = (long long)blockIdx.y * blockDim.x + threadIdx.x; i < g.cap; i += (long long)gridDim.y * blockDim.x) {
     const long long k = m * g.cap + i;
     const bool live = i < n;
     const double r = live ? g.rho[k] : 0.0;
@@ -704,6 +705,11 @@ extern "C" eis_status eis_run_to(eis_ctx* c, double t_end, int64_t max_steps, ei
   return launch(c, max_steps, t_end, out);
 }
 
+static dim3 pack_grid(const eis_ctx* c) {
+  const long long ny = std::min<long long>(65535, std::max<long long>(1, (c->grid.cell_capacity + 255) / 256 / 8));
+  return dim3((unsigned)c->grid.n_members, (unsigned)(c->grid.n_members > 1 ? 1 : ny));
+}
+
 extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double* width, uint8_t* phase,
                                     int64_t* n_cells, double* t, int32_t where) {
   if (!c) return EIS_E_ARG;
@@ -715,7 +721,7 @@ extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double
   const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
   const size_t cells = (size_t)M * cap;
   if (where == EIS_DEVICE) {
-    k_pack<<<(unsigned)M, 256, 0, c->stream>>>(c->e, c->g, rho, mom, width, phase);
+    k_pack<<<pack_grid(c), 256, 0, c->stream>>>(c->e, c->g, rho, mom, width, phase);
     CU(cudaGetLastError());
     if (n_cells) CU(cudaMemcpyAsync(n_cells, c->d_n, M * 8, cudaMemcpyDeviceToDevice, c->stream));
     if (t) CU(cudaMemcpyAsync(t, c->d_t, M * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -724,7 +730,7 @@ extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double
   eis_status s = ensure_pack(c);
   if (s) return s;
   double* pr = c->d_pack;
-  k_pack<<<(unsigned)M, 256, 0, c->stream>>>(c->e, c->g, rho ? pr : nullptr, mom ? pr + cells : nullptr,
+  k_pack<<<pack_grid(c), 256, 0, c->stream>>>(c->e, c->g, rho ? pr : nullptr, mom ? pr + cells : nullptr,
                                              width ? pr + 2 * cells : nullptr, phase ? c->d_u8 : nullptr);
   CU(cudaGetLastError());
   if (rho) CU(cudaMemcpyAsync(rho, pr, cells * 8, cudaMemcpyDeviceToHost, c->stream));
