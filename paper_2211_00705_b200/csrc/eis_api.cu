@@ -444,6 +444,8 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   cudaError_t e3 = cudaFuncSetAttribute(resident_steps<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e4 = cudaFuncSetAttribute(resident_steps<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
   cudaError_t e2 = cudaFuncSetAttribute(resident_steps<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  cudaError_t e5 = cudaFuncSetAttribute(resident_steps<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+  if (e5 != cudaSuccess) { delete c; return EIS_E_CUDA; }
   if (cudaFuncSetAttribute(resident_steps<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
@@ -680,7 +682,9 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
     const unsigned M = (unsigned)c->grid.n_members;
     std::array<int, 5> m{-1, -1, -1, -1, 0};
     if (c->timing) m[0] = timing_event(c);
-    if (c->threads <= 128)
+    if (c->threads <= 128 && M <= 148)  // few members (C1, C2, the paper's tests): no register cap
+      resident_steps<128, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
+    else if (c->threads <= 128)
       resident_steps<128, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else if (c->threads <= 256 && c->minb == 4)
       resident_steps<256, 4><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
