@@ -52,7 +52,9 @@ struct eis_ctx {
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow, *t_wlist;
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
-  int slow_grid, win_grid;
+  int slow_grid, win_grid, win_grid_poll;
+  cudaStream_t stream2 = nullptr;          // tiled: the window kernel beside tiled_fast
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   size_t smem_win;
   TileStats* t_stats;
   long long* t_off;
@@ -256,6 +258,15 @@ static unsigned grid_for(long long count) {
 // ------------------------------------------------------------------------------------------
 // tiled layout (one huge grid): allocation, staging <-> tiles
 // ------------------------------------------------------------------------------------------
+// the side stream of the window kernel that runs beside tiled_fast: highest priority, so its
+// CTAs take the first SM slots tiled_fast frees (it is launched after tiled_fast, and only waits
+// for work tiled_fast publishes: no kernel waits on a kernel launched after it)
+static cudaError_t make_side_stream(cudaStream_t* s) {
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, hi);
+}
+
 static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   const eis_grid* grid = &c->grid;
   const long long cap = grid->cell_capacity;
@@ -278,15 +289,28 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     delete c; return EIS_E_CUDA;
   }
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
-  if (cudaFuncSetAttribute(tiled_win<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+  if (cudaFuncSetAttribute(tiled_win<32, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
+  }
+  {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, tiled_fast<128, 8>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, 16, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_win<32, 16, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
+      delete c; return EIS_E_CUDA;
+    }
   }
   int nsm = 0, per_sm = 0, per_sm_w = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<32, 16>, 32, c->smem_win);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<32, 16, false>, 32, c->smem_win);
   c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
   c->win_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm_w, 1));
+  // the polling instance beside tiled_fast: off by default (measured on C5: 1, 2, 4 CTAs/SM
+  // beside tiled_fast cost tiled_fast more than the overlap saves); EIS_WIN_POLL_PER_SM=k
+  c->win_grid_poll = 0;
+  if (const char* ev = getenv("EIS_WIN_POLL_PER_SM")) c->win_grid_poll = std::max(0, atoi(ev)) * std::max(1, nsm);
   const size_t tc = (size_t)ntiles * capt;
   bool ok = cudaMalloc(&c->d_rho, cap * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cap * 8) == cudaSuccess &&
             cudaMalloc(&c->d_h, cap * 8) == cudaSuccess && cudaMalloc(&c->d_t, 8) == cudaSuccess &&
@@ -301,7 +325,10 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
        cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
-       cudaMalloc(&c->t_wlist, (size_t)ntiles * 12) == cudaSuccess &&
+       cudaMalloc(&c->t_wlist, (size_t)ntiles * 16) == cudaSuccess &&
+       make_side_stream(&c->stream2) == cudaSuccess &&
+       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess &&
        cudaMalloc(&c->t_partf, (size_t)ntiles * 24) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
@@ -330,7 +357,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
   tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
-  tl.ctl[6] = 0; tl.ctl[7] = 0;
+  tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[8] = 0; tl.ctl[9] = 0;
   tl.scal[0] = t0; tl.scal[1] = 0.0; tl.scal[2] = 0.0; tl.scal[3] = 0.0;
 }
 
@@ -479,6 +506,9 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   delete c;
 }
 
@@ -577,6 +607,7 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   CU(cudaGetLastError());
   if (c->tiled) {
     k_tiles_reset<<<1, 1, 0, c->stream>>>(c->tl, c->d_status, t0);
+    CU(cudaMemsetAsync(c->t_wlist, 0, (size_t)c->tl.ntiles * 16, c->stream));  // window ready tags
     if ((c->tl.nbr_left || c->tl.nbr_right) && !c->tl.xbuf)
       return fail(c, EIS_E_ORDER, "rank mode: eis_set_exchange_buffer before eis_set_state%s");
     {
@@ -633,23 +664,32 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
 
 // one large step of the tiled grid: the streaming pass over every tile, then the full step of
 // the listed tiles (and, by its last CTA, the next dt)
-static int timing_event(eis_ctx* c) {  // an event from the pool, recorded on the stream
+static int timing_event(eis_ctx* c, cudaStream_t st = nullptr) {  // an event from the pool, recorded on a stream
   if (c->ev_used == c->ev_pool.size()) {
     cudaEvent_t ev;
     if (cudaEventCreate(&ev) != cudaSuccess) return -1;
     c->ev_pool.push_back(ev);
   }
   const int i = (int)c->ev_used++;
-  cudaEventRecord(c->ev_pool[i], c->stream);
+  cudaEventRecord(c->ev_pool[i], st ? st : c->stream);
   return i;
 }
 
 static void tiled_launch(eis_ctx* c, double t_end) {
   std::array<int, 5> m{-1, -1, -1, -1, 1};
+  // tiled_fast, then (side stream, high priority) a window kernel that takes window jobs as
+  // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
+  if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
   if (c->timing) m[0] = timing_event(c);
   tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[1] = timing_event(c);
-  tiled_win<32, 16><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->win_grid_poll > 0) {
+    cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
+    tiled_win<32, 16, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
+    cudaEventRecord(c->ev_join, c->stream2);
+  }
+  tiled_win<32, 16, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) { m[3] = timing_event(c); c->ev_marks.push_back(m); }

@@ -38,7 +38,7 @@ struct Tiles {
   int* ctl;                        // [0] cur  [1] status  [2] done-counter  [3] steps
   double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
   int* slow;                       // work list of tiles needing the full step of the whole tile
-  int* wlist;                      // work list of (tile, window begin, window end): full step of a window
+  int* wlist;                      // work list of (tile, window begin, window end, ready tag)
   double* partf;                   // per window tile: S_max, h_min, all-h_av of its fast cells
   double* part2;                   // per tiled_slow CTA: S_max, h_min
   long long* wdbg;                 // diagnostics (EIS_WINDOW_DEBUG): per window job of the last step
@@ -49,6 +49,7 @@ struct Tiles {
 };
 // ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] tile-list length  [5] next tile job
 //      [6] window-list length  [7] next window job  [8] window jobs of the last step
+//      [9] tiled_fast CTAs finished (the window kernel running beside tiled_fast polls it)
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -98,7 +99,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
     tl.ctl[8] = tl.ctl[6];  // window jobs of this step (diagnostics)
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0;
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
     if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
       tl.xbuf[XB_DT] = -s;
       tl.xbuf[XB_DT + 1] = hm;
@@ -347,6 +348,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   unif = !(f & 8);
   if (window) {  // partials and width uniformity of the fast cells (outside [wa, wb)), from the
                  // output just written (the window full step only moves them): as cfl_partials
+    __threadfence();  // this CTA's output is read by a window CTA that may run concurrently
     double sf = 0.0, hf = INFINITY;
     bool uf = true;
     for (int c = own_lo + tid; c < own_hi; c += blockDim.x) {
@@ -391,9 +393,11 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     } else {
       tl.part[2 * k] = 0.0;  // neutral: the full-step kernels fold this tile's own partials
       tl.part[2 * k + 1] = INFINITY;
-      if (window) {  // a window of the tile
+      if (window) {  // a window of the tile, published with this step's tag after its data
         const int j = atomicAdd(&tl.ctl[6], 1);
-        tl.wlist[3 * j] = k; tl.wlist[3 * j + 1] = wa; tl.wlist[3 * j + 2] = wb;
+        tl.wlist[4 * j] = k; tl.wlist[4 * j + 1] = wa; tl.wlist[4 * j + 2] = wb;
+        __threadfence();
+        *reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]) = tl.ctl[3] + 1;
       } else {
         tl.slow[atomicAdd(&tl.ctl[4], 1)] = k;
       }
@@ -407,11 +411,14 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
            double t_end) {
   const TGeo g = tile_geo_spec(tl, blockIdx.x);
   const double t = tl.scal[0];
-  if (tl.ctl[1] != 0 || !(t < t_end)) return;  // uniform across the grid: nothing to do
-  double dt = tl.scal[1];
-  if (t + dt > t_end) dt = t_end - t;  // as step_body
-  if (g.hu_in) tiled_fast_body<true>(e, p, tl, g, dt);
-  else tiled_fast_body<false>(e, p, tl, g, dt);
+  if (tl.ctl[1] == 0 && t < t_end) {  // else nothing to do (uniform across the grid)
+    double dt = tl.scal[1];
+    if (t + dt > t_end) dt = t_end - t;  // as step_body
+    if (g.hu_in) tiled_fast_body<true>(e, p, tl, g, dt);
+    else tiled_fast_body<false>(e, p, tl, g, dt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { __threadfence(); atomicAdd(&tl.ctl[9], 1); }  // every CTA, always
 }
 
 // ------------------------------------------------------------------------------------------
@@ -690,8 +697,11 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   __syncthreads();
 }
 
-// tiled_win: persistent CTAs over the window list (launched between tiled_fast and tiled_slow)
-template <int MAXT, int MINB>
+// tiled_win: persistent CTAs over the window list.  POLL (the instance launched beside
+// tiled_fast on a second stream): a job index is waited for until its entry carries this step's
+// tag, or until every tiled_fast CTA has finished and the index is past the list (or a status
+// was raised).  The instance launched after tiled_fast (POLL = false) drains the same list.
+template <int MAXT, int MINB, bool POLL>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
           double t_end) {
@@ -701,18 +711,43 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   const int tid = threadIdx.x;
   const double t = tl.scal[0], dt_given = tl.scal[1];
   if (tl.ctl[1] != 0 || !(t < t_end)) return;
-  const int njobs = tl.ctl[6];
+  const int tag = tl.ctl[3] + 1;
+  volatile int* vctl = tl.ctl;
   for (;;) {
     __syncthreads();
-    if (tid == 0) sh.n_new = atomicAdd(&tl.ctl[7], 1);
+    if (tid == 0) {
+      int j = atomicAdd(&tl.ctl[7], 1);
+      volatile int* ready = reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]);
+      if (POLL) {
+#ifdef EIS_POLL_DEBUG
+        long long spins = 0;
+#endif
+        for (;;) {
+          if (j < vctl[6] && *ready == tag) break;
+          if (vctl[1] != 0 || (vctl[9] >= tl.ntiles && j >= vctl[6])) { j = -1; break; }
+          __nanosleep(256);
+#ifdef EIS_POLL_DEBUG
+          if (++spins == 4000000) {
+            printf("poll stuck: cta %d j %d ctl6 %d ctl7 %d ctl9 %d ntiles %d tag %d ready %d ctl1 %d\n", blockIdx.x, j,
+                   vctl[6], vctl[7], vctl[9], tl.ntiles, tag, j < 4 * tl.ntiles ? *ready : -7, vctl[1]);
+            j = -1; break;
+          }
+#endif
+        }
+      } else if (j >= vctl[6]) {
+        j = -1;
+      }
+      __threadfence();
+      sh.n_new = j;
+    }
     __syncthreads();
     const int j = sh.n_new;
-    if (j >= njobs) break;
+    if (j < 0) break;
     const long long c0 = clock64();
-    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[3 * j], tl.wlist[3 * j + 1], tl.wlist[3 * j + 2], t, t_end, dt_given);
+    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t, t_end, dt_given);
     if (tl.wdbg && tid == 0) {
       long long* d = tl.wdbg + WDBG_FIELDS * (long long)j;
-      d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[3 * j + 2] - tl.wlist[3 * j + 1];
+      d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[4 * j + 2] - tl.wlist[4 * j + 1];
       d[3] = sh.nifc; d[4] = c0;
 #ifdef EIS_PHASE_CLOCK
       // phases: load+list | to arrival at A | arrival A -> arrival B | S4 (DTS) | B -> step end | assembly
@@ -742,7 +777,10 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   Arr A = carve(smem_raw, capg);
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const double t = tl.scal[0], dt_given = tl.scal[1];
-  if (tl.ctl[1] != 0 || !(t < t_end)) return;  // uniform across the grid: nothing to do
+  if (tl.ctl[1] != 0 || !(t < t_end)) {  // uniform across the grid: nothing to do
+    if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }  // (a no-op step's counters)
+    return;
+  }
   double dt = dt_given;
   if (t + dt > t_end) dt = t_end - t;
   // fast tiles' partials (slow tiles hold neutral values here)
@@ -780,7 +818,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (last) {
     __threadfence();
     if (tl.ctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
-    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; }
+    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }
   }
 }
 
@@ -882,7 +920,7 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
     tl.ctl[0] = 1 - tl.ctl[0];
     tl.ctl[3] += 1;
   }
-  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0;
+  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
   double dt = p.cfl * hm / S;
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;
