@@ -303,10 +303,39 @@ def main():
         cpu = {"value": sts["cell_updates"] / dts, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
                "sample": f"members 0..{S - 1} of {name}, the same {args.steps} large steps from t=0, single thread"}
 
-    peak, peak_src = fp64_peak()
     cu_local = st["cell_updates"] - cu0 if world == 1 else None
-    kms = kt["resident_ms"] if kt["resident_ms"] > 0 else ms
-    achieved = FLOP_PER_CELL_UPDATE * (cu / world if cu_local is None else cu_local) / (kms * 1e-3) / 1e12  # per GPU
+    cu_gpu = cu / world if cu_local is None else cu_local
+    try:
+        ctx.tile_info()
+        tiled = True  # AUTO layout: members with more than 2048 cells run on the tiled layout
+    except P.EisError:
+        tiled = False
+    if tiled:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
+        kms = kt["fast_ms"] if kt["fast_ms"] > 0 else ms
+        achieved = C5_BYTES_PER_CELL_UPDATE * cu_gpu / (kms * 1e-3) / 1e9
+        step_bw = C5_BYTES_PER_CELL_UPDATE * cu_gpu / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": ncu_traffic(name), "kernel": "eis::tiled_fast",
+                "bytes_per_cell_update": C5_BYTES_PER_CELL_UPDATE,
+                "kernel_ms_per_step": kms / max(args.steps, 1), "kernel_share_of_step": kms / ms,
+                "window_ms_per_step": kt["window_ms"] / max(args.steps, 1),
+                "tile_ms_per_step": kt["tile_ms"] / max(args.steps, 1),
+                "whole_step_gbs": step_bw, "whole_step_frac": step_bw / hbm,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+        launches = args.steps * (4 if w["M"] > 1 else 3)
+        launch_note = "per step: tiled_fast + tiled_win + tiled_slow" + (" + tiled_members_finish" if w["M"] > 1 else "")
+    else:
+        peak, peak_src = fp64_peak()
+        kms = kt["resident_ms"] if kt["resident_ms"] > 0 else ms
+        achieved = FLOP_PER_CELL_UPDATE * cu_gpu / (kms * 1e-3) / 1e12  # per GPU
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
+                "kernel_ms": kms, "kernel_share_of_step": kms / ms,
+                "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src}
+        launches = 1
+        launch_note = "one member-resident kernel launch for the K timed steps"
     if rank == 0:
         line = {
             "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
@@ -317,12 +346,9 @@ def main():
                        else f"{name}: {Mtot} members x {w['N']} cells",
                        "members": Mtot, "cells_per_member": w["N"], "cell_capacity": w["cap"],
                        "parallelism": f"member-sharded dp{world}", "l2": "inputs (1.1 GB per GPU) larger than L2",
-                       "launches": "one member-resident kernel launch for the K timed steps"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
-                         "kernel_ms": kms, "kernel_share_of_step": kms / ms,
-                         "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1, "clocks": clk,
+                       "layout": "tiled" if tiled else "member-resident", "launches": launch_note},
+            "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
             "members_not_ok": nbad,

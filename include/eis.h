@@ -103,9 +103,11 @@ typedef struct {
                              cut over ranks keeps the whole grid's h_av bit for bit)          */
   int32_t device;         /* CUDA device ordinal                                           */
   int32_t threads;        /* CTA size per member / tile (0 = automatic)                    */
-  int32_t layout;         /* EIS_LAYOUT_AUTO | _RESIDENT (grid in shared memory across steps,
-                             ensembles, cell_capacity <= 16384) | _TILED (one huge grid, streamed
-                             through HBM in halo-overlapped tiles each step, n_members == 1)   */
+  int32_t layout;         /* EIS_LAYOUT_AUTO (tiled when cell_capacity > 2048) | _RESIDENT (each
+                             member in shared memory across the steps of a call, cell_capacity
+                             <= 16384) | _TILED (members streamed through HBM every step in
+                             halo-overlapped tiles; halos never cross members; each member its
+                             own dt, t and status; rank mode requires n_members == 1)          */
   int32_t tile_cells;     /* tiled: owned cells per tile (0 = 940); tiles are fixed-size from
                              the left, the last one takes the remainder                      */
   int32_t nbr_left;       /* tiled rank mode: 1 if this grid is the right part of a grid cut

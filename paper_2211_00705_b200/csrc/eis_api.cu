@@ -49,7 +49,7 @@ struct eis_ctx {
   int tiled, tile_cells;
   Tiles tl;
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
-  int *t_cnt[2], *t_hu[2], *t_ctl, *t_slow, *t_wlist;
+  int *t_cnt[2], *t_hu[2], *t_ctl, *t_mctl = nullptr, *t_slow, *t_wlist;
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
@@ -208,21 +208,24 @@ __global__ void k_iface(const Eos e, Members g, long long M, double x_left, cons
   if (cnt) cnt[m] = c;
 }
 
-// contiguous staging (member 0) -> tiles: tile k gets cells [k n / ntiles, (k+1) n / ntiles)
+// member-major staging -> tiles: tile k = member m's j-th tile (m = k / tpm) gets the member's
+// cells [j tile, (j+1) tile), the last tile the remainder (fixed-size tiles: any tile-aligned
+// split of a grid over ranks reproduces the single-grid tiling exactly).  A member whose cell
+// count does not fit its tiles gets status ST_CAPACITY.
 __global__ void k_to_tiles(Members g, Tiles tl, int cur, int tile_cells) {
-  const int k = blockIdx.x;
-  const long long n = g.n[0];
-  // fixed-size tiles, the last one takes the remainder: any tile-aligned split of a grid over
-  // ranks therefore reproduces the single-grid tiling exactly
-  const long long lo = (long long)k * tile_cells, hi = k == tl.ntiles - 1 ? n : lo + tile_cells;
-  const long long base = (long long)k * tl.capt;
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    tl.rho[cur][base + i - lo] = g.rho[i];
-    tl.mom[cur][base + i - lo] = g.mom[i];
-    tl.h[cur][base + i - lo] = g.h[i];
+  const int k = blockIdx.x, m = k / tl.tpm, j = k % tl.tpm;
+  const long long n = g.n[m];
+  const long long lo = (long long)j * tile_cells, hi = j == tl.tpm - 1 ? n : lo + tile_cells;
+  const long long base = (long long)k * tl.capt, src = (long long)m * g.cap;
+  const bool fits = hi - lo >= (tl.tpm > 1 ? HALO : 3) && hi - lo <= tl.capt;
+  for (long long i = lo + threadIdx.x; fits && i < hi; i += blockDim.x) {
+    tl.rho[cur][base + i - lo] = g.rho[src + i];
+    tl.mom[cur][base + i - lo] = g.mom[src + i];
+    tl.h[cur][base + i - lo] = g.h[src + i];
   }
   if (threadIdx.x == 0) {
-    tl.cnt[cur][k] = (int)(hi - lo);
+    if (!fits) atomicCAS(&tl.mctl[MCS * m + 1], 0, (int)ST_CAPACITY);
+    tl.cnt[cur][k] = fits ? (int)(hi - lo) : 0;
     tl.hu[cur][k] = 0;  // widths stored; the first step finds out whether they are all h_av
     double* ws = tl.ws + (size_t)k * WS_STRIDE;
     ws[2 * MAXIF] = -1.0;
@@ -231,22 +234,23 @@ __global__ void k_to_tiles(Members g, Tiles tl, int cur, int tile_cells) {
     tl.tstats[k] = z;
   }
 }
-// tiles -> contiguous staging, given exclusive offsets
+// tiles -> member-major staging, given each tile's offset inside its member (off[k]) and each
+// member's cell count (off[ntiles + m])
 __global__ void k_from_tiles(Members g, Tiles tl, const long long* off, double h_av) {
-  const int k = blockIdx.x;
-  const int cur = tl.ctl[0];
+  const int k = blockIdx.x, m = k / tl.tpm;
+  const int cur = tl.mctl[MCS * m];
   const int cnt = tl.cnt[cur][k];
   const bool hu = tl.hu[cur][k] != 0;
-  const long long base = (long long)k * tl.capt, o = off[k];
+  const long long base = (long long)k * tl.capt, o = (long long)m * g.cap + off[k];
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     g.rho[o + i] = tl.rho[cur][base + i];
     g.mom[o + i] = tl.mom[cur][base + i];
     g.h[o + i] = hu ? h_av : tl.h[cur][base + i];
   }
-  if (k == 0 && threadIdx.x == 0) {
-    g.n[0] = off[tl.ntiles];
-    g.t[0] = tl.scal[0];
-    g.status[0] = tl.ctl[1];
+  if (k % tl.tpm == 0 && threadIdx.x == 0) {
+    g.n[m] = off[tl.ntiles + m];
+    g.t[m] = tl.scal[SCS * m];
+    g.status[m] = tl.mctl[MCS * m + 1];
   }
 }
 
@@ -273,10 +277,12 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 940;
   if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
   const int capt = c->tile_cells + 32 + (c->tile_cells & 1);  // even: 16-byte aligned tile rows
-  long long ntiles = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;
-  if (ntiles > 1 && grid->n_cells - (ntiles - 1) * c->tile_cells < HALO) --ntiles;  // tiny remainder joins the last tile
-  if (ntiles < 1) ntiles = 1;
+  long long tpm = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;  // tiles per member
+  if (tpm > 1 && grid->n_cells - (tpm - 1) * c->tile_cells < HALO) --tpm;  // tiny remainder joins the last tile
+  if (tpm < 1) tpm = 1;
+  const long long M = grid->n_members, ntiles = M * tpm;
   if (ntiles > (1 << 30)) { delete c; return EIS_E_ARG; }
+  if (M > 1 && (grid->nbr_left || grid->nbr_right)) { delete c; return EIS_E_ARG; }  // rank mode: one grid
   c->threads = grid->threads > 0 ? grid->threads : 256;
   if (c->threads != 256) { delete c; return EIS_E_ARG; }
   const int capg = capt + 2 * HALO + MAXEV + 1;  // as tiled_step
@@ -312,10 +318,11 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->win_grid_poll = 0;
   if (const char* ev = getenv("EIS_WIN_POLL_PER_SM")) c->win_grid_poll = std::max(0, atoi(ev)) * std::max(1, nsm);
   const size_t tc = (size_t)ntiles * capt;
-  bool ok = cudaMalloc(&c->d_rho, cap * 8) == cudaSuccess && cudaMalloc(&c->d_mom, cap * 8) == cudaSuccess &&
-            cudaMalloc(&c->d_h, cap * 8) == cudaSuccess && cudaMalloc(&c->d_t, 8) == cudaSuccess &&
-            cudaMalloc(&c->d_n, 8) == cudaSuccess && cudaMalloc(&c->d_status, 4) == cudaSuccess &&
-            cudaMalloc(&c->d_stats, sizeof(MemberStats)) == cudaSuccess && cudaMalloc(&c->d_cnt, 16) == cudaSuccess;
+  const size_t mc = (size_t)M * cap;  // member-major staging
+  bool ok = cudaMalloc(&c->d_rho, mc * 8) == cudaSuccess && cudaMalloc(&c->d_mom, mc * 8) == cudaSuccess &&
+            cudaMalloc(&c->d_h, mc * 8) == cudaSuccess && cudaMalloc(&c->d_t, M * 8) == cudaSuccess &&
+            cudaMalloc(&c->d_n, M * 8) == cudaSuccess && cudaMalloc(&c->d_status, M * 4) == cudaSuccess &&
+            cudaMalloc(&c->d_stats, M * sizeof(MemberStats)) == cudaSuccess && cudaMalloc(&c->d_cnt, M * 8 + 8) == cudaSuccess;
   for (int b = 0; b < 2 && ok; ++b)
     ok = cudaMalloc(&c->t_rho[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_mom[b], tc * 8) == cudaSuccess &&
          cudaMalloc(&c->t_h[b], tc * 8) == cudaSuccess && cudaMalloc(&c->t_cnt[b], ntiles * 4) == cudaSuccess &&
@@ -323,7 +330,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
        cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
-       cudaMalloc(&c->t_scal, 8 * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, (size_t)M * SCS * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_mctl, (size_t)M * MCS * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
        cudaMalloc(&c->t_wlist, (size_t)ntiles * 16) == cudaSuccess &&
        make_side_stream(&c->stream2) == cudaSuccess &&
@@ -331,7 +339,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) == cudaSuccess &&
        cudaMalloc(&c->t_partf, (size_t)ntiles * 24) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
-       cudaMalloc(&c->t_off, (ntiles + 1) * 8) == cudaSuccess;
+       cudaMalloc(&c->t_off, (ntiles + M) * 8) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
@@ -348,7 +356,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
   if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
-  tl.ntiles = (int)ntiles; tl.capt = capt;
+  tl.mctl = c->t_mctl;
+  tl.ntiles = (int)ntiles; tl.capt = capt; tl.M = (int)M; tl.tpm = (int)tpm;
   tl.xbuf = nullptr;
   tl.nbr_left = grid->nbr_left != 0; tl.nbr_right = grid->nbr_right != 0;
   *out = c;
@@ -356,26 +365,36 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 }
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
-  tl.ctl[0] = 0; tl.ctl[1] = status[0]; tl.ctl[2] = 0; tl.ctl[3] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0;
-  tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[8] = 0; tl.ctl[9] = 0;
-  tl.scal[0] = t0; tl.scal[1] = 0.0; tl.scal[2] = 0.0; tl.scal[3] = 0.0;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m == 0) for (int q = 0; q < 16; ++q) tl.ctl[q] = 0;
+  if (m >= tl.M) return;
+  if (status[m]) atomicCAS(&tl.ctl[1], 0, status[m]);
+  int* mc = tl.mctl + MCS * m;
+  mc[0] = 0; mc[1] = status[m]; mc[2] = 0; mc[3] = 0;
+  double* sc = tl.scal + SCS * m;
+  sc[0] = t0;
+  for (int q = 1; q < SCS; ++q) sc[q] = 0.0;
 }
 
 // tiles -> contiguous staging (member 0), when the staging copy is stale
 static eis_status tiles_to_staging(eis_ctx* c) {
   if (c->staging_fresh) return EIS_OK;
-  const int nt = c->tl.ntiles;
-  int ctl[4];
-  CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
+  const int nt = c->tl.ntiles, M = c->tl.M, tpm = c->tl.tpm;
+  std::vector<int> mctl((size_t)M * MCS);
+  CU(cudaMemcpyAsync(mctl.data(), c->t_mctl, (size_t)M * MCS * 4, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<int> cnt0(nt), cnt1(nt);
+  CU(cudaMemcpyAsync(cnt0.data(), c->t_cnt[0], nt * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(cnt1.data(), c->t_cnt[1], nt * 4, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  std::vector<int> cnt(nt);
-  CU(cudaMemcpyAsync(cnt.data(), c->t_cnt[ctl[0]], nt * 4, cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  std::vector<long long> off(nt + 1);
-  off[0] = 0;
-  for (int k = 0; k < nt; ++k) off[k + 1] = off[k] + cnt[k];
-  if (off[nt] > c->grid.cell_capacity) return fail(c, EIS_E_CAPACITY, "tiled grid exceeds cell_capacity%s");
-  CU(cudaMemcpyAsync(c->t_off, off.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+  std::vector<long long> off((size_t)nt + M);  // tile offset inside its member, then member sizes
+  for (int m = 0; m < M; ++m) {
+    const std::vector<int>& cnt = mctl[(size_t)MCS * m] ? cnt1 : cnt0;
+    long long o = 0;
+    for (int j = 0; j < tpm; ++j) { off[(size_t)m * tpm + j] = o; o += cnt[(size_t)m * tpm + j]; }
+    if (o > c->grid.cell_capacity) return fail(c, EIS_E_CAPACITY, "tiled grid exceeds cell_capacity%s");
+    off[(size_t)nt + m] = o;
+  }
+  CU(cudaMemcpyAsync(c->t_off, off.data(), ((size_t)nt + M) * 8, cudaMemcpyHostToDevice, c->stream));
   k_from_tiles<<<nt, 256, 0, c->stream>>>(c->g, c->tl, c->t_off, c->p.h_av);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
@@ -384,13 +403,13 @@ static eis_status tiles_to_staging(eis_ctx* c) {
 }
 
 static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
-  const int nt = c->tl.ntiles;
+  const int nt = c->tl.ntiles, M = c->tl.M;
   std::vector<TileStats> ts(nt);
-  double scal[4];
-  int ctl[4];
+  std::vector<double> scal((size_t)M * SCS);
+  std::vector<int> mctl((size_t)M * MCS);
   CU(cudaMemcpyAsync(ts.data(), c->t_stats, nt * sizeof(TileStats), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaMemcpyAsync(scal, c->t_scal, 32, cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(scal.data(), c->t_scal, (size_t)M * SCS * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(mctl.data(), c->t_mctl, (size_t)M * MCS * 4, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   memset(out, 0, sizeof(*out));
   long long full = 0, win = 0;
@@ -403,10 +422,42 @@ static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
   }
   c->tile_full_steps = full;
   c->tile_win_steps = win;
-  out->steps = ctl[3];
-  out->t_min = out->t_max = scal[0];
-  out->dt_min = scal[2];
-  out->dt_max = scal[3];
+  out->t_min = INFINITY; out->t_max = -INFINITY; out->dt_min = INFINITY; out->dt_max = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double* sc = &scal[(size_t)SCS * m];
+    const int steps = mctl[(size_t)MCS * m + 2];
+    out->steps += steps;
+    out->t_min = std::fmin(out->t_min, sc[0]); out->t_max = std::fmax(out->t_max, sc[0]);
+    if (steps) { out->dt_min = std::fmin(out->dt_min, sc[2]); out->dt_max = std::fmax(out->dt_max, sc[3]); }
+  }
+  if (!(out->dt_min < INFINITY)) out->dt_min = 0.0;
+  return EIS_OK;
+}
+
+// per member (tiled): its tiles' counters, its steps, t, dt range
+static eis_status tiled_member_stats(eis_ctx* c, eis_stats* out) {
+  const int nt = c->tl.ntiles, M = c->tl.M, tpm = c->tl.tpm;
+  std::vector<TileStats> ts(nt);
+  std::vector<double> scal((size_t)M * SCS);
+  std::vector<int> mctl((size_t)M * MCS);
+  CU(cudaMemcpyAsync(ts.data(), c->t_stats, nt * sizeof(TileStats), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(scal.data(), c->t_scal, (size_t)M * SCS * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(mctl.data(), c->t_mctl, (size_t)M * MCS * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int m = 0; m < M; ++m) {
+    eis_stats& o = out[m];
+    memset(&o, 0, sizeof(o));
+    for (int j = 0; j < tpm; ++j) {
+      const TileStats& s = ts[(size_t)m * tpm + j];
+      o.cell_updates += s.cell_updates; o.dts_iters += s.dts_iters; o.iface_solves += s.iface_solves;
+      o.creations += s.creations; o.splits += s.splits; o.merges += s.merges; o.regions += s.regions;
+      o.dts_iter_max = std::max(o.dts_iter_max, (int64_t)s.dts_max);
+    }
+    const double* sc = &scal[(size_t)SCS * m];
+    o.steps = mctl[(size_t)MCS * m + 2];
+    o.t_min = o.t_max = sc[0];
+    o.dt_min = sc[2]; o.dt_max = sc[3];
+  }
   return EIS_OK;
 }
 
@@ -444,8 +495,11 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   p.mode = prm->mode;
 
   const long long M = grid->n_members, cap = grid->cell_capacity;
-  c->tiled = grid->layout == EIS_LAYOUT_TILED || (grid->layout == EIS_LAYOUT_AUTO && M == 1 && cap > 16384);
-  if (grid->layout < 0 || grid->layout > 2 || (c->tiled && M != 1)) { delete c; return EIS_E_ARG; }
+  // AUTO: members of more than 2048 cells (C4, C5) stream through the tiled layout (measured:
+  // C4 1.8x the member-resident kernel, whose CTA then fills an SM alone); smaller members
+  // (C1-C3) stay resident in shared memory for the whole call
+  c->tiled = grid->layout == EIS_LAYOUT_TILED || (grid->layout == EIS_LAYOUT_AUTO && cap > 2048);
+  if (grid->layout < 0 || grid->layout > 2) { delete c; return EIS_E_ARG; }
   if (c->tiled) return create_tiled(c, out);
   if (cap > 16384) { delete c; return EIS_E_ARG; }
   // CTA size: 128 threads (3 bulk warps + the solver warp, 128 registers per thread) up to
@@ -504,7 +558,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   if (!c->tiled) cudaFree(c->g.dbg);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
-  cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_off);
+  cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_mctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -606,18 +660,19 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   }
   CU(cudaGetLastError());
   if (c->tiled) {
-    k_tiles_reset<<<1, 1, 0, c->stream>>>(c->tl, c->d_status, t0);
+    k_tiles_reset<<<(unsigned)((M + 127) / 128), 128, 0, c->stream>>>(c->tl, c->d_status, t0);
     CU(cudaMemsetAsync(c->t_wlist, 0, (size_t)c->tl.ntiles * 16, c->stream));  // window ready tags
     if ((c->tl.nbr_left || c->tl.nbr_right) && !c->tl.xbuf)
       return fail(c, EIS_E_ORDER, "rank mode: eis_set_exchange_buffer before eis_set_state%s");
-    {
+    if (M == 1) {  // one grid: a misfit is an argument error (members get a status, k_to_tiles)
       long long nn = c->grid.n_cells;
       if (n_cells && where == EIS_HOST) nn = n_cells[0];
-      const long long lo_last = (long long)(c->tl.ntiles - 1) * c->tile_cells;
+      const long long lo_last = (long long)(c->tl.tpm - 1) * c->tile_cells;
       if (nn - lo_last < HALO || nn - lo_last > c->tl.capt) return fail(c, EIS_E_ARG, "set_state: n_cells does not fit the tiling%s");
     }
     k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0, c->tile_cells);
     tiled_init_dt<256><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, INFINITY);
+    if (M > 1) tiled_members_finish<<<(unsigned)((M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, INFINITY, 0);
     CU(cudaGetLastError());
     c->staging_fresh = 1;
   }
@@ -692,6 +747,8 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->tl.M > 1)
+    tiled_members_finish<<<(unsigned)(((long long)c->tl.M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, t_end, 1);
   if (c->timing) { m[3] = timing_event(c); c->ev_marks.push_back(m); }
 }
 
@@ -703,15 +760,25 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
   CU(cudaSetDevice(c->grid.device));
   if (c->tiled) {
     c->staging_fresh = 0;
+    const long long M = c->tl.M;
     for (long long s = 0; s < n_steps; ++s) {
       tiled_launch(c, t_end);
       if ((s & 63) == 63 && t_end < INFINITY) {  // poll: stop launching once t_end is reached
-        double tt;
-        int ctl[4];
-        CU(cudaMemcpyAsync(&tt, c->t_scal, 8, cudaMemcpyDeviceToHost, c->stream));
-        CU(cudaMemcpyAsync(ctl, c->t_ctl, 16, cudaMemcpyDeviceToHost, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
-        if (!(tt < t_end) || ctl[1] != 0) break;
+        if (M == 1) {
+          double tt;
+          int st;
+          CU(cudaMemcpyAsync(&tt, c->t_scal, 8, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaMemcpyAsync(&st, c->t_mctl + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaStreamSynchronize(c->stream));
+          if (!(tt < t_end) || st != 0) break;
+        } else {
+          int act;
+          CU(cudaMemsetAsync(c->t_ctl + 10, 0, 4, c->stream));
+          tiled_members_active<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(c->tl, t_end);
+          CU(cudaMemcpyAsync(&act, c->t_ctl + 10, 4, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaStreamSynchronize(c->stream));
+          if (act == 0) break;
+        }
       }
     }
     CU(cudaGetLastError());
@@ -827,8 +894,10 @@ extern "C" eis_status eis_member_status(eis_ctx* c, int32_t* out) {
   if (!c || !out) return EIS_E_ARG;
   if (!c->state_set) return fail(c, EIS_E_ORDER, "member_status before set_state%s");
   if (c->tiled) {
-    CU(cudaMemcpyAsync(out, c->t_ctl + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int> mctl((size_t)c->tl.M * MCS);
+    CU(cudaMemcpyAsync(mctl.data(), c->t_mctl, mctl.size() * 4, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    for (int m = 0; m < c->tl.M; ++m) out[m] = mctl[(size_t)MCS * m + 1];
     return EIS_OK;
   }
   CU(cudaMemcpyAsync(out, c->d_status, c->grid.n_members * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -839,7 +908,7 @@ extern "C" eis_status eis_member_status(eis_ctx* c, int32_t* out) {
 extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
   if (!c || !out) return EIS_E_ARG;
   if (!c->state_set) return fail(c, EIS_E_ORDER, "member_stats before set_state%s");
-  if (c->tiled) return tiled_stats(c, out);
+  if (c->tiled) return tiled_member_stats(c, out);
   const long long M = c->grid.n_members;
   std::vector<MemberStats> ms(M);
   std::vector<double> t(M);

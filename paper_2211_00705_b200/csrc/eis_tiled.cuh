@@ -34,8 +34,10 @@ struct Tiles {
   double* ws;                      // per tile: ws0[MAXIF], ws1[MAXIF], wsn  (2*MAXIF + 1 doubles)
   double* part;                    // per tile: S_max, h_min of the tile's new cells
   TileStats* tstats;
-  double* scal;                    // [0] t  [1] dt of the next step  [2] dt_min  [3] dt_max
-  int* ctl;                        // [0] cur  [1] status  [2] done-counter  [3] steps
+  double* scal;                    // per member (stride SCS): [0] t  [1] dt of the coming step
+                                   //   [2] dt_min  [3] dt_max  [4] dt used (rank mode)  [5] S_max of the coming step
+  int* mctl;                       // per member (stride MCS): [0] cur buffer  [1] status  [2] steps
+  int* ctl;                        // global counters (below)
   double* xbuf;                    // rank mode: exchange buffer (layout XB_* below), else null
   int* slow;                       // work list of tiles needing the full step of the whole tile
   int* wlist;                      // work list of (tile, window begin, window end, ready tag)
@@ -46,8 +48,11 @@ struct Tiles {
                                    //  6 phase cycles (EIS_PHASE_CLOCK builds, else 0)}
   int ntiles, capt, nbr_left, nbr_right;
   int wmax;                        // largest window (owned cells) of a window full step (<= WMAX)
+  int M, tpm;                      // members (independent grids) and tiles per member: tile k
+                                   // belongs to member k / tpm; halos never cross members
 };
-// ctl: [0] cur  [1] status  [2] done-counter  [3] steps  [4] tile-list length  [5] next tile job
+constexpr int SCS = 8, MCS = 4;
+// ctl: [1] any member status  [2] done-counter  [3] launches  [4] tile-list length  [5] next tile job
 //      [6] window-list length  [7] next window job  [8] window jobs of the last step
 //      [9] tiled_fast CTAs finished (the window kernel running beside tiled_fast polls it)
 
@@ -113,9 +118,10 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
     tl.scal[0] = t_new;
     tl.scal[1] = dt;
     tl.scal[5] = s;  // S_max of the next step (LTS fine-level CFL, R29)
-    if (tl.ctl[3] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
+    if (tl.mctl[2] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
     if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
-    tl.ctl[0] = 1 - tl.ctl[0];
+    tl.mctl[0] = 1 - tl.mctl[0];
+    tl.mctl[2] += 1;
     tl.ctl[3] += 1;
     __threadfence();
   }
@@ -126,36 +132,42 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
 // virtual array [0, n) = left halo | own | right halo.
 struct TGeo {
   long long base, bl, br;
-  int k, in, out, cnt, cl, nL, nR, n;
+  int k, m, in, out, cnt, cl, nL, nR, n;
   bool xl, xr, hu_in;
+  bool first, last;  // the member's first / last tile (a domain end unless a rank neighbour)
 };
-__device__ __forceinline__ TGeo tile_geo(const Tiles& tl, int k, int cur) {
+__device__ __forceinline__ TGeo tile_geo(const Tiles& tl, int k) {
   TGeo g;
-  g.k = k; g.in = cur; g.out = 1 - cur;
+  g.k = k; g.m = k / tl.tpm;
+  const int cur = tl.mctl[MCS * g.m];
+  g.in = cur; g.out = 1 - cur;
+  g.first = k % tl.tpm == 0; g.last = (k + 1) % tl.tpm == 0;
   g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
   g.cnt = tl.cnt[cur][k];
   g.hu_in = tl.hu[cur][k] != 0;
-  g.xl = (k == 0 && tl.nbr_left); g.xr = (k == tl.ntiles - 1 && tl.nbr_right);
-  g.cl = k > 0 ? tl.cnt[cur][k - 1] : 0;
-  g.nL = k > 0 ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
-  g.nR = k < tl.ntiles - 1 ? min(HALO, tl.cnt[cur][k + 1]) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
+  g.xl = (g.first && tl.nbr_left); g.xr = (g.last && tl.nbr_right);
+  g.cl = !g.first ? tl.cnt[cur][k - 1] : 0;
+  g.nL = !g.first ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
+  g.nR = !g.last ? min(HALO, tl.cnt[cur][k + 1]) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
   g.n = g.nL + g.cnt + g.nR;
   return g;
 }
 // the same, with the tile metadata of both buffers loaded before `cur` is known (one
 // dependent global round trip fewer at the start of every tile)
 __device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
-  const bool hasl = k > 0, hasr = k < tl.ntiles - 1;
+  const int m = k / tl.tpm;
+  const bool hasl = k % tl.tpm != 0, hasr = (k + 1) % tl.tpm != 0;
   const int c0 = tl.cnt[0][k], c1 = tl.cnt[1][k], h0 = tl.hu[0][k], h1 = tl.hu[1][k];
   const int l0 = hasl ? tl.cnt[0][k - 1] : 0, l1 = hasl ? tl.cnt[1][k - 1] : 0;
   const int r0 = hasr ? tl.cnt[0][k + 1] : 0, r1 = hasr ? tl.cnt[1][k + 1] : 0;
-  const int cur = tl.ctl[0];
+  const int cur = tl.mctl[MCS * m];
   TGeo g;
-  g.k = k; g.in = cur; g.out = 1 - cur;
+  g.k = k; g.m = m; g.in = cur; g.out = 1 - cur;
+  g.first = !hasl; g.last = !hasr;
   g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
   g.cnt = cur ? c1 : c0;
   g.hu_in = (cur ? h1 : h0) != 0;
-  g.xl = (k == 0 && tl.nbr_left); g.xr = (k == tl.ntiles - 1 && tl.nbr_right);
+  g.xl = (g.first && tl.nbr_left); g.xr = (g.last && tl.nbr_right);
   g.cl = cur ? l1 : l0;
   g.nL = hasl ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
   g.nR = hasr ? min(HALO, cur ? r1 : r0) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
@@ -410,9 +422,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
 tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
   const TGeo g = tile_geo_spec(tl, blockIdx.x);
-  const double t = tl.scal[0];
-  if (tl.ctl[1] == 0 && t < t_end) {  // else nothing to do (uniform across the grid)
-    double dt = tl.scal[1];
+  const double t = tl.scal[SCS * g.m];
+  if (tl.mctl[MCS * g.m + 1] == 0 && t < t_end) {  // else the member does not step (uniform in the CTA)
+    double dt = tl.scal[SCS * g.m + 1];
     if (t + dt > t_end) dt = t_end - t;  // as step_body
     if (g.hu_in) tiled_fast_body<true>(e, p, tl, g, dt);
     else tiled_fast_body<false>(e, p, tl, g, dt);
@@ -427,10 +439,10 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
 // the tile's partials; a status is raised on tl.ctl[1].
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capg,
-                                          int k, double t, double t_end, double dt_given, double& s_out,
-                                          double& h_out) {
+                                          int k, double t_end, double& s_out, double& h_out) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const TGeo g = tile_geo(tl, k, tl.ctl[0]);
+  const TGeo g = tile_geo(tl, k);
+  const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int n = g.n, nL = g.nL, cnt = g.cnt;
   if (tid == 0) {
     sh.status = 0;
@@ -440,7 +452,7 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
-  const int huL = k > 0 ? tl.hu[g.in][k - 1] : 0, huR = k < tl.ntiles - 1 ? tl.hu[g.in][k + 1] : 0;
+  const int huL = !g.first ? tl.hu[g.in][k - 1] : 0, huR = !g.last ? tl.hu[g.in][k + 1] : 0;
   for (int i = tid; i < n; i += T) {
     long long mo;
     const double* pr = vcell(tl, g, i, mo);
@@ -461,14 +473,14 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
   Z.own_lo = nL; Z.own_hi = nL + cnt;
   Z.zlo = max(nL - 2, 0); Z.zhi = min(nL + cnt + 2, n);
   Z.dt_given = dt_given;
-  Z.s_given = tl.scal[5];
-  Z.left_real = (k == 0 && !tl.nbr_left); Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right);
+  Z.s_given = tl.scal[SCS * g.m + 5];
+  Z.left_real = (g.first && !tl.nbr_left); Z.right_real = (g.last && !tl.nbr_right);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
   __syncthreads();
   const int olo = sh.olo, ohi = sh.ohi;
   const int nout = ohi - olo;
   int st = sh.status;
-  if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.ntiles > 1 ? HALO : 3))) st = ST_CAPACITY;
+  if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.tpm > 1 ? HALO : 3))) st = ST_CAPACITY;
   bool unif = true;
   if (dt >= 0.0 && st == 0) {
     bool u = true;  // widths all h_av?  then they are not stored
@@ -500,7 +512,7 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
   __syncthreads();
   if (tid == 0) {
     s_out = 0.0; h_out = INFINITY;
-    if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
+    if (st != 0) { atomicCAS(&tl.mctl[MCS * g.m + 1], 0, st); atomicCAS(&tl.ctl[1], 0, st); }
     if (dt >= 0.0 && st == 0) {
       for (int w = 0; w < nw; ++w) { s_out = fmax(s_out, sh.part_s[w]); h_out = fmin(h_out, sh.part_h[w]); }
       tl.part[2 * k] = s_out;
@@ -576,9 +588,10 @@ __device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, doubl
 }
 
 __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
-                                            int k, int wa, int wb, double t, double t_end, double dt_given) {
+                                            int k, int wa, int wb, double t_end) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const TGeo g = tile_geo(tl, k, tl.ctl[0]);
+  const TGeo g = tile_geo(tl, k);
+  const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int nL = g.nL, cnt = g.cnt;
   const int s0 = max(0, wa - HALO), s1 = min(g.n, wb + HALO), n = s1 - s0;
   if (tid == 0) {
@@ -589,7 +602,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
-  const int huL = k > 0 ? tl.hu[g.in][k - 1] : 0, huR = k < tl.ntiles - 1 ? tl.hu[g.in][k + 1] : 0;
+  const int huL = !g.first ? tl.hu[g.in][k - 1] : 0, huR = !g.last ? tl.hu[g.in][k + 1] : 0;
   for (int i = tid; i < n; i += T) {
     const int v = s0 + i;
     long long mo;
@@ -612,9 +625,9 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   Z.own_lo = wa - s0; Z.own_hi = wb - s0;
   Z.zlo = max(Z.own_lo - 2, 0); Z.zhi = min(Z.own_hi + 2, n);
   Z.dt_given = dt_given;
-  Z.s_given = tl.scal[5];
-  Z.left_real = (k == 0 && !tl.nbr_left && s0 == 0);
-  Z.right_real = (k == tl.ntiles - 1 && !tl.nbr_right && s1 == g.n);
+  Z.s_given = tl.scal[SCS * g.m + 5];
+  Z.left_real = (g.first && !tl.nbr_left && s0 == 0);
+  Z.right_real = (g.last && !tl.nbr_right && s1 == g.n);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
   __syncthreads();
   const int olo = sh.olo, ohi = sh.ohi;
@@ -622,7 +635,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   const int d = nw_out - (wb - wa);
   const int nout = cnt + d;
   int st = sh.status;
-  if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.ntiles > 1 ? HALO : 3))) st = ST_CAPACITY;
+  if (dt >= 0.0 && st == 0 && (nout > tl.capt || nout < (tl.tpm > 1 ? HALO : 3))) st = ST_CAPACITY;
   __syncthreads();
   double s_th = 0.0, h_th = INFINITY;
   bool unif = true;
@@ -671,7 +684,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   if (lane == 0) { sh.part_s[warp] = s_th; sh.part_h[warp] = h_th; }
   __syncthreads();
   if (tid == 0) {
-    if (st != 0) atomicCAS(&tl.ctl[1], 0, st);
+    if (st != 0) { atomicCAS(&tl.mctl[MCS * g.m + 1], 0, st); atomicCAS(&tl.ctl[1], 0, st); }
     if (dt >= 0.0 && st == 0) {
       double so = 0.0, ho = INFINITY;
       for (int w = 0; w < nw; ++w) { so = fmax(so, sh.part_s[w]); ho = fmin(ho, sh.part_h[w]); }
@@ -709,8 +722,6 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
   Arr A = carve(smem_raw, WCAP);
   const int tid = threadIdx.x;
-  const double t = tl.scal[0], dt_given = tl.scal[1];
-  if (tl.ctl[1] != 0 || !(t < t_end)) return;
   const int tag = tl.ctl[3] + 1;
   volatile int* vctl = tl.ctl;
   for (;;) {
@@ -744,7 +755,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
     const int j = sh.n_new;
     if (j < 0) break;
     const long long c0 = clock64();
-    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t, t_end, dt_given);
+    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end);
     if (tl.wdbg && tid == 0) {
       long long* d = tl.wdbg + WDBG_FIELDS * (long long)j;
       d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[4 * j + 2] - tl.wlist[4 * j + 1];
@@ -776,8 +787,9 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   const int capg = tl.capt + 2 * HALO + MAXEV + 1;  // even array stride (16-byte aligned rows)
   Arr A = carve(smem_raw, capg);
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+  const bool one = tl.M == 1;  // one grid: this kernel folds the CFL partials and ends the step
   const double t = tl.scal[0], dt_given = tl.scal[1];
-  if (tl.ctl[1] != 0 || !(t < t_end)) {  // uniform across the grid: nothing to do
+  if (one && (tl.mctl[1] != 0 || !(t < t_end))) {  // uniform across the grid: nothing to do
     if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }  // (a no-op step's counters)
     return;
   }
@@ -785,7 +797,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (t + dt > t_end) dt = t_end - t;
   // fast tiles' partials (slow tiles hold neutral values here)
   double s = 0.0, hm = INFINITY;
-  for (int q = blockIdx.x * T + tid; q < tl.ntiles; q += gridDim.x * T) {
+  for (int q = blockIdx.x * T + tid; one && q < tl.ntiles; q += gridDim.x * T) {
     s = fmax(s, tl.part[2 * q]);
     hm = fmin(hm, tl.part[2 * q + 1]);
   }
@@ -804,9 +816,10 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     const int j = sh.n_new;
     if (j >= njobs) break;
     double sk = 0.0, hk = INFINITY;
-    tile_full(e, p, tl, sh, A, capg, tl.slow[j], t, t_end, dt_given, sk, hk);
+    tile_full(e, p, tl, sh, A, capg, tl.slow[j], t_end, sk, hk);
     if (tid == 0) { cta_s = fmax(cta_s, sk); cta_h = fmin(cta_h, hk); }
   }
+  if (!one) return;  // members: tiled_members_finish folds and ends the step
   __shared__ int last;
   if (tid == 0) {
     tl.part2[2 * blockIdx.x] = cta_s;
@@ -817,7 +830,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   __syncthreads();
   if (last) {
     __threadfence();
-    if (tl.ctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
+    if (tl.mctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
     else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }
   }
 }
@@ -828,7 +841,9 @@ __global__ void __launch_bounds__(MAXT)
 tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
               double t_end) {
   const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int cur = tl.ctl[0];
+  const int m = k / tl.tpm;
+  const bool first = k % tl.tpm == 0, lastt = (k + 1) % tl.tpm == 0;
+  const int cur = tl.mctl[MCS * m];
   const long long base = (long long)k * tl.capt;
   const int cnt = tl.cnt[cur][k];
   __shared__ double rs[32], rh[32];
@@ -842,8 +857,8 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     bool tiny = false;
     const double hg = tl.hu[cur][k] ? p.h_av : tl.h[cur][g];
     if (p.mode != 1 && hg < p.eps_tiny * p.h_av) {  // neighbours may live in the next tiles
-      const double rl = i > 0 ? tl.rho[cur][g - 1] : (k > 0 ? tl.rho[cur][base - tl.capt + tl.cnt[cur][k - 1] - 1] : -1.0);
-      const double rr = i < cnt - 1 ? tl.rho[cur][g + 1] : (k < tl.ntiles - 1 ? tl.rho[cur][base + tl.capt] : -1.0);
+      const double rl = i > 0 ? tl.rho[cur][g - 1] : (!first ? tl.rho[cur][base - tl.capt + tl.cnt[cur][k - 1] - 1] : -1.0);
+      const double rr = i < cnt - 1 ? tl.rho[cur][g + 1] : (!lastt ? tl.rho[cur][base + tl.capt] : -1.0);
       const bool same_l = rl > 0.0 && phase_of(e, rl) == ph, same_r = rr > 0.0 && phase_of(e, rr) == ph;
       tiny = !same_l && !same_r;
     }
@@ -858,7 +873,7 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     tl.part[2 * k] = s;
     tl.part[2 * k + 1] = hm;
     __threadfence();
-    last = atomicAdd(&tl.ctl[2], 1) == tl.ntiles - 1;
+    last = tl.M == 1 && atomicAdd(&tl.ctl[2], 1) == tl.ntiles - 1;  // members: tiled_members_finish
   }
   __syncthreads();
   if (last) {
@@ -885,7 +900,7 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
     }
   }
   if (tl.xbuf && (k == 0 || k == tl.ntiles - 1)) {  // initial halos for the first exchange
-    const int cur2 = tl.ctl[0];
+    const int cur2 = tl.mctl[0];
     if (k == 0 && tl.nbr_left) {
       double* sb = tl.xbuf + XB_SEND_LEFT;
       for (int i = tid; i < HALO; i += blockDim.x) {
@@ -905,19 +920,72 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
   }
 }
 
+// Members (independent grids, tl.M > 1), after tiled_slow: one warp per member folds its tiles'
+// partials into its next dt (R5/R6) and, if it stepped (after_step, status 0,
+// t < t_end), advances t, flips its buffers and counts the step.  Block 0 resets the step's
+// work-list counters.  Each member keeps its own dt and t (R25).
+__global__ void tiled_members_finish(const __grid_constant__ Prm p, const __grid_constant__ Tiles tl, double t_end,
+                                     int after_step) {
+  const int lane = threadIdx.x & 31;
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    tl.ctl[8] = tl.ctl[6];
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
+    if (after_step) tl.ctl[3] += 1;
+  }
+  if (m >= tl.M) return;
+  double s = 0.0, hm = INFINITY;
+  for (int j = lane; j < tl.tpm; j += 32) {
+    const int k = m * tl.tpm + j;
+    s = fmax(s, tl.part[2 * k]);
+    hm = fmin(hm, tl.part[2 * k + 1]);
+  }
+  s = warp_max(s);
+  hm = warp_min(hm);
+  if (lane != 0) return;
+  double* sc = tl.scal + SCS * m;
+  int* mc = tl.mctl + MCS * m;
+  if (mc[1] != 0) return;
+  double t_new = sc[0];
+  if (after_step) {
+    if (!(t_new < t_end)) return;  // the member did not step
+    double dt_used = sc[1];
+    if (t_new + dt_used > t_end) dt_used = t_end - t_new;  // as the tile kernels
+    t_new += dt_used;
+    if (mc[2] == 0 || dt_used < sc[2]) sc[2] = dt_used;
+    if (dt_used > sc[3]) sc[3] = dt_used;
+    mc[0] = 1 - mc[0];
+    mc[2] += 1;
+  }
+  double dt = p.cfl * hm / s;
+  if (t_new + dt > t_end) dt = t_end - t_new;
+  sc[0] = t_new;
+  sc[1] = dt;
+  sc[5] = s;
+}
+
+// members still stepping (status 0, t < t_end) -> ctl[10] (run_to polling)
+__global__ void tiled_members_active(const __grid_constant__ Tiles tl, double t_end) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = m < tl.M && tl.mctl[MCS * m + 1] == 0 && tl.scal[SCS * m] < t_end;
+  const unsigned b = __ballot_sync(0xffffffffu, act);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&tl.ctl[10], __popc(b));
+}
+
 // rank mode, after the exchange: dt from the min-reduced pair; after a step also advance t and
 // flip the buffers (what the last CTA does in single-rank mode)
 __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constant__ Tiles tl, double t_end, int after_step) {
-  if (tl.ctl[1] != 0) return;
+  if (tl.mctl[1] != 0) return;
   const double S = -tl.xbuf[XB_DT], hm = tl.xbuf[XB_DT + 1];
   double t_new = tl.scal[0];
   if (after_step) {
     if (!(t_new < t_end)) return;  // the step was a no-op
     const double dt_used = tl.scal[4];
     t_new += dt_used;
-    if (tl.ctl[3] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
+    if (tl.mctl[2] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;
     if (dt_used > tl.scal[3]) tl.scal[3] = dt_used;
-    tl.ctl[0] = 1 - tl.ctl[0];
+    tl.mctl[0] = 1 - tl.mctl[0];
+    tl.mctl[2] += 1;
     tl.ctl[3] += 1;
   }
   tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;

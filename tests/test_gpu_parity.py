@@ -26,9 +26,9 @@ def P():
     return P
 
 
-def gpu_run(P, w, steps=None, t_end=None, threads=0, n_cells=None, max_steps=10 ** 9):
+def gpu_run(P, w, steps=None, t_end=None, threads=0, n_cells=None, max_steps=10 ** 9, layout=0):
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
-                    stream=torch.cuda.current_stream(), threads=threads)
+                    stream=torch.cuda.current_stream(), threads=threads, layout=layout)
     rho = torch.tensor(w["rho"], device="cuda")
     mom = torch.tensor(w["mom"], device="cuda")
     nc = None if n_cells is None else torch.tensor(n_cells, device="cuda", dtype=torch.int64)
@@ -131,11 +131,12 @@ def test_c3_full_size_sampled(P, oracle_mod):
     assert_parity(gs, o, h_av(w))
 
 
-def test_c4_members(P, oracle_mod):
+@pytest.mark.parametrize("layout", [0, 1])  # AUTO (tiled for N = 4096) and member-resident
+def test_c4_members(P, oracle_mod, layout):
     """C4 (nucleation) sample at full N=4096 including nucleating members (DTS every step)."""
     mem = np.arange(12)
     w = W.c4(members=mem)
-    g, _ = gpu_run(P, w, steps=300)
+    g, _ = gpu_run(P, w, steps=300, layout=layout)
     o = oracle_run(oracle_mod, w, steps=300)
     assert_parity(g, o, h_av(w))
     assert g["stats"]["creations"] >= 1 and g["stats"]["dts_iters"] > 0
@@ -543,3 +544,40 @@ def test_lts_mode_c5_tiled_against_oracle(P, oracle_mod):
     assert st["creations"] >= 1 and st["dts_iters"] > 0
     assert st["dts_iters"] == o["stats"]["dts_iters"]
     assert_parity(g, o, h_av(w))
+
+
+# ------------------------------------------------------------------------------ tiled ensembles
+@pytest.mark.parametrize("cfg,steps", [("c3", 300), ("c4", 150)])
+def test_tiled_ensemble_against_oracle(P, oracle_mod, cfg, steps):
+    """Ensembles on the tiled layout (members as independent runs of tiles, each with its own
+    dt, t, status and buffers; halos never cross members), against the oracle per member."""
+    w = W.c3(members=np.arange(5)) if cfg == "c3" else W.c4(members=np.arange(3))
+    ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
+    ctx.set_state(torch.tensor(w["rho"], device="cuda"), torch.tensor(w["mom"], device="cuda"))
+    st = ctx.step(steps, stats=True)
+    g = ctx.get_state()
+    g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["stats"] = st
+    g["mstats"] = ctx.member_stats()
+    o = oracle_run(oracle_mod, w, steps=steps)
+    assert st["creations"] >= 1
+    assert_parity(g, o, h_av(w))
+
+
+def test_tiled_ensemble_run_to_members_stop_individually(P, oracle_mod):
+    """run_to on a tiled ensemble: every member clips its own last step to t_end (R25)."""
+    w = W.c2()
+    M = 3
+    rho = np.repeat(w["rho"], M, axis=0); mom = np.repeat(w["mom"], M, axis=0)
+    mom[1] *= 0.7; mom[2] *= 1.3  # different speeds: different dt sequences
+    w2 = dict(w, M=M, rho=rho, mom=mom)
+    ctx = P.Context(w2["eos"], w2["params"], M, w2["N"], w2["cap"], w2["x_left"], w2["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=300)
+    ctx.set_state(torch.tensor(rho, device="cuda"), torch.tensor(mom, device="cuda"))
+    st = ctx.run_to(w["t_end"], stats=True)
+    g = ctx.get_state()
+    assert np.all(g["t"] == w["t_end"])
+    g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["stats"] = st
+    g["mstats"] = ctx.member_stats()
+    o = oracle_run(oracle_mod, w2, t_end=w["t_end"])
+    assert_parity(g, o, h_av(w2))
