@@ -17,6 +17,10 @@
 #include "eis_resident.cuh"
 #include "eis_tiled.cuh"
 
+#ifndef EIS_FAST_MINB
+#define EIS_FAST_MINB 8  // tiled_fast CTAs of 128 threads per SM (register budget 64)
+#endif
+
 using namespace eis;
 
 struct eis_ctx {
@@ -301,7 +305,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, tiled_fast<128, 8>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, 16, true>) != cudaSuccess ||
+    if (cudaFuncGetAttributes(&fa, tiled_fast<128, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, 16, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, 16, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
       delete c; return EIS_E_CUDA;
@@ -736,7 +740,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
   if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
   if (c->timing) m[0] = timing_event(c);
-  tiled_fast<128, 8><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_fast<128, EIS_FAST_MINB><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);

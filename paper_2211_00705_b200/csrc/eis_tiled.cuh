@@ -208,11 +208,11 @@ constexpr int FW = 60;      // cells updated per window: the pairs of lanes 1..3
 // and by uniform widths (HU).  A cell of another phase (or spinodal, or non-positive) and the
 // right cell of a creation-candidate edge are "special": their index range [slo, shi] decides
 // between the fast result and a full step of a window around them.
-template <bool HU, bool LIQ>
+template <bool HU, bool LIQ, bool MASKED>
 __device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB], const double2 (&mv)[FB], int w0,
                                            int nw, int nwin, int n, int own_lo, int own_hi, double dt, double dt_hav,
                                            double h_av, const double* ih, double* orho, double* omom, double* oh,
-                                           int& slo, int& shi, bool& unif, double& snum, double& sden,
+                                           unsigned bmask, int& slo, int& shi, bool& unif, double& snum, double& sden,
                                            double& h_part) {
   const int lane = threadIdx.x & 31;
   const double a = LIQ ? e.a_l : e.a_v;
@@ -221,6 +221,7 @@ __device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB]
 #pragma unroll
   for (int b = 0; b < FB; ++b) {
     if (w0 + nw * b >= nwin) break;  // warp-uniform
+    if (MASKED && !(bmask >> b & 1)) continue;  // a window of the other specialisation
     const int c0 = FW * (w0 + nw * b) - 2 + 2 * lane, c1 = c0 + 1;
     const double r0 = rv[b].x, r1 = rv[b].y, m0 = mv[b].x, m1 = mv[b].y;
     const double u0 = m0 * rcp_fast(r0), u1 = m1 * rcp_fast(r1);
@@ -327,17 +328,29 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
         }
       }
     }
-    // specialisation: liquid if the batch (windows spread over the tile) has a liquid cell;
-    // warps that differ make the tile take the whole-tile full step
-    bool anyl = false;
+    // specialisation per window: liquid if any of its 64 loaded cells is liquid.  Every edge
+    // lies inside some window's loaded cells, so a phase boundary always leaves a special cell
+    // (the cell of the other phase) and the tile takes a window or whole-tile full step.
+    unsigned lmask = 0, vmask = 0;
 #pragma unroll
-    for (int b = 0; b < FB; ++b) anyl |= w0 + nw * b < nwin && (rv[b].x >= e.rho_min || rv[b].y >= e.rho_min);
-    const bool liq = __any_sync(0xffffffffu, anyl);
-    phases |= liq ? 2 : 1;
-    if (liq) fast_pairs<HU, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
-                                  slo, shi, unif, snum, sden, h_part);
-    else fast_pairs<HU, false>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
-                               slo, shi, unif, snum, sden, h_part);
+    for (int b = 0; b < FB; ++b) {
+      if (w0 + nw * b >= nwin) break;  // warp-uniform
+      vmask |= __any_sync(0xffffffffu, rv[b].x >= e.rho_min || rv[b].y >= e.rho_min) ? 0u : 1u << b;
+      lmask |= vmask >> b & 1 ? 0u : 1u << b;
+    }
+    phases |= (lmask ? 2 : 0) | (vmask ? 1 : 0);
+    if (!vmask)
+      fast_pairs<HU, true, false>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                  lmask, slo, shi, unif, snum, sden, h_part);
+    else if (!lmask)
+      fast_pairs<HU, false, false>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                   vmask, slo, shi, unif, snum, sden, h_part);
+    else {  // a batch whose windows differ in phase (rare): each window with its own
+      fast_pairs<HU, true, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                 lmask, slo, shi, unif, snum, sden, h_part);
+      fast_pairs<HU, false, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
+                                  vmask, slo, shi, unif, snum, sden, h_part);
+    }
   }
   // S_max of this lane's new cells: |m| rcp(rho) (+ a below, as cfl_partials; one phase)
   const double s_lane = warp_max(snum * rcp_fast(sden));
@@ -354,9 +367,11 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   const int f = fl_or;
   // owned cells within HALO (+1 for the edge) of a special cell need the full step: window [wa, wb)
   const int wa = max(own_lo, s_lo - 1 - HALO), wb = min(own_hi, s_hi + 2 + HALO);
+  // both phases in the tile: its windows of one phase see the other phase's cells as special
+  // (so wa < wb); the window full step handles the boundary, the fast cells are single-phase
   const bool mixed = (f & 3) == 3;
   const bool fast = !mixed && wa >= wb;
-  const bool window = !fast && !mixed && wb - wa <= tl.wmax;
+  const bool window = !fast && wa < wb && wb - wa <= tl.wmax;
   unif = !(f & 8);
   if (window) {  // partials and width uniformity of the fast cells (outside [wa, wb)), from the
                  // output just written (the window full step only moves them): as cfl_partials
