@@ -17,6 +17,9 @@
 #include "eis_resident.cuh"
 #include "eis_tiled.cuh"
 
+#ifndef EIS_WIN_MINB
+#define EIS_WIN_MINB 16  // one-warp window CTAs per SM (register budget 128)
+#endif
 #ifndef EIS_FAST_MINB
 #define EIS_FAST_MINB 8  // tiled_fast CTAs of 128 threads per SM (register budget 64)
 #endif
@@ -299,14 +302,14 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     delete c; return EIS_E_CUDA;
   }
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
-  if (cudaFuncSetAttribute(tiled_win<32, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
-      cudaFuncSetAttribute(tiled_win<32, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+  if (cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, tiled_fast<128, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, 16, true>) != cudaSuccess ||
-        cudaFuncGetAttributes(&fa, tiled_win<32, 16, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
+    if (cudaFuncGetAttributes(&fa, tiled_fast<128, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
       delete c; return EIS_E_CUDA;
     }
@@ -314,7 +317,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   int nsm = 0, per_sm = 0, per_sm_w = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, grid->device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiled_slow<256, 4>, 256, c->smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<32, 16, false>, 32, c->smem_win);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, tiled_win<32, EIS_WIN_MINB, false>, 32, c->smem_win);
   c->slow_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm, 1));
   c->win_grid = (int)std::min<long long>(ntiles, (long long)std::max(nsm, 1) * std::max(per_sm_w, 1));
   // the polling instance beside tiled_fast: off by default (measured on C5: 1, 2, 4 CTAs/SM
@@ -744,10 +747,10 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
-    tiled_win<32, 16, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
+    tiled_win<32, EIS_WIN_MINB, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
     cudaEventRecord(c->ev_join, c->stream2);
   }
-  tiled_win<32, 16, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);

@@ -95,6 +95,9 @@ struct CtaShared {
 #ifdef EIS_PHASE_CLOCK
   long long tclk[10];  // development: clock64 at phase boundaries of the last step (thread 0)
 #endif
+#ifdef EIS_DTS_CLOCK
+  long long dclk[5];   // development: DTS cycles in boundary rounds, in updates; iterations; blocks; Newton its
+#endif
 };
 // development probes (-DEIS_PHASE_CLOCK): clock64 at step start (0), arrivals of the solver
 // warp (1, 3) and of warp 0 (2, 4) at barriers A and B, step end (5), S4 start/end (6, 7).
@@ -244,6 +247,10 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
   __syncwarp();
   long long l = 0;
   int err = 0;
+#ifdef EIS_DTS_CLOCK
+  long long dc0 = clock64();
+  if (lane == 0) sh.dclk[3] += 1;
+#endif
   for (int part = 0; part < 2 && !err; ++part) {  // part 0: Part 1 iterations; part 1: fluxes at U*
     for (;;) {
       for (int j0 = 1; j0 < K; j0 += 2) {  // (a) interior edges at W^l, two per round
@@ -257,6 +264,9 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
               if (s.iters < 0) err = ST_NEWTON;
               Fe0[j] = s.F0; Fe1[j] = s.F1; we[j] = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
               ++solves;
+#ifdef EIS_DTS_CLOCK
+              atomicAdd(reinterpret_cast<unsigned long long*>(&sh.dclk[4]), (unsigned long long)s.iters);
+#endif
             }
           } else if (hl == 0) {
             hll(e, pl, rl, ml, ml / rl, rr, mr, mr / rr, Fe0[j], Fe1[j]);
@@ -266,6 +276,9 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       }
       err = __reduce_max_sync(0xffffffffu, err);
       __syncwarp();
+#ifdef EIS_DTS_CLOCK
+      { const long long c = clock64(); if (lane == 0) sh.dclk[0] += c - dc0; dc0 = c; }
+#endif
       if (err || part == 1) break;
       double res_nb = 0.0, res_t = 0.0;  // (b) relaxed moving-cell update (R13)
       int bad = 0;
@@ -288,6 +301,9 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       if (lane < K) { W0[lane] = w0; W1[lane] = w1; }
       __syncwarp();
       ++l;
+#ifdef EIS_DTS_CLOCK
+      { const long long c = clock64(); if (lane == 0) { sh.dclk[1] += c - dc0; sh.dclk[2] += 1; } dc0 = c; }
+#endif
       if (bad) { err = bad; break; }
       if (res_nb < p.tol_nb && res_t < p.tol_tiny) break;
       if (l >= p.dts_max_iter) { err = ST_DTS_CAP; break; }

@@ -199,7 +199,10 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 // the arithmetic).  Outputs of a tile that turns out not plain are overwritten by the full step.
 // ------------------------------------------------------------------------------------------
 #ifndef EIS_FB
-#define EIS_FB 2
+#define EIS_FB 1
+#endif
+#ifndef EIS_FAST_PIPE
+#define EIS_FAST_PIPE 0
 #endif
 constexpr int FB = EIS_FB;  // windows per warp per batch
 constexpr int FW = 60;      // cells updated per window: the pairs of lanes 1..30
@@ -287,10 +290,15 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int k = g.k, n = g.n, own_lo = g.nL, own_hi = g.nL + g.cnt;
   const double h_av = p.h_av, dt_hav = dt / h_av;
-  if (tid == 0) { fl_or = 0; s_lo = 1 << 30; s_hi = -1; }
-  // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
   const double* const rin = tl.rho[g.in];
   const long long mo_t = tl.mom[g.in] - rin;
+  if (tid == 0) {  // the whole tile's requests in flight at once: bulk L2 prefetch of rho and mom
+    const unsigned bytes = (unsigned)(((g.cnt + 1) & ~1) * 8);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rin + g.base), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rin + g.base + mo_t), "r"(bytes) : "memory");
+    fl_or = 0; s_lo = 1 << 30; s_hi = -1;
+  }
+  // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
   const double* const segL = g.xl ? tl.xbuf + XB_RECV_LEFT + HALO - g.nL : rin + g.bl + g.cl - g.nL;
   const long long moL = g.xl ? HALO : mo_t;
   const double* const segO = rin + g.base - g.nL;
@@ -306,11 +314,11 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   double snum = 0.0, sden = 1.0;  // max |m|/rho of the new cells, by cross-multiplication
   double h_part = HU ? h_av : INFINITY;
   const int nwin = (n + FW - 1) / FW;  // windows update cells [0, 60 nwin)
-  for (int w0 = warp; w0 < nwin; w0 += nw * FB) {
-    double2 rv[FB], mv[FB];
+  // loads of the window batch starting at window w: placeholders past the tile
+  auto load_batch = [&](int w, double2 (&rv)[FB], double2 (&mv)[FB]) {
 #pragma unroll
-    for (int b = 0; b < FB; ++b) {  // all loads of the batch first
-      const int wi = w0 + nw * b;
+    for (int b = 0; b < FB; ++b) {
+      const int wi = w + nw * b;
       const int c0 = FW * wi - 2 + 2 * lane;
       rv[b] = make_double2(1.0, 1.0); mv[b] = make_double2(0.0, 0.0);
       if (wi < nwin) {
@@ -328,6 +336,18 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
         }
       }
     }
+  };
+  double2 rv[FB], mv[FB];
+#if EIS_FAST_PIPE
+  load_batch(warp, rv, mv);
+#endif
+  for (int w0 = warp; w0 < nwin; w0 += nw * FB) {
+#if EIS_FAST_PIPE
+    double2 rn[FB], mn[FB];  // the next batch's loads in flight during this batch's arithmetic
+    load_batch(w0 + nw * FB, rn, mn);
+#else
+    load_batch(w0, rv, mv);
+#endif
     // specialisation per window: liquid if any of its 64 loaded cells is liquid.  Every edge
     // lies inside some window's loaded cells, so a phase boundary always leaves a special cell
     // (the cell of the other phase) and the tile takes a window or whole-tile full step.
@@ -351,6 +371,10 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       fast_pairs<HU, false, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
                                   vmask, slo, shi, unif, snum, sden, h_part);
     }
+#if EIS_FAST_PIPE
+#pragma unroll
+    for (int b = 0; b < FB; ++b) { rv[b] = rn[b]; mv[b] = mn[b]; }
+#endif
   }
   // S_max of this lane's new cells: |m| rcp(rho) (+ a below, as cfl_partials; one phase)
   const double s_lane = warp_max(snum * rcp_fast(sden));

@@ -7,8 +7,8 @@ import numpy as np
 import torch
 import paper_2211_00705_b200 as P
 from paper_2211_00705_b200 import workloads as W
-w = W.c5()
-ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+w = W.c4() if os.environ.get("WL") == "C4" else W.c5()
+ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
                 stream=torch.cuda.current_stream(), layout=2)
 ctx.set_state(torch.from_numpy(w["rho"]).cuda(), torch.from_numpy(w["mom"]).cuda())
 nt = ctx.tile_info()["n_tiles"]
