@@ -201,6 +201,9 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 #ifndef EIS_FB
 #define EIS_FB 1
 #endif
+#ifndef EIS_FAST_STATIC_IN
+#define EIS_FAST_STATIC_IN 1
+#endif
 #ifndef EIS_FAST_PIPE
 #define EIS_FAST_PIPE 0
 #endif
@@ -283,15 +286,16 @@ __device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB]
 
 constexpr int WMAX = 160;  // owned cells of a full-step window (larger: the whole tile)
 
-template <bool HU>
+template <bool HU, int IN>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
+  const int BIN = IN >= 0 ? IN : g.in, BOUT = 1 - BIN;  // IN = -1: dynamic
   __shared__ double ps[32], ph[32];
   __shared__ int fl_or, s_lo, s_hi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int k = g.k, n = g.n, own_lo = g.nL, own_hi = g.nL + g.cnt;
   const double h_av = p.h_av, dt_hav = dt / h_av;
-  const double* const rin = tl.rho[g.in];
-  const long long mo_t = tl.mom[g.in] - rin;
+  const double* const rin = tl.rho[BIN];
+  const long long mo_t = tl.mom[BIN] - rin;
   if (tid == 0) {  // the whole tile's requests in flight at once: bulk L2 prefetch of rho and mom
     const unsigned bytes = (unsigned)(((g.cnt + 1) & ~1) * 8);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rin + g.base), "r"(bytes) : "memory");
@@ -304,10 +308,10 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   const double* const segO = rin + g.base - g.nL;
   const double* const segR = g.xr ? tl.xbuf + XB_RECV_RIGHT - own_hi : rin + g.br - own_hi;
   const long long moR = g.xr ? HALO : mo_t;
-  double* const orho = tl.rho[g.out] + g.base - own_lo;  // indexed by the virtual cell
-  double* const omom = tl.mom[g.out] + g.base - own_lo;
-  double* const oh = tl.h[g.out] + g.base - own_lo;
-  const double* const ih = tl.h[g.in] + g.base - own_lo;
+  double* const orho = tl.rho[BOUT] + g.base - own_lo;  // indexed by the virtual cell
+  double* const omom = tl.mom[BOUT] + g.base - own_lo;
+  double* const oh = tl.h[BOUT] + g.base - own_lo;
+  const double* const ih = tl.h[BIN] + g.base - own_lo;
   int slo = 1 << 30, shi = -1;  // special cells (see fast_windows)
   bool unif = true;      // output widths all h_av
   int phases = 0;        // 1 vapour, 2 liquid: the warps' specialisations
@@ -435,8 +439,8 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       for (int w = 0; w < nw; ++w) { s = fmax(s, ps[w]); hm = fmin(hm, ph[w]); }
       tl.part[2 * k] = s + ((f & 3) == 1 ? e.a_v : e.a_l);
       tl.part[2 * k + 1] = hm;
-      tl.cnt[g.out][k] = g.cnt;
-      tl.hu[g.out][k] = unif ? 1 : 0;
+      tl.cnt[BOUT][k] = g.cnt;
+      tl.hu[BOUT][k] = unif ? 1 : 0;
       tl.ws[(size_t)k * WS_STRIDE + 2 * MAXIF] = 0.0;  // no boundary: no warm start
       tl.tstats[k].cell_updates += g.cnt;
       if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
@@ -465,8 +469,18 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (tl.mctl[MCS * g.m + 1] == 0 && t < t_end) {  // else the member does not step (uniform in the CTA)
     double dt = tl.scal[SCS * g.m + 1];
     if (t + dt > t_end) dt = t_end - t;  // as step_body
-    if (g.hu_in) tiled_fast_body<true>(e, p, tl, g, dt);
-    else tiled_fast_body<false>(e, p, tl, g, dt);
+#if EIS_FAST_STATIC_IN
+    if (g.in) {
+      if (g.hu_in) tiled_fast_body<true, 1>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 1>(e, p, tl, g, dt);
+    } else {
+      if (g.hu_in) tiled_fast_body<true, 0>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 0>(e, p, tl, g, dt);
+    }
+#else
+    if (g.hu_in) tiled_fast_body<true, -1>(e, p, tl, g, dt);
+    else tiled_fast_body<false, -1>(e, p, tl, g, dt);
+#endif
   }
   __syncthreads();
   if (threadIdx.x == 0) { __threadfence(); atomicAdd(&tl.ctl[9], 1); }  // every CTA, always
