@@ -23,10 +23,10 @@ MODE_SPLIT, MODE_EXPLICIT, MODE_LTS = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(HERE, "eiso.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
-            os.path.getmtime(src), os.path.getmtime(os.path.join(HERE, "eiso.h"))):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", LIB_PATH, src, "-lm"])
+    srcs = [os.path.join(HERE, f) for f in ("eiso.c", "lax.c")]
+    deps = srcs + [os.path.join(HERE, f) for f in ("eiso.h", "lax.h")]
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(map(os.path.getmtime, deps)):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", LIB_PATH, *srcs, "-lm"])
     return LIB_PATH
 
 
@@ -103,6 +103,9 @@ def lib():
         L.eiso_member_status.argtypes = [C.c_void_p, P(C.c_int32)]
         L.eiso_member_stats.argtypes = [C.c_void_p, C.c_int64, P(Stats)]
         L.eiso_destroy.argtypes = [C.c_void_p]
+        L.eiso_lax_riemann.argtypes = [d, P(d), P(d), d, P(d), P(d), P(d), P(C.c_int32)]
+        L.eiso_lax_flux.argtypes = [d, P(d), P(d), P(d)]
+        L.eiso_lax_run.argtypes = [C.c_void_p, P(d), P(d), P(d), P(d), C.c_void_p]
         _lib = L
     return _lib
 
@@ -252,3 +255,54 @@ class Sim:
         st = Stats()
         lib().eiso_member_stats(self._ctx, int(m), C.byref(st))
         return st.as_dict()
+
+
+# ---------------- Lax shock tube (oracle/lax.c) ----------------
+
+class LaxCase(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("gamma", "rho_l", "u_l", "p_l", "rho_r", "u_r", "p_r", "x_left",
+                                          "x_right")] + \
+               [("n", C.c_int64)] + [(n, C.c_double) for n in ("alpha", "theta_nb", "cfl", "t_end", "tol_nb",
+                                                                "tol_tiny")] + \
+               [("dts_max_iter", C.c_int64), ("implicit_block", C.c_int32)]
+
+
+class LaxStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("dts_iters", C.c_int64), ("dts_max", C.c_int64),
+                ("riemann_solves", C.c_int64), ("t", C.c_double), ("status", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+LAX_DEFAULT = dict(gamma=1.4, rho_l=0.445, u_l=0.698, p_l=3.528, rho_r=0.5, u_r=0.0, p_r=0.571,
+                   x_left=-5.0, x_right=5.0, n=100, alpha=1e-2, theta_nb=0.9, cfl=0.8, t_end=1.0,
+                   tol_nb=1e-3, tol_tiny=1e-1, dts_max_iter=10 ** 8, implicit_block=1)
+
+
+def lax_case(**kw) -> LaxCase:
+    d = dict(LAX_DEFAULT)
+    d.update(kw)
+    return LaxCase(**d)
+
+
+def lax_riemann(gamma, wl, wr, xi=0.0):
+    """Exact gamma-law Riemann solution sampled at x/t = xi: (prim (rho,u,p), p*, u*, iters)."""
+    a = (C.c_double * 3)(*wl)
+    b = (C.c_double * 3)(*wr)
+    out = (C.c_double * 3)()
+    ps, us, it = C.c_double(), C.c_double(), C.c_int32()
+    s = lib().eiso_lax_riemann(C.c_double(gamma), a, b, C.c_double(xi), out, C.byref(ps), C.byref(us), C.byref(it))
+    if s:
+        raise ValueError(f"eiso_lax_riemann status {s}")
+    return np.array(out[:]), ps.value, us.value, it.value
+
+
+def lax_run(case: LaxCase):
+    """Runs one Lax case; returns (rho, mom, E, x_faces, stats dict)."""
+    nc = case.n + 1
+    rho, mom, E = np.zeros(nc), np.zeros(nc), np.zeros(nc)
+    xf = np.zeros(nc + 1)
+    st = LaxStats()
+    lib().eiso_lax_run(C.byref(case), _dp(rho), _dp(mom), _dp(E), _dp(xf), C.byref(st))
+    return rho, mom, E, xf, st.as_dict()

@@ -14,6 +14,6 @@ for k in tiled_fast tiled_win tiled_slow; do
 done
 ls -la gpurun_out | tail -5
 python bench.py --workload C3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-python bench.py --workload C4 --members 2048 --steps 200 --no-e2e > gpurun_out/bench_c4_sample.json 2>&1
+bash tools/profile_c4.sh
 ncu --set full --clock-control none --import-source on -k regex:resident_steps -s 1 -c 1 \
     -o gpurun_out/prof_bench_c3_resident python bench.py --workload C3 --steps 100 --no-cpu --no-e2e > gpurun_out/ncu_full_c3.log 2>&1
