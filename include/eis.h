@@ -219,6 +219,50 @@ eis_status eis_window_diag(eis_ctx* ctx, int64_t* out, int64_t capacity, int64_t
 eis_status eis_set_timing(eis_ctx* ctx, int32_t enable);
 eis_status eis_get_timing(eis_ctx* ctx, double* ms /* [4] */, int64_t* launches);
 
+/* ---------------------------------------------------------------------------------------
+ * Lax shock tube with one small cell (the paper's first test): a batch of
+ * independent cases of the full 1D Euler equations of an ideal gas, each on a fixed mesh of
+ * N + 1 cells -- N/2 cells of width h = (x_right - x_left)/N left of x_left + (N/2) h, the small
+ * cell of width alpha*h, N/2 cells of width h -- run from the Riemann data (left state for the
+ * cells left of the small cell, right state from it on) to t_end.  Every step: dt = cfl h /
+ * S_max (S_max = max |u| + c over every cell but the small one when implicit_block, over all
+ * cells and with h_min otherwise; the last step clipped to t_end), exact Riemann fluxes
+ * on every face, transmissive ends, the explicit update (fixed mesh) outside
+ * {k-1, k, k+1}, and Algorithm 2 on {k-1, k, k+1} with dtau = theta dt, theta_k =
+ * alpha, the residual of P:1128-1131 and the stop rule max(res_{k+-1}) < tol_nb, res_k <
+ * tol_tiny.  Readings L1-L7: DESIGN.md §3.
+ *
+ * One CTA per case; cases run concurrently.  cases and stats: HOST arrays of n_cases records.
+ * rho, mom, E: DEVICE arrays of n_cases * stride doubles; case c's final conserved state is at
+ * [c*stride, c*stride + n + 1).  Requirements: n even, 6 <= n, n + 2 <= stride, n <= 4094,
+ * alpha > 0, theta_nb > 0, cfl > 0, gamma > 1 (EIS_E_ARG otherwise).  Case failures (vacuum or
+ * a non-positive pressure: EIS_E_NONPOS_DENSITY; Riemann Newton: EIS_E_NEWTON; DTS cap:
+ * EIS_E_DTS_CAP) are reported in stats[c].status and do not fail the call.  Runs on `stream`
+ * (a cudaStream_t, NULL = legacy default) and synchronises it.  No context needed.
+ * --------------------------------------------------------------------------------------- */
+typedef struct {
+  double gamma;                      /* ratio of specific heats (1.4)                */
+  double rho_l, u_l, p_l;            /* Riemann data, left                                    */
+  double rho_r, u_r, p_r;            /* Riemann data, right                                   */
+  double x_left, x_right;            /* domain of the N regular cells ([-5, 5])       */
+  int64_t n;                         /* N                                                     */
+  double alpha, theta_nb, cfl, t_end;
+  double tol_nb, tol_tiny;           /* 1e-3, 1e-1                                   */
+  int64_t dts_max_iter;
+  int32_t implicit_block;            /* 1: Algorithm 2 on {k-1, k, k+1}; 0: all explicit      */
+  int32_t reserved;
+} eis_lax_case;
+
+typedef struct {
+  int64_t steps, dts_iters, dts_max, riemann_solves;
+  double t;
+  int32_t status;
+  int32_t reserved;
+} eis_lax_stats;
+
+eis_status eis_lax_run(const eis_lax_case* cases, int64_t n_cases, int64_t stride, double* rho, double* mom,
+                       double* E, eis_lax_stats* stats, void* stream);
+
 /* Last error message of the context (static storage owned by the context). */
 const char* eis_last_error(const eis_ctx* ctx);
 

@@ -75,7 +75,7 @@ class Thresholds(C.Structure):
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
            "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info", "eis_set_timing",
-           "eis_get_timing", "eis_window_diag")
+           "eis_get_timing", "eis_window_diag", "eis_lax_run")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
 XB_REC = 3 * HALO + 1
@@ -113,6 +113,7 @@ def lib():
         L.eis_set_exchange_buffer.argtypes = [vp, vp]
         L.eis_step_local.argtypes = [vp, d]
         L.eis_step_finish.argtypes = [vp, d, i32]
+        L.eis_lax_run.argtypes = [P(LaxCase), i64, i64, vp, vp, vp, P(LaxStats), vp]
         for s in SYMBOLS:
             if s not in ("eis_last_error", "eis_destroy"):
                 getattr(L, s).restype = C.c_int
@@ -137,6 +138,54 @@ def eis_thresholds_of(eos: dict) -> dict:
     if s:
         raise EisError(f"eis_thresholds_of: {STATUS.get(s, s)}")
     return {n: getattr(t, n) for n, _ in t._fields_}
+
+
+class LaxCase(C.Structure):
+    """eis_lax_case (include/eis.h): one Lax shock tube with a small cell."""
+    _fields_ = [(n, C.c_double) for n in ("gamma", "rho_l", "u_l", "p_l", "rho_r", "u_r", "p_r", "x_left",
+                                          "x_right")] + [("n", C.c_int64)] + \
+               [(n, C.c_double) for n in ("alpha", "theta_nb", "cfl", "t_end", "tol_nb", "tol_tiny")] + \
+               [("dts_max_iter", C.c_int64), ("implicit_block", C.c_int32), ("reserved", C.c_int32)]
+
+
+class LaxStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("dts_iters", C.c_int64), ("dts_max", C.c_int64),
+                ("riemann_solves", C.c_int64), ("t", C.c_double), ("status", C.c_int32), ("reserved", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+# the paper's Lax setup (P:1160-1168) and DTS stop rule (P:1132)
+LAX_DEFAULT = dict(gamma=1.4, rho_l=0.445, u_l=0.698, p_l=3.528, rho_r=0.5, u_r=0.0, p_r=0.571, x_left=-5.0,
+                   x_right=5.0, n=100, alpha=1e-2, theta_nb=0.9, cfl=0.8, t_end=1.0, tol_nb=1e-3, tol_tiny=1e-1,
+                   dts_max_iter=10 ** 9, implicit_block=1)
+
+
+def lax_run(cases, stream=None):
+    """eis_lax_run: a batch of Lax cases (dicts overriding LAX_DEFAULT), one CTA each, on the
+    current CUDA device.  Returns (rho, mom, E) as (n_cases, stride) device tensors (row c holds
+    case c's n + 1 cells) and the per-case stats dicts."""
+    import torch
+    recs = []
+    for kw in cases:
+        d = dict(LAX_DEFAULT)
+        d.update(kw)
+        recs.append(LaxCase(**d))
+    n = len(recs)
+    stride = max(r.n for r in recs) + 2
+    arr = (LaxCase * n)(*recs)
+    st = (LaxStats * n)()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rho, mom, E = (torch.zeros((n, stride), dtype=torch.float64, device=dev) for _ in range(3))
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    s = lib().eis_lax_run(arr, n, stride, C.c_void_p(rho.data_ptr()), C.c_void_p(mom.data_ptr()),
+                          C.c_void_p(E.data_ptr()), st, C.c_void_p(sh))
+    if s:
+        raise EisError(f"eis_lax_run: {STATUS.get(s, s)}")
+    return rho, mom, E, [x.as_dict() for x in st]
 
 
 def _ptr(a):

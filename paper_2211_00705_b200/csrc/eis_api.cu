@@ -16,6 +16,7 @@
 #include "eis.h"
 #include "eis_resident.cuh"
 #include "eis_tiled.cuh"
+#include "eis_lax.cuh"
 
 #ifndef EIS_WIN_MINB
 #define EIS_WIN_MINB 16  // one-warp window CTAs per SM (register budget 128)
@@ -959,4 +960,38 @@ extern "C" eis_status eis_step_finish(eis_ctx* c, double t_end, int32_t after_st
   tiled_finish<<<1, 1, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
   CU(cudaGetLastError());
   return EIS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Lax shock tube batches (include/eis.h): validation, one launch, stats back.
+// ---------------------------------------------------------------------------------------------
+extern "C" eis_status eis_lax_run(const eis_lax_case* cases, int64_t n_cases, int64_t stride, double* rho,
+                                  double* mom, double* E, eis_lax_stats* stats, void* stream) {
+  if (!cases || !stats || !rho || !mom || !E || n_cases <= 0 || n_cases > (int64_t)INT32_MAX) return EIS_E_ARG;
+  int64_t nmax = 0;
+  for (int64_t i = 0; i < n_cases; ++i) {
+    const eis_lax_case& c = cases[i];
+    if (c.n < 6 || (c.n & 1) || c.n > lax::LAX_MAX_N || c.n + 2 > stride || !(c.alpha > 0.0) ||
+        !(c.theta_nb > 0.0) || !(c.cfl > 0.0) || !(c.gamma > 1.0) || !(c.x_right > c.x_left) ||
+        !(c.t_end >= 0.0) || c.dts_max_iter < 1)
+      return EIS_E_ARG;
+    nmax = std::max(nmax, c.n);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = lax::smem_bytes((int)nmax);
+  if (cudaFuncSetAttribute(lax::lax_cases, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return EIS_E_CUDA;
+  eis_lax_case* d_cases = nullptr;
+  eis_lax_stats* d_stats = nullptr;
+  if (cudaMallocAsync(&d_cases, sizeof(eis_lax_case) * n_cases, st) != cudaSuccess ||
+      cudaMallocAsync(&d_stats, sizeof(eis_lax_stats) * n_cases, st) != cudaSuccess)
+    return EIS_E_CUDA;
+  cudaMemcpyAsync(d_cases, cases, sizeof(eis_lax_case) * n_cases, cudaMemcpyHostToDevice, st);
+  lax::lax_cases<<<(unsigned)n_cases, lax::LAX_THREADS, smem, st>>>(d_cases, stride, rho, mom, E, d_stats);
+  const cudaError_t le = cudaGetLastError();
+  cudaMemcpyAsync(stats, d_stats, sizeof(eis_lax_stats) * n_cases, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_cases, st);
+  cudaFreeAsync(d_stats, st);
+  const cudaError_t se = cudaStreamSynchronize(st);
+  return le == cudaSuccess && se == cudaSuccess ? EIS_OK : EIS_E_CUDA;
 }

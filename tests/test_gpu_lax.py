@@ -1,0 +1,91 @@
+"""GPU parity of the Lax shock-tube batches (eis_lax_run, paper_2211_00705_b200/csrc/eis_lax.cuh;
+PAPER.md:1143-1201) against the CPU oracle (oracle/lax.c): final conserved states within relative
+L1 1e-9 per component, identical step counts and DTS iteration counts, on the cases of
+tab:iterations (tests/golden/lax_iterations.txt) run as one batch, explicit-only cases and seeded
+Riemann data."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+REL_L1 = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2211_00705_b200 as P
+    return P
+
+
+def _cases():
+    cs = []
+    for th in (0.9, 0.1):
+        for N in (100, 200, 400):
+            for a in (1e-2, 1e-4, 1e-6):
+                cs.append(dict(n=N, alpha=a, theta_nb=th))
+    for N in (100, 200, 400):
+        cs.append(dict(n=N, alpha=1e-2, theta_nb=1e-2))
+    cs.append(dict(n=100, alpha=1.0, implicit_block=0))
+    cs.append(dict(n=400, alpha=1.0, implicit_block=0))
+    cs.append(dict(n=64, alpha=0.5, implicit_block=0, t_end=0.5))
+    rng = np.random.default_rng(2211)
+    for i in range(6):  # seeded Riemann data, ragged N
+        cs.append(dict(n=int(rng.integers(3, 160)) * 2, alpha=float(10 ** rng.uniform(-6, -1)),
+                       theta_nb=float(rng.uniform(0.05, 1.0)), rho_l=float(rng.uniform(0.2, 2)),
+                       u_l=float(rng.uniform(-1, 1)), p_l=float(rng.uniform(0.2, 4)), rho_r=float(rng.uniform(0.2, 2)),
+                       u_r=float(rng.uniform(-1, 1)), p_r=float(rng.uniform(0.2, 4)), t_end=float(rng.uniform(0.2, 1))))
+    return cs
+
+
+def _rel_l1(a, b):
+    return np.abs(a - b).sum() / max(np.abs(b).sum(), 1e-300)
+
+
+def _oracle(O, kw):
+    d = {k: v for k, v in kw.items()}
+    return O.lax_run(O.lax_case(**d))
+
+
+def test_lax_batch_parity(P, oracle_mod):
+    O = oracle_mod
+    cases = _cases()
+    rho, mom, E, stats = P.lax_run(cases)
+    rho, mom, E = rho.cpu().numpy(), mom.cpu().numpy(), E.cpu().numpy()
+    for i, kw in enumerate(cases):
+        r, m, e, xf, so = _oracle(O, kw)
+        sg = stats[i]
+        assert sg["status"] == 0 and so["status"] == 0, (kw, sg, so)
+        assert sg["steps"] == so["steps"], (kw, sg, so)
+        assert sg["dts_iters"] == so["dts_iters"] and sg["dts_max"] == so["dts_max"], (kw, sg, so)
+        assert sg["riemann_solves"] == so["riemann_solves"], (kw, sg, so)
+        assert sg["t"] == pytest.approx(so["t"], rel=1e-15)
+        nc = kw["n"] + 1
+        for got, ref in ((rho[i, :nc], r), (mom[i, :nc], m), (E[i, :nc], e)):
+            assert _rel_l1(got, ref) <= REL_L1, (kw, _rel_l1(got, ref))
+
+
+def test_lax_theta_alpha_at_scale(P, oracle_mod):
+    """theta_{k+-1} = alpha = 1e-4 (~4e4 DTS iterations per step): GPU vs oracle at
+    N = 100, and the printed O(1/alpha) growth for N = 100, 200, 400 within the R23 factor 1.5."""
+    O = oracle_mod
+    cases = [dict(n=N, alpha=1e-4, theta_nb=1e-4) for N in (100, 200, 400)]
+    rho, mom, E, stats = P.lax_run(cases)
+    printed = {100: 43470, 200: 34356, 400: 24178}  # tests/golden/lax_iterations.txt
+    for kw, sg in zip(cases, stats):
+        assert sg["status"] == 0
+        avg = sg["dts_iters"] / sg["steps"]
+        assert printed[kw["n"]] / 1.5 <= avg <= printed[kw["n"]] * 1.5, (kw, avg)
+    r, m, e, xf, so = _oracle(O, cases[0])
+    assert stats[0]["dts_iters"] == so["dts_iters"] and stats[0]["steps"] == so["steps"]
+    assert _rel_l1(rho[0, :101].cpu().numpy(), r) <= REL_L1
+
+
+def test_lax_bad_arguments(P):
+    for bad in (dict(n=101), dict(n=4), dict(alpha=0.0), dict(theta_nb=-1.0), dict(n=5000)):
+        with pytest.raises(P.EisError):
+            P.lax_run([bad])
