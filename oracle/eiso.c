@@ -593,6 +593,145 @@ out:
   return st;
 }
 
+/* ---- Newton-like solve of the implicit system (mode NEWTON; readings N1-N5) ----
+ * The fixed point of Algorithm 2's Part 1 is the implicit moving-cell system W = T(W),
+ * T_i(W) = (h_i^n / h_i(W)) U_i^n - (dt / h_i(W)) (F_{i+1/2}(W) - F_{i-1/2}(W)),
+ * h_i(W) = h_i^n + (w_{i+1/2}(W) - w_{i-1/2}(W)) dt, outer fluxes as in dts_block (N1).  It is
+ * solved by a chord Newton iteration on R(W) = W - T(W) from W^0 = U^n with a forward-difference
+ * Jacobian at W^0, eps_q = 1e-7 max(|W_q|, 1) (N2), dense Gaussian elimination with partial
+ * pivoting; stop when the step satisfies max_q |dW_q| / max(|W_q|, 1) <= 1e-10, or when it no
+ * longer halves after the second chord step (the rounding floor of the inner Riemann solves,
+ * N3); the Jacobian is refreshed at the current iterate every 8 chord steps.  *iters_out counts
+ * evaluations of T (1 + 2K for R and the Jacobian, 1 per further chord step, N4).  Part 2 is
+ * Algorithm 2's. */
+static int newton_T(eiso_ctx* c, int64_t m, int64_t a, int64_t K, const edge_t* E, double dt, const double* X,
+                    double* T, double* F0, double* F1, double* w, int64_t* nsolves) {
+  int64_t base = m * c->cap;
+  const double* rho = c->rho + base;
+  const double* mom = c->mom + base;
+  const double* h = c->h + base;
+  F0[0] = E[a].F0; F1[0] = E[a].F1; w[0] = E[a].w;
+  F0[K] = E[a + K].F0; F1[K] = E[a + K].F1; w[K] = E[a + K].w;
+  for (int64_t j = 1; j < K; ++j) {
+    int kind;
+    int st = edge_flux(c, X[2 * (j - 1)], X[2 * (j - 1) + 1], X[2 * j], X[2 * j + 1], &F0[j], &F1[j], &w[j], &kind,
+                       nsolves);
+    if (st) return st;
+  }
+  for (int64_t i = 0; i < K; ++i) {
+    double hl = h[a + i] + (w[i + 1] - w[i]) * dt;
+    if (!(hl > 0.0)) return EISO_E_WIDTH;
+    T[2 * i] = (h[a + i] / hl) * rho[a + i] - (dt / hl) * (F0[i + 1] - F0[i]);
+    T[2 * i + 1] = (h[a + i] / hl) * mom[a + i] - (dt / hl) * (F1[i + 1] - F1[i]);
+  }
+  return 0;
+}
+
+/* J x = b by Gaussian elimination with partial pivoting (J, b overwritten; x = b on return) */
+static int dense_solve(int64_t n, double* J, double* b) {
+  for (int64_t p = 0; p < n; ++p) {
+    int64_t piv = p;
+    for (int64_t i = p + 1; i < n; ++i)
+      if (fabs(J[i * n + p]) > fabs(J[piv * n + p])) piv = i;
+    if (!(fabs(J[piv * n + p]) > 0.0)) return 1;
+    if (piv != p) {
+      for (int64_t q = 0; q < n; ++q) { double t = J[p * n + q]; J[p * n + q] = J[piv * n + q]; J[piv * n + q] = t; }
+      double t = b[p]; b[p] = b[piv]; b[piv] = t;
+    }
+    for (int64_t i = p + 1; i < n; ++i) {
+      double f = J[i * n + p] / J[p * n + p];
+      for (int64_t q = p; q < n; ++q) J[i * n + q] -= f * J[p * n + q];
+      b[i] -= f * b[p];
+    }
+  }
+  for (int64_t p = n - 1; p >= 0; --p) {
+    double s = b[p];
+    for (int64_t q = p + 1; q < n; ++q) s -= J[p * n + q] * b[q];
+    b[p] = s / J[p * n + p];
+  }
+  return 0;
+}
+
+static int newton_jacobian(eiso_ctx* c, int64_t m, int64_t a, int64_t K, const edge_t* E, double dt, const double* X,
+                           const double* T, double* J, double* Xp, double* Tp, double* F0, double* F1, double* w,
+                           int64_t* nsolves) {
+  int64_t n = 2 * K;
+  for (int64_t q = 0; q < n; ++q) {
+    memcpy(Xp, X, sizeof(double) * n);
+    double eps = 1e-7 * fmax(fabs(X[q]), 1.0);
+    Xp[q] += eps;
+    int st = newton_T(c, m, a, K, E, dt, Xp, Tp, F0, F1, w, nsolves);
+    if (st) return st;
+    for (int64_t i = 0; i < n; ++i) J[i * n + q] = (i == q ? 1.0 : 0.0) - (Tp[i] - T[i]) / eps;
+  }
+  return 0;
+}
+
+static int newton_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t* E, double dt,
+                        double* rho_new, double* mom_new, double* h_new, int64_t* iters_out, int64_t* nsolves) {
+  int64_t base = m * c->cap;
+  const double* rho = c->rho + base;
+  const double* mom = c->mom + base;
+  const double* h = c->h + base;
+  int64_t K = b - a + 1, n = 2 * K;
+  double* X = (double*)malloc(sizeof(double) * (5 * n + 3 * (K + 1) + n * n * 2));
+  double *T = X + n, *R = T + n, *Xp = R + n, *Tp = Xp + n;
+  double *F0 = Tp + n, *F1 = F0 + (K + 1), *w = F1 + (K + 1);
+  double *J = w + (K + 1), *LU = J + n * n;
+  int* ph0 = (int*)malloc(sizeof(int) * K);
+  int st = 0;
+  int64_t evals = 0;
+  for (int64_t i = 0; i < K; ++i) {
+    X[2 * i] = rho[a + i]; X[2 * i + 1] = mom[a + i];
+    ph0[i] = phase_of(&c->e, rho[a + i]);
+  }
+  st = newton_T(c, m, a, K, E, dt, X, T, F0, F1, w, nsolves);
+  ++evals;
+  if (st) goto out;
+  st = newton_jacobian(c, m, a, K, E, dt, X, T, J, Xp, Tp, F0, F1, w, nsolves);
+  evals += n;
+  if (st) goto out;
+  double prev = INFINITY;
+  for (int64_t it = 1;; ++it) {
+    if (it > c->prm.dts_max_iter) { st = EISO_E_DTS_CAP; goto out; }
+    for (int64_t i = 0; i < n; ++i) R[i] = -(X[i] - T[i]);
+    memcpy(LU, J, sizeof(double) * n * n);
+    if (dense_solve(n, LU, R)) { st = EISO_E_NEWTON; goto out; }
+    double step = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      X[i] += R[i];
+      step = fmax(step, fabs(R[i]) / fmax(fabs(X[i]), 1.0));
+    }
+    for (int64_t i = 0; i < K; ++i)
+      if (!(X[2 * i] > 0.0) || phase_of(&c->e, X[2 * i]) != ph0[i]) { st = EISO_E_SPINODAL; goto out; }
+    if (step <= 1e-10 || (it >= 2 && step >= 0.5 * prev)) break;  /* N3 */
+    prev = step;
+    st = newton_T(c, m, a, K, E, dt, X, T, F0, F1, w, nsolves);
+    ++evals;
+    if (st) goto out;
+    if (it % 8 == 0) {  /* refresh the chord Jacobian at the current iterate */
+      st = newton_jacobian(c, m, a, K, E, dt, X, T, J, Xp, Tp, F0, F1, w, nsolves);
+      evals += n;
+      if (st) goto out;
+    }
+  }
+  *iters_out = evals;
+  /* Part 2: fluxes at U* and the conservative moving-cell update */
+  st = newton_T(c, m, a, K, E, dt, X, T, F0, F1, w, nsolves);
+  if (st) goto out;
+  for (int64_t i = 0; i < K; ++i) {
+    double hn = h[a + i] + (w[i + 1] - w[i]) * dt;
+    if (!(hn > 0.0)) { st = EISO_E_WIDTH; goto out; }
+    h_new[a + i] = hn;
+    rho_new[a + i] = (h[a + i] / hn) * rho[a + i] - (dt / hn) * (F0[i + 1] - F0[i]);
+    mom_new[a + i] = (h[a + i] / hn) * mom[a + i] - (dt / hn) * (F1[i + 1] - F1[i]);
+  }
+out:
+  free(X);
+  free(ph0);
+  return st;
+}
+
 /* Explicit time-accurate local time stepping (LTS) on an implicit block [a, b]: the paper's
  * comparison method, the reduced Mueller-Stiriba scheme of the disabled passage
  * P:1068-1091, readings R29-R31.  The tiny cells of the block advance with 2^n0 sub-steps of
@@ -791,6 +930,8 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     int64_t b = i - 1, it = 0;
     if (P->mode == EISO_MODE_LTS)
       st = lts_block(c, m, a, b, E, dt, Smax, rho_new, mom_new, h_new, &it, &S->iface_solves);
+    else if (P->mode == EISO_MODE_NEWTON)
+      st = newton_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
     else
       st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
     if (st) goto out;

@@ -33,7 +33,7 @@ enum {
   EISO_E_WIDTH = 8, EISO_E_CAPACITY = 9, EISO_E_UNSUPPORTED = 12
 };
 enum { EISO_VAP = 0, EISO_LIQ = 1, EISO_SPIN = 2 };
-enum { EISO_MODE_SPLIT = 0, EISO_MODE_EXPLICIT = 1, EISO_MODE_LTS = 2 };
+enum { EISO_MODE_SPLIT = 0, EISO_MODE_EXPLICIT = 1, EISO_MODE_LTS = 2, EISO_MODE_NEWTON = 3 };
 
 typedef struct {
   double a_v2;       /* vapour  p = a_v2 * rho              */
@@ -52,7 +52,8 @@ typedef struct {
   double newton_rtol;         /* R14 */
   double newton_gtol;         /* R14 */
   int32_t newton_max_iter, armijo_max; /* R14; Armijo halvings (Kelley)          */
-  int32_t mode;               /* EISO_MODE_SPLIT (Alg. 1-2) | EISO_MODE_EXPLICIT | EISO_MODE_LTS */
+  int32_t mode;               /* EISO_MODE_SPLIT (Alg. 1-2) | EISO_MODE_EXPLICIT | EISO_MODE_LTS |
+                               EISO_MODE_NEWTON (Alg. 2's implicit system by chord Newton, N1-N5) */
 } eiso_params;
 
 /* derived thresholds (R3) */

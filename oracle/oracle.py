@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
 
 VAP, LIQ, SPIN = 0, 1, 2
-MODE_SPLIT, MODE_EXPLICIT, MODE_LTS = 0, 1, 2
+MODE_SPLIT, MODE_EXPLICIT, MODE_LTS, MODE_NEWTON = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:

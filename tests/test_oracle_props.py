@@ -289,7 +289,7 @@ def _totals(st):
     return (st["h"][0, :n] * st["rho"][0, :n]).sum(), (st["h"][0, :n] * st["mom"][0, :n]).sum()
 
 
-@pytest.mark.parametrize("mode", [0, 2])
+@pytest.mark.parametrize("mode", [0, 2, 3])
 def test_conservation_through_creation_and_dts(oracle_mod, mode):
     """Sum h U changes only by the boundary fluxes (P:621 'by construction ... preserves
     conservation'; R17 creation; flux bounding P:601).  C2 data; 60 steps through creation,
@@ -456,3 +456,74 @@ def test_single_phase_rarefaction_convergence(oracle_mod, N):
         exact[xi >= du / 2 + a] = r
         res[n] = np.abs(st["rho"][0, :n] - exact).sum() * (2.0 / n)
     assert res[2 * N] < res[N]
+
+
+def _e2_with(oracle_mod, mode, **prm):
+    old = dict(PRM)
+    PRM.update(prm)
+    try:
+        return _e2_run(oracle_mod, mode)
+    finally:
+        PRM.clear()
+        PRM.update(old)
+
+
+def test_newton_mode_is_the_fixed_point_of_dts(oracle_mod):
+    """Mode NEWTON (readings N1-N5) solves the implicit system whose fixed point Algorithm 2's
+    Part 1 iterates to.  DTS run with tolerances 1e6 / 1e6 times tighter than the paper's
+     must land on the Newton solution: on the cavitation test E2 the two independent
+    solvers agree to 1e-12 relative L1 (at the paper's tolerances they differ by ~1e-8)."""
+    g, eos, s3, st3 = _e2_with(oracle_mod, 3)
+    _, _, s0, st0 = _e2_with(oracle_mod, 0, tol_nb=1e-9, tol_tiny=1e-7)
+    assert s3.member_status()[0] == 0 and s0.member_status()[0] == 0
+    assert st3["steps"] == st0["steps"] == int(g["large_steps"])
+    a, b = s3.get_state(), s0.get_state()
+    n = int(a["n"][0])
+    assert n == int(b["n"][0])
+    for k in ("rho", "mom", "h"):
+        assert np.abs(a[k][0, :n] - b[k][0, :n]).sum() <= 1e-12 * np.abs(b[k][0, :n]).sum(), k
+    xs = [i["x"] for i in s3.interfaces()]
+    assert xs[1] - xs[0] == pytest.approx(g["bubble_width_t_end"], rel=1e-5)  # P:1264
+
+
+def test_newton_mode_nucleation_e3(oracle_mod):
+    """Mode NEWTON on the nucleation test E3: the printed droplet width
+    and step count (R21) as with DTS, the DTS result within the DTS tolerance, and a
+    few evaluations per region instead of the rounding-sensitive DTS counts (R28: ~2.9e6 DTS
+    iterations here, 1.37e6 printed)."""
+    from conftest import eos_363K, read_golden
+    from test_oracle_pins import _run_363K
+    eos = eos_363K()
+    old = dict(W.PARAMS)
+    W.PARAMS["mode"] = 3
+    try:
+        g, s, st = _run_363K(oracle_mod, eos, "nuc")
+    finally:
+        W.PARAMS.clear()
+        W.PARAMS.update(old)
+    assert s.member_status()[0] == 0
+    xs = [i["x"] for i in s.interfaces()]
+    assert xs[1] - xs[0] == pytest.approx(g["droplet_width_t_end"], rel=2e-2)
+    assert abs(st["steps"] - g["large_steps"]) <= 4
+    assert st["dts_iters"] < 20 * st["regions"]
+
+
+def test_newton_mode_c4_droplet(oracle_mod):
+    """A C4 member with a one-cell droplet (BASELINE configs[3]), 300 steps: mode NEWTON agrees
+    with DTS within DTS's own convergence error (~1e-8 relative L1) and needs fewer than a third
+    of the evaluations (~8 vs ~34 per region)."""
+    w = W.c4(members=[1])
+    out = {}
+    for mode in (0, 3):
+        prm = dict(w["params"])
+        prm["mode"] = mode
+        s = oracle_mod.Sim(w["eos"], prm, 1, w["N"], w["cap"], w["x_left"], w["x_right"])
+        s.set_state(w["rho"], w["mom"])
+        st = s.step(300)
+        assert s.member_status()[0] == 0
+        out[mode] = (s.get_state(), st)
+    (a, sa), (b, sb) = out[3], out[0]
+    n = int(a["n"][0])
+    assert n == int(b["n"][0]) and sa["regions"] == sb["regions"] > 0
+    assert np.abs(a["rho"][0, :n] - b["rho"][0, :n]).sum() <= 1e-6 * np.abs(b["rho"][0, :n]).sum()
+    assert 3 * sa["dts_iters"] < sb["dts_iters"]
