@@ -55,23 +55,38 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--members", type=int, default=0, help="profiling only: fewer ensemble members")
     ap.add_argument("--start-steps", type=int, default=0, help="profiling only: untimed steps before the timed launch")
+    ap.add_argument("--mode", type=int, default=None, choices=[0, 1, 2, 3],
+                    help="implicit-region treatment: 0 split/DTS (default, the paper), 1 explicit, 2 LTS, 3 Newton")
     a = ap.parse_args()
+    global MODE
+    MODE = a.mode
     if a.steps is None:
         a.steps = 500 if a.workload == "C5" else 2000
     return a
 
 
+MODE = None  # --mode: the implicit-region treatment (default: the workload's, SPLIT = the paper's DTS)
+MODE_NAMES = {0: "split (dual time stepping)", 1: "explicit", 2: "local time stepping", 3: "newton (chord Newton)"}
+
+
+def with_mode(w):
+    if MODE is not None:
+        w["params"] = dict(w["params"])
+        w["params"]["mode"] = MODE
+    return w
+
+
 def workload(name, members=None):
     from paper_2211_00705_b200 import workloads as W
     if name == "C3":
-        return W.c3(members=members) if members is not None else W.c3()
+        return with_mode(W.c3(members=members) if members is not None else W.c3())
     if name == "C4":
-        return W.c4(members=members) if members is not None else W.c4()
+        return with_mode(W.c4(members=members) if members is not None else W.c4())
     if name == "C1":
-        return W.c1()
+        return with_mode(W.c1())
     if name == "C5":
-        return W.c5(n_cells=members) if members is not None else W.c5()
-    return W.c2()
+        return with_mode(W.c5(n_cells=members) if members is not None else W.c5())
+    return with_mode(W.c2())
 
 
 def total_members(name):
@@ -346,7 +361,8 @@ def main():
                        else f"{name}: {Mtot} members x {w['N']} cells",
                        "members": Mtot, "cells_per_member": w["N"], "cell_capacity": w["cap"],
                        "parallelism": f"member-sharded dp{world}", "l2": "inputs (1.1 GB per GPU) larger than L2",
-                       "layout": "tiled" if tiled else "member-resident", "launches": launch_note},
+                       "layout": "tiled" if tiled else "member-resident", "launches": launch_note,
+                       "implicit_regions": MODE_NAMES[w["params"].get("mode", 0)]},
             "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
@@ -363,7 +379,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     from paper_2211_00705_b200 import workloads as W
     from paper_2211_00705_b200.decomp import RankGrid
     n_glob = args.members or (1 << 27)   # --members: profiling only, fewer cells
-    w = W.c5(n_cells=n_glob)
+    w = with_mode(W.c5(n_cells=n_glob))
     stream = torch.cuda.current_stream()
     rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
                   tile=int(os.environ.get("EIS_TILE", "940")),
@@ -372,6 +388,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     mom_l = np.zeros(rg.cap)
     rho_l[:rg.n] = w["rho"][0, rg.c0:rg.c1]
     mom_l[:rg.n] = w["mom"][0, rg.c0:rg.c1]
+    mode = w["params"].get("mode", 0)
     del w
     rho_d = torch.from_numpy(rho_l).cuda()
     mom_d = torch.from_numpy(mom_l).cuda()
@@ -455,6 +472,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
             "config": {"workload": f"C5: one grid of {n_glob} cells, 4096-cell random segments",
                        "cells": n_glob, "parallelism": f"tile-aligned grid slices x{world}, halo exchange + CFL min",
                        "l2": "state (2 GB) larger than L2",
+                       "implicit_regions": MODE_NAMES[mode],
                        "launches": "per step: tiled_fast + tiled_win + tiled_slow"
                        + (" + NCCL halo exchange / all-reduce + tiled_finish" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

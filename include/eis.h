@@ -60,9 +60,13 @@ enum { EIS_HOST = 0, EIS_DEVICE = 1 };
 enum {
   EIS_MODE_SPLIT = 0,    /* Algorithms 1-2: dual time stepping on the tiny cells' neighbourhoods        */
   EIS_MODE_EXPLICIT = 1, /* global explicit, dt from all cells                                          */
-  EIS_MODE_LTS = 2       /* explicit local time stepping of the tiny cells (the paper's comparison method,
+  EIS_MODE_LTS = 2,      /* explicit local time stepping of the tiny cells (the paper's comparison method,
                             P:472-482; readings R29-R31); stats count its sub-steps as
                             dts_iters ("local iterations")                                               */
+  EIS_MODE_NEWTON = 3    /* as SPLIT, with Algorithm 2's implicit system W = T(W) solved by a chord Newton
+                            iteration (forward-difference Jacobian at U^n) instead of dual time stepping:
+                            the paper's "Newton-like approach" (readings N1-N5); stats
+                            count evaluations of T as dts_iters                                          */
 };
 enum { EIS_VAP = 0, EIS_LIQ = 1, EIS_SPIN = 2 };
 enum { EIS_LAYOUT_AUTO = 0, EIS_LAYOUT_RESIDENT = 1, EIS_LAYOUT_TILED = 2 };
@@ -90,7 +94,7 @@ typedef struct {
   double newton_gtol;        /* R14: 1e-12 (scaled residual)                               */
   int32_t newton_max_iter;   /* R14: 50                                                    */
   int32_t armijo_max;        /* Armijo halvings (Kelley): 30                       */
-  int32_t mode;              /* EIS_MODE_SPLIT | EIS_MODE_EXPLICIT | EIS_MODE_LTS          */
+  int32_t mode;              /* EIS_MODE_SPLIT | _EXPLICIT | _LTS | _NEWTON                */
   int32_t reserved;
 } eis_params;
 

@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EIS_LIB") or os.path.join(HERE, "libeis.so")  # EIS_LIB: a variant build (tools)
 
 EIS_HOST, EIS_DEVICE = 0, 1
-MODE_SPLIT, MODE_EXPLICIT, MODE_LTS = 0, 1, 2
+MODE_SPLIT, MODE_EXPLICIT, MODE_LTS, MODE_NEWTON = 0, 1, 2, 3
 LAYOUT_AUTO, LAYOUT_RESIDENT, LAYOUT_TILED = 0, 1, 2
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_ORDER", 3: "E_NONPOS_DENSITY", 4: "E_SPINODAL", 5: "E_NEWTON",
           6: "E_CREATION", 7: "E_DTS_CAP", 8: "E_WIDTH", 9: "E_CAPACITY", 10: "E_CUDA", 11: "E_NCCL",

@@ -480,7 +480,8 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
     return EIS_E_ARG;
   if (!(prm->cfl > 0) || !(prm->eps_tiny > 0) || !(prm->eps_split > prm->eps_tiny) || !(prm->theta_nb > 0) ||
       prm->newton_max_iter < 1 || prm->armijo_max < 0 || prm->armijo_max > 31 || prm->dts_max_iter < 1 ||
-      (prm->mode != EIS_MODE_SPLIT && prm->mode != EIS_MODE_EXPLICIT && prm->mode != EIS_MODE_LTS))
+      (prm->mode != EIS_MODE_SPLIT && prm->mode != EIS_MODE_EXPLICIT && prm->mode != EIS_MODE_LTS &&
+       prm->mode != EIS_MODE_NEWTON))
     return EIS_E_ARG;
   eis_thresholds th;
   if (eis_thresholds_of(eos, &th) != EIS_OK) return EIS_E_ARG;

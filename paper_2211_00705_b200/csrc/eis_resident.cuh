@@ -330,6 +330,231 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
 }
 
 // ------------------------------------------------------------------------------------------
+// Mode NEWTON (readings N1-N5): Algorithm 2's implicit system W = T(W) on the
+// block [a, b] by a chord Newton iteration, one warp.  Lane i < K owns cell i: its state X_i,
+// T_i(X), U_i^n and its row of the block-tridiagonal Jacobian of R = X - T (2x2 blocks L_i, D_i,
+// U_i), built by forward differences: perturbing one unknown of cell j changes only edges j and
+// j+1, which the two half warps re-solve in one round (warm-started from the base solution);
+// lanes j-1, j, j+1 then form their column entries.  The linear solve is a block Thomas sweep
+// across the lanes (2x2 inverses, shuffles).  Same blocks, outer fluxes and Part 2 as dts_block.
+// ------------------------------------------------------------------------------------------
+struct NtRow {  // lane i's row of the block-tridiagonal Jacobian
+  double L[4], D[4], U[4];  // row-major 2x2
+};
+
+__device__ __forceinline__ void nt_set_col(double (&B)[4], int c, double v0, double v1) {
+  if (c == 0) { B[0] = v0; B[2] = v1; } else { B[1] = v0; B[3] = v1; }
+}
+
+// T_i from the edge values left (g0l, g1l, wl) and right (g0r, g1r, wr) of cell i
+__device__ __forceinline__ bool nt_T(double rn0, double rn1, double hn, double dt, double g0l, double g1l, double wl,
+                                     double g0r, double g1r, double wr, double& t0, double& t1) {
+  const double hl = __dadd_rn(hn, __dmul_rn(wr - wl, dt));
+  if (!(hl > 0.0)) return false;
+  t0 = (hn / hl) * rn0 - (dt / hl) * (g0r - g0l);
+  t1 = (hn / hl) * rn1 - (dt / hl) * (g1r - g1l);
+  return true;
+}
+
+// flux of the edge between cells (rl, ml) and (rr, mr) of phases pl, pr (of U^n) by a half warp;
+// returns false if the boundary solve failed.  x0/x1: warm start in, root out (interface edges).
+__device__ __forceinline__ bool nt_edge(const Eos& e, const Prm& p, double rl, double ml, double rr, double mr, int pl,
+                                        int pr, double& x0, double& x1, unsigned hmask, int hl, int half, double& F0,
+                                        double& F1, double& w, long long& solves) {
+  if (pl != pr) {
+    IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, x0, x1, hmask, hl, half * 16);
+    F0 = s.F0; F1 = s.F1; w = s.w; x0 = s.pV; x1 = s.pL;
+    if (hl == 0) ++solves;
+    return s.iters >= 0;
+  }
+  hll(e, pl, rl, ml, ml / rl, rr, mr, mr / rr, F0, F1);
+  w = 0.0;
+  return true;
+}
+
+__device__ __noinline__ int newton_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
+                                         const double* F0, const double* F1, const uint8_t* fl, int a, int b, double dt,
+                                         long long& it_out, long long& solves, int& remesh) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const int K = b - a + 1;
+  double* sc = sh.dts;
+  double* W0 = sc;               // [MAXB] the current iterate X (broadcast for the edge solves)
+  double* W1 = sc + MAXB;
+  double* Fe0 = sc + 2 * MAXB;   // [MAXB+1] edge values at X (edges 0 and K: the outer fluxes)
+  double* Fe1 = Fe0 + MAXB + 1;
+  double* we = Fe1 + MAXB + 1;
+  double* xs0 = we + MAXB + 1;   // warm starts of the interface edges
+  double* xs1 = xs0 + MAXB + 1;
+  if (lane == 0) {
+    double g0, g1, w;
+    edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
+    Fe0[0] = g0; Fe1[0] = g1; we[0] = w;
+    edge_view(sh, fl, F0, F1, b + 1, 0, g0, g1, w);
+    Fe0[K] = g0; Fe1[K] = g1; we[K] = w;
+  }
+  if (lane >= 1 && lane < K) {
+    const Ifc* s = find_ifc(sh, a + lane);
+    xs0[lane] = s ? s->pV : -1.0;
+    xs1[lane] = s ? s->pL : -1.0;
+  }
+  double rn0 = 1.0, rn1 = 0.0, hn = 1.0, X0 = 1.0, X1 = 0.0, T0 = 0.0, T1 = 0.0;
+  int ph0 = 0;
+  if (lane < K) {
+    rn0 = rho[a + lane]; rn1 = mom[a + lane]; hn = h[a + lane];
+    ph0 = phase_of(e, rn0);
+    X0 = rn0; X1 = rn1;
+    W0[lane] = X0; W1[lane] = X1;
+  }
+  __syncwarp();
+  int err = 0;
+  long long evals = 0;
+  // edges 1..K-1 at X (two per round), then T_i on lanes i < K
+  auto eval_T = [&]() {
+    for (int j0 = 1; j0 < K; j0 += 2) {
+      const int j = j0 + half;
+      if (j < K) {
+        double x0 = xs0[j], x1 = xs1[j], g0, g1, w;
+        const bool ok = nt_edge(e, p, W0[j - 1], W1[j - 1], W0[j], W1[j], phase_of(e, rho[a + j - 1]),
+                                phase_of(e, rho[a + j]), x0, x1, hmask, hl, half, g0, g1, w, solves);
+        if (hl == 0) {
+          if (!ok) err = ST_NEWTON;
+          Fe0[j] = g0; Fe1[j] = g1; we[j] = w; xs0[j] = x0; xs1[j] = x1;
+        }
+      }
+      __syncwarp();
+    }
+    err = __reduce_max_sync(FULL, err);
+    if (!err && lane < K && !nt_T(rn0, rn1, hn, dt, Fe0[lane], Fe1[lane], we[lane], Fe0[lane + 1], Fe1[lane + 1],
+                                  we[lane + 1], T0, T1))
+      err = ST_WIDTH;
+    err = __reduce_max_sync(FULL, err);
+    ++evals;
+  };
+  NtRow J;
+  for (int q = 0; q < 4; ++q) { J.L[q] = 0.0; J.D[q] = 0.0; J.U[q] = 0.0; }
+  // forward-difference Jacobian of R = X - T at X (N2): one round per unknown (j, c)
+  auto jacobian = [&]() {
+    for (int j = 0; j < K && !err; ++j) {
+      for (int c = 0; c < 2 && !err; ++c) {
+        const double xq = __shfl_sync(FULL, c == 0 ? X0 : X1, j);
+        const double eps = 1e-7 * fmax(fabs(xq), 1.0);
+        const double pj0 = W0[j] + (c == 0 ? eps : 0.0), pj1 = W1[j] + (c == 1 ? eps : 0.0);
+        // half 0: edge j (cells j-1 | j'), half 1: edge j+1 (cells j' | j+1)
+        const int ed = j + half;
+        double g0 = 0.0, g1 = 0.0, w = 0.0;
+        bool ok = true;
+        if (ed >= 1 && ed < K) {
+          double x0 = xs0[ed], x1 = xs1[ed];
+          const double rl = half ? pj0 : W0[j - 1], ml = half ? pj1 : W1[j - 1];
+          const double rr = half ? W0[j + 1] : pj0, mr = half ? W1[j + 1] : pj1;
+          ok = nt_edge(e, p, rl, ml, rr, mr, phase_of(e, rho[a + ed - 1]), phase_of(e, rho[a + ed]), x0, x1, hmask, hl,
+                       half, g0, g1, w, solves);
+        }
+        err = __reduce_max_sync(FULL, ok ? 0 : ST_NEWTON);
+        if (err) break;
+        // perturbed edge j from lane 0 (half 0), edge j+1 from lane 16 (half 1); outer edges fixed
+        double pl0 = __shfl_sync(FULL, g0, 0), pl1 = __shfl_sync(FULL, g1, 0), plw = __shfl_sync(FULL, w, 0);
+        double pr0 = __shfl_sync(FULL, g0, 16), pr1 = __shfl_sync(FULL, g1, 16), prw = __shfl_sync(FULL, w, 16);
+        if (j == 0) { pl0 = Fe0[0]; pl1 = Fe1[0]; plw = we[0]; }
+        if (j == K - 1) { pr0 = Fe0[K]; pr1 = Fe1[K]; prw = we[K]; }
+        double t0, t1;
+        bool okT = true;
+        if (lane == j - 1) {  // row j-1: edges j-1 (base), j (perturbed) -> U block
+          okT = nt_T(rn0, rn1, hn, dt, Fe0[lane], Fe1[lane], we[lane], pl0, pl1, plw, t0, t1);
+          nt_set_col(J.U, c, -(t0 - T0) / eps, -(t1 - T1) / eps);
+        } else if (lane == j) {  // row j: both perturbed edges -> D block
+          okT = nt_T(rn0, rn1, hn, dt, pl0, pl1, plw, pr0, pr1, prw, t0, t1);
+          nt_set_col(J.D, c, (c == 0 ? 1.0 : 0.0) - (t0 - T0) / eps, (c == 1 ? 1.0 : 0.0) - (t1 - T1) / eps);
+        } else if (lane == j + 1 && lane < K) {  // row j+1: edges j+1 (perturbed), j+2 (base) -> L block
+          okT = nt_T(rn0, rn1, hn, dt, pr0, pr1, prw, Fe0[lane + 1], Fe1[lane + 1], we[lane + 1], t0, t1);
+          nt_set_col(J.L, c, -(t0 - T0) / eps, -(t1 - T1) / eps);
+        }
+        err = __reduce_max_sync(FULL, okT ? 0 : ST_WIDTH);
+      }
+    }
+    evals += 2 * K;
+  };
+  eval_T();
+  if (!err) jacobian();
+  double prev = INFINITY;
+  for (long long it = 1; !err; ++it) {
+    if (it > p.dts_max_iter) { err = ST_DTS_CAP; break; }
+    // block Thomas on J d = -(X - T): forward sweep (lane i receives lane i-1's D'^-1 U and D'^-1 r')
+    double Dp[4] = {J.D[0], J.D[1], J.D[2], J.D[3]};
+    double r0 = -(X0 - T0), r1 = -(X1 - T1);
+    double M[4] = {0.0, 0.0, 0.0, 0.0}, y0 = 0.0, y1 = 0.0;
+    bool sing = false;
+    for (int i = 0; i < K; ++i) {
+      if (lane == i) {  // finish row i: D'_i^-1 U_i and D'_i^-1 r'_i
+        const double det = Dp[0] * Dp[3] - Dp[1] * Dp[2];
+        if (!(fabs(det) > 0.0) || !isfinite(det)) sing = true;
+        const double id = 1.0 / det;
+        const double I0 = Dp[3] * id, I1 = -Dp[1] * id, I2 = -Dp[2] * id, I3 = Dp[0] * id;
+        M[0] = I0 * J.U[0] + I1 * J.U[2]; M[1] = I0 * J.U[1] + I1 * J.U[3];
+        M[2] = I2 * J.U[0] + I3 * J.U[2]; M[3] = I2 * J.U[1] + I3 * J.U[3];
+        y0 = I0 * r0 + I1 * r1; y1 = I2 * r0 + I3 * r1;
+      }
+      if (i + 1 < K) {
+        const double m0 = __shfl_sync(FULL, M[0], i), m1 = __shfl_sync(FULL, M[1], i);
+        const double m2 = __shfl_sync(FULL, M[2], i), m3 = __shfl_sync(FULL, M[3], i);
+        const double q0 = __shfl_sync(FULL, y0, i), q1 = __shfl_sync(FULL, y1, i);
+        if (lane == i + 1) {  // D'_{i+1} = D - L M, r' = r - L y
+          Dp[0] -= J.L[0] * m0 + J.L[1] * m2; Dp[1] -= J.L[0] * m1 + J.L[1] * m3;
+          Dp[2] -= J.L[2] * m0 + J.L[3] * m2; Dp[3] -= J.L[2] * m1 + J.L[3] * m3;
+          r0 -= J.L[0] * q0 + J.L[1] * q1; r1 -= J.L[2] * q0 + J.L[3] * q1;
+        }
+      }
+    }
+    if (__any_sync(FULL, sing)) { err = ST_NEWTON; break; }
+    double d0 = y0, d1 = y1;  // back substitution: d_i = y_i - M_i d_{i+1}
+    for (int i = K - 2; i >= 0; --i) {
+      const double n0 = __shfl_sync(FULL, d0, i + 1), n1 = __shfl_sync(FULL, d1, i + 1);
+      if (lane == i) { d0 = y0 - (M[0] * n0 + M[1] * n1); d1 = y1 - (M[2] * n0 + M[3] * n1); }
+    }
+    double step = 0.0;
+    bool bad = false;
+    if (lane < K) {
+      X0 += d0; X1 += d1;
+      step = fmax(fabs(d0) / fmax(fabs(X0), 1.0), fabs(d1) / fmax(fabs(X1), 1.0));
+      W0[lane] = X0; W1[lane] = X1;
+      bad = !(X0 > 0.0) || phase_of(e, X0) != ph0;
+    }
+    step = warp_max(step);
+    __syncwarp();
+    if (__any_sync(FULL, bad)) { err = ST_SPINODAL; break; }
+    if (step <= 1e-10 || (it >= 2 && step >= 0.5 * prev)) break;  // N3
+    prev = step;
+    eval_T();
+    if (err) break;
+    if (it % 8 == 0) jacobian();
+  }
+  if (!err) {  // Part 2: fluxes at U* = X and the conservative update
+    eval_T();
+    --evals;  // Part 2's edge fluxes are not an iteration (as the oracle counts)
+  }
+  if (!err && lane < K) {
+    const double hn1 = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
+    if (!(hn1 > 0.0)) err = ST_WIDTH;
+    else {
+      rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
+      mom[a + lane] = (hn / hn1) * rn1 - (dt / hn1) * (Fe1[lane + 1] - Fe1[lane]);
+      h[a + lane] = hn1;
+      if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
+    }
+  }
+  if (lane >= 1 && lane < K && !err) {  // keep the converged boundary states for the next step
+    Ifc* s = const_cast<Ifc*>(find_ifc(sh, a + lane));
+    if (s) { s->pV = xs0[lane]; s->pL = xs1[lane]; }
+  }
+  err = __reduce_max_sync(FULL, err);
+  __syncwarp();
+  it_out = evals;
+  return err;
+}
+
+// ------------------------------------------------------------------------------------------
 // Explicit local time stepping (mode LTS, the paper's comparison method, the
 // disabled passage P:1068-1091, readings R29-R31) on one implicit block [a, b] by one warp: the
 // tiny cells advance with 2^n0 sub-steps of dtau = dt / 2^n0 (dtau <= C_CFL h_T / S_max, R29),
@@ -803,8 +1028,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         if (b < Z.zlo || a >= Z.zhi) continue;  // tiles: a block wholly in the halo is not needed
         if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
-        const int err = p.mode == 2 ? lts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, smax_step, it, sv, remesh)
-                                    : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
+        const int err = p.mode == 2   ? lts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, smax_step, it, sv, remesh)
+                        : p.mode == 3 ? newton_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh)
+                                      : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
         if (err && lane == 0) set_status(sh, err);
         if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)
           if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); atomicMax(&sh.c_dtsmax, (unsigned long long)it); }

@@ -166,7 +166,7 @@ def test_363K_cavitation_on_gpu(P):
     assert eos["a_v2"] * g["rho"][0, k] == pytest.approx(g_["p_V_star"], abs=0.05)
 
 
-def _e3_workload():
+def _e3_workload(mode=0):
     """The paper's nucleation test: vapour at 70 kPa, u = +-2.7 m/s, 363.15 K."""
     eos = eos_363K()
     g_ = read_golden("nucleation_363K.txt")
@@ -174,6 +174,7 @@ def _e3_workload():
     r = g_["p_init"] / eos["a_v2"]
     prm = dict(W.PARAMS)
     prm["cfl"] = 0.5
+    prm["mode"] = mode
     rho = np.zeros((1, cap)); mom = np.zeros((1, cap))
     rho[0, :N] = r
     mom[0, :N // 2] = r * g_["u_init"]
@@ -581,3 +582,69 @@ def test_tiled_ensemble_run_to_members_stop_individually(P, oracle_mod):
     g["mstats"] = ctx.member_stats()
     o = oracle_run(oracle_mod, w2, t_end=w["t_end"])
     assert_parity(g, o, h_av(w2))
+
+
+# ------------------------------------------------------------------------------ Newton mode
+def _newton_counts_close(g, o, rel=0.05):
+    """Evaluation counts (N4) may differ where a chord step's stop test (N3) sits at the rounding
+    floor of the inner Riemann solves; the totals agree within a few per cent."""
+    a, b = g["stats"]["dts_iters"], o["stats"]["dts_iters"]
+    assert abs(a - b) <= rel * max(b, 1), (a, b)
+
+
+def test_newton_mode_e2_e3_against_oracle(P, oracle_mod):
+    """EIS_MODE_NEWTON (readings N1-N5) on the paper's cavitation (E2) and nucleation (E3) tests:
+    the printed bubble / droplet widths and step counts, state parity with the oracle's Newton
+    mode, a few evaluations per region (E3: thousands instead of ~3e6 DTS iterations)."""
+    g_, w = _e2_workload(3)
+    g, _ = gpu_run(P, w, t_end=w["t_end"])
+    o = oracle_run(oracle_mod, w, t_end=w["t_end"])
+    assert g["status"][0] == 0
+    assert g["stats"]["steps"] == o["stats"]["steps"] == int(g_["large_steps"])
+    assert_parity(g, o, h_av(w))
+    _newton_counts_close(g, o)
+    xs = [i["x"] for i in g["ifc"]]
+    assert xs[1] - xs[0] == pytest.approx(g_["bubble_width_t_end"], rel=1e-5)
+    gn, wn = _e3_workload(3)
+    g, _ = gpu_run(P, wn, t_end=wn["t_end"])
+    o = oracle_run(oracle_mod, wn, t_end=wn["t_end"])
+    assert g["status"][0] == 0 and g["stats"]["steps"] == o["stats"]["steps"]
+    assert_parity(g, o, h_av(wn))
+    _newton_counts_close(g, o)
+    assert g["stats"]["dts_iters"] < 20 * g["stats"]["regions"]
+    xs = [i["x"] for i in g["ifc"]]
+    assert xs[1] - xs[0] == pytest.approx(gn["droplet_width_t_end"], rel=2e-2)
+
+
+def test_newton_mode_ensembles_against_oracle(P, oracle_mod):
+    """Newton mode on C2, C3 members (member-resident kernel) and C4 members (tiled layout)."""
+    w = W.c2()
+    w["params"] = dict(w["params"]); w["params"]["mode"] = 3
+    g, _ = gpu_run(P, w, t_end=w["t_end"])
+    o = oracle_run(oracle_mod, w, t_end=w["t_end"])
+    assert o["stats"]["regions"] > 0
+    assert_parity(g, o, h_av(w))
+    _newton_counts_close(g, o)
+    for cfg, steps, layout in (("c3", 200, 0), ("c4", 200, 2)):
+        w = W.c3(members=np.arange(6)) if cfg == "c3" else W.c4(members=np.arange(4))
+        w["params"] = dict(w["params"]); w["params"]["mode"] = 3
+        g, _ = gpu_run(P, w, steps=steps, layout=layout)
+        o = oracle_run(oracle_mod, w, steps=steps)
+        assert_parity(g, o, h_av(w))
+        _newton_counts_close(g, o)
+
+
+def test_newton_mode_c5_tiled_against_oracle(P, oracle_mod):
+    """Newton mode through the tiled layout's window and whole-tile full steps (reduced C5)."""
+    w = W.c5(n_cells=30 * 940 + 311)
+    w["params"] = dict(w["params"]); w["params"]["mode"] = 3
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
+    ctx.set_state(torch.tensor(w["rho"], device="cuda"), torch.tensor(w["mom"], device="cuda"))
+    st = ctx.step(150, stats=True)
+    g = ctx.get_state()
+    g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["mstats"] = [st]; g["stats"] = st
+    o = oracle_run(oracle_mod, w, steps=150)
+    assert st["creations"] >= 1 and st["regions"] > 0
+    assert_parity(g, o, h_av(w))
+    _newton_counts_close(g, o)
