@@ -64,6 +64,7 @@ struct eis_ctx {
   cudaStream_t stream2 = nullptr;          // tiled: the window kernel beside tiled_fast
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   size_t smem_win;
+  size_t smem_fast = 0;  // tiled_fast staging (EIS_FAST_TMA builds)
   TileStats* t_stats;
   long long* t_off;
   int staging_fresh;
@@ -302,6 +303,11 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (cudaFuncSetAttribute(tiled_slow<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
+#if EIS_FAST_TMA
+  c->smem_fast = 2 * sizeof(double) * (size_t)((capt + 1) & ~1);
+  if (cudaFuncSetAttribute(tiled_fast<128, EIS_FAST_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess) { delete c; return EIS_E_CUDA; }
+#endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
   if (cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
@@ -745,7 +751,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
   if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
   if (c->timing) m[0] = timing_event(c);
-  tiled_fast<128, EIS_FAST_MINB><<<c->tl.ntiles, 128, 0, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_fast<128, EIS_FAST_MINB><<<c->tl.ntiles, 128, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);

@@ -204,6 +204,9 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 #ifndef EIS_FAST_STATIC_IN
 #define EIS_FAST_STATIC_IN 1
 #endif
+#ifndef EIS_FAST_TMA
+#define EIS_FAST_TMA 0
+#endif
 #ifndef EIS_FAST_PIPE
 #define EIS_FAST_PIPE 0
 #endif
@@ -296,12 +299,40 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   const double h_av = p.h_av, dt_hav = dt / h_av;
   const double* const rin = tl.rho[BIN];
   const long long mo_t = tl.mom[BIN] - rin;
+#if EIS_FAST_TMA
+  // the tile's own cells staged in shared memory by the bulk-copy engine (one mbarrier, one
+  // phase): interior windows then read shared memory; the halo windows read global memory
+  extern __shared__ __align__(16) double tsm[];
+  __shared__ __align__(8) unsigned long long tbar;
+  const int capr = (tl.capt + 1) & ~1;
+  const double* const s_rho = tsm - own_lo;  // indexed by the virtual cell
+  const double* const s_mom = tsm + capr - own_lo;
+  const unsigned tbar_a = (unsigned)__cvta_generic_to_shared(&tbar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tbar_a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const unsigned bytes = (unsigned)(((g.cnt + 1) & ~1) * 8);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tbar_a), "r"(2 * bytes) : "memory");
+    if (bytes) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"((unsigned)__cvta_generic_to_shared(tsm)), "l"(rin + g.base), "r"(bytes), "r"(tbar_a) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"((unsigned)__cvta_generic_to_shared(tsm + capr)), "l"(rin + g.base + mo_t), "r"(bytes),
+                   "r"(tbar_a) : "memory");
+    }
+    fl_or = 0; s_lo = 1 << 30; s_hi = -1;
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+               " @!P1 bra WAIT_%=;\n}" ::"r"(tbar_a) : "memory");
+#else
   if (tid == 0) {  // the whole tile's requests in flight at once: bulk L2 prefetch of rho and mom
     const unsigned bytes = (unsigned)(((g.cnt + 1) & ~1) * 8);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rin + g.base), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rin + g.base + mo_t), "r"(bytes) : "memory");
     fl_or = 0; s_lo = 1 << 30; s_hi = -1;
   }
+#endif
   // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
   const double* const segL = g.xl ? tl.xbuf + XB_RECV_LEFT + HALO - g.nL : rin + g.bl + g.cl - g.nL;
   const long long moL = g.xl ? HALO : mo_t;
@@ -327,8 +358,13 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       rv[b] = make_double2(1.0, 1.0); mv[b] = make_double2(0.0, 0.0);
       if (wi < nwin) {
         if (FW * wi - 2 >= own_lo && FW * wi + 62 <= own_hi) {  // interior window: aligned pairs
+#if EIS_FAST_TMA
+          rv[b] = *reinterpret_cast<const double2*>(s_rho + c0);
+          mv[b] = *reinterpret_cast<const double2*>(s_mom + c0);
+#else
           rv[b] = *reinterpret_cast<const double2*>(segO + c0);
           mv[b] = *reinterpret_cast<const double2*>(segO + c0 + mo_t);
+#endif
         } else {
           const int ca = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0), cb = c0 + 1 < 0 ? 0 : (c0 + 1 >= n ? n - 1 : c0 + 1);
           const double* pa = ca < own_lo ? segL : (ca < own_hi ? segO : segR);
