@@ -230,7 +230,8 @@ def main():
     w = workload(name, np.arange(lo, hi) if name in ("C3", "C4") else None)
     stream = torch.cuda.current_stream()
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], device=local,
-                    stream=stream, threads=int(os.environ.get("EIS_THREADS", "0")))
+                    stream=stream, threads=int(os.environ.get("EIS_THREADS", "0")),
+                    tile_cells=int(os.environ.get("EIS_TILE", "0")))
     rho_d = torch.from_numpy(w["rho"]).cuda()
     mom_d = torch.from_numpy(w["mom"]).cuda()
     t_end = w.get("t_end", float("inf"))
@@ -382,7 +383,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     w = with_mode(W.c5(n_cells=n_glob))
     stream = torch.cuda.current_stream()
     rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
-                  tile=int(os.environ.get("EIS_TILE", "940")),
+                  tile=int(os.environ.get("EIS_TILE", "1400")),
                   stream=stream)
     rho_l = np.zeros(rg.cap)
     mom_l = np.zeros(rg.cap)

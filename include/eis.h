@@ -112,7 +112,7 @@ typedef struct {
                              <= 16384) | _TILED (members streamed through HBM every step in
                              halo-overlapped tiles; halos never cross members; each member its
                              own dt, t and status; rank mode requires n_members == 1)          */
-  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 940); tiles are fixed-size from
+  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 1400); tiles are fixed-size from
                              the left, the last one takes the remainder                      */
   int32_t nbr_left;       /* tiled rank mode: 1 if this grid is the right part of a grid cut
                              over ranks (its left halo arrives through the exchange buffer)  */

@@ -283,7 +283,7 @@ static cudaError_t make_side_stream(cudaStream_t* s) {
 static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   const eis_grid* grid = &c->grid;
   const long long cap = grid->cell_capacity;
-  c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 940;
+  c->tile_cells = grid->tile_cells > 0 ? grid->tile_cells : 1400;
   if (c->tile_cells < 4 * HALO || c->tile_cells > 8192) { delete c; return EIS_E_ARG; }
   const int capt = c->tile_cells + 32 + (c->tile_cells & 1);  // even: 16-byte aligned tile rows
   long long tpm = (grid->n_cells + c->tile_cells - 1) / c->tile_cells;  // tiles per member

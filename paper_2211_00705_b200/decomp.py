@@ -55,7 +55,7 @@ class RankGrid:
     """This rank's slice of one tiled grid.  For world == 1 it is a plain tiled context."""
 
     def __init__(self, eos: dict, params: dict, n_global: int, x_left: float, x_right: float, rank: int,
-                 world: int, tile: int = 940, device: int = 0, stream=None, group=None, slack: int = 16):
+                 world: int, tile: int = 1400, device: int = 0, stream=None, group=None, slack: int = 16):
         self.rank, self.world, self.group = rank, world, group
         self.c0, self.c1 = rank_slice(n_global, tile, rank, world)
         self.n = self.c1 - self.c0
@@ -92,7 +92,7 @@ class VirtualRanks:
     """P rank slices of one grid on ONE device, exchanged by device copies (no NCCL, no kernel
     waits on another): exercises the rank-mode library path against the 1-rank run."""
 
-    def __init__(self, eos, params, n_global, x_left, x_right, world, tile=940, device=0, stream=None):
+    def __init__(self, eos, params, n_global, x_left, x_right, world, tile=1400, device=0, stream=None):
         self.parts = []
         for r in range(world):
             g = RankGrid.__new__(RankGrid)
