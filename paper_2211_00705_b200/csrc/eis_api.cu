@@ -367,6 +367,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
         cudaMemset(c->t_wdbg, 0, (size_t)ntiles * WDBG_FIELDS * 8) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
     tl.wdbg = c->t_wdbg;
   }
+  tl.poll = c->win_grid_poll > 0 ? 1 : 0;
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
   if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;

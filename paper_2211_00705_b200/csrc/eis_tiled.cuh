@@ -48,6 +48,7 @@ struct Tiles {
                                    //  6 phase cycles (EIS_PHASE_CLOCK builds, else 0)}
   int ntiles, capt, nbr_left, nbr_right;
   int wmax;                        // largest window (owned cells) of a window full step (<= WMAX)
+  int poll;                        // a window kernel polls beside tiled_fast (EIS_WIN_POLL_PER_SM)
   int M, tpm;                      // members (independent grids) and tiles per member: tile k
                                    // belongs to member k / tpm; halos never cross members
 };
@@ -478,7 +479,8 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       tl.cnt[BOUT][k] = g.cnt;
       tl.hu[BOUT][k] = unif ? 1 : 0;
       tl.ws[(size_t)k * WS_STRIDE + 2 * MAXIF] = 0.0;  // no boundary: no warm start
-      tl.tstats[k].cell_updates += g.cnt;
+      // fire-and-forget reduction: no load in the CTA's last instructions
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tl.tstats[k].cell_updates), (unsigned long long)g.cnt);
       if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
       if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
     } else {
@@ -518,8 +520,10 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     else tiled_fast_body<false, -1>(e, p, tl, g, dt);
 #endif
   }
-  __syncthreads();
-  if (threadIdx.x == 0) { __threadfence(); atomicAdd(&tl.ctl[9], 1); }  // every CTA, always
+  if (tl.poll) {  // count finished CTAs for the polling window kernel (every CTA, always)
+    __syncthreads();
+    if (threadIdx.x == 0) { __threadfence(); atomicAdd(&tl.ctl[9], 1); }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
