@@ -1029,7 +1029,9 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
         const int err = p.mode == 2   ? lts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, smax_step, it, sv, remesh)
+#ifndef EIS_NO_NEWTON
                         : p.mode == 3 ? newton_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh)
+#endif
                                       : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
         if (err && lane == 0) set_status(sh, err);
         if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)

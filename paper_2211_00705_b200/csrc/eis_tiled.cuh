@@ -534,7 +534,7 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
 __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capg,
                                           int k, double t_end, double& s_out, double& h_out) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const TGeo g = tile_geo(tl, k);
+  const TGeo g = tile_geo_spec(tl, k);
   const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int n = g.n, nL = g.nL, cnt = g.cnt;
   if (tid == 0) {
@@ -683,7 +683,7 @@ __device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, doubl
 __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
                                             int k, int wa, int wb, double t_end) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const TGeo g = tile_geo(tl, k);
+  const TGeo g = tile_geo_spec(tl, k);
   const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int nL = g.nL, cnt = g.cnt;
   const int s0 = max(0, wa - HALO), s1 = min(g.n, wb + HALO), n = s1 - s0;
