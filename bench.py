@@ -200,8 +200,13 @@ def reference_arm(args):
         "impl": "reference", "metric": "fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": ({"workload": "C5 (CPU oracle sample)", "cells": S} if name == "C5" else
-                   {"workload": f"{name} (CPU oracle sample)", "members": S, "cells_per_member": N}),
+        # the same workload as the eis arm's line; each step times a bounded sample of it
+        "config": ({"workload": f"C5: one grid of {1 << 27} cells, 4096-cell random segments", "cells": 1 << 27,
+                    "parallelism": "1 host core (CPU oracle)", "sample_cells": S} if name == "C5" else
+                   {"workload": (f"{name}: {total_members(name)} members x {N} cells" +
+                                 (", cavitation ensemble" if name == "C3" else "")),
+                    "members": total_members(name), "cells_per_member": N,
+                    "parallelism": "1 host core (CPU oracle)", "sample_members": S}),
         "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
