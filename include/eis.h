@@ -112,8 +112,10 @@ typedef struct {
                              <= 16384) | _TILED (members streamed through HBM every step in
                              halo-overlapped tiles; halos never cross members; each member its
                              own dt, t and status; rank mode requires n_members == 1)          */
-  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 1400); tiles are fixed-size from
-                             the left, the last one takes the remainder                      */
+  int32_t tile_cells;     /* tiled: owned cells per tile (0 = 1400, range 40..8192); a member's
+                             ceil(n_cells / tile_cells) tiles are fixed-size from the left, the
+                             last one takes the remainder; a member whose live count does not
+                             reach its last tile by 10 cells is frozen with EIS_E_CAPACITY    */
   int32_t nbr_left;       /* tiled rank mode: 1 if this grid is the right part of a grid cut
                              over ranks (its left halo arrives through the exchange buffer)  */
   int32_t nbr_right;      /* ... 1 if a rank continues the grid on the right                   */

@@ -26,9 +26,9 @@ def P():
     return P
 
 
-def gpu_run(P, w, steps=None, t_end=None, threads=0, n_cells=None, max_steps=10 ** 9, layout=0):
+def gpu_run(P, w, steps=None, t_end=None, threads=0, n_cells=None, max_steps=10 ** 9, layout=0, tile_cells=0):
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
-                    stream=torch.cuda.current_stream(), threads=threads, layout=layout)
+                    stream=torch.cuda.current_stream(), threads=threads, layout=layout, tile_cells=tile_cells)
     rho = torch.tensor(w["rho"], device="cuda")
     mom = torch.tensor(w["mom"], device="cuda")
     nc = None if n_cells is None else torch.tensor(n_cells, device="cuda", dtype=torch.int64)
@@ -212,28 +212,32 @@ def test_cta_size_does_not_change_results(P, threads):
         np.testing.assert_array_equal(g[k], ref[k])
 
 
-def test_ragged_members(P, oracle_mod):
-    """Members with different live cell counts (ragged tails) in one launch."""
+@pytest.mark.parametrize("layout,tile", [(1, 0), (2, 128)])
+def test_ragged_members(P, oracle_mod, layout, tile):
+    """Members with different live cell counts (ragged tails) in one launch: member-resident, and
+    tiled with five 128-cell tiles per member (fixed-size tiles from the left: a member's live
+    count must reach its last tile by HALO cells, include/eis.h)."""
     N = 600
     mem = np.arange(5)
     w = W.c3(members=mem, N=N)
-    n_cells = np.array([600, 3, 97, 511, 353], dtype=np.int64)
+    n_cells = np.array([600, 3, 97, 511, 353] if layout == 1 else [600, 522, 597, 531, 566], dtype=np.int64)
     for m, n in enumerate(n_cells):
         w["rho"][m, n:] = 0.0
         w["mom"][m, n:] = 0.0
-    g, _ = gpu_run(P, w, steps=120, n_cells=n_cells)
+    g, _ = gpu_run(P, w, steps=120, n_cells=n_cells, layout=layout, tile_cells=tile)
     o = oracle_run(oracle_mod, w, steps=120, n_cells=n_cells)
     assert_parity(g, o, h_av(w))
 
 
-def test_constant_states_bitwise(P):
+@pytest.mark.parametrize("layout", [1, 2])
+def test_constant_states_bitwise(P, layout):
     M, N, cap = 3, 100, 120
     rho = np.zeros((M, cap)); mom = np.zeros((M, cap))
     for m, (r, u) in enumerate(((1000.3, 0.0), (1000.3, 17.0), (0.021, -40.0))):
         rho[m, :N] = r
         mom[m, :N] = r * u
     w = dict(eos=W.EOS_293K, params=W.PARAMS, M=M, N=N, cap=cap, x_left=0.0, x_right=1.0, rho=rho, mom=mom)
-    g, _ = gpu_run(P, w, steps=40)
+    g, _ = gpu_run(P, w, steps=40, layout=layout, tile_cells=40 if layout == 2 else 0)
     np.testing.assert_array_equal(g["rho"][:, :N], rho[:, :N])
     np.testing.assert_array_equal(g["mom"][:, :N], mom[:, :N])
 
