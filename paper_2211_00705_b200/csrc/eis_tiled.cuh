@@ -206,7 +206,7 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 #define EIS_FAST_STATIC_IN 1
 #endif
 #ifndef EIS_FAST_TMA
-#define EIS_FAST_TMA 0
+#define EIS_FAST_TMA 1  // the tile's own cells staged in shared memory by cp.async.bulk (0: L2 prefetch)
 #endif
 #ifndef EIS_FAST_PIPE
 #define EIS_FAST_PIPE 0
