@@ -205,7 +205,7 @@ eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
 
 /* Tiled-layout diagnostics (EIS_E_ARG for a member-resident context): the number of tiles, and
  * the tile-steps since eis_set_state that took the full step of the whole tile, or of a window
- * of at most 160 owned cells around the tile's special cells (phase boundaries, creation
+ * of at most 150 owned cells around the tile's special cells (phase boundaries, creation
  * candidates), rather than only the single-phase fast path.  Synchronises the stream. */
 eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps);
 

@@ -288,7 +288,10 @@ __device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB]
   }
 }
 
-constexpr int WMAX = 160;  // owned cells of a full-step window (larger: the whole tile)
+#ifndef EIS_WMAX
+#define EIS_WMAX 150  // (window CTA shared memory: 16 one-warp CTAs per SM fit, the register limit)
+#endif
+constexpr int WMAX = EIS_WMAX;  // owned cells of a full-step window (larger: the whole tile)
 
 template <bool HU, int IN>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
