@@ -126,6 +126,13 @@ typedef struct {
   int64_t member, edge;   /* edge e lies between cells e-1 and e                           */
   double x;               /* x_left + widths summed left to right (fixed order, no FMA)    */
   int32_t left_phase, right_phase;
+  /* the phase-boundary Riemann problem (App. A, kinetic relation R2) of the two
+   * adjacent cells' current states, solved from the HLLC estimate:           */
+  double w;               /* speed of the phase boundary                                   */
+  double z;               /* mass flux through it, z = -rho (u - w) (same on both sides)    */
+  double p_vap, p_liq;    /* star pressures on the vapour and liquid sides                 */
+  int32_t solve_status;   /* 0, or EIS_E_NEWTON if that solve did not converge             */
+  int32_t reserved;
 } eis_interface;
 
 typedef struct {
@@ -171,8 +178,9 @@ eis_status eis_get_state(eis_ctx* ctx, double* rho, double* mom, double* width, 
                          int64_t* n_cells, double* t, int32_t where);
 
 /* Phase boundaries of the current state, member-major and left to right, into a host array of
- * `capacity` records; *count gets the total (EIS_E_CAPACITY if it exceeds capacity; out == NULL
- * is a pure count query). */
+ * `capacity` records, each with the Riemann solution of its two adjacent cells (one half warp
+ * per boundary); *count gets the total (EIS_E_CAPACITY if it exceeds capacity; out == NULL is a
+ * pure count query). */
 eis_status eis_interfaces(eis_ctx* ctx, eis_interface* out, int64_t capacity, int64_t* count);
 
 /* Per-member status codes (host array of n_members). */

@@ -1068,7 +1068,22 @@ int eiso_interfaces(const eiso_ctx* c, eiso_interface* out, int64_t capacity, in
       if (i + 1 < n) {
         int a = phase_of(&c->e, rho[i]), b = phase_of(&c->e, rho[i + 1]);
         if (a != b) {
-          if (k < capacity && out) { out[k].member = m; out[k].edge = i + 1; out[k].x = x; out[k].left_phase = a; out[k].right_phase = b; }
+          if (k < capacity && out) {
+            out[k].member = m; out[k].edge = i + 1; out[k].x = x; out[k].left_phase = a; out[k].right_phase = b;
+            /* the phase-boundary Riemann problem of the two adjacent cells (App. A) */
+            const double* mom = c->mom + m * c->cap;
+            side_t sm = {rho[i], mom[i] / rho[i], a}, sp = {rho[i + 1], mom[i + 1] / rho[i + 1], b};
+            eiso_iface s;
+            out[k].solve_status = 0; out[k].reserved = 0;
+            out[k].w = out[k].z = out[k].p_vap = out[k].p_liq = 0.0;
+            if (a == SPIN || b == SPIN || interface_solve(&c->e, &c->prm, sm, sp, &s) != 0) {
+              out[k].solve_status = EISO_E_NEWTON;
+            } else {
+              out[k].w = s.w; out[k].z = s.z;
+              out[k].p_vap = a == VAP ? s.p_minus : s.p_plus;
+              out[k].p_liq = a == VAP ? s.p_plus : s.p_minus;
+            }
+          }
           ++k;
         }
       }

@@ -82,7 +82,11 @@ typedef struct {
   double t_min, t_max, dt_min, dt_max;
 } eiso_stats;
 
-typedef struct { int64_t member, edge; double x; int32_t left_phase, right_phase; } eiso_interface;
+typedef struct {
+  int64_t member, edge; double x; int32_t left_phase, right_phase;
+  double w, z, p_vap, p_liq;  /* Riemann solution of the two adjacent cells (App. A)        */
+  int32_t solve_status, reserved;
+} eiso_interface;
 
 typedef struct eiso_ctx eiso_ctx;
 

@@ -54,7 +54,9 @@ class Grid(C.Structure):
 
 class Interface(C.Structure):
     _fields_ = [("member", C.c_int64), ("edge", C.c_int64), ("x", C.c_double),
-                ("left_phase", C.c_int32), ("right_phase", C.c_int32)]
+                ("left_phase", C.c_int32), ("right_phase", C.c_int32),
+                ("w", C.c_double), ("z", C.c_double), ("p_vap", C.c_double), ("p_liq", C.c_double),
+                ("solve_status", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -270,7 +272,8 @@ class Context:
         arr = (Interface * max(cnt.value, 1))()
         self._check(lib().eis_interfaces(self._ctx, arr, cnt.value, C.byref(cnt)), "eis_interfaces")
         return [{"member": a.member, "edge": a.edge, "x": a.x, "left_phase": a.left_phase,
-                 "right_phase": a.right_phase} for a in arr[:cnt.value]]
+                 "right_phase": a.right_phase, "w": a.w, "z": a.z, "p_vap": a.p_vap, "p_liq": a.p_liq,
+                 "solve_status": a.solve_status} for a in arr[:cnt.value]]
 
     def member_status(self) -> np.ndarray:
         out = np.zeros(self.M, dtype=np.int32)

@@ -217,6 +217,32 @@ __global__ void k_iface(const Eos e, Members g, long long M, double x_left, cons
   if (cnt) cnt[m] = c;
 }
 
+// the phase-boundary Riemann problem of each reported boundary's two adjacent cells (App. A),
+// one half warp per boundary, cold-started from the HLLC estimate
+__global__ void k_iface_solve(const Eos e, const Prm p, Members g, eis_interface* out, long long total) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
+  if (j >= total) return;  // a whole half warp: the solver's syncs stay within it
+  const eis_interface b = out[j];
+  const long long i = b.member * g.cap + b.edge;
+  const double rl = g.rho[i - 1], ml = g.mom[i - 1], rr = g.rho[i], mr = g.mom[i];
+  const bool vap_left = b.left_phase == VAP;
+  const bool ok = (b.left_phase == VAP || b.left_phase == LIQ) && (b.right_phase == VAP || b.right_phase == LIQ);
+  IfaceSol s;
+  s.iters = -1;
+  if (ok) s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, vap_left, -1.0, -1.0, hmask, hl, half * 16);
+  if (hl == 0) {
+    const bool conv = ok && s.iters >= 0;
+    out[j].w = conv ? s.w : 0.0;
+    out[j].z = conv ? -s.F0 : 0.0;  // F_PB = (-z, ...)
+    out[j].p_vap = conv ? s.pV : 0.0;
+    out[j].p_liq = conv ? s.pL : 0.0;
+    out[j].solve_status = conv ? 0 : EIS_E_NEWTON;
+    out[j].reserved = 0;
+  }
+}
+
 // member-major staging -> tiles: tile k = member m's j-th tile (m = k / tpm) gets the member's
 // cells [j tile, (j+1) tile), the last tile the remainder (fixed-size tiles: any tile-aligned
 // split of a grid over ranks reproduces the single-grid tiling exactly).  A member whose cell
@@ -897,6 +923,7 @@ extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t cap
     CU(cudaMalloc(&d_off, M * 8));
     CU(cudaMemcpyAsync(d_off, off.data(), M * 8, cudaMemcpyHostToDevice, c->stream));
     k_iface<<<nb, 128, 0, c->stream>>>(c->e, c->g, M, c->grid.x_left, d_off, nullptr, c->d_if, total);
+    k_iface_solve<<<(unsigned)((total + 7) / 8), 128, 0, c->stream>>>(c->e, c->p, c->g, c->d_if, total);
     CU(cudaGetLastError());
     const long long ncopy = total < capacity ? total : capacity;
     CU(cudaMemcpyAsync(out, c->d_if, ncopy * sizeof(eis_interface), cudaMemcpyDeviceToHost, c->stream));

@@ -652,3 +652,31 @@ def test_newton_mode_c5_tiled_against_oracle(P, oracle_mod):
     assert st["creations"] >= 1 and st["regions"] > 0
     assert_parity(g, o, h_av(w))
     _newton_counts_close(g, o)
+
+
+def test_interface_report_against_oracle(P, oracle_mod):
+    """eis_interfaces' Riemann report (w, z, star pressures of each boundary's adjacent cells;
+    one half warp per boundary) against the oracle's: the cavitation test E2 at t_end (the
+    paper's printed star state, P:1277 / P:1264) and C3 members after 300 steps."""
+    g_, w = _e2_workload(0)
+    g, _ = gpu_run(P, w, t_end=w["t_end"])
+    o = oracle_run(oracle_mod, w, t_end=w["t_end"])
+    assert len(g["ifc"]) == len(o["ifc"]) == 2
+    for a, b in zip(g["ifc"], o["ifc"]):
+        assert a["solve_status"] == b["solve_status"] == 0
+        for k in ("w", "z", "p_vap", "p_liq"):
+            assert a[k] == pytest.approx(b[k], rel=1e-9, abs=1e-12), k
+        assert a["p_vap"] == pytest.approx(g_["p_V_star"], abs=1e-6)
+        assert a["p_liq"] == pytest.approx(g_["p_L_star"], abs=1e-6)
+        assert abs(a["w"]) == pytest.approx(g_["w"], abs=1e-6)
+    w = W.c3(members=np.arange(6))
+    g, _ = gpu_run(P, w, steps=300)
+    o = oracle_run(oracle_mod, w, steps=300)
+    assert len(g["ifc"]) == len(o["ifc"]) > 0
+    for a, b in zip(g["ifc"], o["ifc"]):
+        assert (a["member"], a["edge"]) == (b["member"], b["edge"])
+        assert a["solve_status"] == b["solve_status"] == 0
+        for k in ("p_vap", "p_liq"):
+            assert a[k] == pytest.approx(b[k], rel=1e-9), k
+        for k in ("w", "z"):
+            assert a[k] == pytest.approx(b[k], rel=1e-7, abs=1e-9), k

@@ -123,3 +123,30 @@ def test_nucleation_run_droplet_width(oracle_mod, eos):
     xs = [i["x"] for i in s.interfaces()]
     assert xs[1] - xs[0] == pytest.approx(g["droplet_width_t_end"], rel=2e-2)
     assert abs(st["steps"] - g["large_steps"]) <= 4
+
+
+def test_interface_report_cavitation_star_state(oracle_mod, eos):
+    """eis_interfaces' Riemann report (App. A) at the end of the cavitation run: the bubble's
+    adjacent cells hold the exact star states, so the reported star pressures and boundary
+    speed are the paper's printed ones (P:1277 p_V*, p_L*; P:1264 w) to the printed digits."""
+    g, s, st = _run_363K(oracle_mod, eos, "cav")
+    ifc = s.interfaces()
+    assert len(ifc) == 2 and all(i["solve_status"] == 0 for i in ifc)
+    for i, sign in zip(ifc, (-1.0, 1.0)):
+        assert i["p_vap"] == pytest.approx(g["p_V_star"], abs=1e-6)
+        assert i["p_liq"] == pytest.approx(g["p_L_star"], abs=1e-6)
+        assert i["w"] == pytest.approx(sign * g["w"], abs=1e-6)
+        assert i["z"] * sign > 0  # evaporation: mass flows from the liquid into the bubble
+
+
+def test_interface_report_nucleation(oracle_mod, eos):
+    """The same report on the nucleation run: the droplet's boundary speed is the printed w
+    (2.03e-4 m/s) and the star pressures agree with P:1390 within the scheme's
+    smearing of the outer waves (1e-6 relative)."""
+    g, s, st = _run_363K(oracle_mod, eos, "nuc")
+    ifc = s.interfaces()
+    assert len(ifc) == 2 and all(i["solve_status"] == 0 for i in ifc)
+    for i, sign in zip(ifc, (-1.0, 1.0)):
+        assert i["w"] == pytest.approx(sign * g["w"], rel=2e-2)
+        assert i["p_vap"] == pytest.approx(g["p_V_star"], rel=1e-6)
+        assert i["p_liq"] == pytest.approx(g["p_L_star"], rel=1e-6)
