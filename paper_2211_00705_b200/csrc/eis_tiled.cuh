@@ -534,6 +534,23 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
 // the remesh, CFL partials, warm-start table, stats.  Returns (via s_out/h_out on thread 0)
 // the tile's partials; a status is raised on tl.ctl[1].
 // ------------------------------------------------------------------------------------------
+// per-tile counters as fire-and-forget reductions (no load in the CTA's critical path)
+__device__ __forceinline__ void tstats_add(const Tiles& tl, int k, long long cells, const CtaShared& sh, bool window) {
+  TileStats& ts = tl.tstats[k];
+  auto add = [](long long* a, long long v) {
+    if (v) atomicAdd(reinterpret_cast<unsigned long long*>(a), (unsigned long long)v);
+  };
+  add(&ts.cell_updates, cells);
+  add(&ts.dts_iters, (long long)sh.c_dts);
+  add(&ts.iface_solves, (long long)sh.c_solves);
+  add(&ts.regions, (long long)sh.c_regions);
+  if (sh.c_dtsmax) atomicMax(reinterpret_cast<unsigned long long*>(&ts.dts_max), (unsigned long long)sh.c_dtsmax);
+  add(window ? &ts.win_steps : &ts.full_steps, 1);
+  add(&ts.creations, sh.st.creations);  // owned events only (step_body)
+  add(&ts.splits, sh.st.splits);
+  add(&ts.merges, sh.st.merges);
+}
+
 __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capg,
                                           int k, double t_end, double& s_out, double& h_out) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
@@ -618,16 +635,7 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
       double* ws = tl.ws + (size_t)k * WS_STRIDE;
       for (int q = 0; q < MAXIF; ++q) { ws[q] = sh.ws0[q]; ws[MAXIF + q] = sh.ws1[q]; }
       ws[2 * MAXIF] = (double)sh.wsn;
-      TileStats& ts = tl.tstats[k];
-      ts.cell_updates += cnt;
-      ts.dts_iters += (long long)sh.c_dts;
-      ts.iface_solves += (long long)sh.c_solves;
-      ts.regions += (long long)sh.c_regions;
-      if ((long long)sh.c_dtsmax > ts.dts_max) ts.dts_max = (long long)sh.c_dtsmax;
-      ts.full_steps += 1;
-      ts.creations += sh.st.creations;  // owned events only (step_body)
-      ts.splits += sh.st.splits;
-      ts.merges += sh.st.merges;
+      tstats_add(tl, k, cnt, sh, false);
     }
   }
   __syncthreads();
@@ -791,16 +799,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
       double* ws = tl.ws + (size_t)k * WS_STRIDE;
       for (int q = 0; q < MAXIF; ++q) { ws[q] = sh.ws0[q]; ws[MAXIF + q] = sh.ws1[q]; }
       ws[2 * MAXIF] = (double)sh.wsn;
-      TileStats& ts = tl.tstats[k];
-      ts.cell_updates += cnt;
-      ts.dts_iters += (long long)sh.c_dts;
-      ts.iface_solves += (long long)sh.c_solves;
-      ts.regions += (long long)sh.c_regions;
-      if ((long long)sh.c_dtsmax > ts.dts_max) ts.dts_max = (long long)sh.c_dtsmax;
-      ts.win_steps += 1;
-      ts.creations += sh.st.creations;
-      ts.splits += sh.st.splits;
-      ts.merges += sh.st.merges;
+      tstats_add(tl, k, cnt, sh, true);
     }
   }
   __syncthreads();
