@@ -138,6 +138,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def job_rates(dist, torch, world, st, ms):
+    """DTS iterations/s and interface solves/s of the whole job (the paper's "local
+    iterations", P:1324), and simulated time per wall-second (the timed steps start at t = 0)."""
+    n = [int(st["dts_iters"]), int(st["iface_solves"])]
+    if world > 1:
+        c = torch.tensor(n, device="cuda", dtype=torch.int64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        n = [int(x) for x in c.tolist()]
+    sec = ms * 1e-3
+    return {"dts_iters_per_s": n[0] / sec, "iface_solves_per_s": n[1] / sec,
+            "sim_time_per_wall_s": {"min_member": st["t_min"] / sec, "max_member": st["t_max"] / sec}}
+
+
 def fp64_peak():
     p = os.path.join(ROOT, "profiles", "fp64_peak.json")
     if os.path.exists(p):
@@ -286,6 +299,7 @@ def main():
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
         cu, nbad = int(c[0].item()), int(c[1].item())
     value = cu / (ms * 1e-3)
+    rates = job_rates(dist, torch, world, st, ms)
 
     # end to end through the public API with pinned host buffers: set_state(host) + K steps
     # + get_state(host), one user call sequence per K steps
@@ -373,7 +387,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
-            "members_not_ok": nbad,
+            "members_not_ok": nbad, "rates": rates,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -432,6 +446,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
         cu, nbad = int(c[0].item()), int(c[1].item())
     value = cu / (ms * 1e-3)
+    rates = job_rates(dist, torch, world, st, ms)
 
     e2e = None
     if not args.no_e2e:
@@ -493,7 +508,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * (3 if world == 1 else 4), "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
-            "members_not_ok": nbad,
+            "members_not_ok": nbad, "rates": rates,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
