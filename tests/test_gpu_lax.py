@@ -89,3 +89,23 @@ def test_lax_bad_arguments(P):
     for bad in (dict(n=101), dict(n=4), dict(alpha=0.0), dict(theta_nb=-1.0), dict(n=5000)):
         with pytest.raises(P.EisError):
             P.lax_run([bad])
+
+
+def test_lax_maximum_mesh_and_many_cases(P, oracle_mod):
+    """The largest mesh a case may use (N = 4094, 4095 cells in shared memory) next to 200 small
+    seeded cases in one launch; the big case and a sample of the small ones against the oracle."""
+    O = oracle_mod
+    rng = np.random.default_rng(7)
+    cases = [dict(n=4094, alpha=1e-3, theta_nb=0.9, t_end=0.05)]
+    for i in range(200):
+        cases.append(dict(n=int(rng.integers(3, 60)) * 2, alpha=float(10 ** rng.uniform(-5, -1)),
+                          theta_nb=float(rng.uniform(0.1, 1.0)), t_end=float(rng.uniform(0.05, 0.5))))
+    rho, mom, E, stats = P.lax_run(cases)
+    assert all(s["status"] == 0 for s in stats)
+    for i in [0] + list(range(1, 201, 20)):
+        kw = cases[i]
+        r, m, e, xf, so = _oracle(O, kw)
+        assert stats[i]["steps"] == so["steps"] and stats[i]["dts_iters"] == so["dts_iters"], (i, kw)
+        nc = kw["n"] + 1
+        for got, ref in ((rho[i, :nc], r), (mom[i, :nc], m), (E[i, :nc], e)):
+            assert _rel_l1(got.cpu().numpy(), ref) <= REL_L1, (i, kw)

@@ -552,11 +552,12 @@ def test_lts_mode_c5_tiled_against_oracle(P, oracle_mod):
 
 
 # ------------------------------------------------------------------------------ tiled ensembles
-@pytest.mark.parametrize("cfg,steps", [("c3", 300), ("c4", 150)])
-def test_tiled_ensemble_against_oracle(P, oracle_mod, cfg, steps):
+@pytest.mark.parametrize("cfg,steps,mode", [("c3", 300, 0), ("c4", 150, 0), ("c4", 150, 2), ("c3", 200, 3)])
+def test_tiled_ensemble_against_oracle(P, oracle_mod, cfg, steps, mode):
     """Ensembles on the tiled layout (members as independent runs of tiles, each with its own
     dt, t, status and buffers; halos never cross members), against the oracle per member."""
     w = W.c3(members=np.arange(5)) if cfg == "c3" else W.c4(members=np.arange(3))
+    w["params"] = dict(w["params"]); w["params"]["mode"] = mode  # DTS, LTS or Newton regions
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
                     stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED)
     ctx.set_state(torch.tensor(w["rho"], device="cuda"), torch.tensor(w["mom"], device="cuda"))
