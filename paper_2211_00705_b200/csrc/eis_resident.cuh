@@ -95,6 +95,9 @@ struct CtaShared {
 #ifdef EIS_PHASE_CLOCK
   long long tclk[10];  // development: clock64 at phase boundaries of the last step (thread 0)
 #endif
+#ifdef EIS_FINE_CLOCK
+  long long fclk[8];   // development: thread 0's clock after S2, P1, barrier A, S4, barrier B, creations, remesh
+#endif
 #ifdef EIS_DTS_CLOCK
   long long dclk[5];   // development: DTS cycles in boundary rounds, in updates; iterations; blocks; Newton its
 #endif
@@ -107,6 +110,11 @@ struct CtaShared {
 #define EIS_ARRIVE(i) do { if ((threadIdx.x & 31) == 0) { if (warp == SW) sh.tclk[i] = clock64(); if (warp == 0) sh.tclk[(i) + 1] = clock64(); } } while (0)
 #else
 #define EIS_TCLK(i) do { } while (0)
+#endif
+#ifdef EIS_FINE_CLOCK
+#define EIS_FCLK(i) do { if (threadIdx.x == 0) sh.fclk[i] = clock64(); } while (0)
+#else
+#define EIS_FCLK(i) do { } while (0)
 #define EIS_ARRIVE(i) do { } while (0)
 #endif
 
@@ -977,6 +985,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         sh.ifc[lane].pL = warm ? sh.ws1[lane] : -1.0;
       }
       __syncwarp();
+      EIS_FCLK(7);
       // ---------------- S2: explicit phase-boundary solves (App. A), half warps ----------------
       for (int k = half; k < nif; k += 2) {
         Ifc& f = sh.ifc[k];
@@ -994,6 +1003,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       }
       __syncwarp();
     }
+    EIS_FCLK(0);
     // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2) ----------------
     if (warp < nbulk) {
       double parts[2];
@@ -1004,6 +1014,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     s_part = warp_max(s_part);
     h_part = warp_min(h_part);
     if (lane == 0) { sh.part_s[warp] = s_part; sh.part_h[warp] = h_part; }  // folded after barrier A
+    EIS_FCLK(1);
     EIS_ARRIVE(1);
     __syncthreads();  // ---------------- barrier A ----------------
 
@@ -1016,6 +1027,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     const double dt_hav = dt / p.h_av;
     const int ntrg = sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG;
     int remesh = 0;
+    EIS_FCLK(2);
 
     if (warp == SW) {
       // ---------------- S4: dual time stepping on every block (a9) ----------------
@@ -1042,6 +1054,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
 #ifdef EIS_PHASE_CLOCK
       if (lane == 0) sh.tclk[7] = clock64();
 #endif
+      EIS_FCLK(3);
       // ---------------- S5: cells next to explicit phase boundaries (a7) ----------------
       const int nif = sh.nifc;
       for (int q = lane; q < 2 * nif; q += 32) {
@@ -1066,6 +1079,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     if (remesh) sh.remesh = 1;
     EIS_ARRIVE(3);
     __syncthreads();  // ---------------- barrier B ----------------
+    EIS_FCLK(4);
 
     // ---------------- creations (a6): acceptance (R16), solves, neighbour updates ----------------
     if (ntrg) {
@@ -1111,6 +1125,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     }
     // ---------------- remesh (a10; R9, R10): events -> shifts -> scatter ----------------
     int n_new = n;
+    EIS_FCLK(5);
     if (sh.remesh) {
       if (tid == 0) { sh.nmev = 0; sh.nsev = 0; sh.ngrp = 0; }
       __syncthreads();
@@ -1232,6 +1247,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       }
     }
     __syncthreads();
+    EIS_FCLK(6);
     if (tid == 0) {
       EIS_TCLK(5);
       MemberStats& st = sh.st;

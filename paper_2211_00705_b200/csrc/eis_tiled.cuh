@@ -865,6 +865,12 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       q[4] = sh.tclk[5] - sh.tclk[3];
       q[5] = clock64() - sh.tclk[5];
 #endif
+#if defined(EIS_FINE_CLOCK) && defined(EIS_PHASE_CLOCK)
+      // load+list | S1+S2 | P1 | barrier A + dt | S4+S5+P2+barrier B | creations | remesh + assembly
+      d[4] = sh.tclk[0] - c0;
+      d[5] = sh.fclk[7] - sh.tclk[0]; d[6] = sh.fclk[1] - sh.fclk[0]; d[7] = sh.fclk[2] - sh.fclk[1];
+      d[8] = sh.fclk[4] - sh.fclk[2]; d[9] = sh.fclk[0] - sh.fclk[7]; d[10] = clock64() - sh.fclk[5];
+#endif
     }
   }
 }
