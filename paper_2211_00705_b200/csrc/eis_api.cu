@@ -52,6 +52,7 @@ struct eis_ctx {
   long long* d_cnt; // scratch: per-member interface counts / offsets
   eis_interface* d_if;
   long long if_cap;
+  long long* d_ifoff = nullptr;  // per-member offsets of eis_interfaces (n_members entries)
   int state_set;
   // tiled layout (one huge grid, C5): tile buffers; d_rho/d_mom/d_h stay the contiguous staging
   int tiled, tile_cells;
@@ -597,6 +598,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   cudaFree(c->d_rho); cudaFree(c->d_mom); cudaFree(c->d_h); cudaFree(c->d_t); cudaFree(c->d_n);
   cudaFree(c->d_status); cudaFree(c->d_stats); cudaFree(c->d_u8); cudaFree(c->d_pack); cudaFree(c->d_cnt);
   cudaFree(c->d_if);
+  cudaFree(c->d_ifoff);
   if (!c->tiled) cudaFree(c->g.dbg);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
@@ -919,8 +921,8 @@ extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t cap
       CU(cudaMalloc(&c->d_if, total * sizeof(eis_interface)));
       c->if_cap = total;
     }
-    long long* d_off = nullptr;
-    CU(cudaMalloc(&d_off, M * 8));
+    if (!c->d_ifoff) CU(cudaMalloc(&c->d_ifoff, M * 8));
+    long long* d_off = c->d_ifoff;
     CU(cudaMemcpyAsync(d_off, off.data(), M * 8, cudaMemcpyHostToDevice, c->stream));
     k_iface<<<nb, 128, 0, c->stream>>>(c->e, c->g, M, c->grid.x_left, d_off, nullptr, c->d_if, total);
     k_iface_solve<<<(unsigned)((total + 7) / 8), 128, 0, c->stream>>>(c->e, c->p, c->g, c->d_if, total);
@@ -928,7 +930,6 @@ extern "C" eis_status eis_interfaces(eis_ctx* c, eis_interface* out, int64_t cap
     const long long ncopy = total < capacity ? total : capacity;
     CU(cudaMemcpyAsync(out, c->d_if, ncopy * sizeof(eis_interface), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    cudaFree(d_off);
   }
   return (out && total > capacity) ? EIS_E_CAPACITY : EIS_OK;
 }
@@ -1018,9 +1019,11 @@ extern "C" eis_status eis_lax_run(const eis_lax_case* cases, int64_t n_cases, in
     return EIS_E_CUDA;
   eis_lax_case* d_cases = nullptr;
   eis_lax_stats* d_stats = nullptr;
-  if (cudaMallocAsync(&d_cases, sizeof(eis_lax_case) * n_cases, st) != cudaSuccess ||
-      cudaMallocAsync(&d_stats, sizeof(eis_lax_stats) * n_cases, st) != cudaSuccess)
+  if (cudaMallocAsync(&d_cases, sizeof(eis_lax_case) * n_cases, st) != cudaSuccess) return EIS_E_CUDA;
+  if (cudaMallocAsync(&d_stats, sizeof(eis_lax_stats) * n_cases, st) != cudaSuccess) {
+    cudaFreeAsync(d_cases, st);
     return EIS_E_CUDA;
+  }
   cudaMemcpyAsync(d_cases, cases, sizeof(eis_lax_case) * n_cases, cudaMemcpyHostToDevice, st);
   lax::lax_cases<<<(unsigned)n_cases, lax::LAX_THREADS, smem, st>>>(d_cases, stride, rho, mom, E, d_stats);
   const cudaError_t le = cudaGetLastError();
