@@ -153,7 +153,7 @@ struct IfaceProb {
 };
 
 __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, double pV, double pL,
-                                           double G[2], double J[4], double aux[2]) {
+                                           double G[2], double J[4], double aux[2], double daux[4]) {
   if (!(pV > 0.0)) return false;
   const double rVs = pV * e.inv_av2;
   const double rLs = e.rho0 + (pL - e.p0) * e.inv_al2;
@@ -187,6 +187,8 @@ __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, dou
   J[1] = (sL + 2.0 * z * zL * jv + z2 * sL * dvL) * e.inv_p0;
   J[2] = (dfV * e.inv_av2 + zV * jv + z * sV * dvV) * e.inv_av;
   J[3] = (dfL * e.inv_al2 + zL * jv + z * sL * dvL) * e.inv_av;
+  daux[0] = zV; daux[1] = zL;           // d aux / d (pV, pL): z, then f(rho_V*; rho_V)
+  daux[2] = dfV * e.inv_av2; daux[3] = 0.0;
   return true;
 }
 
@@ -198,7 +200,7 @@ struct CreateProb {
 };
 
 __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, double pA, double pB,
-                                            double G[2], double J[4], double aux[2]) {
+                                            double G[2], double J[4], double aux[2], double* /*daux: unused*/) {
   const bool cav = (P.A == LIQ);
   const double rA = cav ? e.rho0 + (pA - e.p0) * e.inv_al2 : pA * e.inv_av2;
   const double rB = cav ? pB * e.inv_av2 : e.rho0 + (pB - e.p0) * e.inv_al2;
@@ -249,22 +251,33 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
 // within ~rtol of the root (the oracle tests the step against rtol itself, one extra iteration).
 // Returns the iteration count (>= 0) or -1; aux holds the value at the returned iterate.
 // ---------------------------------------------------------------------------------------
-template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*)>
+template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*, double*),
+          bool LIN>
 __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, double aux[2],
                          unsigned mask, int hl, int base_lane) {
-  double G[2], J[4];
-  if (!EVAL(e, P, x0, x1, G, J, aux)) return -1;
+  double G[2], J[4], da[4];
+  if (!EVAL(e, P, x0, x1, G, J, aux, da)) return -1;
   for (int it = 0; it < p.newton_max_iter; ++it) {
     const double det = J[0] * J[3] - J[1] * J[2];
     if (!(fabs(det) > 0.0) || !isfinite(det)) return -1;
     const double idet = __drcp_rn(det);
     const double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
     const double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
+    // quadratic regime (LIN, reading R14d): a residual already <= 1e-6 whose Newton step is
+    // within sqrt(rtol) of the iterate puts x + d within ~|d|^2 <= rtol of the root: accept it
+    // without another evaluation, the auxiliary values to first order (error O(|d|^2))
+    if (LIN && fmax(fabs(G[0]), fabs(G[1])) <= 1e-6 && fabs(d0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
+        fabs(d1) <= p.newton_stol * fmax(fabs(x1), e.p0)) {
+      aux[0] += da[0] * d0 + da[1] * d1;
+      aux[1] += da[2] * d0 + da[3] * d1;
+      x0 += d0; x1 += d1;
+      return it + 1;
+    }
     const double n0 = G[0] * G[0] + G[1] * G[1];
     // the full step first, on every lane alike (no divergence, no shuffles): accepted almost always
-    double y0 = x0 + d0, y1 = x1 + d1, Gy[2], Jy[4], ay[2];
+    double y0 = x0 + d0, y1 = x1 + d1, Gy[2], Jy[4], ay[2], dy[4];
     const double c1 = 1.0 - 1e-4;
-    bool ok = EVAL(e, P, y0, y1, Gy, Jy, ay) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= c1 * c1 * n0;
+    bool ok = EVAL(e, P, y0, y1, Gy, Jy, ay, dy) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= c1 * c1 * n0;
     double s0 = d0, s1 = d1;
     if (!ok) {  // lane-parallel back-tracking: lane k tries lambda = 2^-(k+1), then 2^-(k+17)
       int acc = -1;
@@ -273,7 +286,7 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
         const double lam = __longlong_as_double((long long)(1023 - k) << 52);  // 2^-k
         y0 = x0 + lam * d0; y1 = x1 + lam * d1;
         const double cl = 1.0 - 1e-4 * lam;
-        const bool okk = k <= p.armijo_max && EVAL(e, P, y0, y1, Gy, Jy, ay) &&
+        const bool okk = k <= p.armijo_max && EVAL(e, P, y0, y1, Gy, Jy, ay, dy) &&
                          Gy[0] * Gy[0] + Gy[1] * Gy[1] <= cl * cl * n0;
         const unsigned b = __ballot_sync(mask, okk) & mask;
         if (b) {
@@ -283,6 +296,7 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
           Gy[0] = __shfl_sync(mask, Gy[0], src); Gy[1] = __shfl_sync(mask, Gy[1], src);
           for (int q = 0; q < 4; ++q) Jy[q] = __shfl_sync(mask, Jy[q], src);
           ay[0] = __shfl_sync(mask, ay[0], src); ay[1] = __shfl_sync(mask, ay[1], src);
+          if (LIN) for (int q = 0; q < 4; ++q) dy[q] = __shfl_sync(mask, dy[q], src);
         }
       }
       if (acc < 0) return fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol ? it : -1;  // rounding floor
@@ -292,12 +306,17 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
     G[0] = Gy[0]; G[1] = Gy[1];
     for (int q = 0; q < 4; ++q) J[q] = Jy[q];
     aux[0] = ay[0]; aux[1] = ay[1];
+    if (LIN) for (int q = 0; q < 4; ++q) da[q] = dy[q];
     if (fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol && fabs(s0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
         fabs(s1) <= p.newton_stol * fmax(fabs(x1), e.p0))
       return it + 1;
   }
   return -1;
 }
+
+#ifndef EIS_NEWTON_LIN
+#define EIS_NEWTON_LIN true
+#endif
 
 // HLLC starting value (Eq. (17)), vapour left / liquid right, mirrored when the
 // liquid is on the left; clamped to [0.01 p0, 4 p0] (R14b).
@@ -331,11 +350,11 @@ __device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, doub
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
   }
-  int it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+  int it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
-    it = newton_hw<IfaceProb, iface_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+    it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   }
   IfaceSol s;
   s.iters = it;
@@ -360,7 +379,7 @@ __device__ __noinline__ CreateSol create_solve_hw(const Eos& e, const Prm& p, in
                                                   int base_lane) {
   CreateProb P{phase_outer, rl, rr, ur - ul};
   double x0 = e.p0, x1 = e.p0, aux[2];
-  const int it = newton_hw<CreateProb, create_eval>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+  const int it = newton_hw<CreateProb, create_eval, false>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   CreateSol s;
   s.iters = it;
   if (it < 0) return s;
