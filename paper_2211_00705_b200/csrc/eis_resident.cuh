@@ -252,6 +252,9 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
     w0 = rn0; w1 = rn1;
     W0[lane] = w0; W1[lane] = w1;
   }
+  // loop invariants of the relaxed update and of the residual (one reciprocal each)
+  const double i1r = 1.0 / (1.0 + r), qr = r * i1r, rsc = (1.0 + r) / dtau;
+  const double tol_l = tin ? p.tol_tiny : p.tol_nb;  // this lane's stop threshold
   __syncwarp();
   long long l = 0;
   int err = 0;
@@ -288,23 +291,22 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       { const long long c = clock64(); if (lane == 0) sh.dclk[0] += c - dc0; dc0 = c; }
 #endif
       if (err || part == 1) break;
-      double res_nb = 0.0, res_t = 0.0;  // (b) relaxed moving-cell update (R13)
+      bool conv = true;  // (b) relaxed moving-cell update (R13) and this lane's residual
       int bad = 0;
       if (lane < K) {
         const double hl_ = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
         if (!(hl_ > 0.0)) bad = ST_WIDTH;
-        const double q = r / (1.0 + r);
-        const double n0 = w0 / (1.0 + r) + q * ((hn / hl_) * rn0 - (dt / hl_) * (Fe0[lane + 1] - Fe0[lane]));
-        const double n1 = w1 / (1.0 + r) + q * ((hn / hl_) * rn1 - (dt / hl_) * (Fe1[lane + 1] - Fe1[lane]));
-        const double r0 = fabs((1.0 + r) * (n0 - w0) / (dtau * fmax(fabs(w0), 1.0)));
-        const double r1 = fabs((1.0 + r) * (n1 - w1) / (dtau * fmax(fabs(w1), 1.0)));
-        const double ri = fmax(r0, r1);
-        if (tin) res_t = ri; else res_nb = ri;
+        const double ih = 1.0 / hl_, a0 = hn * ih, a1 = dt * ih;
+        const double n0 = w0 * i1r + qr * (a0 * rn0 - a1 * (Fe0[lane + 1] - Fe0[lane]));
+        const double n1 = w1 * i1r + qr * (a0 * rn1 - a1 * (Fe1[lane + 1] - Fe1[lane]));
+        const double r0 = fabs(rsc * (n0 - w0) / fmax(fabs(w0), 1.0));
+        const double r1 = fabs(rsc * (n1 - w1) / fmax(fabs(w1), 1.0));
+        conv = fmax(r0, r1) < tol_l;
         w0 = n0; w1 = n1;
         if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
       }
-      res_nb = warp_max(res_nb);
-      res_t = warp_max(res_t);
+      // max over tiny cells < tol_tiny and over the others < tol_nb  <=>  every lane below its own
+      conv = __all_sync(0xffffffffu, conv);
       bad = __reduce_max_sync(0xffffffffu, bad);
       if (lane < K) { W0[lane] = w0; W1[lane] = w1; }
       __syncwarp();
@@ -313,7 +315,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       { const long long c = clock64(); if (lane == 0) { sh.dclk[1] += c - dc0; sh.dclk[2] += 1; } dc0 = c; }
 #endif
       if (bad) { err = bad; break; }
-      if (res_nb < p.tol_nb && res_t < p.tol_tiny) break;
+      if (conv) break;
       if (l >= p.dts_max_iter) { err = ST_DTS_CAP; break; }
     }
   }

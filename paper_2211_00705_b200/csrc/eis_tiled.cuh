@@ -702,6 +702,9 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     sh.status = 0;
     reset_counters(sh);
     memset(&sh.st, 0, sizeof(sh.st));
+#ifdef EIS_DTS_CLOCK
+    for (int q = 0; q < 5; ++q) sh.dclk[q] = 0;
+#endif
     const double* ws = tl.ws + (size_t)k * WS_STRIDE;
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
@@ -864,6 +867,10 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       q[3] = sh.tclk[7] - sh.tclk[6];
       q[4] = sh.tclk[5] - sh.tclk[3];
       q[5] = clock64() - sh.tclk[5];
+#endif
+#ifdef EIS_DTS_CLOCK
+      for (int q = 0; q < 5; ++q) d[5 + q] = sh.dclk[q];
+      d[10] = (long long)sh.c_solves;
 #endif
 #if defined(EIS_FINE_CLOCK) && defined(EIS_PHASE_CLOCK)
       // load+list | S1+S2 | P1 | barrier A + dt | S4+S5+P2+barrier B | creations | remesh + assembly
