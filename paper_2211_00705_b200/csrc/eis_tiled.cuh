@@ -136,31 +136,18 @@ struct TGeo {
   int k, m, in, out, cnt, cl, nL, nR, n;
   bool xl, xr, hu_in;
   bool first, last;  // the member's first / last tile (a domain end unless a rank neighbour)
+  bool huL, huR;     // tile_geo_spec: the neighbour tiles' uniform-width flags (read buffer)
 };
-__device__ __forceinline__ TGeo tile_geo(const Tiles& tl, int k) {
-  TGeo g;
-  g.k = k; g.m = k / tl.tpm;
-  const int cur = tl.mctl[MCS * g.m];
-  g.in = cur; g.out = 1 - cur;
-  g.first = k % tl.tpm == 0; g.last = (k + 1) % tl.tpm == 0;
-  g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
-  g.cnt = tl.cnt[cur][k];
-  g.hu_in = tl.hu[cur][k] != 0;
-  g.xl = (g.first && tl.nbr_left); g.xr = (g.last && tl.nbr_right);
-  g.cl = !g.first ? tl.cnt[cur][k - 1] : 0;
-  g.nL = !g.first ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
-  g.nR = !g.last ? min(HALO, tl.cnt[cur][k + 1]) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
-  g.n = g.nL + g.cnt + g.nR;
-  return g;
-}
-// the same, with the tile metadata of both buffers loaded before `cur` is known (one
-// dependent global round trip fewer at the start of every tile)
+// (the tile metadata of both buffers is loaded before `cur` is known: one dependent global
+// round trip fewer at the start of every tile)
 __device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
   const int m = k / tl.tpm;
   const bool hasl = k % tl.tpm != 0, hasr = (k + 1) % tl.tpm != 0;
   const int c0 = tl.cnt[0][k], c1 = tl.cnt[1][k], h0 = tl.hu[0][k], h1 = tl.hu[1][k];
   const int l0 = hasl ? tl.cnt[0][k - 1] : 0, l1 = hasl ? tl.cnt[1][k - 1] : 0;
   const int r0 = hasr ? tl.cnt[0][k + 1] : 0, r1 = hasr ? tl.cnt[1][k + 1] : 0;
+  const int hl0 = hasl ? tl.hu[0][k - 1] : 0, hl1 = hasl ? tl.hu[1][k - 1] : 0;  // (dropped where unused)
+  const int hr0 = hasr ? tl.hu[0][k + 1] : 0, hr1 = hasr ? tl.hu[1][k + 1] : 0;
   const int cur = tl.mctl[MCS * m];
   TGeo g;
   g.k = k; g.m = m; g.in = cur; g.out = 1 - cur;
@@ -168,6 +155,8 @@ __device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
   g.base = (long long)k * tl.capt; g.bl = g.base - tl.capt; g.br = g.base + tl.capt;
   g.cnt = cur ? c1 : c0;
   g.hu_in = (cur ? h1 : h0) != 0;
+  g.huL = (cur ? hl1 : hl0) != 0;
+  g.huR = (cur ? hr1 : hr0) != 0;
   g.xl = (g.first && tl.nbr_left); g.xr = (g.last && tl.nbr_right);
   g.cl = cur ? l1 : l0;
   g.nL = hasl ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
@@ -565,7 +554,7 @@ __device__ __forceinline__ void tile_full(const Eos& e, const Prm& p, const Tile
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
-  const int huL = !g.first ? tl.hu[g.in][k - 1] : 0, huR = !g.last ? tl.hu[g.in][k + 1] : 0;
+  const int huL = g.huL, huR = g.huR;
   for (int i = tid; i < n; i += T) {
     long long mo;
     const double* pr = vcell(tl, g, i, mo);
@@ -709,7 +698,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     sh.wsn = (int)ws[2 * MAXIF];
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
-  const int huL = !g.first ? tl.hu[g.in][k - 1] : 0, huR = !g.last ? tl.hu[g.in][k + 1] : 0;
+  const int huL = g.huL, huR = g.huR;
   for (int i = tid; i < n; i += T) {
     const int v = s0 + i;
     long long mo;
