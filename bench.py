@@ -244,8 +244,9 @@ def main():
     if name == "C5":
         return main_c5(args, torch, dist, P, world, rank, local)
     Mtot = args.members or total_members(name)
-    lo, hi = rank * Mtot // world, (rank + 1) * Mtot // world
-    w = workload(name, np.arange(lo, hi) if name in ("C3", "C4") else None)
+    # members interleaved over ranks (r, r + P, ...): the costly nucleating C4 members spread evenly
+    # (SURVEY 8(e)); results do not depend on the sharding
+    w = workload(name, np.arange(rank, Mtot, world) if name in ("C3", "C4") else None)
     stream = torch.cuda.current_stream()
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], device=local,
                     stream=stream, threads=int(os.environ.get("EIS_THREADS", "0")),
@@ -380,7 +381,7 @@ def main():
             "config": {"workload": f"{name}: {Mtot} members x {w['N']} cells, cavitation ensemble" if name == "C3"
                        else f"{name}: {Mtot} members x {w['N']} cells",
                        "members": Mtot, "cells_per_member": w["N"], "cell_capacity": w["cap"],
-                       "parallelism": f"member-sharded dp{world}", "l2": "inputs (1.1 GB per GPU) larger than L2",
+                       "parallelism": f"member-sharded dp{world} (interleaved)", "l2": "inputs (1.1 GB per GPU) larger than L2",
                        "layout": "tiled" if tiled else "member-resident", "launches": launch_note,
                        "implicit_regions": MODE_NAMES[w["params"].get("mode", 0)]},
             "roofline": roof,
