@@ -142,6 +142,23 @@ def test_c4_members(P, oracle_mod, layout):
     assert g["stats"]["creations"] >= 1 and g["stats"]["dts_iters"] > 0
 
 
+def test_c4_full_size_sampled(P, oracle_mod):
+    """BASELINE configs[3] at full size in the bench launch configuration (16,384 members x 4096
+    cells, 2,000 steps, AUTO -> tiled layout); sampled members (nucleating ones among them)
+    recomputed by the oracle."""
+    w = W.c4()
+    g, _ = gpu_run(P, w, steps=2000)
+    assert int((g["status"] != 0).sum()) == 0
+    sample = np.array([0, 1, 2, 777, 5000, 9999, 12345, 16383])
+    ws = W.c4(members=sample)
+    o = oracle_run(oracle_mod, ws, steps=2000)
+    gs = {k: g[k][sample] for k in ("rho", "mom", "h", "n", "t", "status")}
+    gs["mstats"] = [g["mstats"][m] for m in sample]
+    gs["ifc"] = [dict(i, member=int(np.where(sample == i["member"])[0][0])) for i in g["ifc"] if i["member"] in set(sample.tolist())]
+    assert_parity(gs, o, h_av(w))
+    assert sum(o["mstats"][m]["creations"] for m in range(len(sample))) >= 1
+
+
 def test_363K_cavitation_on_gpu(P):
     """The paper's cavitation test on the GPU path: 166 large steps,
     bubble width and the vapour star pressure plateau."""
