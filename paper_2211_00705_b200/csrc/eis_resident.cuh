@@ -299,9 +299,9 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
         const double ih = 1.0 / hl_, a0 = hn * ih, a1 = dt * ih;
         const double n0 = w0 * i1r + qr * (a0 * rn0 - a1 * (Fe0[lane + 1] - Fe0[lane]));
         const double n1 = w1 * i1r + qr * (a0 * rn1 - a1 * (Fe1[lane + 1] - Fe1[lane]));
-        const double r0 = fabs(rsc * (n0 - w0) / fmax(fabs(w0), 1.0));
-        const double r1 = fabs(rsc * (n1 - w1) / fmax(fabs(w1), 1.0));
-        conv = fmax(r0, r1) < tol_l;
+        // res = |(1 + r)(W^{l+1} - W^l)| / (dtau max(|W^l|, 1)) < tol, multiplied out (no division)
+        conv = fabs(rsc * (n0 - w0)) < tol_l * fmax(fabs(w0), 1.0) &&
+               fabs(rsc * (n1 - w1)) < tol_l * fmax(fabs(w1), 1.0);
         w0 = n0; w1 = n1;
         if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
       }
