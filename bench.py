@@ -250,7 +250,7 @@ def main():
     stream = torch.cuda.current_stream()
     ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], device=local,
                     stream=stream, threads=int(os.environ.get("EIS_THREADS", "0")),
-                    tile_cells=int(os.environ.get("EIS_TILE", "0")))
+                    tile_cells=int(os.environ.get("EIS_TILE", "0")), layout=int(os.environ.get("EIS_LAYOUT", "0")))
     rho_d = torch.from_numpy(w["rho"]).cuda()
     mom_d = torch.from_numpy(w["mom"]).cuda()
     t_end = w.get("t_end", float("inf"))
