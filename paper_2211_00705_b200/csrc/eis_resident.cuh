@@ -255,6 +255,10 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
   // loop invariants of the relaxed update and of the residual (one reciprocal each)
   const double i1r = 1.0 / (1.0 + r), qr = r * i1r, rsc = (1.0 + r) / dtau;
   const double tol_l = tin ? p.tol_tiny : p.tol_nb;  // this lane's stop threshold
+  // phases of U^n by cell (the edges' HLL / boundary choice is fixed for the step)
+  const unsigned vapm = __ballot_sync(0xffffffffu, lane < K && ph0 == VAP);
+  const unsigned liqm = __ballot_sync(0xffffffffu, lane < K && ph0 == LIQ);
+  auto phase_n = [&](int c) { return (vapm >> c & 1u) ? VAP : ((liqm >> c & 1u) ? LIQ : SPIN); };
   __syncwarp();
   long long l = 0;
   int err = 0;
@@ -268,7 +272,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
         const int j = j0 + half;
         if (j < K) {
           const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j];
-          const int pl = phase_of(e, rho[a + j - 1]), pr = phase_of(e, rho[a + j]);  // phases of U^n
+          const int pl = phase_n(j - 1), pr = phase_n(j);  // phases of U^n
           if (pl != pr) {
             IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
             if (hl == 0) {
