@@ -35,7 +35,7 @@ constexpr int MAXTRG = 8;    // creation triggers per member per step
 constexpr int MAXBLK = 8;    // implicit blocks per member
 constexpr int MAXB = 8;      // cells per implicit block
 constexpr int MAXEV = 16;    // remesh events (merge edges, split cells) per member per step
-constexpr int DTS_SCRATCH = 64;
+constexpr int DTS_SCRATCH = 72;
 
 // flag byte per index i (cell i and its LEFT edge i share the byte)
 enum : uint8_t {
@@ -226,6 +226,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
   double* we = Fe1 + MAXB + 1;
   double* xs0 = we + MAXB + 1;
   double* xs1 = xs0 + MAXB + 1;
+  double* Wu = xs1 + MAXB + 1;   // [MAXB] velocities of the iterate (one division per cell, by its lane)
   if (lane == 0) {
     double g0, g1, w;
     edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
@@ -250,7 +251,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
     dtau = theta * dt;
     r = dtau / dt;
     w0 = rn0; w1 = rn1;
-    W0[lane] = w0; W1[lane] = w1;
+    W0[lane] = w0; W1[lane] = w1; Wu[lane] = w1 / w0;
   }
   // loop invariants of the relaxed update and of the residual (one reciprocal each)
   const double i1r = 1.0 / (1.0 + r), qr = r * i1r, rsc = (1.0 + r) / dtau;
@@ -271,10 +272,10 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       for (int j0 = 1; j0 < K; j0 += 2) {  // (a) interior edges at W^l, two per round
         const int j = j0 + half;
         if (j < K) {
-          const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j];
+          const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j], ul = Wu[j - 1], ur = Wu[j];
           const int pl = phase_n(j - 1), pr = phase_n(j);  // phases of U^n
           if (pl != pr) {
-            IfaceSol s = iface_solve_hw(e, p, rl, ml / rl, rr, mr / rr, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
+            IfaceSol s = iface_solve_hw(e, p, rl, ul, rr, ur, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
             if (hl == 0) {
               if (s.iters < 0) err = ST_NEWTON;
               Fe0[j] = s.F0; Fe1[j] = s.F1; we[j] = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
@@ -284,7 +285,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
 #endif
             }
           } else if (hl == 0) {
-            hll(e, pl, rl, ml, ml / rl, rr, mr, mr / rr, Fe0[j], Fe1[j]);
+            hll(e, pl, rl, ml, ul, rr, mr, ur, Fe0[j], Fe1[j]);
             we[j] = 0.0;
           }
         }
@@ -312,7 +313,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       // max over tiny cells < tol_tiny and over the others < tol_nb  <=>  every lane below its own
       conv = __all_sync(0xffffffffu, conv);
       bad = __reduce_max_sync(0xffffffffu, bad);
-      if (lane < K) { W0[lane] = w0; W1[lane] = w1; }
+      if (lane < K) { W0[lane] = w0; W1[lane] = w1; Wu[lane] = w1 / w0; }
       __syncwarp();
       ++l;
 #ifdef EIS_DTS_CLOCK
