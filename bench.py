@@ -10,14 +10,18 @@ start from the seeded initial state (so they include the creation step); the sta
 resident in HBM and larger than the 126 MB L2.
 
 --workload C3: BASELINE configs[2], the batched cavitation ensemble (65,536 grids of N=1024,
-2000 steps) as ONE launch of the member-resident kernel (eis_step(K)); C4 likewise.
+2000 steps) as ONE launch of the member-resident kernel (eis_step(K)); --workload C4: BASELINE
+configs[3] (16,384 grids of N=4096), tiled layout through EIS_LAYOUT_AUTO (three launches per
+step plus the per-member finish).  --mode selects the implicit-region treatment (default: the
+paper's dual time stepping).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eis|reference] [--workload C3|C4|C1|C2|C5]
+                  [--mode 0|1|2|3]
 
 Multi-GPU (torchrun): C5 cuts the grid into tile-aligned rank slices: per step the local
 kernels, a 10-cell halo exchange with the neighbour ranks and an all-reduce(MIN) of the CFL pair
-(paper_2211_00705_b200.decomp); C3/C4 shard members contiguously with no collective in the data
-path.  Scaling "strong" (the problem is fixed); timing is the max over ranks.
+(paper_2211_00705_b200.decomp); C3/C4 interleave members over ranks with no collective in the
+data path.  Scaling "strong" (the problem is fixed); timing is the max over ranks.
 --impl reference times the CPU oracle (oracle/) on a bounded member sample (rank 0 only).
 """
 from __future__ import annotations
