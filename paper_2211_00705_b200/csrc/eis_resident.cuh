@@ -88,6 +88,7 @@ struct CtaShared {
   int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
   int olo, ohi;  // tiles: owned output range after the remesh
+  int pf_j, pf_k, pf_wa, pf_wb;  // tiles: the next window job, claimed during the current one
   int fbits;     // tiles: phase bits of the smem grid (fast-path test)
   int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
   unsigned long long c_dts, c_solves, c_regions, c_dtsmax;

@@ -680,8 +680,13 @@ __device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, doubl
   }
 }
 
+// PF: after the step body, thread 0 claims the next window job and loads its list entry into
+// registers (jn, kn, wan, wbn; jn = -1 when the list is exhausted); the loads complete during the
+// assembly and the caller publishes them, so the next job starts without those round trips.
+template <bool PF>
 __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
-                                            int k, int wa, int wb, double t_end) {
+                                            int k, int wa, int wb, double t_end, int& jn, int& kn, int& wan,
+                                            int& wbn) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const TGeo g = tile_geo_spec(tl, k);
   const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
@@ -725,6 +730,11 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   Z.left_real = (g.first && !tl.nbr_left && s0 == 0);
   Z.right_real = (g.last && !tl.nbr_right && s1 == g.n);
   const double dt = step_body(e, p, sh, A, t, t_end, Z);
+  if (PF && tid == 0) {
+    jn = atomicAdd(&tl.ctl[7], 1);
+    if (jn < tl.ctl[6]) { kn = tl.wlist[4 * jn]; wan = tl.wlist[4 * jn + 1]; wbn = tl.wlist[4 * jn + 2]; }
+    else jn = -1;
+  }
   __syncthreads();
   const int olo = sh.olo, ohi = sh.ohi;
   const int nw_out = ohi - olo;
@@ -797,6 +807,33 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   __syncthreads();
 }
 
+// EIS_WINDOW_DEBUG record of window job j (thread 0, after its full step)
+__device__ __forceinline__ void window_dbg(const Tiles& tl, const CtaShared& sh, int j, int wa, int wb, long long c0) {
+  long long* d = tl.wdbg + WDBG_FIELDS * (long long)j;
+  d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = wb - wa;
+  d[3] = sh.nifc; d[4] = c0;
+#ifdef EIS_PHASE_CLOCK
+  // phases: load+list | to arrival at A | arrival A -> arrival B | S4 (DTS) | B -> step end | assembly
+  long long* q = d + 5;
+  q[0] = sh.tclk[0] - c0;
+  q[1] = sh.tclk[1] - sh.tclk[0];
+  q[2] = sh.tclk[3] - sh.tclk[1];
+  q[3] = sh.tclk[7] - sh.tclk[6];
+  q[4] = sh.tclk[5] - sh.tclk[3];
+  q[5] = clock64() - sh.tclk[5];
+#endif
+#ifdef EIS_DTS_CLOCK
+  for (int q = 0; q < 5; ++q) d[5 + q] = sh.dclk[q];
+  d[10] = (long long)sh.c_solves;
+#endif
+#if defined(EIS_FINE_CLOCK) && defined(EIS_PHASE_CLOCK)
+  // load+list | S1+S2 | P1 | barrier A + dt | S4+S5+P2+barrier B | creations | remesh + assembly
+  d[4] = sh.tclk[0] - c0;
+  d[5] = sh.fclk[7] - sh.tclk[0]; d[6] = sh.fclk[1] - sh.fclk[0]; d[7] = sh.fclk[2] - sh.fclk[1];
+  d[8] = sh.fclk[4] - sh.fclk[2]; d[9] = sh.fclk[0] - sh.fclk[7]; d[10] = clock64() - sh.fclk[5];
+#endif
+}
+
 // tiled_win: persistent CTAs over the window list.  POLL (the instance launched beside
 // tiled_fast on a second stream): a job index is waited for until its entry carries this step's
 // tag, or until every tiled_fast CTA has finished and the index is past the list (or a status
@@ -811,6 +848,27 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   const int tid = threadIdx.x;
   const int tag = tl.ctl[3] + 1;
   volatile int* vctl = tl.ctl;
+  if (!POLL) {  // the next job is claimed during the current one's assembly (tile_window<true>)
+    if (tid == 0) {
+      const int j = atomicAdd(&tl.ctl[7], 1);
+      const bool ok = j < tl.ctl[6];
+      sh.pf_j = ok ? j : -1;
+      if (ok) { sh.pf_k = tl.wlist[4 * j]; sh.pf_wa = tl.wlist[4 * j + 1]; sh.pf_wb = tl.wlist[4 * j + 2]; }
+    }
+    __syncthreads();
+    for (;;) {
+      const int j = sh.pf_j, k = sh.pf_k, wa = sh.pf_wa, wb = sh.pf_wb;
+      if (j < 0) break;
+      __syncthreads();  // every lane has read the job before thread 0 replaces it
+      const long long c0 = clock64();
+      int jn = -1, kn = 0, wan = 0, wbn = 0;
+      tile_window<true>(e, p, tl, sh, A, WCAP, k, wa, wb, t_end, jn, kn, wan, wbn);
+      if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, wa, wb, c0);
+      if (tid == 0) { sh.pf_j = jn; sh.pf_k = kn; sh.pf_wa = wan; sh.pf_wb = wbn; }
+      __syncthreads();
+    }
+    return;
+  }
   for (;;) {
     __syncthreads();
     if (tid == 0) {
@@ -842,32 +900,10 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
     const int j = sh.n_new;
     if (j < 0) break;
     const long long c0 = clock64();
-    tile_window(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end);
-    if (tl.wdbg && tid == 0) {
-      long long* d = tl.wdbg + WDBG_FIELDS * (long long)j;
-      d[0] = clock64() - c0; d[1] = (long long)sh.c_dts; d[2] = tl.wlist[4 * j + 2] - tl.wlist[4 * j + 1];
-      d[3] = sh.nifc; d[4] = c0;
-#ifdef EIS_PHASE_CLOCK
-      // phases: load+list | to arrival at A | arrival A -> arrival B | S4 (DTS) | B -> step end | assembly
-      long long* q = d + 5;
-      q[0] = sh.tclk[0] - c0;
-      q[1] = sh.tclk[1] - sh.tclk[0];
-      q[2] = sh.tclk[3] - sh.tclk[1];
-      q[3] = sh.tclk[7] - sh.tclk[6];
-      q[4] = sh.tclk[5] - sh.tclk[3];
-      q[5] = clock64() - sh.tclk[5];
-#endif
-#ifdef EIS_DTS_CLOCK
-      for (int q = 0; q < 5; ++q) d[5 + q] = sh.dclk[q];
-      d[10] = (long long)sh.c_solves;
-#endif
-#if defined(EIS_FINE_CLOCK) && defined(EIS_PHASE_CLOCK)
-      // load+list | S1+S2 | P1 | barrier A + dt | S4+S5+P2+barrier B | creations | remesh + assembly
-      d[4] = sh.tclk[0] - c0;
-      d[5] = sh.fclk[7] - sh.tclk[0]; d[6] = sh.fclk[1] - sh.fclk[0]; d[7] = sh.fclk[2] - sh.fclk[1];
-      d[8] = sh.fclk[4] - sh.fclk[2]; d[9] = sh.fclk[0] - sh.fclk[7]; d[10] = clock64() - sh.fclk[5];
-#endif
-    }
+    int jn, kn, wan, wbn;
+    tile_window<false>(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
+                       wan, wbn);
+    if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
   }
 }
 
