@@ -1,7 +1,8 @@
-"""DTS vs explicit LTS on the paper's cavitation (E2) and nucleation (E3) tests, GPU and CPU
-oracle: local iterations and wall time (the paper's P:1311-1332,
-P:1424-1444).  E3 with LTS needs ~1e6 sub-steps per large step: run to --e3-t (default 3e-5,
-7 large steps) for both methods.  Prints one JSON line."""
+"""DTS vs explicit LTS vs the Newton-like solve on the paper's cavitation (E2) and nucleation (E3)
+tests, GPU and CPU oracle: local iterations and wall time (the paper's
+P:1311-1332).  E3 with LTS needs ~1e6 sub-steps per large step: LTS runs E3 only to
+the first arg (default 3e-5, 7 large steps), DTS and Newton run it to 3e-5 and to t_end = 5e-4.
+Prints one JSON line."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
@@ -30,9 +31,9 @@ def setup(kind, mode):
 
 
 out = {}
-for kind, t_end in (("E2", 5e-4), ("E3", e3_t)):
-    for mode, name in ((0, "DTS"), (2, "LTS")):
-        eos, prm, N, cap, rho, mom = setup(kind, mode)
+for kind, t_end, modes in (("E2", 5e-4, (0, 2, 3)), ("E3", e3_t, (0, 2, 3)), ("E3full", 5e-4, (0, 3))):
+    for mode, name in ((m, {0: "DTS", 2: "LTS", 3: "NEWTON"}[m]) for m in modes):
+        eos, prm, N, cap, rho, mom = setup(kind[:2], mode)
         ctx = P.Context(eos, prm, 1, N, cap, -2.0, 2.0, stream=torch.cuda.current_stream())
         ctx.set_state(torch.tensor(rho, device="cuda"), torch.tensor(mom, device="cuda"))
         ctx.run_to(t_end)  # warm-up (module load, first launch)
@@ -50,6 +51,10 @@ for kind in ("E2", "E3"):
     d, l = out[f"{kind}_DTS"], out[f"{kind}_LTS"]
     out[f"{kind}_ratio"] = {"local_iterations_lts_over_dts": l["local_iterations_gpu"] / max(d["local_iterations_gpu"], 1),
                             "gpu_time_lts_over_dts": l["gpu_s"] / d["gpu_s"]}
+for kind in ("E2", "E3", "E3full"):
+    d, nt = out[f"{kind}_DTS"], out[f"{kind}_NEWTON"]
+    out[f"{kind}_newton"] = {"evaluations_over_dts_iterations": nt["local_iterations_gpu"] / max(d["local_iterations_gpu"], 1),
+                             "gpu_time_newton_over_dts": nt["gpu_s"] / d["gpu_s"]}
 out["paper"] = {"E2": {"local_iterations": {"LTS": 1941, "DTS": 355}, "time_s": {"LTS": 4.93, "DTS": 2.94}, "cite": "P:1324-1325"},
                 "E3": {"local_iterations": {"LTS": 27154016, "DTS": 1367460}, "time_s": {"LTS": 9811, "DTS": 509}, "cite": "P:1435-1436"}}
 print(json.dumps(out))
