@@ -21,6 +21,9 @@
 #ifndef EIS_WIN_MINB
 #define EIS_WIN_MINB 16  // one-warp window CTAs per SM (register budget 128)
 #endif
+#ifndef EIS_FAST_T
+#define EIS_FAST_T 128  // tiled_fast threads per CTA (one CTA per tile)
+#endif
 #ifndef EIS_FAST_MINB
 #define EIS_FAST_MINB 8  // tiled_fast CTAs of 128 threads per SM (register budget 64)
 #endif
@@ -332,7 +335,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
 #if EIS_FAST_TMA
   c->smem_fast = 2 * sizeof(double) * (size_t)((capt + 1) & ~1);
-  if (cudaFuncSetAttribute(tiled_fast<128, EIS_FAST_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess) { delete c; return EIS_E_CUDA; }
 #endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
@@ -342,7 +345,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, tiled_fast<128, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
+    if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
       delete c; return EIS_E_CUDA;
@@ -780,7 +783,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
   if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
   if (c->timing) m[0] = timing_event(c);
-  tiled_fast<128, EIS_FAST_MINB><<<c->tl.ntiles, 128, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  tiled_fast<EIS_FAST_T, EIS_FAST_MINB><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
