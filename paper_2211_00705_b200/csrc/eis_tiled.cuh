@@ -848,7 +848,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   const int tid = threadIdx.x;
   const int tag = tl.ctl[3] + 1;
   volatile int* vctl = tl.ctl;
-  if (!POLL) {  // the next job is claimed during the current one's assembly (tile_window<true>)
+  if constexpr (!POLL) {  // the next job is claimed during the current one's assembly (tile_window<true>)
     if (tid == 0) {
       const int j = atomicAdd(&tl.ctl[7], 1);
       const bool ok = j < tl.ctl[6];
@@ -867,8 +867,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       if (tid == 0) { sh.pf_j = jn; sh.pf_k = kn; sh.pf_wa = wan; sh.pf_wb = wbn; }
       __syncthreads();
     }
-    return;
-  }
+  } else {
   for (;;) {
     __syncthreads();
     if (tid == 0) {
@@ -904,6 +903,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
     tile_window<false>(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
                        wan, wbn);
     if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
+  }
   }
 }
 
