@@ -868,42 +868,42 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       __syncthreads();
     }
   } else {
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-      int j = atomicAdd(&tl.ctl[7], 1);
-      volatile int* ready = reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]);
-      if (POLL) {
+    for (;;) {
+      __syncthreads();
+      if (tid == 0) {
+        int j = atomicAdd(&tl.ctl[7], 1);
+        volatile int* ready = reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]);
+        if (POLL) {
 #ifdef EIS_POLL_DEBUG
-        long long spins = 0;
+          long long spins = 0;
 #endif
-        for (;;) {
-          if (j < vctl[6] && *ready == tag) break;
-          if (vctl[1] != 0 || (vctl[9] >= tl.ntiles && j >= vctl[6])) { j = -1; break; }
-          __nanosleep(256);
+          for (;;) {
+            if (j < vctl[6] && *ready == tag) break;
+            if (vctl[1] != 0 || (vctl[9] >= tl.ntiles && j >= vctl[6])) { j = -1; break; }
+            __nanosleep(256);
 #ifdef EIS_POLL_DEBUG
-          if (++spins == 4000000) {
-            printf("poll stuck: cta %d j %d ctl6 %d ctl7 %d ctl9 %d ntiles %d tag %d ready %d ctl1 %d\n", blockIdx.x, j,
-                   vctl[6], vctl[7], vctl[9], tl.ntiles, tag, j < 4 * tl.ntiles ? *ready : -7, vctl[1]);
-            j = -1; break;
+            if (++spins == 4000000) {
+              printf("poll stuck: cta %d j %d ctl6 %d ctl7 %d ctl9 %d ntiles %d tag %d ready %d ctl1 %d\n", blockIdx.x, j,
+                     vctl[6], vctl[7], vctl[9], tl.ntiles, tag, j < 4 * tl.ntiles ? *ready : -7, vctl[1]);
+              j = -1; break;
+            }
+#endif
           }
-#endif
+        } else if (j >= vctl[6]) {
+          j = -1;
         }
-      } else if (j >= vctl[6]) {
-        j = -1;
+        __threadfence();
+        sh.n_new = j;
       }
-      __threadfence();
-      sh.n_new = j;
+      __syncthreads();
+      const int j = sh.n_new;
+      if (j < 0) break;
+      const long long c0 = clock64();
+      int jn, kn, wan, wbn;
+      tile_window<false>(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
+                         wan, wbn);
+      if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
     }
-    __syncthreads();
-    const int j = sh.n_new;
-    if (j < 0) break;
-    const long long c0 = clock64();
-    int jn, kn, wan, wbn;
-    tile_window<false>(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
-                       wan, wbn);
-    if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
-  }
   }
 }
 
