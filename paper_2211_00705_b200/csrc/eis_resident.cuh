@@ -1007,6 +1007,11 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
           if (s.iters < 0) zone_status_e(sh, Z, ed, ST_NEWTON);
           f.F0 = s.F0; f.F1 = s.F1; f.w = s.w; f.pV = s.pV; f.pL = s.pL;
           if (Z.own_lo < ed && ed <= Z.own_hi) atomicAdd(&sh.c_solves, 1ull);
+#ifdef EIS_S2_COUNT  // development: explicit boundary solves and their Newton iterations
+          atomicAdd(reinterpret_cast<unsigned long long*>(&sh.dclk[3]), 1ull);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&sh.dclk[4]), (unsigned long long)s.iters);
+          if (f.pV > 0.0 && warm) atomicAdd(reinterpret_cast<unsigned long long*>(&sh.dclk[2]), 1ull);
+#endif
         }
       }
       __syncwarp();
