@@ -432,7 +432,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   unif = !(f & 8);
   if (window) {  // partials and width uniformity of the fast cells (outside [wa, wb)), from the
                  // output just written (the window full step only moves them): as cfl_partials
-    __threadfence();  // this CTA's output is read by a window CTA that may run concurrently
+    if (tl.poll) __threadfence();  // output read by a window CTA running concurrently (polling mode)
     double sf = 0.0, hf = INFINITY;
     bool uf = true;
     for (int c = own_lo + tid; c < own_hi; c += blockDim.x) {
@@ -481,8 +481,10 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       if (window) {  // a window of the tile, published with this step's tag after its data
         const int j = atomicAdd(&tl.ctl[6], 1);
         tl.wlist[4 * j] = k; tl.wlist[4 * j + 1] = wa; tl.wlist[4 * j + 2] = wb;
-        __threadfence();
-        *reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]) = tl.ctl[3] + 1;
+        if (tl.poll) {  // only a concurrently polling window kernel reads the entry before this kernel ends
+          __threadfence();
+          *reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]) = tl.ctl[3] + 1;
+        }
       } else {
         tl.slow[atomicAdd(&tl.ctl[4], 1)] = k;
       }
