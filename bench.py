@@ -473,9 +473,10 @@ def main_c5(args, torch, dist, P, world, rank, local):
             t = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
+        # a single grid moves only its live cells (rho, mom in; rho, mom, h, n, t out)
         e2e = {"value": cu / te, "unit": "cell-updates/s",
-               "h2d_bytes_per_step": 2 * 8 * rg.cap * world / max(args.steps, 1),
-               "d2h_bytes_per_step": (3 * 8 * rg.cap + 16) * world / max(args.steps, 1),
+               "h2d_bytes_per_step": 2 * 8 * rg.n * world / max(args.steps, 1),
+               "d2h_bytes_per_step": (3 * 8 * int(out["n"][0]) + 16) * world / max(args.steps, 1),
                "note": "one set_state(host pinned) + K steps + get_state(host pinned) per rank; bytes / K"}
 
     cpu = None

@@ -19,7 +19,8 @@
  *
  * Conventions
  *  - Layout: structure of arrays, member-major, fp64: rho[m*cap + i], mom[m*cap + i] (= rho u),
- *    width[m*cap + i]; only i < n_cells[m] is live.  cap = eis_grid.cell_capacity.
+ *    width[m*cap + i]; only i < n_cells[m] is live (entries beyond are unspecified: a single
+ *    grid moves only its live cells between host and device).  cap = eis_grid.cell_capacity.
  *  - where = EIS_HOST: pointers are host memory (copied with cudaMemcpyAsync on the context's
  *    stream, then the call synchronises).  where = EIS_DEVICE: device pointers on grid.device,
  *    accessed stream-ordered on grid.stream (no synchronisation unless stated).

@@ -685,8 +685,12 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   if (!rho || !mom || (where != EIS_HOST && where != EIS_DEVICE)) return fail(c, EIS_E_ARG, "set_state: bad argument%s");
   CU(cudaSetDevice(c->grid.device));
   const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
-  const size_t bytes = (size_t)M * cap * 8;
+  size_t bytes = (size_t)M * cap * 8;
   const cudaMemcpyKind kind = where == EIS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (M == 1 && where == EIS_HOST) {  // one grid from the host: only its live cells cross the link
+    const long long nn = n_cells ? n_cells[0] : c->grid.n_cells;
+    if (nn >= 3 && nn <= cap) bytes = (size_t)nn * 8;
+  }
   CU(cudaMemcpyAsync(c->d_rho, rho, bytes, kind, c->stream));
   CU(cudaMemcpyAsync(c->d_mom, mom, bytes, kind, c->stream));
   if (width) CU(cudaMemcpyAsync(c->d_h, width, bytes, kind, c->stream));
@@ -891,10 +895,17 @@ extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double
   k_pack<<<pack_grid(c), 256, 0, c->stream>>>(c->e, c->g, rho ? pr : nullptr, mom ? pr + cells : nullptr,
                                              width ? pr + 2 * cells : nullptr, phase ? c->d_u8 : nullptr);
   CU(cudaGetLastError());
-  if (rho) CU(cudaMemcpyAsync(rho, pr, cells * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (mom) CU(cudaMemcpyAsync(mom, pr + cells, cells * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (width) CU(cudaMemcpyAsync(width, pr + 2 * cells, cells * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (phase) CU(cudaMemcpyAsync(phase, c->d_u8, cells, cudaMemcpyDeviceToHost, c->stream));
+  size_t ncopy = cells;  // one grid: only its live cells cross the link (the rest is unspecified)
+  if (M == 1) {
+    long long nn = 0;
+    CU(cudaMemcpyAsync(&nn, c->d_n, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (nn > 0 && nn <= cap) ncopy = (size_t)nn;
+  }
+  if (rho) CU(cudaMemcpyAsync(rho, pr, ncopy * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (mom) CU(cudaMemcpyAsync(mom, pr + cells, ncopy * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (width) CU(cudaMemcpyAsync(width, pr + 2 * cells, ncopy * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (phase) CU(cudaMemcpyAsync(phase, c->d_u8, ncopy, cudaMemcpyDeviceToHost, c->stream));
   if (n_cells) CU(cudaMemcpyAsync(n_cells, c->d_n, M * 8, cudaMemcpyDeviceToHost, c->stream));
   if (t) CU(cudaMemcpyAsync(t, c->d_t, M * 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
