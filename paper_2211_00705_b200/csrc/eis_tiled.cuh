@@ -1,16 +1,19 @@
-// eis_tiled.cuh — the tiled streaming kernels for one huge grid (BASELINE configs[4], C5).
+// eis_tiled.cuh — the tiled streaming kernels for huge grids (BASELINE configs[4], C5) and for
+// ensembles of large members (C4; each member its own run of tiles).
 //
-// The grid is cut into tiles of about TILE cells, each stored with slack (capt cells) so that
-// creations and splits insert locally; ping-pong buffers (step n reads buffer cur, writes
-// 1-cur).  A step is two launches:
-//   tiled_fast (one CTA per tile, no shared-memory staging, high occupancy): streams the tile
-//     plus HALO cells of each neighbour through registers in warp windows and, when the tile is
-//     plain (one phase over tile + halos, no creation candidate), completes its step: HLL
-//     fluxes (a3), update (a7), the next step's CFL partials (a2).  Otherwise it appends the
-//     tile to the work list.  Widths are not stored for tiles whose widths are all h_av.
-//   tiled_slow (persistent CTAs, dynamic work list): runs the member-resident step body (the
-//     whole method, a1-a11) on each listed tile held in shared memory, then the last CTA folds
-//     the CFL partials into the next dt (R5/R6).
+// A grid is cut into fixed-size tiles (1400 owned cells by default), each stored with slack
+// (capt cells) so that creations and splits insert locally; ping-pong buffers (step n reads
+// buffer cur, writes 1-cur).  A step is three launches (plus tiled_members_finish for ensembles):
+//   tiled_fast (one CTA per tile, high occupancy): stages the tile's own cells in shared memory
+//     with a TMA bulk copy, streams them plus HALO cells of each neighbour through registers in
+//     warp windows and, where the tile is plain (no cell of another phase, spinodal or creation
+//     candidate), completes its step: HLL fluxes (a3), update (a7), the next step's CFL
+//     partials (a2).  Otherwise it lists a window of <= WMAX owned cells around the special
+//     cells, or the whole tile.  Widths are not stored for tiles whose widths are all h_av.
+//   tiled_win (persistent one-warp CTAs): the member-resident step body (the whole method,
+//     a1-a11) on each listed window plus halos, assembled in place into the tile output.
+//   tiled_slow (persistent CTAs, dynamic work list): the same on whole tiles, then the last CTA
+//     folds the CFL partials into the next dt (R5/R6).
 // The halo is computed redundantly by both neighbours with identical inputs and code, so every
 // decision at a tile boundary (boundary solves, creations, DTS blocks, merges) is taken
 // identically on both sides; ownership: a created cell at a tile boundary and a merge group
@@ -185,8 +188,9 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 // and 31 are halo, so every store is an aligned 16-byte pair) written to the output tile with
 // the next step's CFL partials (a2) -- the same expressions as step_body's bulk passes, so a
 // plain tile's result is the full step's bit for bit.  Interior windows load and store cell
-// pairs as 16-byte vectors.  Windows are loaded in batches of FB (all loads in flight before
-// the arithmetic).  Outputs of a tile that turns out not plain are overwritten by the full step.
+// pairs as 16-byte vectors (from the shared-memory copy of the tile; the two halo windows from
+// global memory).  FB windows per warp iteration (1: more would spill at 64 registers).  Outputs
+// of a tile that turns out not plain are overwritten by the window / whole-tile full step.
 // ------------------------------------------------------------------------------------------
 #ifndef EIS_FB
 #define EIS_FB 1
