@@ -1,4 +1,6 @@
-// eis_resident.cuh — the member-resident large-step kernel (ensembles C1-C4).
+// eis_resident.cuh — the member-resident large-step kernel (ensembles of members up to 2048
+// cells under EIS_LAYOUT_AUTO: C1-C3), and step_body, the whole large step on a grid in shared
+// memory, which the tiled window / whole-tile kernels (eis_tiled.cuh) reuse.
 //
 // One CTA owns one member (an independent 1D grid, R25) for a whole eis_step / eis_run_to
 // call: the grid is loaded from HBM into shared memory once, advanced n_steps large steps of
@@ -16,7 +18,8 @@
 //     S1 tiny cells, implicit blocks, flags, from the boundary list                    (a8)
 //     S2 explicit phase-boundary solves, warm-started from the previous step, half warps (a5)
 //     -- barrier A (dt) --
-//     S4 dual time stepping on every implicit block                                     (a9)
+//     S4 every implicit block: dual time stepping (a9), or local time stepping (mode LTS)
+//        or the chord Newton solve (mode NEWTON)
 //     S5 moving-cell update of the cells next to phase boundaries                       (a7)
 //   bulk warps (all others; the solver joins when done), dynamic 32-wide windows:
 //     P1 per edge: u = m/rho, HLL flux (a3), creation trigger (a4), S_max / h_min (a2)
