@@ -144,6 +144,11 @@ typedef struct {
   int64_t creations, splits, merges, regions;
   double t_min, t_max, dt_min, dt_max;
   int64_t dts_iter_max;   /* most dual-time iterations one implicit block took in one step */
+  /* discrete decisions taken within the rounding-error bound of their own threshold test
+   * (the paper's round-off warning P:1133-1135): DTS stop / continue,
+   * creation trigger (R7), tiny / merge / split width thresholds (R4).  Such a decision
+   * may flip between two correct fp64 implementations (it never changes a result here). */
+  int64_t decision_margin_warnings;
 } eis_stats;
 
 typedef struct { double rho_min, rho_tilde, p_tilde, tau, a_v; } eis_thresholds;

@@ -172,6 +172,22 @@ static int creation_trigger(const eos_t* e, int ph, double rl, double ul, double
   return single_phase_phi(e, VAP, rl, ul, rr, ur, e->rho_tilde) < 0.0;
 }
 
+/* Decision margins (the paper's round-off warning P:1133-1135).  A discrete decision
+ * "x < threshold" is marginal when |x - threshold| is within MARGIN_ULPS times the rounding-error
+ * bound of evaluating x: two correct fp64 implementations may then decide differently.  Counted
+ * per member in eiso_stats.decision_margin_warnings; never changes a result. */
+#define MARGIN_ULPS 16.0
+static int trigger_marginal(const eos_t* e, int ph, double rl, double ul, double rr, double ur) {
+  double thr = ph == LIQ ? e->rho_min : e->rho_tilde;
+  double fl = wave_f(e, ph, thr, rl), fr = wave_f(e, ph, thr, rr);
+  double phi = fl + fr + (ur - ul);
+  return fabs(phi) <= MARGIN_ULPS * DBL_EPSILON * (fabs(fl) + fabs(fr) + fabs(ul) + fabs(ur));
+}
+/* width threshold h < eps h_av (tiny / merge, R4) or h > eps h_av (split) */
+static int width_marginal(double h, double thr) {
+  return fabs(h - thr) <= MARGIN_ULPS * DBL_EPSILON * thr;
+}
+
 /* kinetic relation z = tau p_V [[g + e_kin]] with interface-relative e_kin = z^2 v^2 / 2
  * (reading R2):  A z^2 - z + B = 0, A = tau p_V [[v^2]]/2, B = tau p_V [[g]];
  * the root continuous in A -> 0 is z = 2B / (1 + sqrt(1 - 4AB)). */
@@ -524,7 +540,8 @@ static int edge_flux(eiso_ctx* c, double rl, double ml, double rr, double mr, do
  * cells < tol_tiny.  Part 2: fluxes at U* and the conservative update.
  * Parity unpinned beyond invariants (DTS fixed point, conservation): DESIGN.md §3. */
 static int dts_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t* E, double dt,
-                     double* rho_new, double* mom_new, double* h_new, int64_t* iters_out, int64_t* nsolves) {
+                     double* rho_new, double* mom_new, double* h_new, int64_t* iters_out, int64_t* nsolves,
+                     int64_t* margins) {
   int64_t base = m * c->cap;
   const double* rho = c->rho + base;
   const double* mom = c->mom + base;
@@ -548,6 +565,7 @@ static int dts_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t*
   F0[K] = E[b + 1].F0; F1[K] = E[b + 1].F1; w[K] = E[b + 1].w;
   int64_t l;
   int done = 0;
+  int prev_cont_robust = 1; /* decision margin of the previous iteration's "continue" */
   for (l = 0; l < c->prm.dts_max_iter; ++l) {
     for (int64_t j = 1; j < K; ++j) { /* (a) interior fluxes at W^l */
       int kind;
@@ -555,6 +573,7 @@ static int dts_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t*
       if (st) goto out;
     }
     double res_nb = 0.0, res_t = 0.0;
+    int stop_robust = 1, cont_robust = 0;
     for (int64_t i = 0; i < K; ++i) { /* (b) relaxed moving-cell update */
       hl[i] = h[a + i] + (w[i + 1] - w[i]) * dt;
       if (!(hl[i] > 0.0)) { st = EISO_E_WIDTH; goto out; }
@@ -565,7 +584,22 @@ static int dts_block(eiso_ctx* c, int64_t m, int64_t a, int64_t b, const edge_t*
       double r1 = fabs((1.0 + r[i]) * (N1[i] - W1[i]) / (dtau[i] * fmax(fabs(W1[i]), 1.0)));
       double ri = fmax(r0, r1);
       if (tiny[a + i]) res_t = fmax(res_t, ri); else res_nb = fmax(res_nb, ri);
+      /* margins: res_i against its tolerance, within the rounding-error bound of N - W */
+      double tol = tiny[a + i] ? c->prm.tol_tiny : c->prm.tol_nb;
+      for (int comp = 0; comp < 2; ++comp) {
+        double Wc = comp ? W1[i] : W0[i], Un = comp ? mom[a + i] : rho[a + i];
+        double FL = comp ? F1[i] : F0[i], FR = comp ? F1[i + 1] : F0[i + 1], rc = comp ? r1 : r0;
+        double err = MARGIN_ULPS * DBL_EPSILON *
+                     (fabs(Wc) + q * (fabs((h[a + i] / hl[i]) * Un) + (dt / hl[i]) * (fabs(FL) + fabs(FR)))) *
+                     (1.0 + r[i]) / (dtau[i] * fmax(fabs(Wc), 1.0));
+        if (!(rc < tol - err)) stop_robust = 0;
+        if (rc >= tol + err) cont_robust = 1;
+      }
     }
+    if (res_nb < c->prm.tol_nb && res_t < c->prm.tol_tiny) {
+      if (!stop_robust || !prev_cont_robust) ++*margins;
+    }
+    prev_cont_robust = cont_robust;
     for (int64_t i = 0; i < K; ++i) {
       W0[i] = N0[i]; W1[i] = N1[i];
       if (!(W0[i] > 0.0) || phase_of(&c->e, W0[i]) != ph0[i]) { st = EISO_E_SPINODAL; goto out; }
@@ -891,6 +925,7 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     if (E[ed].kind != 0 || inreg[ed - 1] || inreg[ed]) continue;
     int phe = ph[ed];
     double ul = mom[ed - 1] / rho[ed - 1], ur = mom[ed] / rho[ed];
+    if (trigger_marginal(e, phe, rho[ed - 1], ul, rho[ed], ur)) S->decision_margin_warnings++;
     if (!creation_trigger(e, phe, rho[ed - 1], ul, rho[ed], ur)) continue;
     if (E[ed - 1].kind == 2) continue;
     eiso_creation cr;
@@ -933,7 +968,7 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     else if (P->mode == EISO_MODE_NEWTON)
       st = newton_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
     else
-      st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
+      st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves, &S->decision_margin_warnings);
     if (st) goto out;
     S->dts_iters += it;
     S->regions++;
@@ -947,6 +982,10 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     if (i > 0 && E[i].kind == 2) { R0[q] = E[i].rhoB; R1[q] = E[i].momB; RH[q] = E[i].hB; ++q; }
     R0[q] = rho_new[i]; R1[q] = mom_new[i]; RH[q] = h_new[i]; ++q;
   }
+  for (int64_t i = 0; i < n; ++i) /* width decisions of the cells whose width changed (R4) */
+    if (h_new[i] != h[i] && (width_marginal(h_new[i], P->eps_tiny * c->h_av) ||
+                             width_marginal(h_new[i], P->eps_split * c->h_av)))
+      S->decision_margin_warnings++;
   for (int64_t i = 0; i < q; ++i) {
     if (!(R0[i] > 0.0)) { st = EISO_E_NONPOS_DENSITY; goto out; }
     RP[i] = phase_of(e, R0[i]);
@@ -1010,6 +1049,7 @@ static void accumulate(const eiso_ctx* c, eiso_stats* out) {
     out->steps += s->steps; out->cell_updates += s->cell_updates; out->dts_iters += s->dts_iters;
     out->iface_solves += s->iface_solves; out->creations += s->creations; out->splits += s->splits;
     out->merges += s->merges; out->regions += s->regions;
+    out->decision_margin_warnings += s->decision_margin_warnings;
     if (c->t[m] < out->t_min) out->t_min = c->t[m];
     if (c->t[m] > out->t_max) out->t_max = c->t[m];
     if (s->steps && s->dt_min < out->dt_min) out->dt_min = s->dt_min;

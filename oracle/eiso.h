@@ -80,6 +80,12 @@ typedef struct {
 typedef struct {
   int64_t steps, cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
   double t_min, t_max, dt_min, dt_max;
+  /* discrete decisions taken within the rounding-error bound of their own threshold test
+   * (the paper's round-off warning P:1133-1135): DTS stop / continue,
+   * creation trigger (R7), tiny / merge / split width thresholds (R4).  Such a decision
+   * can flip between two correct fp64 implementations; the parity tests accept a differing
+   * DTS count only in a member that logged one. */
+  int64_t decision_margin_warnings;
 } eiso_stats;
 
 typedef struct {

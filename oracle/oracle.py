@@ -60,7 +60,8 @@ class Creation(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("steps", "cell_updates", "dts_iters", "iface_solves",
                                          "creations", "splits", "merges", "regions")] + \
-               [(n, C.c_double) for n in ("t_min", "t_max", "dt_min", "dt_max")]
+               [(n, C.c_double) for n in ("t_min", "t_max", "dt_min", "dt_max")] + \
+               [("decision_margin_warnings", C.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

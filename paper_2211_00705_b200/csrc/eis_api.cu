@@ -159,7 +159,8 @@ __global__ void k_validate(const Eos e, Members g, double t0) {
   const long long m = blockIdx.x;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  const long long n = g.n[m];
+  const long long n_in = g.n[m];
+  const long long n = n_in < 0 ? 0 : (n_in > g.cap ? g.cap : n_in);  // never read past the member's row
   for (long long lo = (long long)blockIdx.y * VALIDATE_CHUNK; lo < n; lo += (long long)gridDim.y * VALIDATE_CHUNK) {
     const long long hi = min(n, lo + VALIDATE_CHUNK);
     for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -172,7 +173,7 @@ __global__ void k_validate(const Eos e, Members g, double t0) {
   if (threadIdx.x == 0) {
     int st = bad;
     if (blockIdx.y == 0) {
-      if (n < 3 || n > g.cap) st = ST_CAPACITY;
+      if (n_in < 3 || n_in > g.cap) st = ST_CAPACITY;
       g.t[m] = t0;
       MemberStats z;
       memset(&z, 0, sizeof(z));
@@ -462,6 +463,7 @@ static eis_status tiled_stats(eis_ctx* c, eis_stats* out) {
     out->cell_updates += s.cell_updates; out->dts_iters += s.dts_iters; out->iface_solves += s.iface_solves;
     out->creations += s.creations; out->splits += s.splits; out->merges += s.merges; out->regions += s.regions;
     out->dts_iter_max = std::max(out->dts_iter_max, (int64_t)s.dts_max);
+    out->decision_margin_warnings += s.margins;
     full += s.full_steps;
     win += s.win_steps;
   }
@@ -497,6 +499,7 @@ static eis_status tiled_member_stats(eis_ctx* c, eis_stats* out) {
       o.cell_updates += s.cell_updates; o.dts_iters += s.dts_iters; o.iface_solves += s.iface_solves;
       o.creations += s.creations; o.splits += s.splits; o.merges += s.merges; o.regions += s.regions;
       o.dts_iter_max = std::max(o.dts_iter_max, (int64_t)s.dts_max);
+      o.decision_margin_warnings += s.margins;
     }
     const double* sc = &scal[(size_t)SCS * m];
     o.steps = mctl[(size_t)MCS * m + 2];
@@ -536,6 +539,9 @@ extern "C" eis_status eis_create(const eis_eos* eos, const eis_params* prm, cons
   p.cfl = prm->cfl; p.eps_split = prm->eps_split; p.eps_tiny = prm->eps_tiny; p.theta_nb = prm->theta_nb;
   p.tol_nb = prm->tol_nb; p.tol_tiny = prm->tol_tiny; p.newton_rtol = prm->newton_rtol; p.newton_gtol = prm->newton_gtol;
   p.newton_stol = std::sqrt(prm->newton_rtol);
+  p.lin_gtol = std::sqrt(prm->newton_gtol);  // R14d: the quadratic regime starts below sqrt(gtol)
+  if (const char* ev = getenv("EIS_NEWTON_STOL")) p.newton_stol = atof(ev);  // development knobs
+  if (const char* ev = getenv("EIS_LIN_GTOL")) p.lin_gtol = atof(ev);
   p.h_av = grid->h_av > 0 ? grid->h_av : (grid->x_right - grid->x_left) / (double)grid->n_cells;  // fixed (R9)
   p.dts_max_iter = prm->dts_max_iter; p.newton_max_iter = prm->newton_max_iter; p.armijo_max = prm->armijo_max;
   p.mode = prm->mode;
@@ -687,6 +693,21 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   const long long M = c->grid.n_members, cap = c->grid.cell_capacity;
   size_t bytes = (size_t)M * cap * 8;
   const cudaMemcpyKind kind = where == EIS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // every host-side argument check before the first copy is queued (the caller's buffers are
+  // then never read after an error return)
+  if (n_cells && where == EIS_HOST)
+    for (long long m = 0; m < M; ++m)
+      if (n_cells[m] < 3 || n_cells[m] > cap) return fail(c, EIS_E_ARG, "set_state: n_cells out of range%s");
+  if (c->tiled) {
+    if ((c->tl.nbr_left || c->tl.nbr_right) && !c->tl.xbuf)
+      return fail(c, EIS_E_ORDER, "rank mode: eis_set_exchange_buffer before eis_set_state%s");
+    if (M == 1) {  // one grid: a misfit is an argument error (members get a status, k_to_tiles)
+      long long nn = c->grid.n_cells;
+      if (n_cells && where == EIS_HOST) nn = n_cells[0];
+      const long long lo_last = (long long)(c->tl.tpm - 1) * c->tile_cells;
+      if (nn - lo_last < HALO || nn - lo_last > c->tl.capt) return fail(c, EIS_E_ARG, "set_state: n_cells does not fit the tiling%s");
+    }
+  }
   if (M == 1 && where == EIS_HOST) {  // one grid from the host: only its live cells cross the link
     const long long nn = n_cells ? n_cells[0] : c->grid.n_cells;
     if (nn >= 3 && nn <= cap) bytes = (size_t)nn * 8;
@@ -696,10 +717,6 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   if (width) CU(cudaMemcpyAsync(c->d_h, width, bytes, kind, c->stream));
   else k_fill<<<grid_for(M * cap), 256, 0, c->stream>>>(c->d_h, M * cap, c->p.h_av);
   if (n_cells) {
-    if (where == EIS_HOST) {
-      for (long long m = 0; m < M; ++m)
-        if (n_cells[m] < 3 || n_cells[m] > cap) return fail(c, EIS_E_ARG, "set_state: n_cells out of range%s");
-    }
     CU(cudaMemcpyAsync(c->d_n, n_cells, M * 8, kind, c->stream));
   } else {
     k_fill_ll<<<grid_for(M), 256, 0, c->stream>>>(c->d_n, M, c->grid.n_cells);
@@ -713,14 +730,6 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   if (c->tiled) {
     k_tiles_reset<<<(unsigned)((M + 127) / 128), 128, 0, c->stream>>>(c->tl, c->d_status, t0);
     CU(cudaMemsetAsync(c->t_wlist, 0, (size_t)c->tl.ntiles * 16, c->stream));  // window ready tags
-    if ((c->tl.nbr_left || c->tl.nbr_right) && !c->tl.xbuf)
-      return fail(c, EIS_E_ORDER, "rank mode: eis_set_exchange_buffer before eis_set_state%s");
-    if (M == 1) {  // one grid: a misfit is an argument error (members get a status, k_to_tiles)
-      long long nn = c->grid.n_cells;
-      if (n_cells && where == EIS_HOST) nn = n_cells[0];
-      const long long lo_last = (long long)(c->tl.tpm - 1) * c->tile_cells;
-      if (nn - lo_last < HALO || nn - lo_last > c->tl.capt) return fail(c, EIS_E_ARG, "set_state: n_cells does not fit the tiling%s");
-    }
     k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0, c->tile_cells);
     tiled_init_dt<256><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, INFINITY);
     if (M > 1) tiled_members_finish<<<(unsigned)((M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, INFINITY, 0);
@@ -761,6 +770,7 @@ static eis_status collect_stats(eis_ctx* c, eis_stats* out) {
     out->iface_solves += s.iface_solves; out->creations += s.creations; out->splits += s.splits;
     out->merges += s.merges; out->regions += s.regions;
     out->dts_iter_max = std::max(out->dts_iter_max, (int64_t)s.dts_max);
+    out->decision_margin_warnings += s.margins;
     out->t_min = std::fmin(out->t_min, t[m]); out->t_max = std::fmax(out->t_max, t[m]);
     if (s.steps) out->dt_min = std::fmin(out->dt_min, s.dt_min);
     out->dt_max = std::fmax(out->dt_max, s.dt_max);
@@ -909,6 +919,13 @@ extern "C" eis_status eis_get_state(eis_ctx* c, double* rho, double* mom, double
   if (n_cells) CU(cudaMemcpyAsync(n_cells, c->d_n, M * 8, cudaMemcpyDeviceToHost, c->stream));
   if (t) CU(cudaMemcpyAsync(t, c->d_t, M * 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (ncopy < cells) {  // the contract's tail (include/eis.h): zeros and phase 255 past n_cells
+    const size_t tail = cells - ncopy;
+    if (rho) memset(rho + ncopy, 0, tail * 8);
+    if (mom) memset(mom + ncopy, 0, tail * 8);
+    if (width) memset(width + ncopy, 0, tail * 8);
+    if (phase) memset(phase + ncopy, 255, tail);
+  }
   return EIS_OK;
 }
 
@@ -979,6 +996,7 @@ extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
     o.steps = s.steps; o.cell_updates = s.cell_updates; o.dts_iters = s.dts_iters; o.iface_solves = s.iface_solves;
     o.creations = s.creations; o.splits = s.splits; o.merges = s.merges; o.regions = s.regions;
     o.t_min = o.t_max = t[m]; o.dt_min = s.dt_min; o.dt_max = s.dt_max; o.dts_iter_max = s.dts_max;
+    o.decision_margin_warnings = s.margins;
   }
   return EIS_OK;
 }

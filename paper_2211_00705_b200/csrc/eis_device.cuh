@@ -26,6 +26,7 @@ struct Eos {
 
 struct Prm {
   double cfl, eps_split, eps_tiny, theta_nb, tol_nb, tol_tiny, newton_rtol, newton_gtol, newton_stol, h_av;
+  double lin_gtol;  // quadratic-regime acceptance (R14d) only below this scaled residual; 0: off
   long long dts_max_iter;
   int newton_max_iter, armijo_max, mode;
 };
@@ -120,21 +121,33 @@ __device__ __forceinline__ void hll_fast(double a, double rl, double ml, double 
   F0 = f0; F1 = f1;
 }
 
+// Decision margins: a threshold decision is marginal when its test value
+// lies within MARGIN_ULPS times the rounding-error bound of its own evaluation; counted in
+// eis_stats.decision_margin_warnings, never used to decide anything.
+constexpr double MARGIN_EPS = 16.0 * 2.220446049250313e-16;
+__device__ __forceinline__ bool width_marginal(double h, double thr) { return fabs(h - thr) <= MARGIN_EPS * thr; }
+
 // Creation trigger, reading R7: liquid edge cavitates iff Phi(rho_min) > 0, vapour edge
 // nucleates iff Phi(rho_tilde) < 0, Phi(r) = f(r; r_L) + f(r; r_R) + du.  Exact pre-filters:
 // ln y >= 1 - 1/y gives Phi_liq(rho_min) <= du - a(1 - rho_min^2/(r_L r_R))... (no trigger when
 // du <= a_l (1 - rho_min^2/(r_L r_R)) for two rarefactions); nucleation needs du < 0.
-__device__ __forceinline__ bool creation_trigger(const Eos& e, int ph, double rl, double ul, double rr, double ur) {
+// marg: set when the test value Phi lies within its rounding-error bound of 0 (only reached past
+// the pre-filters, whose 1e-9 m/s margin is far above that bound)
+__device__ __forceinline__ bool creation_trigger(const Eos& e, int ph, double rl, double ul, double rr, double ur,
+                                                 bool& marg) {
   double du = ur - ul;
   if (ph == LIQ) {
     // pre-filter (exact, ln y <= y - 1): both rarefactions and du <= a_l (1 - rho_min^2/(r_L r_R)),
     // in product form with a 1e-9 m/s margin so rounding never hides a trigger
     const double x = rl * rr;
     if (rl >= e.rho_min && rr >= e.rho_min && du * x <= e.a_l * (x - e.rho_min * e.rho_min) - 1e-9 * x) return false;
-    return wave_f(e.a_l, e.rho_min, rl) + wave_f(e.a_l, e.rho_min, rr) + du > 0.0;
+  } else if (du >= 0.0) {
+    return false;
   }
-  if (du >= 0.0) return false;
-  return wave_f(e.a_v, e.rho_tilde, rl) + wave_f(e.a_v, e.rho_tilde, rr) + du < 0.0;
+  const double a = ph == LIQ ? e.a_l : e.a_v, thr = ph == LIQ ? e.rho_min : e.rho_tilde;
+  const double fl = wave_f(a, thr, rl), fr = wave_f(a, thr, rr), phi = fl + fr + du;
+  marg = fabs(phi) <= MARGIN_EPS * (fabs(fl) + fabs(fr) + fabs(ul) + fabs(ur));
+  return ph == LIQ ? phi > 0.0 : phi < 0.0;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -260,13 +273,16 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
   for (int it = 0; it < p.newton_max_iter; ++it) {
     const double det = J[0] * J[3] - J[1] * J[2];
     if (!(fabs(det) > 0.0) || !isfinite(det)) return -1;
+    // R14d needs a well-conditioned Jacobian (the O(|d|^2) constant grows like 1/|det|): no
+    // shortcut when det has cancelled to below 1e-8 of its terms
+    const bool wellc = fabs(det) >= 1e-8 * (fabs(J[0] * J[3]) + fabs(J[1] * J[2]));
     const double idet = __drcp_rn(det);
     const double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
     const double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
-    // quadratic regime (LIN, reading R14d): a residual already <= 1e-6 whose Newton step is
+    // quadratic regime (LIN, reading R14d): a residual already <= sqrt(gtol) whose Newton step is
     // within sqrt(rtol) of the iterate puts x + d within ~|d|^2 <= rtol of the root: accept it
     // without another evaluation, the auxiliary values to first order (error O(|d|^2))
-    if (LIN && fmax(fabs(G[0]), fabs(G[1])) <= 1e-6 && fabs(d0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
+    if (LIN && wellc && fmax(fabs(G[0]), fabs(G[1])) <= p.lin_gtol && fabs(d0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
         fabs(d1) <= p.newton_stol * fmax(fabs(x1), e.p0)) {
       aux[0] += da[0] * d0 + da[1] * d1;
       aux[1] += da[2] * d0 + da[3] * d1;

@@ -66,6 +66,7 @@ struct MemberStats {
   long long steps, cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
   double dt_min, dt_max;
   long long dts_max;
+  long long margins;  // decision_margin_warnings (eis.h): decisions within their rounding-error bound
 };
 
 struct Members {  // global (HBM) state, member-major SoA
@@ -94,7 +95,7 @@ struct CtaShared {
   int pf_j, pf_k, pf_wa, pf_wb;  // tiles: the next window job, claimed during the current one
   int fbits;     // tiles: phase bits of the smem grid (fast-path test)
   int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
-  unsigned long long c_dts, c_solves, c_regions, c_dtsmax;
+  unsigned long long c_dts, c_solves, c_regions, c_dtsmax, c_margin;
   MemberStats st;
 #ifdef EIS_PHASE_CLOCK
   long long tclk[10];  // development: clock64 at phase boundaries of the last step (thread 0)
@@ -166,10 +167,11 @@ __device__ __forceinline__ bool region_at(const Eos& e, const Prm& p, const doub
 // moving-cell update: h^{n+1} = h + (wR - wL) dt, U^{n+1} = (h/h^{n+1}) U - (dt/h^{n+1}) dF
 __device__ __forceinline__ int cell_update(double* rho, double* mom, double* h, int i, double FL0, double FL1,
                                            double wL, double FR0, double FR1, double wR, double dt, const Prm& p,
-                                           int& remesh) {
+                                           int& remesh, int& marg) {
   const double hn = h[i];
   const double hn1 = __dadd_rn(hn, __dmul_rn(wR - wL, dt));  // no contraction: the oracle's roundings
   if (!(hn1 > 0.0)) return ST_WIDTH;
+  if (hn1 != hn && (width_marginal(hn1, p.eps_tiny * p.h_av) || width_marginal(hn1, p.eps_split * p.h_av))) marg = 1;
   const double q = hn / hn1, c = dt / hn1;
   rho[i] = q * rho[i] - c * (FR0 - FL0);
   mom[i] = q * mom[i] - c * (FR1 - FL1);
@@ -218,7 +220,7 @@ __device__ __forceinline__ int remesh_shift(const CtaShared& sh, int ntrg, int i
 // ------------------------------------------------------------------------------------------
 __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
                                       const double* F0, const double* F1, const uint8_t* fl, int a, int b, double dt,
-                                      long long& it_out, long long& solves, int& remesh) {
+                                      long long& it_out, long long& solves, int& remesh, int& marg) {
   const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   const int K = b - a + 1;
@@ -267,6 +269,7 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
   __syncwarp();
   long long l = 0;
   int err = 0;
+  bool prev_cont_robust = true;  // decision margin of the last "continue"
 #ifdef EIS_DTS_CLOCK
   long long dc0 = clock64();
   if (lane == 0) sh.dclk[3] += 1;
@@ -300,22 +303,33 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       { const long long c = clock64(); if (lane == 0) sh.dclk[0] += c - dc0; dc0 = c; }
 #endif
       if (err || part == 1) break;
-      bool conv = true;  // (b) relaxed moving-cell update (R13) and this lane's residual
+      bool conv = true, rstop = true, rcont = false;  // (b) relaxed moving-cell update (R13) and this lane's residual
       int bad = 0;
       if (lane < K) {
         const double hl_ = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
         if (!(hl_ > 0.0)) bad = ST_WIDTH;
         const double ih = 1.0 / hl_, a0 = hn * ih, a1 = dt * ih;
-        const double n0 = w0 * i1r + qr * (a0 * rn0 - a1 * (Fe0[lane + 1] - Fe0[lane]));
-        const double n1 = w1 * i1r + qr * (a0 * rn1 - a1 * (Fe1[lane + 1] - Fe1[lane]));
+        const double fL0 = Fe0[lane], fR0 = Fe0[lane + 1], fL1 = Fe1[lane], fR1 = Fe1[lane + 1];
+        const double n0 = w0 * i1r + qr * (a0 * rn0 - a1 * (fR0 - fL0));
+        const double n1 = w1 * i1r + qr * (a0 * rn1 - a1 * (fR1 - fL1));
         // res = |(1 + r)(W^{l+1} - W^l)| / (dtau max(|W^l|, 1)) < tol, multiplied out (no division)
-        conv = fabs(rsc * (n0 - w0)) < tol_l * fmax(fabs(w0), 1.0) &&
-               fabs(rsc * (n1 - w1)) < tol_l * fmax(fabs(w1), 1.0);
+        const double d0 = fabs(rsc * (n0 - w0)), d1 = fabs(rsc * (n1 - w1));
+        const double t0 = tol_l * fmax(fabs(w0), 1.0), t1 = tol_l * fmax(fabs(w1), 1.0);
+        conv = d0 < t0 && d1 < t1;
+        // decision margins: the rounding-error bound of W^{l+1} - W^l on the residual's scale
+        const double e0 = MARGIN_EPS * rsc * (fabs(w0) + qr * (fabs(a0 * rn0) + a1 * (fabs(fL0) + fabs(fR0))));
+        const double e1 = MARGIN_EPS * rsc * (fabs(w1) + qr * (fabs(a0 * rn1) + a1 * (fabs(fL1) + fabs(fR1))));
+        rstop = d0 < t0 - e0 && d1 < t1 - e1;
+        rcont = d0 >= t0 + e0 || d1 >= t1 + e1;
         w0 = n0; w1 = n1;
         if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
       }
       // max over tiny cells < tol_tiny and over the others < tol_nb  <=>  every lane below its own
       conv = __all_sync(0xffffffffu, conv);
+      rstop = __all_sync(0xffffffffu, rstop);
+      rcont = __any_sync(0xffffffffu, rcont);
+      if (conv && (!rstop || !prev_cont_robust)) marg += 1;
+      prev_cont_robust = rcont;
       bad = __reduce_max_sync(0xffffffffu, bad);
       if (lane < K) { W0[lane] = w0; W1[lane] = w1; Wu[lane] = w1 / w0; }
       __syncwarp();
@@ -328,16 +342,19 @@ __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh,
       if (l >= p.dts_max_iter) { err = ST_DTS_CAP; break; }
     }
   }
+  bool wm = false;  // width decision margin of this lane's cell
   if (!err && lane < K) {  // Part 2 (b): conservative update with F_left, F*, F_right
     const double hn1 = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
     if (!(hn1 > 0.0)) err = ST_WIDTH;
     else {
+      wm = hn1 != hn && (width_marginal(hn1, p.eps_tiny * p.h_av) || width_marginal(hn1, p.eps_split * p.h_av));
       rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
       mom[a + lane] = (hn / hn1) * rn1 - (dt / hn1) * (Fe1[lane + 1] - Fe1[lane]);
       h[a + lane] = hn1;
       if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
     }
   }
+  marg += __popc(__ballot_sync(0xffffffffu, wm));
   if (lane >= 1 && lane < K && !err) {  // keep the converged boundary states for the next step
     Ifc* s = const_cast<Ifc*>(find_ifc(sh, a + lane));
     if (s) { s->pV = xs0[lane]; s->pL = xs1[lane]; }
@@ -879,11 +896,13 @@ __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShar
         const int pl = phase_of(e, rl);
         if (pl == pc && pc != SPIN) {
           const double uc = mom[cj] / rc, ul = mom[cj - 1] / rl;
-          if (cj - 1 >= Z.zlo && cj < Z.zhi && creation_trigger(e, pc, rl, ul, rc, uc) &&
-              !region_at(e, p_ref, rho, h, n, cj - 1) && !region_at(e, p_ref, rho, h, n, cj)) {  // R16
+          bool marg = false;
+          if (cj - 1 >= Z.zlo && cj < Z.zhi && !region_at(e, p_ref, rho, h, n, cj - 1) &&
+              !region_at(e, p_ref, rho, h, n, cj) && creation_trigger(e, pc, rl, ul, rc, uc, marg)) {  // R16
             const int k = atomicAdd(&sh.ntrg, 1);
             if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
           }
+          if (marg && Z.own_lo < cj && cj <= Z.own_hi) atomicAdd(&sh.c_margin, 1ull);  // owned edge
         } else if (pl != pc && !(fl[cj] & F_IF)) {
           zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
         }
@@ -1056,14 +1075,18 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         if (b < Z.zlo || a >= Z.zhi) continue;  // tiles: a block wholly in the halo is not needed
         if (b - a + 1 > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
         long long it = 0, sv = 0;
+        int mg = 0;
         const int err = p.mode == 2   ? lts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, smax_step, it, sv, remesh)
 #ifndef EIS_NO_NEWTON
                         : p.mode == 3 ? newton_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh)
 #endif
-                                      : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh);
+                                      : dts_block(e, p, sh, rho, mom, h, F0, F1, fl, a, b, dt, it, sv, remesh, mg);
         if (err && lane == 0) set_status(sh, err);
         if (a >= Z.own_lo && a < Z.own_hi) {  // count a block once (its first cell's owner)
-          if (lane == 0) { atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); atomicMax(&sh.c_dtsmax, (unsigned long long)it); }
+          if (lane == 0) {
+            atomicAdd(&sh.c_dts, (unsigned long long)it); atomicAdd(&sh.c_regions, 1ull); atomicMax(&sh.c_dtsmax, (unsigned long long)it);
+            if (mg) atomicAdd(&sh.c_margin, (unsigned long long)mg);
+          }
           if (hl == 0 && sv) atomicAdd(&sh.c_solves, (unsigned long long)sv);
         }
       }
@@ -1083,8 +1106,10 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         double a0, a1, wa, b0, b1, wb;
         edge_view(sh, fl, F0, F1, i, 1, a0, a1, wa);
         edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
-        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, remesh);
+        int mg = 0;
+        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, remesh, mg);
         if (err) zone_status(sh, Z, i, err);
+        if (mg && i >= Z.own_lo && i < Z.own_hi) atomicAdd(&sh.c_margin, 1ull);
       }
       for (int k = lane; k < nif; k += 32) { sh.ws0[k] = sh.ifc[k].pV; sh.ws1[k] = sh.ifc[k].pL; }
       if (lane == 0) sh.wsn = nif;
@@ -1127,9 +1152,10 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
         double a0, a1, wa, b0, b1, wb;
         edge_view(sh, fl, F0, F1, i, 1, a0, a1, wa);
         edge_view(sh, fl, F0, F1, i + 1, 0, b0, b1, wb);
-        int rm = 0;
-        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, rm);
+        int rm = 0, mg = 0;
+        const int err = cell_update(rho, mom, h, i, a0, a1, wa, b0, b1, wb, dt, p, rm, mg);
         if (err) zone_status(sh, Z, i, err);
+        if (mg && i >= Z.own_lo && i < Z.own_hi) atomicAdd(&sh.c_margin, 1ull);
       }
       if (tid == 0) sh.remesh = 1;
       __syncthreads();
@@ -1303,7 +1329,7 @@ __device__ __forceinline__ Arr carve(unsigned char* smem_raw, int C) {
 __device__ __forceinline__ void reset_counters(CtaShared& sh) {
   sh.wsn = -1; sh.nblk = 0; sh.ntrg = 0; sh.remesh = 0;
   sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
-  sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0; sh.c_dtsmax = 0;
+  sh.c_dts = 0; sh.c_solves = 0; sh.c_regions = 0; sh.c_dtsmax = 0; sh.c_margin = 0;
   sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
 }
 
@@ -1368,6 +1394,7 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
     st.dts_iters += (long long)sh.c_dts;
     st.iface_solves += (long long)sh.c_solves;
     st.regions += (long long)sh.c_regions;
+    st.margins += (long long)sh.c_margin;
     if ((long long)sh.c_dtsmax > st.dts_max) st.dts_max = (long long)sh.c_dtsmax;
     g.n[m] = n;
     g.t[m] = t;

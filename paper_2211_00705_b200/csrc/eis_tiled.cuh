@@ -28,6 +28,7 @@ constexpr int HALO = 10;  // halo cells per side: >= MAXB + 2 keeps every needed
 struct TileStats {
   long long cell_updates, dts_iters, iface_solves, creations, splits, merges, regions;
   long long dts_max, full_steps, win_steps;  // steps this tile took the whole-tile / window full step
+  long long margins;                         // decision_margin_warnings (eis.h)
 };
 
 struct Tiles {
@@ -539,6 +540,7 @@ __device__ __forceinline__ void tstats_add(const Tiles& tl, int k, long long cel
   add(&ts.dts_iters, (long long)sh.c_dts);
   add(&ts.iface_solves, (long long)sh.c_solves);
   add(&ts.regions, (long long)sh.c_regions);
+  add(&ts.margins, (long long)sh.c_margin);
   if (sh.c_dtsmax) atomicMax(reinterpret_cast<unsigned long long*>(&ts.dts_max), (unsigned long long)sh.c_dtsmax);
   add(window ? &ts.win_steps : &ts.full_steps, 1);
   add(&ts.creations, sh.st.creations);  // owned events only (step_body)

@@ -1,8 +1,15 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
 inputs.  Tolerance (BASELINE north_star): relative L1 <= 1e-9 on rho and rho*u per member
 (sum_i h_i |U_gpu - U_orc| / sum_i h_i |U_orc|), equal live-cell counts, statuses and event
-counts, interface positions within 1e-9 h_av.  Discrete decisions (creation, merge, split,
-tiny, DTS stop) must coincide, which the equal counts check."""
+counts, interface positions within 1e-9 h_av; element-wise, every cell's content h U within
+1e-10 of a full cell's content h_av max(|U|, 1) (R32).  Discrete decisions
+(creation, merge, split, tiny, DTS stop) must coincide: per member the DTS iteration and
+boundary-solve counts are equal, except in a member where either side logged a decision-margin
+warning (a decision within the rounding-error bound of its own test);
+every such accepted mismatch is tallied in gpurun_out/decision_parity.json."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -14,6 +21,23 @@ pytestmark = pytest.mark.gpu
 from paper_2211_00705_b200 import workloads as W  # noqa: E402
 
 TOL = 1e-9
+EL_TOL = 1e-10  # element-wise, on cell contents (R32)
+REPORT = {}     # test -> decision-parity tallies (written at the end of the session)
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _decision_report():
+    yield
+    if REPORT:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(root, "gpurun_out", "decision_parity.json"), "w") as f:
+            json.dump(REPORT, f, indent=1, sort_keys=True)
+
+
+def _tally(name, key, n=1):
+    d = REPORT.setdefault(name, {})
+    d[key] = d.get(key, 0) + n
 
 
 @pytest.fixture(scope="module")
@@ -54,7 +78,19 @@ def oracle_run(oracle_mod, w, steps=None, t_end=None, n_cells=None):
     return o
 
 
-def assert_parity(g, o, h_av, counts=("creations", "splits", "merges", "regions"), dts_exact=False):
+def _caller():
+    import inspect
+    for f in inspect.stack()[2:]:
+        if f.function.startswith("test_"):
+            return f.function
+    return "?"
+
+
+def assert_parity(g, o, h_av, counts=("creations", "splits", "merges", "regions"), name=None):
+    """Member by member: statuses, live counts, relative L1 (north_star), element-wise contents
+    (R32), event counts, DTS iteration and boundary-solve counts (decision parity: a difference
+    only where a decision-margin warning was logged), times, interfaces."""
+    name = name or _caller()
     M = len(o["n"])
     np.testing.assert_array_equal(g["status"], o["status"])
     np.testing.assert_array_equal(g["n"], o["n"])
@@ -64,16 +100,27 @@ def assert_parity(g, o, h_av, counts=("creations", "splits", "merges", "regions"
             den = np.sum(o["h"][m, :n] * np.abs(o[k][m, :n]))
             err = np.sum(o["h"][m, :n] * np.abs(g[k][m, :n] - o[k][m, :n])) / den
             assert err <= TOL, (m, k, err)
+            # element-wise (R32): the cell content h U against a full cell's, so a tiny cell's
+            # state -- fixed by Algorithm 2 only to its stop tolerance -- is weighted by
+            # its width; every other cell is held to 1e-10 relative (max(|U|, 1) for rho u ~ 0)
+            el = o["h"][m, :n] * np.abs(g[k][m, :n] - o[k][m, :n]) / (h_av * np.maximum(np.abs(o[k][m, :n]), 1.0))
+            assert el.max() <= EL_TOL, (m, k, float(el.max()), int(el.argmax()))
         gs, os_ = g["mstats"][m], o["mstats"][m]
+        flagged = gs.get("decision_margin_warnings", 0) + os_.get("decision_margin_warnings", 0) > 0
+        _tally(name, "members")
+        if flagged:
+            _tally(name, "members_with_margin_warnings")
         assert gs["steps"] == os_["steps"] and gs["creations"] == os_["creations"], m
-        # A split/merge decision can flip at an exact threshold tie (h == 2 h_av to the last bit
-        # on one side, 1 ulp above on the other; seen once in 6 x 2000 C3 member-steps): the
-        # mesh then differs for a few steps and the totals by at most one event per tie.
+        # event counts: equal, or at most one apart where a decision was marginal (a split at
+        # h == 2 h_av to the last bit on one side and 1 ulp above on the other)
         for c in counts:
-            assert abs(gs[c] - os_[c]) <= 1, (m, c, gs[c], os_[c])
+            assert gs[c] == os_[c] or (flagged and abs(gs[c] - os_[c]) <= 1), (m, c, gs[c], os_[c])
+        # decision parity: the same DTS stop decisions unless one was marginal
+        for c in ("dts_iters", "iface_solves"):
+            if gs[c] != os_[c]:
+                assert flagged, ("unflagged decision mismatch", m, c, gs[c], os_[c])
+                _tally(name, c + "_mismatch_flagged")
         assert abs(gs["cell_updates"] - os_["cell_updates"]) <= 1e-5 * os_["cell_updates"], m
-        if dts_exact:
-            assert gs["dts_iters"] == os_["dts_iters"], m
         np.testing.assert_allclose(g["t"][m], o["t"][m], rtol=1e-12)
     assert len(g["ifc"]) == len(o["ifc"])
     for a, b in zip(g["ifc"], o["ifc"]):
@@ -91,8 +138,9 @@ def test_c1_two_phase_riemann(P, oracle_mod):
     w = W.c1()
     g, _ = gpu_run(P, w, t_end=w["t_end"])
     o = oracle_run(oracle_mod, w, t_end=w["t_end"])
-    assert_parity(g, o, h_av(w), dts_exact=True)
+    assert_parity(g, o, h_av(w))
     assert o["stats"]["iface_solves"] == g["stats"]["iface_solves"]
+    assert o["stats"]["dts_iters"] == g["stats"]["dts_iters"] == 0
 
 
 @pytest.mark.parametrize("mode", [W.MODE_SPLIT, W.MODE_EXPLICIT])
@@ -698,3 +746,178 @@ def test_interface_report_against_oracle(P, oracle_mod):
             assert a[k] == pytest.approx(b[k], rel=1e-9), k
         for k in ("w", "z"):
             assert a[k] == pytest.approx(b[k], rel=1e-7, abs=1e-9), k
+
+
+# ------------------------------------------------------------------------------ decision parity
+def _e3_case():
+    return _e3_workload()[1], None, 0, 0
+
+
+ONE_STEP = {
+    "C2": (lambda: (W.c2(), 150, 0, 0)),
+    "C3": (lambda: (W.c3(members=np.array([0, 1, 2, 3, 17, 100, 4097, 30000, 65535])), 300, 0, 0)),
+    "C4": (lambda: (W.c4(members=np.arange(16)), 300, 0, 0)),
+    "C5": (lambda: (W.c5(n_cells=1 << 16), 200, 2, 1024)),
+    "E2": (lambda: (_e2_workload(0)[1], 166, 0, 0)),
+    "E3": (lambda: (_e3_workload()[1], 146, 0, 0)),
+}
+
+
+@pytest.mark.parametrize("case", list(ONE_STEP))
+def test_decision_parity_one_step(P, oracle_mod, case):
+    """Every large step from the SAME state: before each step the GPU context is set to the
+    oracle's current state (widths included), both take one step, and per member the DTS
+    iteration, boundary-solve, region and creation counts of that step must be equal -- unless
+    either side logged a decision-margin warning in that step (a DTS stop within the rounding
+    bound of its residual test).  Starting from identical inputs, no earlier
+    divergence can excuse a later mismatch.  The new states agree element-wise (R32)."""
+    w, K, layout, tile = ONE_STEP[case]()
+    s = oracle_mod.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"])
+    s.set_state(w["rho"], w["mom"])
+    ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=layout, tile_cells=tile)
+    M = w["M"]
+    hav = h_av(w)
+    keys = ("dts_iters", "iface_solves", "regions", "creations", "decision_margin_warnings")
+    prev = [dict.fromkeys(keys, 0) for _ in range(M)]
+    name = f"one_step[{case}]"
+    for step in range(K):
+        o = s.get_state()
+        ctx.set_state(o["rho"], o["mom"], width=o["h"], n_cells=o["n"].astype(np.int64))
+        ctx.step(1)
+        s.step(1)
+        gms = ctx.member_stats()
+        g = ctx.get_state()
+        o2 = s.get_state()
+        np.testing.assert_array_equal(ctx.member_status(), s.member_status())
+        np.testing.assert_array_equal(g["n"], o2["n"])
+        for m in range(M):
+            om = s.member_stats(m)
+            d_o = {k: om[k] - prev[m][k] for k in keys}
+            prev[m] = {k: om[k] for k in keys}
+            d_g = {k: gms[m][k] for k in keys}  # set_state restarts the GPU counters
+            flagged = d_o["decision_margin_warnings"] + d_g["decision_margin_warnings"] > 0
+            _tally(name, "member_steps")
+            _tally(name, "margin_warnings_gpu", d_g["decision_margin_warnings"])
+            _tally(name, "margin_warnings_oracle", d_o["decision_margin_warnings"])
+            assert d_g["creations"] == d_o["creations"] and d_g["regions"] == d_o["regions"], (step, m)
+            for c in ("dts_iters", "iface_solves"):
+                if d_g[c] != d_o[c]:
+                    assert flagged, ("unflagged decision mismatch", step, m, c, d_g[c], d_o[c])
+                    _tally(name, c + "_mismatch_flagged")
+            n = int(o2["n"][m])
+            for k in ("rho", "mom"):
+                el = o2["h"][m, :n] * np.abs(g[k][m, :n] - o2[k][m, :n]) / (hav * np.maximum(np.abs(o2[k][m, :n]), 1.0))
+                assert el.max() <= EL_TOL, (step, m, k, float(el.max()))
+
+
+def test_c5_full_size_prefix_elementwise(P, oracle_mod):
+    """BASELINE configs[4] at full size in the bench launch configuration (2^27 cells, 1400-cell
+    tiles, the driver's 20 timed steps from t = 0) against the oracle run on the first 2^20
+    cells (256 whole segments): waves cross fewer than 20 cells per 20 steps, so cells
+    [0, 2^20 - 600) of the full grid see nothing of the prefix's transmissive right end and
+    must agree with the oracle element by element (R32) with the same events (creations and
+    merges left of the cut shift both index ranges alike)."""
+    steps, S = 20, 1 << 20
+    w = W.c5()
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=1400)
+    ctx.set_state(torch.from_numpy(w["rho"]).cuda(), torch.from_numpy(w["mom"]).cuda())
+    st = ctx.step(steps, stats=True)
+    assert ctx.member_status()[0] == 0
+    g = ctx.get_state()
+    del w
+    wp = W.c5(n_cells=S)
+    sim = oracle_mod.Sim(wp["eos"], wp["params"], 1, wp["N"], wp["cap"], wp["x_left"], wp["x_right"])
+    sim.set_state(wp["rho"], wp["mom"])
+    so = sim.step(steps)
+    o = sim.get_state()
+    cut = S - 600
+    hav = h_av(wp)
+    assert abs(int(g["n"][0]) - int(o["n"][0])) < 1 << 27  # (different grids: live counts differ)
+    for k in ("rho", "mom", "h"):
+        a, b = g[k][0, :cut], o[k][0, :cut]
+        el = o["h"][0, :cut] * np.abs(a - b) / (hav * np.maximum(np.abs(b), 1.0)) if k != "h" else np.abs(a - b) / hav
+        assert el.max() <= EL_TOL, (k, float(el.max()), int(el.argmax()))
+    # the prefix's events all happened left of the cut except near its right end: the GPU grid
+    # has at least as many creations as the oracle's prefix, and the first cut cells' phases match
+    assert st["creations"] >= so["creations"] > 0
+    rt = oracle_mod.thresholds(W.EOS_293K)["rho_tilde"]
+    assert np.array_equal(g["rho"][0, :cut] <= rt, o["rho"][0, :cut] <= rt)
+
+
+# ------------------------------------------------------------------------------ R11, fault injection
+def _two_bubbles(M=1):
+    """Two tiny vapour cells separated by ONE liquid cell (R11): the regions {k-1, k, k+1} and
+    {k+1, k+2, k+3} overlap at k+1 and merge into one K = 5 block.  Liquid and vapour near
+    mechanical equilibrium, at rest; phase transfer moves the boundaries slowly."""
+    N, cap = 200, 232
+    h_av = 1.0 / N
+    rV = 0.02
+    pV = W.EOS_293K["a_v2"] * rV
+    rL = W.EOS_293K["rho0"] + (pV - W.EOS_293K["p0"]) / W.EOS_293K["a_l"] ** 2
+    rho = np.full((M, cap), 0.0); mom = np.zeros((M, cap)); h = np.zeros((M, cap))
+    rho[:, :N] = rL
+    h[:, :N] = h_av
+    k = 100
+    for m in range(M):
+        rho[m, k] = rho[m, k + 2] = rV
+        h[m, k] = h[m, k + 2] = 0.2 * h_av
+        h[m, k + 1] = 0.8 * h_av  # (a liquid cell between the bubbles, not tiny)
+        mom[m, :N] = rho[m, :N] * (3.0 * np.sin(np.arange(N) * (m + 1)))  # a little motion
+    return dict(eos=W.EOS_293K, params=W.PARAMS, M=M, N=N, cap=cap, x_left=0.0, x_right=1.0,
+                rho=rho, mom=mom, h=h)
+
+
+@pytest.mark.parametrize("layout", [1, 2])
+def test_overlapping_regions_block_k5(P, oracle_mod, layout):
+    """R11: two tiny cells sharing a neighbour form one K = 5 implicit block, iterated with each
+    cell's own dtau_i; GPU (member-resident and tiled) against the oracle."""
+    w = _two_bubbles(M=2)
+    ctx = P.Context(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=layout, tile_cells=100 if layout == 2 else 0)
+    ctx.set_state(w["rho"], w["mom"], width=w["h"])
+    st = ctx.step(30, stats=True)
+    g = ctx.get_state(); g["status"] = ctx.member_status(); g["ifc"] = ctx.interfaces(); g["mstats"] = ctx.member_stats()
+    s = oracle_mod.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"])
+    s.set_state(w["rho"], w["mom"], width=w["h"])
+    so = s.step(30)
+    o = s.get_state(); o["status"] = s.member_status(); o["ifc"] = s.interfaces()
+    o["mstats"] = [s.member_stats(m) for m in range(w["M"])]
+    assert so["regions"] > 0 and so["dts_iters"] > 0
+    assert_parity(g, o, h_av(w))
+    assert st["dts_iters"] == so["dts_iters"] or st["decision_margin_warnings"] + so["decision_margin_warnings"] > 0
+
+
+def test_newton_failure_freezes_only_its_member(P, oracle_mod):
+    """EIS_E_NEWTON: with one Newton iteration allowed, the phase-boundary solve of
+    member 0 (C1's liquid | vapour interface) cannot converge: member 0 stops with that status
+    at its first step, member 1 (single-phase, no boundary) keeps stepping, on both sides."""
+    w = W.c1()
+    prm = dict(w["params"], newton_max_iter=1)
+    rho = np.vstack([w["rho"], np.where(w["rho"] > 0, 1000.0, 0.0)])
+    mom = np.vstack([w["mom"], np.where(w["rho"] > 0, 1000.0 * 3.0, 0.0)])
+    ww = dict(w, params=prm, M=2, rho=rho, mom=mom)
+    g, _ = gpu_run(P, ww, steps=10)
+    o = oracle_run(oracle_mod, ww, steps=10)
+    assert list(g["status"]) == list(o["status"]) == [5, 0]
+    assert g["mstats"][1]["steps"] == o["mstats"][1]["steps"] == 10
+    assert g["mstats"][0]["steps"] == o["mstats"][0]["steps"] == 0
+    np.testing.assert_array_equal(g["rho"][1], o["rho"][1])
+
+
+def test_dts_cap_freezes_only_its_member(P, oracle_mod):
+    """EIS_E_DTS_CAP: with l_max = 2 the implicit region of the cavitating member
+    (C2's bubble, which needs more pseudo-time iterations) hits the cap and freezes; the
+    constant-state member keeps stepping, on both sides."""
+    w = W.c2()
+    prm = dict(w["params"], dts_max_iter=2)
+    rho = np.vstack([w["rho"], w["rho"]])
+    mom = np.vstack([w["mom"], np.zeros_like(w["mom"])])
+    ww = dict(w, params=prm, M=2, rho=rho, mom=mom)
+    g, _ = gpu_run(P, ww, steps=40)
+    o = oracle_run(oracle_mod, ww, steps=40)
+    assert list(g["status"]) == list(o["status"]) == [7, 0]
+    assert g["mstats"][1]["steps"] == o["mstats"][1]["steps"] == 40
+    assert g["mstats"][0]["steps"] == o["mstats"][0]["steps"]
+    np.testing.assert_array_equal(g["rho"][1], o["rho"][1])

@@ -75,7 +75,17 @@ def test_nucleation_star_state(oracle_mod, eos):
     assert c["w_r"] == pytest.approx(g["w"], abs=1e-6)
 
 
-def _run_363K(oracle_mod, eos, kind):
+_RUNS = {}
+
+
+def _run_363K(oracle_mod, eos, kind, mode=0):
+    """The paper's 363.15 K run (cached: the nucleation run takes seconds)."""
+    if (kind, mode) not in _RUNS:
+        _RUNS[(kind, mode)] = _run_363K_fresh(oracle_mod, eos, kind, mode)
+    return _RUNS[(kind, mode)]
+
+
+def _run_363K_fresh(oracle_mod, eos, kind, mode):
     g = read_golden("cavitation_363K.txt" if kind == "cav" else "nucleation_363K.txt")
     N, cap = 400, 416
     if kind == "cav":
@@ -86,6 +96,7 @@ def _run_363K(oracle_mod, eos, kind):
         uL = g["u_init"]
     prm = dict(W.PARAMS)
     prm["cfl"] = 0.5  # P:1233 / P:1367
+    prm["mode"] = mode
     s = oracle_mod.Sim(eos, prm, 1, N, cap, -2.0, 2.0)  # h0 = 1e-2 on [-2, 2]
     rho = np.zeros((1, cap))
     mom = np.zeros((1, cap))
@@ -150,3 +161,45 @@ def test_interface_report_nucleation(oracle_mod, eos):
         assert i["w"] == pytest.approx(sign * g["w"], rel=2e-2)
         assert i["p_vap"] == pytest.approx(g["p_V_star"], rel=1e-6)
         assert i["p_liq"] == pytest.approx(g["p_L_star"], rel=1e-6)
+
+
+def test_cavitation_dts_local_iterations(oracle_mod, eos):
+    """Alg. 2's stop rule and residual against the paper's count of local
+    iterations for the cavitation test: 355 DTS iterations over the 166 large steps
+    (tab:comp_costs_2); the oracle gives 335.  Mistakes in the loop move the total by
+    more than 10 % (measured with this oracle: theta_nb 0.5 instead of 0.9 -> 429; tol_nb 1e-4
+    instead of 1e-3 -> 405; the two tolerances swapped -> 286).  Every stop decision of this run
+    is clear of its rounding floor (no decision-margin warning), so the count is a property of
+    the method, not of the arithmetic."""
+    g, s, st = _run_363K(oracle_mod, eos, "cav")
+    assert st["steps"] == int(g["large_steps"])
+    assert st["dts_iters"] == pytest.approx(g["dts_local_iterations"], rel=0.10)
+    assert st["decision_margin_warnings"] == 0
+
+
+@pytest.mark.slow
+def test_nucleation_dts_local_iterations_rounding_regime(oracle_mod, eos):
+    """The nucleation test's count (tab:comp_costs_3: 1,367,460 DTS iterations over 143
+    steps) sits in the regime the paper warns about (with dtau_k ~ 6e-12 "only few
+    meaningful digits" remain).  Pinned two ways (reading R28): the total is within a factor 3
+    of the printed one, and the oracle's own decision-margin accounting flags the DTS stop of
+    (nearly) every large step as lying within the rounding-error bound of its residual test,
+    which is why no tighter agreement with the printed count can be expected from any fp64
+    implementation."""
+    g, s, st = _run_363K(oracle_mod, eos, "nuc")
+    assert s.member_status()[0] == 0
+    ratio = st["dts_iters"] / g["dts_local_iterations"]
+    assert 1 / 3 <= ratio <= 3, ratio
+    assert st["decision_margin_warnings"] >= 0.8 * st["regions"], (st["decision_margin_warnings"], st["regions"])
+
+
+def test_a_l_363K_back_derivation_reproduces_the_committed_value():
+    """tests/golden/derive_a_l_363K.py (oracle only) reproduces the committed a_l from the
+    printed created width h_V."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "derive_a_l_363K", os.path.join(os.path.dirname(__file__), "golden", "derive_a_l_363K.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.derive() == pytest.approx(read_golden("eos_363K.txt")["a_l"], abs=5e-5)

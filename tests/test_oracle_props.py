@@ -321,7 +321,7 @@ def test_conservation_through_creation_and_dts(oracle_mod, mode):
     assert s.member_status()[0] == 0
 
 
-def _e2_run(oracle_mod, mode, t_end=5e-4, steps=None):
+def _e2_run(oracle_mod, mode, t_end=5e-4, steps=None, **over):
     from conftest import eos_363K, read_golden
     eos = eos_363K()
     g = read_golden("cavitation_363K.txt")
@@ -330,6 +330,7 @@ def _e2_run(oracle_mod, mode, t_end=5e-4, steps=None):
     prm = dict(PRM)
     prm["cfl"] = 0.5
     prm["mode"] = mode
+    prm.update(over)  # a copy: the shared W.PARAMS is never modified
     s = oracle_mod.Sim(eos, prm, 1, N, cap, -2.0, 2.0)
     rho = np.zeros((1, cap)); mom = np.zeros((1, cap))
     rho[0, :N] = r
@@ -388,6 +389,8 @@ def test_lts_substeps_follow_the_fine_cfl(oracle_mod):
         s.step(1)
         assert s.member_stats(0)["dts_iters"] - before == 2 ** n0
 
+
+def test_split_equals_explicit_without_tiny_cells(oracle_mod):
     """Mode degeneracy (SPEC S:592): with no tiny cell Algorithm 1 is the explicit scheme."""
     w = W.c1()
     outs = []
@@ -459,13 +462,7 @@ def test_single_phase_rarefaction_convergence(oracle_mod, N):
 
 
 def _e2_with(oracle_mod, mode, **prm):
-    old = dict(PRM)
-    PRM.update(prm)
-    try:
-        return _e2_run(oracle_mod, mode)
-    finally:
-        PRM.clear()
-        PRM.update(old)
+    return _e2_run(oracle_mod, mode, **prm)
 
 
 def test_newton_mode_is_the_fixed_point_of_dts(oracle_mod):
@@ -494,13 +491,7 @@ def test_newton_mode_nucleation_e3(oracle_mod):
     from conftest import eos_363K, read_golden
     from test_oracle_pins import _run_363K
     eos = eos_363K()
-    old = dict(W.PARAMS)
-    W.PARAMS["mode"] = 3
-    try:
-        g, s, st = _run_363K(oracle_mod, eos, "nuc")
-    finally:
-        W.PARAMS.clear()
-        W.PARAMS.update(old)
+    g, s, st = _run_363K(oracle_mod, eos, "nuc", mode=3)
     assert s.member_status()[0] == 0
     xs = [i["x"] for i in s.interfaces()]
     assert xs[1] - xs[0] == pytest.approx(g["droplet_width_t_end"], rel=2e-2)
