@@ -22,7 +22,7 @@ Multi-GPU (torchrun): C5 cuts the grid into tile-aligned rank slices: per step t
 kernels, a 10-cell halo exchange with the neighbour ranks and an all-reduce(MIN) of the CFL pair
 (paper_2211_00705_b200.decomp); C3/C4 interleave members over ranks with no collective in the
 data path.  Scaling "strong" (the problem is fixed); timing is the max over ranks.
---impl reference times the CPU oracle (oracle/) on a bounded member sample (rank 0 only).
+--impl reference times the CPU oracle (oracle/, OpenMP over the host cores) on a bounded sample (rank 0 only).
 """
 from __future__ import annotations
 
@@ -172,20 +172,60 @@ def ncu_traffic(workload_name):
     return None
 
 
-def cpu_sample_size(K, N):
-    return int(min(4096, max(1, round(1.5e8 / (K * N)))))
+def host_threads():
+    """Host cores this process may use (the oracle's OpenMP thread count)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
-def c5_cpu_cells(K):
-    """Oracle sample of C5: the first whole 4096-cell segments, ~6e7 cell-updates in total
-    (10-30 s of one host core)."""
-    return int(max(2, min(256, round(6e7 / (K * 4096))))) * 4096
+def cpu_sample_size(K, N, threads=1):
+    return int(min(4096, max(1, round(1.5e8 * threads / (K * N)))))
 
 
-def run_oracle(name, members, steps):
+def c5_cpu_cells(K, threads=1):
+    """Oracle sample of C5: the first whole 4096-cell segments, ~6e7 cell-updates per host core
+    (10-30 s of host-core time)."""
+    return int(max(2, min(1024, round(6e7 * threads / (K * 4096))))) * 4096
+
+
+def c4_cpu_members():
+    """SURVEY §8(d)'s C4 subset: every 64th member plus the 32 with the largest single-phase
+    star pressure of the converging vapour (all nucleating), in member order."""
+    from oracle import oracle as O
+    from paper_2211_00705_b200 import workloads as W
+    w = W.c4(N=4)  # (the per-member data of C4 on a 4-cell stub: cells 0 and 3 carry rho, +u0 and -u0)
+    M = w["M"]
+    rho = w["rho"][:, 0]
+    u0 = w["mom"][:, 0] / rho
+    del w
+    pstar = np.array([O.pressure(W.EOS_293K, O.VAP, O.single_phase_star(W.EOS_293K, O.VAP, rho[m], u0[m], rho[m], -u0[m]))
+                      for m in range(M)])
+    top = np.argsort(-pstar, kind="stable")[:32]
+    return np.union1d(np.arange(0, M, 64), top)
+
+
+def cpu_sample(name, K, threads):
+    """(members or cells argument of workload(), description) of the oracle's bounded sample."""
+    if name == "C5":
+        S = c5_cpu_cells(max(K, 1), threads)
+        return S, f"the first {S} cells (whole segments) of C5, {K} large steps from t=0"
+    if name == "C4":
+        mem = c4_cpu_members()
+        return mem, (f"{len(mem)} members of C4 (every 64th + the 32 largest single-phase p*, SURVEY 8(d)), "
+                     f"{K} large steps from t=0; throughput of the subset, extrapolated to the ensemble")
+    if name in ("C1", "C2"):
+        return None, f"{name}, {K} large steps from t=0"
+    N = {"C3": 1024}[name]
+    S = cpu_sample_size(max(K, 1), N, threads)
+    return np.arange(S), f"members 0..{S - 1} of {name}, {K} large steps from t=0"
+
+
+def run_oracle(name, members, steps, threads=1):
     from oracle import oracle as O
     w = workload(name, members)
-    s = O.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"])
+    s = O.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], threads=threads)
     s.set_state(w["rho"], w["mom"])
     t0 = time.perf_counter()
     st = s.step(steps) if "steps" in w else s.run_to(w["t_end"], steps)
@@ -193,38 +233,40 @@ def run_oracle(name, members, steps):
     return st, dt
 
 
+def cpu_baseline(name, K, warmup=0):
+    """The oracle as it stands, OpenMP over the host's cores (members, or one grid's cells and
+    regions), on a bounded sample of the workload."""
+    th = host_threads()
+    members, sample = cpu_sample(name, K, th)
+    if warmup:
+        run_oracle(name, 4096 if name == "C5" else (members[:th] if members is not None else None), warmup, th)
+    st, dt = run_oracle(name, members, K, th)
+    return {"value": st["cell_updates"] / dt, "unit": "cell-updates/s", "cores": th, "kind": "oracle",
+            "sample": sample + f", {th} OpenMP threads"}, dt
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     name = args.workload
+    cpu, dt = cpu_baseline(name, args.steps, args.warmup)
+    v = cpu["value"]
     if name == "C5":
-        S = N = c5_cpu_cells(max(args.steps, 1))
-        if args.warmup:
-            run_oracle(name, 4096, args.warmup)
-        st, dt = run_oracle(name, S, args.steps)
-        sample = f"the first {S} cells (whole segments) of the C5 recipe, {args.steps} large steps from t=0"
+        cfg = {"workload": f"C5: one grid of {1 << 27} cells, 4096-cell random segments", "cells": 1 << 27,
+               "parallelism": f"{cpu['cores']} host cores (CPU oracle, OpenMP)"}
     else:
         N = {"C3": 1024, "C4": 4096, "C1": 200, "C2": 1000}[name]
-        S = cpu_sample_size(max(args.steps, 1), N)
-        members = np.arange(S)
-        if args.warmup:
-            run_oracle(name, members[:1], args.warmup)
-        st, dt = run_oracle(name, members, args.steps)
-        sample = f"members 0..{S - 1} of {name}, {args.steps} large steps from t=0 (after {args.warmup} warm-up steps on member 0)"
-    v = st["cell_updates"] / dt
+        cfg = {"workload": (f"{name}: {total_members(name)} members x {N} cells" +
+                            (", cavitation ensemble" if name == "C3" else "")),
+               "members": total_members(name), "cells_per_member": N,
+               "parallelism": f"{cpu['cores']} host cores (CPU oracle, OpenMP)"}
     print(json.dumps({
         "impl": "reference", "metric": "fp64 cell-updates/s", "value": v, "unit": "cell-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         # the same workload as the eis arm's line; each step times a bounded sample of it
-        "config": ({"workload": f"C5: one grid of {1 << 27} cells, 4096-cell random segments", "cells": 1 << 27,
-                    "parallelism": "1 host core (CPU oracle)", "sample_cells": S} if name == "C5" else
-                   {"workload": (f"{name}: {total_members(name)} members x {N} cells" +
-                                 (", cavitation ensemble" if name == "C3" else "")),
-                    "members": total_members(name), "cells_per_member": N,
-                    "parallelism": "1 host core (CPU oracle)", "sample_members": S}),
-        "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "config": cfg, "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -338,10 +380,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        S = cpu_sample_size(max(args.steps, 1), w["N"])
-        sts, dts = run_oracle(name, np.arange(S) if name in ("C3", "C4") else None, args.steps)
-        cpu = {"value": sts["cell_updates"] / dts, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-               "sample": f"members 0..{S - 1} of {name}, the same {args.steps} large steps from t=0, single thread"}
+        cpu, _ = cpu_baseline(name, args.steps)
 
     cu_local = st["cell_updates"] - cu0 if world == 1 else None
     cu_gpu = cu / world if cu_local is None else cu_local
@@ -481,10 +520,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        S = c5_cpu_cells(max(args.steps, 1))
-        sts, dts = run_oracle("C5", S, args.steps)
-        cpu = {"value": sts["cell_updates"] / dts, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-               "sample": f"the first {S} cells (whole segments) of C5, the same {args.steps} large steps, single thread"}
+        cpu, _ = cpu_baseline("C5", args.steps)
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
     # dominant kernel: the fast pass streams every cell of this rank's grid once per step

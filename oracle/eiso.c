@@ -22,6 +22,9 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -434,7 +437,24 @@ struct eiso_ctx {
   int32_t* status;
   eiso_stats* mstats;
   int state_set;
+  int nthreads;  /* OpenMP threads: over members (M > 1) or over cells / regions (M == 1) */
+  struct scratch { void* p; size_t bytes; } * scr;  /* per-thread step work space, reused */
 };
+
+/* step work space of n cells, grown on demand (the arrays of one step, carved in order) */
+static void* scratch_get(struct scratch* s, size_t bytes) {
+  if (s->bytes < bytes) {
+    free(s->p);
+    s->p = malloc(bytes);
+    s->bytes = s->p ? bytes : 0;
+  }
+  return s->p;
+}
+static void* carve(char** cur, size_t bytes) {
+  void* r = *cur;
+  *cur += (bytes + 63) & ~(size_t)63;
+  return r;
+}
 
 int eiso_create(const eiso_eos* eos, const eiso_params* prm, int64_t M, int64_t N, int64_t cap,
                 double xl, double xr, eiso_ctx** out) {
@@ -454,23 +474,37 @@ int eiso_create(const eiso_eos* eos, const eiso_params* prm, int64_t M, int64_t 
   c->n = (int64_t*)calloc(M, sizeof(int64_t));
   c->status = (int32_t*)calloc(M, sizeof(int32_t));
   c->mstats = (eiso_stats*)calloc(M, sizeof(eiso_stats));
+  c->nthreads = 1;
+  c->scr = (struct scratch*)calloc(1, sizeof(struct scratch));
   *out = c;
+  return 0;
+}
+
+int eiso_set_threads(eiso_ctx* c, int nthreads) {
+  if (!c || nthreads < 1) return EISO_E_ARG;
+  for (int k = 0; k < c->nthreads; ++k) free(c->scr[k].p);
+  free(c->scr);
+  c->nthreads = nthreads;
+  c->scr = (struct scratch*)calloc(nthreads, sizeof(struct scratch));
   return 0;
 }
 
 void eiso_destroy(eiso_ctx* c) {
   if (!c) return;
   free(c->rho); free(c->mom); free(c->h); free(c->tiny); free(c->t); free(c->n); free(c->status); free(c->mstats);
+  for (int k = 0; k < c->nthreads; ++k) free(c->scr[k].p);
+  free(c->scr);
   free(c);
 }
 
 /* tiny flag: width below eps_tiny*h_av and no same-phase neighbour to merge with (P:303,
  * P:746, Fig. 4 caption P:389; readings R4, R9) */
-static void mark_tiny(eiso_ctx* c, int64_t m) {
+static void mark_tiny(eiso_ctx* c, int64_t m, int nth) {
   int64_t n = c->n[m];
   double* rho = c->rho + m * c->cap;
   double* h = c->h + m * c->cap;
   uint8_t* tiny = c->tiny + m * c->cap;
+#pragma omp parallel for num_threads(nth) if (nth > 1)
   for (int64_t i = 0; i < n; ++i) {
     int ph = phase_of(&c->e, rho[i]);
     int same_l = i > 0 && phase_of(&c->e, rho[i - 1]) == ph;
@@ -497,7 +531,7 @@ int eiso_set_state(eiso_ctx* c, const double* rho, const double* mom, const doub
       if (!(rho[k] > 0)) c->status[m] = EISO_E_NONPOS_DENSITY;
       else if (phase_of(&c->e, rho[k]) == SPIN) c->status[m] = EISO_E_SPINODAL;
     }
-    if (c->status[m] == EISO_OK) mark_tiny(c, m);
+    if (c->status[m] == EISO_OK) mark_tiny(c, m, c->nthreads);
   }
   c->state_set = 1;
   return 0;
@@ -862,7 +896,13 @@ out:
 /* One large time step of one member: Algorithm 1 extended by the moving mesh
  * (§2.3, §3.4) and phase creation (App. B).  Order of sub-steps: DESIGN.md
  * §2. */
-static int step_member(eiso_ctx* c, int64_t m, double t_end) {
+/* One large step of member m (Algorithm 1 with the moving mesh, App. B creation, Algorithm 2).
+ * nth > 1 spreads the per-cell, per-edge and per-region loops over OpenMP threads: every cell,
+ * edge and region is computed exactly as with one thread (no value depends on another thread's
+ * work; S_max / h_min are exact max / min; counters are integer sums), the creation acceptance
+ * (leftmost wins) and the remesh stay serial, and a failure reports the status of the first
+ * failing cell / edge / region in index order -- so results are bitwise those of nth = 1. */
+static int step_member(eiso_ctx* c, int64_t m, double t_end, int nth, struct scratch* scr) {
   const eos_t* e = &c->e;
   const eiso_params* P = &c->prm;
   int64_t n = c->n[m], base = m * c->cap;
@@ -872,76 +912,112 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
   uint8_t* tiny = c->tiny + base;
   eiso_stats* S = &c->mstats[m];
   int st = 0;
-  int* ph = (int*)malloc(sizeof(int) * n);
-  uint8_t* inreg = (uint8_t*)calloc(n, 1);
-  edge_t* E = (edge_t*)calloc(n + 1, sizeof(edge_t));
-  double* rho_new = (double*)malloc(sizeof(double) * n);
-  double* mom_new = (double*)malloc(sizeof(double) * n);
-  double* h_new = (double*)malloc(sizeof(double) * n);
-  /* remesh buffers: each old cell can emit at most 1 created + 2 split halves */
-  double* R0 = (double*)malloc(sizeof(double) * (3 * n + 2));
-  double* R1 = (double*)malloc(sizeof(double) * (3 * n + 2));
-  double* RH = (double*)malloc(sizeof(double) * (3 * n + 2));
-  int* RP = (int*)malloc(sizeof(int) * (3 * n + 2));
+  /* work arrays of the step (remesh buffers: each old cell emits at most 1 created + 2 split
+   * halves), carved from the calling thread's reused work space */
+  const size_t nr = 3 * (size_t)n + 2;
+  char* cur = (char*)scratch_get(scr, 64 * 12 + sizeof(int) * n + n + sizeof(edge_t) * (n + 1) + 3 * sizeof(double) * n +
+                                           3 * sizeof(double) * nr + sizeof(int) * nr + sizeof(int64_t) * (nr + 1));
+  if (!cur) return EISO_E_CAPACITY;
+  int* ph = (int*)carve(&cur, sizeof(int) * n);
+  uint8_t* inreg = (uint8_t*)carve(&cur, n);
+  edge_t* E = (edge_t*)carve(&cur, sizeof(edge_t) * (n + 1));
+  double* rho_new = (double*)carve(&cur, sizeof(double) * n);
+  double* mom_new = (double*)carve(&cur, sizeof(double) * n);
+  double* h_new = (double*)carve(&cur, sizeof(double) * n);
+  double* R0 = (double*)carve(&cur, sizeof(double) * nr);
+  double* R1 = (double*)carve(&cur, sizeof(double) * nr);
+  double* RH = (double*)carve(&cur, sizeof(double) * nr);
+  int* RP = (int*)carve(&cur, sizeof(int) * nr);
+  int64_t* partner = (int64_t*)carve(&cur, sizeof(int64_t) * (nr + 1));
+  int64_t* blk = NULL; /* implicit blocks [blk[2k], blk[2k+1]] */
+  int* bst = NULL;
+  int64_t nb = 0, first = INT64_MAX;
 
   /* 1. phases and the CFL time step (readings R5, R6):
    *    S = max over all cells of |u| + a; h_min over non-tiny cells (all cells when EXPLICIT). */
   double Smax = 0.0, hmin = INFINITY;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(max : Smax) reduction(min : hmin, first)
   for (int64_t i = 0; i < n; ++i) {
     ph[i] = phase_of(e, rho[i]);
-    if (!(rho[i] > 0.0)) { st = EISO_E_NONPOS_DENSITY; goto out; }
-    if (ph[i] == SPIN) { st = EISO_E_SPINODAL; goto out; }
+    if (!(rho[i] > 0.0) || ph[i] == SPIN) { if (i < first) first = i; continue; }
     double s = fabs(mom[i] / rho[i]) + sound(e, ph[i]);
     if (s > Smax) Smax = s;
     if ((P->mode == EISO_MODE_EXPLICIT || !tiny[i]) && h[i] < hmin) hmin = h[i];
   }
+  if (first < n) { st = !(rho[first] > 0.0) ? EISO_E_NONPOS_DENSITY : EISO_E_SPINODAL; goto out; }
   double dt = P->cfl * hmin / Smax;
   if (c->t[m] + dt > t_end) dt = t_end - c->t[m]; /* last step clipped (run_to) */
 
   /* 2. implicit regions {k-1, k, k+1} around tiny cells, overlapping ones merged
    *    (SPLIT: dual time stepping; LTS: local time stepping of the tiny cells) */
-  if (P->mode != EISO_MODE_EXPLICIT) {
-    for (int64_t k = 0; k < n; ++k) {
-      if (!tiny[k]) continue;
-      if (k == 0 || k == n - 1) { st = EISO_E_UNSUPPORTED; goto out; }
-      inreg[k - 1] = inreg[k] = inreg[k + 1] = 1;
-    }
-  }
+  const int split = P->mode != EISO_MODE_EXPLICIT;
+  if (split && (tiny[0] || tiny[n - 1])) { st = EISO_E_UNSUPPORTED; goto out; }
+#pragma omp parallel for num_threads(nth) if (nth > 1)
+  for (int64_t i = 0; i < n; ++i) inreg[i] = split && (tiny[i] || (i > 0 && tiny[i - 1]) || (i < n - 1 && tiny[i + 1]));
 
   /* 3. edge fluxes from U^n (Alg. 1 Step 1(a)); edge e lies between cells e-1 and e; the domain
    *    ends use a transmissive ghost = copy of the end cell (reading R15).  Edges interior to an
    *    implicit block are left to Algorithm 2. */
-  for (int64_t ed = 0; ed <= n; ++ed) {
-    int64_t L = ed == 0 ? 0 : ed - 1, R = ed == n ? n - 1 : ed;
-    if (ed > 0 && ed < n && inreg[L] && inreg[R]) { E[ed].kind = -1; continue; }
-    st = edge_flux(c, rho[L], mom[L], rho[R], mom[R], &E[ed].F0, &E[ed].F1, &E[ed].w, &E[ed].kind, &S->iface_solves);
-    if (st) goto out;
+  {
+    int64_t solves = 0;
+    first = INT64_MAX;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(+ : solves) reduction(min : first)
+    for (int64_t ed = 0; ed <= n; ++ed) {
+      int64_t L = ed == 0 ? 0 : ed - 1, R = ed == n ? n - 1 : ed;
+      if (ed > 0 && ed < n && inreg[L] && inreg[R]) { E[ed].kind = -1; continue; }
+      if (edge_flux(c, rho[L], mom[L], rho[R], mom[R], &E[ed].F0, &E[ed].F1, &E[ed].w, &E[ed].kind, &solves) &&
+          ed < first)
+        first = ed;
+    }
+    S->iface_solves += solves;
+    if (first != INT64_MAX) { /* the first failing edge's status */
+      int64_t ed = first, L = ed == 0 ? 0 : ed - 1, R = ed == n ? n - 1 : ed, dummy = 0;
+      st = edge_flux(c, rho[L], mom[L], rho[R], mom[R], &E[ed].F0, &E[ed].F1, &E[ed].w, &E[ed].kind, &dummy);
+      goto out;
+    }
   }
 
   /* 4. phase creation (App. B steps (i)-(v)) on eligible edges (reading R16): interior,
    *    same phase, both cells explicit; increasing edge order, an edge whose left neighbour
-   *    edge was accepted is skipped (leftmost wins). */
-  for (int64_t ed = 1; ed < n; ++ed) {
-    if (E[ed].kind != 0 || inreg[ed - 1] || inreg[ed]) continue;
-    int phe = ph[ed];
-    double ul = mom[ed - 1] / rho[ed - 1], ur = mom[ed] / rho[ed];
-    if (trigger_marginal(e, phe, rho[ed - 1], ul, rho[ed], ur)) S->decision_margin_warnings++;
-    if (!creation_trigger(e, phe, rho[ed - 1], ul, rho[ed], ur)) continue;
-    if (E[ed - 1].kind == 2) continue;
-    eiso_creation cr;
-    if (creation_solve(e, P, phe, rho[ed - 1], ul, rho[ed], ur, &cr) != 0) { st = EISO_E_CREATION; goto out; }
-    E[ed].kind = 2;
-    E[ed].Fl0 = cr.Fl0; E[ed].Fl1 = cr.Fl1; E[ed].wl = cr.w_l;
-    E[ed].Fr0 = cr.Fr0; E[ed].Fr1 = cr.Fr1; E[ed].wr = cr.w_r;
-    E[ed].rhoB = cr.rho_B;
-    E[ed].momB = cr.rho_B * cr.u_B;
-    E[ed].hB = (cr.w_r - cr.w_l) * dt; /* created width (w_right - w_left) dt, P:1581 / P:1608 */
-    S->creations++;
+   *    edge was accepted is skipped (leftmost wins).  The trigger tests are independent per edge
+   *    (kind 3 marks a triggered edge), the acceptance runs in edge order, the solves again per
+   *    edge. */
+  {
+    int64_t marg = 0, ncre = 0;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(+ : marg)
+    for (int64_t ed = 1; ed < n; ++ed) {
+      if (E[ed].kind != 0 || inreg[ed - 1] || inreg[ed]) continue;
+      int phe = ph[ed];
+      double ul = mom[ed - 1] / rho[ed - 1], ur = mom[ed] / rho[ed];
+      if (trigger_marginal(e, phe, rho[ed - 1], ul, rho[ed], ur)) marg++;
+      if (creation_trigger(e, phe, rho[ed - 1], ul, rho[ed], ur)) E[ed].kind = 3;
+    }
+    S->decision_margin_warnings += marg;
+    for (int64_t ed = 1; ed < n; ++ed)
+      if (E[ed].kind == 3) E[ed].kind = E[ed - 1].kind == 2 ? 0 : 2;
+    first = INT64_MAX;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(+ : ncre) reduction(min : first)
+    for (int64_t ed = 1; ed < n; ++ed) {
+      if (E[ed].kind != 2) continue;
+      double ul = mom[ed - 1] / rho[ed - 1], ur = mom[ed] / rho[ed];
+      eiso_creation cr;
+      if (creation_solve(e, P, ph[ed], rho[ed - 1], ul, rho[ed], ur, &cr) != 0) { if (ed < first) first = ed; continue; }
+      E[ed].Fl0 = cr.Fl0; E[ed].Fl1 = cr.Fl1; E[ed].wl = cr.w_l;
+      E[ed].Fr0 = cr.Fr0; E[ed].Fr1 = cr.Fr1; E[ed].wr = cr.w_r;
+      E[ed].rhoB = cr.rho_B;
+      E[ed].momB = cr.rho_B * cr.u_B;
+      E[ed].hB = (cr.w_r - cr.w_l) * dt; /* created width (w_right - w_left) dt, P:1581 / P:1608 */
+      ncre++;
+    }
+    S->creations += ncre;
+    if (first != INT64_MAX) { st = EISO_E_CREATION; goto out; }
   }
 
   /* 5. explicit moving-cell update of every cell outside the implicit blocks (Alg. 1 Step 1(b)
    *    in the form (12)): h^{n+1} = h^n + (w_R - w_L) dt,
    *    U^{n+1} = (h^n/h^{n+1}) U^n - (dt/h^{n+1}) (F_R - F_L). */
+  first = INT64_MAX;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(min : first)
   for (int64_t i = 0; i < n; ++i) {
     if (inreg[i]) continue;
     const edge_t* El = &E[i];
@@ -951,27 +1027,43 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     double FR0 = Er->kind == 2 ? Er->Fl0 : Er->F0, FR1 = Er->kind == 2 ? Er->Fl1 : Er->F1;
     double wR = Er->kind == 2 ? Er->wl : Er->w;
     double hn = h[i] + (wR - wL) * dt;
-    if (!(hn > 0.0)) { st = EISO_E_WIDTH; goto out; }
+    if (!(hn > 0.0)) { if (i < first) first = i; continue; }
     h_new[i] = hn;
     rho_new[i] = (h[i] / hn) * rho[i] - (dt / hn) * (FR0 - FL0);
     mom_new[i] = (h[i] / hn) * mom[i] - (dt / hn) * (FR1 - FL1);
   }
+  if (first != INT64_MAX) { st = EISO_E_WIDTH; goto out; }
 
-  /* 6. Algorithm 2 on every implicit block (Alg. 1 Step 2), or local time stepping (LTS mode) */
+  /* 6. Algorithm 2 on every implicit block (Alg. 1 Step 2), or local time stepping (LTS mode):
+   *    the blocks are listed in cell order, solved independently, the first failure reported */
   for (int64_t i = 0; i < n;) {
     if (!inreg[i]) { ++i; continue; }
     int64_t a = i;
     while (i < n && inreg[i]) ++i;
-    int64_t b = i - 1, it = 0;
-    if (P->mode == EISO_MODE_LTS)
-      st = lts_block(c, m, a, b, E, dt, Smax, rho_new, mom_new, h_new, &it, &S->iface_solves);
-    else if (P->mode == EISO_MODE_NEWTON)
-      st = newton_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves);
-    else
-      st = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &S->iface_solves, &S->decision_margin_warnings);
-    if (st) goto out;
-    S->dts_iters += it;
-    S->regions++;
+    if (nb % 64 == 0) blk = (int64_t*)realloc(blk, sizeof(int64_t) * 2 * (nb + 64));
+    blk[2 * nb] = a; blk[2 * nb + 1] = i - 1; ++nb;
+  }
+  if (nb) {
+    bst = (int*)calloc(nb, sizeof(int));
+    int64_t iters = 0, solves = 0, marg = 0;
+#pragma omp parallel for num_threads(nth) if (nth > 1) schedule(dynamic, 1) reduction(+ : iters, solves, marg)
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t a = blk[2 * k], b = blk[2 * k + 1], it = 0;
+      if (P->mode == EISO_MODE_LTS)
+        bst[k] = lts_block(c, m, a, b, E, dt, Smax, rho_new, mom_new, h_new, &it, &solves);
+      else if (P->mode == EISO_MODE_NEWTON)
+        bst[k] = newton_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &solves);
+      else
+        bst[k] = dts_block(c, m, a, b, E, dt, rho_new, mom_new, h_new, &it, &solves, &marg);
+      iters += it;
+    }
+    S->iface_solves += solves;
+    S->decision_margin_warnings += marg;
+    for (int64_t k = 0; k < nb; ++k) {
+      if (bst[k]) { st = bst[k]; goto out; }
+      S->regions++;
+    }
+    S->dts_iters += iters;
   }
 
   /* 7. remesh (readings R9, R10): insert created cells -> merge cells with
@@ -982,17 +1074,22 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     if (i > 0 && E[i].kind == 2) { R0[q] = E[i].rhoB; R1[q] = E[i].momB; RH[q] = E[i].hB; ++q; }
     R0[q] = rho_new[i]; R1[q] = mom_new[i]; RH[q] = h_new[i]; ++q;
   }
+  int64_t wmarg = 0;
+  first = INT64_MAX;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(+ : wmarg)
   for (int64_t i = 0; i < n; ++i) /* width decisions of the cells whose width changed (R4) */
     if (h_new[i] != h[i] && (width_marginal(h_new[i], P->eps_tiny * c->h_av) ||
                              width_marginal(h_new[i], P->eps_split * c->h_av)))
-      S->decision_margin_warnings++;
+      wmarg++;
+  S->decision_margin_warnings += wmarg;
+#pragma omp parallel for num_threads(nth) if (nth > 1) reduction(min : first)
   for (int64_t i = 0; i < q; ++i) {
-    if (!(R0[i] > 0.0)) { st = EISO_E_NONPOS_DENSITY; goto out; }
     RP[i] = phase_of(e, R0[i]);
-    if (RP[i] == SPIN) { st = EISO_E_SPINODAL; goto out; }
+    if ((!(R0[i] > 0.0) || RP[i] == SPIN) && i < first) first = i;
   }
+  if (first != INT64_MAX) { st = !(R0[first] > 0.0) ? EISO_E_NONPOS_DENSITY : EISO_E_SPINODAL; goto out; }
   /* merge partner: the same-phase neighbour; both -> the smaller, ties to the left */
-  int64_t* partner = (int64_t*)malloc(sizeof(int64_t) * (q + 1));
+#pragma omp parallel for num_threads(nth) if (nth > 1)
   for (int64_t i = 0; i < q; ++i) {
     partner[i] = -1;
     if (!(RH[i] < P->eps_tiny * c->h_av)) continue;
@@ -1016,7 +1113,6 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
     ++q2;
     i = j + 1;
   }
-  free(partner);
   int64_t q3 = 0;
   for (int64_t i = 0; i < q2; ++i) q3 += (RH[i] > P->eps_split * c->h_av) ? 2 : 1;
   if (q3 > c->cap) { st = EISO_E_CAPACITY; goto out; }
@@ -1030,15 +1126,22 @@ static int step_member(eiso_ctx* c, int64_t m, double t_end) {
   }
   S->cell_updates += n;
   c->n[m] = q3;
-  mark_tiny(c, m);
+  mark_tiny(c, m, nth);
   c->t[m] += dt;
   S->steps++;
   if (S->steps == 1 || dt < S->dt_min) S->dt_min = dt;
   if (dt > S->dt_max) S->dt_max = dt;
 out:
-  free(ph); free(inreg); free(E); free(rho_new); free(mom_new); free(h_new);
-  free(R0); free(R1); free(RH); free(RP);
+  free(blk); free(bst);
   return st;
+}
+
+static int thread_slot(void) {
+#ifdef _OPENMP
+  return omp_get_thread_num();
+#else
+  return 0;
+#endif
 }
 
 static void accumulate(const eiso_ctx* c, eiso_stats* out) {
@@ -1060,8 +1163,12 @@ static void accumulate(const eiso_ctx* c, eiso_stats* out) {
 int eiso_step(eiso_ctx* c, int64_t n_steps, eiso_stats* out) {
   if (!c) return EISO_E_ARG;
   if (!c->state_set) return EISO_E_ORDER;
+  /* members in parallel (each member's steps in order), or one member's loops in parallel */
+  const int nth = c->nthreads, inner = c->M > 1 ? 1 : nth;
+#pragma omp parallel for num_threads(nth) if (nth > 1 && c->M > 1) schedule(dynamic, 1)
   for (int64_t m = 0; m < c->M; ++m)
-    for (int64_t k = 0; k < n_steps && c->status[m] == EISO_OK; ++k) c->status[m] = step_member(c, m, INFINITY);
+    for (int64_t k = 0; k < n_steps && c->status[m] == EISO_OK; ++k)
+      c->status[m] = step_member(c, m, INFINITY, inner, &c->scr[thread_slot()]);
   if (out) accumulate(c, out);
   return 0;
 }
@@ -1069,9 +1176,11 @@ int eiso_step(eiso_ctx* c, int64_t n_steps, eiso_stats* out) {
 int eiso_run_to(eiso_ctx* c, double t_end, int64_t max_steps, eiso_stats* out) {
   if (!c) return EISO_E_ARG;
   if (!c->state_set) return EISO_E_ORDER;
+  const int nth = c->nthreads, inner = c->M > 1 ? 1 : nth;
+#pragma omp parallel for num_threads(nth) if (nth > 1 && c->M > 1) schedule(dynamic, 1)
   for (int64_t m = 0; m < c->M; ++m)
     for (int64_t k = 0; k < max_steps && c->status[m] == EISO_OK && c->t[m] < t_end; ++k)
-      c->status[m] = step_member(c, m, t_end);
+      c->status[m] = step_member(c, m, t_end, inner, &c->scr[thread_slot()]);
   if (out) accumulate(c, out);
   return 0;
 }

@@ -116,6 +116,9 @@ int  eiso_create(const eiso_eos* eos, const eiso_params* prm, int64_t n_members,
                  int64_t cell_capacity, double x_left, double x_right, eiso_ctx** out);
 int  eiso_set_state(eiso_ctx* c, const double* rho, const double* mom, const double* width,
                     const int64_t* n_cells, double t0);
+/* OpenMP threads (default 1): over members when n_members > 1, else over the cells, edges and
+ * implicit regions of the one member; results are bitwise those of one thread */
+int  eiso_set_threads(eiso_ctx* c, int nthreads);
 int  eiso_step(eiso_ctx* c, int64_t n_steps, eiso_stats* out);
 int  eiso_run_to(eiso_ctx* c, double t_end, int64_t max_steps, eiso_stats* out);
 int  eiso_get_state(const eiso_ctx* c, double* rho, double* mom, double* width, uint8_t* phase,

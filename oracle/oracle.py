@@ -16,7 +16,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
-CFLAGS = ["-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+CFLAGS = ["-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
 
 VAP, LIQ, SPIN = 0, 1, 2
 MODE_SPLIT, MODE_EXPLICIT, MODE_LTS, MODE_NEWTON = 0, 1, 2, 3
@@ -99,6 +99,7 @@ def lib():
         L.eiso_creation_solve.argtypes = [P(Eos), P(Params), C.c_int, d, d, d, d, P(Creation)]
         L.eiso_create.argtypes = [P(Eos), P(Params), C.c_int64, C.c_int64, C.c_int64, d, d, P(C.c_void_p)]
         L.eiso_set_state.argtypes = [C.c_void_p, P(d), P(d), P(d), P(C.c_int64), d]
+        L.eiso_set_threads.argtypes = [C.c_void_p, C.c_int]
         L.eiso_step.argtypes = [C.c_void_p, C.c_int64, P(Stats)]
         L.eiso_run_to.argtypes = [C.c_void_p, d, C.c_int64, P(Stats)]
         L.eiso_get_state.argtypes = [C.c_void_p, P(d), P(d), P(d), P(C.c_uint8), P(C.c_int64), P(d)]
@@ -192,7 +193,7 @@ class Sim:
     """Oracle simulation context (eiso_create ... eiso_destroy), host arrays only."""
 
     def __init__(self, eos: dict, params: dict, n_members: int, n_cells: int, capacity: int,
-                 x_left: float, x_right: float):
+                 x_left: float, x_right: float, threads: int = 1):
         self.M, self.N, self.cap = int(n_members), int(n_cells), int(capacity)
         self._ctx = C.c_void_p()
         self._eos = make_eos(eos)
@@ -201,6 +202,12 @@ class Sim:
                               float(x_left), float(x_right), C.byref(self._ctx))
         if s:
             raise ValueError(f"eiso_create status {s}")
+        self.set_threads(threads)
+
+    def set_threads(self, n: int):
+        """OpenMP threads: over members (M > 1) or over one member's cells and regions."""
+        if lib().eiso_set_threads(self._ctx, int(n)):
+            raise ValueError("eiso_set_threads")
 
     def __del__(self):
         if getattr(self, "_ctx", None) and self._ctx.value and _lib is not None:

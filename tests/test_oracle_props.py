@@ -518,3 +518,35 @@ def test_newton_mode_c4_droplet(oracle_mod):
     assert n == int(b["n"][0]) and sa["regions"] == sb["regions"] > 0
     assert np.abs(a["rho"][0, :n] - b["rho"][0, :n]).sum() <= 1e-6 * np.abs(b["rho"][0, :n]).sum()
     assert 3 * sa["dts_iters"] < sb["dts_iters"]
+
+
+# ---------------------------------------------------------------------------- OpenMP oracle
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5", "c5_newton", "c3_lts"])
+def test_threads_are_bitwise_identical(oracle_mod, cfg):
+    """The threaded oracle (over members, or over one member's cells / edges / regions) gives
+    the one-thread result bit for bit: states, widths, counts, clocks, statuses."""
+    steps = 60
+    if cfg == "c2":
+        w = W.c2()
+    elif cfg == "c4":
+        w = W.c4(members=np.array([0, 1, 2, 3, 777, 9999]), N=512)
+    elif cfg.startswith("c3"):
+        w = W.c3(members=np.arange(5), N=256)
+        w["params"] = dict(w["params"], mode=2)
+    else:
+        w = W.c5(n_cells=1 << 15)
+        if cfg == "c5_newton":
+            w["params"] = dict(w["params"], mode=3)
+    out = []
+    for th in (1, 4):
+        s = oracle_mod.Sim(w["eos"], w["params"], w["M"], w["N"], w["cap"], w["x_left"], w["x_right"], threads=th)
+        s.set_state(w["rho"], w["mom"])
+        st = s.step(steps)
+        o = s.get_state()
+        out.append((st, o, s.member_status(), [s.member_stats(m) for m in range(w["M"])]))
+    (s1, o1, z1, m1), (s4, o4, z4, m4) = out
+    assert s1["regions"] > 0 or s1["creations"] > 0
+    assert s1 == s4 and m1 == m4
+    np.testing.assert_array_equal(z1, z4)
+    for k in ("rho", "mom", "h", "n", "t"):
+        np.testing.assert_array_equal(o1[k], o4[k])
