@@ -270,14 +270,16 @@ typedef struct {
   double tol_nb, tol_tiny;           /* 1e-3, 1e-1                                   */
   int64_t dts_max_iter;
   int32_t implicit_block;            /* 1: Algorithm 2 on {k-1, k, k+1}; 0: all explicit      */
-  int32_t reserved;
+  int32_t dts_loop;                  /* Algorithm 2 by 0: one warp (dts_warp, the member-resident
+                                        kernels' loop); 1: one thread (dts_thread, the tiled
+                                        window path's loop) -- same arithmetic, same bits      */
 } eis_lax_case;
 
 typedef struct {
   int64_t steps, dts_iters, dts_max, riemann_solves;
   double t;
   int32_t status;
-  int32_t reserved;
+  int32_t margins;                   /* DTS stop decisions within their rounding-error bound   */
 } eis_lax_stats;
 
 eis_status eis_lax_run(const eis_lax_case* cases, int64_t n_cases, int64_t stride, double* rho, double* mom,

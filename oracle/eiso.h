@@ -16,6 +16,10 @@
  *   EOS, thresholds, HLL, interface solve, creation solve, CFL rule  -> pinned
  *   (paper-printed values P:1244, P:1263-1264, P:1277, P:1297, P:1390, P:1410, P:1422,
  *    closed forms, brute force, invariants).
+ *   DTS loop (Alg. 2 stop rule, residual, pseudo steps)             -> pinned by the paper's
+ *   local-iteration counts: cavitation 355 within 10 % (a wrong theta, tolerance or
+ *   residual moves it further), nucleation 1,367,460 within the rounding regime of
+ *   reading R28 (factor 3, every stop flagged by the decision-margin accounting).
  *   DTS iteration counts at 293 K, C4/C5 long-time dynamics           -> parity unpinned
  *   beyond the invariants (constant states, conservation, mode degeneracy, DTS fixed point).
  */

@@ -147,21 +147,21 @@ class LaxCase(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("gamma", "rho_l", "u_l", "p_l", "rho_r", "u_r", "p_r", "x_left",
                                           "x_right")] + [("n", C.c_int64)] + \
                [(n, C.c_double) for n in ("alpha", "theta_nb", "cfl", "t_end", "tol_nb", "tol_tiny")] + \
-               [("dts_max_iter", C.c_int64), ("implicit_block", C.c_int32), ("reserved", C.c_int32)]
+               [("dts_max_iter", C.c_int64), ("implicit_block", C.c_int32), ("dts_loop", C.c_int32)]
 
 
 class LaxStats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("dts_iters", C.c_int64), ("dts_max", C.c_int64),
-                ("riemann_solves", C.c_int64), ("t", C.c_double), ("status", C.c_int32), ("reserved", C.c_int32)]
+                ("riemann_solves", C.c_int64), ("t", C.c_double), ("status", C.c_int32), ("margins", C.c_int32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 # the paper's Lax setup and DTS stop rule
 LAX_DEFAULT = dict(gamma=1.4, rho_l=0.445, u_l=0.698, p_l=3.528, rho_r=0.5, u_r=0.0, p_r=0.571, x_left=-5.0,
                    x_right=5.0, n=100, alpha=1e-2, theta_nb=0.9, cfl=0.8, t_end=1.0, tol_nb=1e-3, tol_tiny=1e-1,
-                   dts_max_iter=10 ** 9, implicit_block=1)
+                   dts_max_iter=10 ** 9, implicit_block=1, dts_loop=0)
 
 
 def lax_run(cases, stream=None):

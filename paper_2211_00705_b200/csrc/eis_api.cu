@@ -65,6 +65,9 @@ struct eis_ctx {
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
+  int dts_grid = 0;                        // window split: dts_jobs CTAs (one warp each)
+  DtsJob* t_djobs = nullptr;
+  unsigned char* t_wsave = nullptr;
   cudaStream_t stream2 = nullptr;          // tiled: the window kernel beside tiled_fast
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   size_t smem_win;
@@ -341,13 +344,17 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 #endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
   if (cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
-      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 2>) != cudaSuccess || cudaFuncGetAttributes(&fa, dts_jobs) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
       delete c; return EIS_E_CUDA;
     }
@@ -362,6 +369,10 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   // beside tiled_fast cost tiled_fast more than the overlap saves); EIS_WIN_POLL_PER_SM=k
   c->win_grid_poll = 0;
   if (const char* ev = getenv("EIS_WIN_POLL_PER_SM")) c->win_grid_poll = std::max(0, atoi(ev)) * std::max(1, nsm);
+  // window split (dual time stepping only; EIS_WIN_SPLIT=0: every window step in one kernel)
+  int split = c->p.mode == 0 && c->win_grid_poll == 0;
+  if (const char* ev = getenv("EIS_WIN_SPLIT")) split = split && atoi(ev) != 0;
+  c->dts_grid = std::max(nsm, 1) * 16;
   const size_t tc = (size_t)ntiles * capt;
   const size_t mc = (size_t)M * cap;  // member-major staging
   bool ok = cudaMalloc(&c->d_rho, mc * 8) == cudaSuccess && cudaMalloc(&c->d_mom, mc * 8) == cudaSuccess &&
@@ -385,6 +396,10 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaMalloc(&c->t_partf, (size_t)ntiles * 24) == cudaSuccess &&
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + M) * 8) == cudaSuccess;
+  const long long djcap = 4 * ntiles;  // DTS jobs per step (windows hold one block, rarely more)
+  if (ok && split)
+    ok = cudaMalloc(&c->t_djobs, (size_t)djcap * sizeof(DtsJob)) == cudaSuccess &&
+         cudaMalloc(&c->t_wsave, (size_t)ntiles * WSAVE) == cudaSuccess;
   if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
@@ -399,6 +414,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     tl.wdbg = c->t_wdbg;
   }
   tl.poll = c->win_grid_poll > 0 ? 1 : 0;
+  tl.split = split; tl.djcap = split ? (int)djcap : 0; tl.djobs = c->t_djobs; tl.wsave = c->t_wsave;
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
   if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
@@ -611,6 +627,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   if (!c->tiled) cudaFree(c->g.dbg);
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
+  cudaFree(c->t_djobs); cudaFree(c->t_wsave);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_mctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -804,7 +821,13 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     tiled_win<32, EIS_WIN_MINB, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
     cudaEventRecord(c->ev_join, c->stream2);
   }
-  tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->tl.split) {  // part A, the DTS jobs (one lane per block), part B
+    tiled_win<32, EIS_WIN_MINB, false, 1><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+    dts_jobs<<<c->dts_grid, 32, 0, c->stream>>>(c->e, c->p, c->tl);
+    tiled_win<32, EIS_WIN_MINB, false, 2><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  } else {
+    tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+  }
   if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);

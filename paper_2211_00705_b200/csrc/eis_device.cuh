@@ -264,8 +264,10 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
 // within ~rtol of the root (the oracle tests the step against rtol itself, one extra iteration).
 // Returns the iteration count (>= 0) or -1; aux holds the value at the returned iterate.
 // ---------------------------------------------------------------------------------------
+// HALF = false: the same iteration by one thread, the Armijo candidates tried in order (the first
+// accepted k is the smallest: the result is the half warp's bit for bit).
 template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*, double*),
-          bool LIN>
+          bool LIN, bool HALF = true>
 __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, double aux[2],
                          unsigned mask, int hl, int base_lane) {
   double G[2], J[4], da[4];
@@ -295,7 +297,17 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
     const double c1 = 1.0 - 1e-4;
     bool ok = EVAL(e, P, y0, y1, Gy, Jy, ay, dy) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= c1 * c1 * n0;
     double s0 = d0, s1 = d1;
-    if (!ok) {  // lane-parallel back-tracking: lane k tries lambda = 2^-(k+1), then 2^-(k+17)
+    if (!ok && !HALF) {  // back-tracking, lambda = 2^-k in order
+      int acc = -1;
+      for (int k = 1; k <= p.armijo_max && acc < 0; ++k) {
+        const double lam = __longlong_as_double((long long)(1023 - k) << 52);  // 2^-k
+        y0 = x0 + lam * d0; y1 = x1 + lam * d1;
+        const double cl = 1.0 - 1e-4 * lam;
+        if (EVAL(e, P, y0, y1, Gy, Jy, ay, dy) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= cl * cl * n0) acc = k;
+      }
+      if (acc < 0) return fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol ? it : -1;  // rounding floor
+      s0 = y0 - x0; s1 = y1 - x1;
+    } else if (!ok) {  // lane-parallel back-tracking: lane k tries lambda = 2^-(k+1), then 2^-(k+17)
       int acc = -1;
       for (int round = 0; round * 16 + 1 <= p.armijo_max && acc < 0; ++round) {
         const int k = round * 16 + hl + 1;
@@ -350,12 +362,13 @@ struct IfaceSol {
   int iters;  // -1 on failure
 };
 
-// Phase-boundary Riemann solve by a half warp.  (rm, um) minus (left) state, (rp, up) plus.
-// Warm start: if x_init0 > 0 use (x_init0, x_init1) as the first iterate, else HLLC.
-// Outputs F_PB = (-z, -z u_V* + p_V*) (vapour side R17), w = u_V* + z v_V*.
-__device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, double rm, double um, double rp,
-                                                double up, bool vap_minus, double x_init0, double x_init1,
-                                                unsigned mask, int hl, int base_lane) {
+// Phase-boundary Riemann solve by a half warp (HALF) or one thread.  (rm, um) minus (left)
+// state, (rp, up) plus.  Warm start: if x_init0 > 0 use (x_init0, x_init1) as the first iterate,
+// else HLLC.  Outputs F_PB = (-z, -z u_V* + p_V*) (vapour side R17), w = u_V* + z v_V*.
+template <bool HALF>
+__device__ __forceinline__ IfaceSol iface_solve_x(const Eos& e, const Prm& p, double rm, double um, double rp,
+                                                  double up, bool vap_minus, double x_init0, double x_init1,
+                                                  unsigned mask, int hl, int base_lane) {
   IfaceProb P;
   if (vap_minus) { P.rV = rm; P.uV = um; P.rL = rp; P.uL = up; P.sV = -1.0; }
   else { P.rV = rp; P.uV = up; P.rL = rm; P.uL = um; P.sV = 1.0; }
@@ -366,11 +379,11 @@ __device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, doub
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
   }
-  int it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+  int it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN, HALF>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
-    it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN>(e, p, P, x0, x1, aux, mask, hl, base_lane);
+    it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN, HALF>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   }
   IfaceSol s;
   s.iters = it;
@@ -382,6 +395,15 @@ __device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, doub
   s.F0 = -z;
   s.F1 = -z * uVs + x0;
   return s;
+}
+__device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, double rm, double um, double rp,
+                                                double up, bool vap_minus, double x_init0, double x_init1,
+                                                unsigned mask, int hl, int base_lane) {
+  return iface_solve_x<true>(e, p, rm, um, rp, up, vap_minus, x_init0, x_init1, mask, hl, base_lane);
+}
+__device__ __noinline__ IfaceSol iface_solve_t(const Eos& e, const Prm& p, double rm, double um, double rp,
+                                               double up, bool vap_minus, double x_init0, double x_init1) {
+  return iface_solve_x<false>(e, p, rm, um, rp, up, vap_minus, x_init0, x_init1, 0u, 0, 0);
 }
 
 struct CreateSol {

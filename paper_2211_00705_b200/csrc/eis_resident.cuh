@@ -30,13 +30,13 @@
 //   remesh (a10): event lists (merge pairs, splits, creations) -> per-cell shift -> scatter
 #pragma once
 #include "eis_device.cuh"
+#include "eis_dts.cuh"
 
 namespace eis {
 
 constexpr int MAXIF = 16;    // phase boundaries per member
 constexpr int MAXTRG = 8;    // creation triggers per member per step
 constexpr int MAXBLK = 8;    // implicit blocks per member
-constexpr int MAXB = 8;      // cells per implicit block
 constexpr int MAXEV = 16;    // remesh events (merge edges, split cells) per member per step
 constexpr int DTS_SCRATCH = 72;
 
@@ -88,6 +88,7 @@ struct CtaShared {
   Grp grp[MAXEV];
   int mev[MAXEV], sev[MAXEV];
   int blkA[MAXBLK], blkB[MAXBLK];
+  int dj[MAXBLK];  // window split: the DTS job of each block (-1: none)
   int tc[MAXIF];
   int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
@@ -218,151 +219,161 @@ __device__ __forceinline__ int remesh_shift(const CtaShared& sh, int ntrg, int i
 // from its previous iterate; cell updates by lanes 0..K-1; residual (R8) by warp max.
 // Outer fluxes F_left, F_right are the explicit step's (flux bounding).
 // ------------------------------------------------------------------------------------------
+// the isothermal two-phase system for the generic loop (eis_dts.cuh): interior edges are phase
+// boundaries (Appendix-A solve by the half warp, warm-started from the previous iterate) or HLL
+// (P:1103); phases are those of U^n (an iterate leaving its phase is ST_SPINODAL, R27)
+struct TwoPhaseDts {
+  static constexpr int NV = 2;
+  // past the loop's scratch (W at offset 0): star pressures of the interior boundaries (warm
+  // starts) xs0, xs1 [MAXB + 1] and the iterate's velocities Wu [MAXB] (one division per cell)
+  static constexpr int XS0 = dts_scratch<2>(), XS1 = XS0 + MAXB + 1, WU = XS1 + MAXB + 1;
+  const Eos& e;
+  const Prm& p;
+  unsigned vapm, liqm;
+  int solves;
+  __device__ __forceinline__ int phase_n(int c) const { return (vapm >> c & 1u) ? VAP : ((liqm >> c & 1u) ? LIQ : SPIN); }
+  __device__ __forceinline__ int edge(int j, double* W, double* Fe, double* we, int half, int hl, unsigned hmask) {
+    const double rl = W[j - 1], ml = W[MAXB + j - 1], rr = W[j], mr = W[MAXB + j], ul = W[WU + j - 1], ur = W[WU + j];
+    const int pl = phase_n(j - 1), pr = phase_n(j);  // phases of U^n
+    int err = 0;
+    if (pl != pr) {
+      IfaceSol s = iface_solve_hw(e, p, rl, ul, rr, ur, pl == VAP, W[XS0 + j], W[XS1 + j], hmask, hl, half * 16);
+      if (hl == 0) {
+        if (s.iters < 0) err = ST_NEWTON;
+        Fe[j] = s.F0; Fe[MAXB + 1 + j] = s.F1; we[j] = s.w; W[XS0 + j] = s.pV; W[XS1 + j] = s.pL;
+        ++solves;
+      }
+    } else if (hl == 0) {
+      hll(e, pl, rl, ml, ul, rr, mr, ur, Fe[j], Fe[MAXB + 1 + j]);
+      we[j] = 0.0;
+    }
+    return err;
+  }
+  __device__ __forceinline__ int check(int lane, const double (&w)[2]) const {
+    return (!(w[0] > 0.0) || phase_of(e, w[0]) != phase_n(lane)) ? ST_SPINODAL : 0;
+  }
+  __device__ __forceinline__ void store(double* W, int lane, const double (&w)[2]) { W[WU + lane] = w[1] / w[0]; }
+};
+static_assert(dts_scratch<2>() + 3 * MAXB + 2 <= DTS_SCRATCH, "dts scratch");
+
 __device__ __noinline__ int dts_block(const Eos& e, const Prm& p, CtaShared& sh, double* rho, double* mom, double* h,
                                       const double* F0, const double* F1, const uint8_t* fl, int a, int b, double dt,
                                       long long& it_out, long long& solves, int& remesh, int& marg) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
-  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  const int lane = threadIdx.x & 31;
   const int K = b - a + 1;
   double* sc = sh.dts;
-  double* W0 = sc;               // [MAXB]
-  double* W1 = sc + MAXB;        // [MAXB]
-  double* Fe0 = sc + 2 * MAXB;   // [MAXB+1]
-  double* Fe1 = Fe0 + MAXB + 1;
-  double* we = Fe1 + MAXB + 1;
-  double* xs0 = we + MAXB + 1;
-  double* xs1 = xs0 + MAXB + 1;
-  double* Wu = xs1 + MAXB + 1;   // [MAXB] velocities of the iterate (one division per cell, by its lane)
-  if (lane == 0) {
+  double* Fe = sc + 2 * MAXB;
+  double* we = Fe + 2 * (MAXB + 1);
+  if (lane == 0) {  // outer edges: the explicit step's fluxes and speeds
     double g0, g1, w;
     edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
-    Fe0[0] = g0; Fe1[0] = g1; we[0] = w;
+    Fe[0] = g0; Fe[MAXB + 1] = g1; we[0] = w;
     edge_view(sh, fl, F0, F1, b + 1, 0, g0, g1, w);
-    Fe0[K] = g0; Fe1[K] = g1; we[K] = w;
+    Fe[K] = g0; Fe[MAXB + 1 + K] = g1; we[K] = w;
   }
   if (lane >= 1 && lane < K) {  // warm start of interior boundaries from the last step
     const Ifc* s = find_ifc(sh, a + lane);
-    xs0[lane] = s ? s->pV : -1.0;
-    xs1[lane] = s ? s->pL : -1.0;
+    sc[TwoPhaseDts::XS0 + lane] = s ? s->pV : -1.0;
+    sc[TwoPhaseDts::XS1 + lane] = s ? s->pL : -1.0;
   }
-  double rn0 = 0, rn1 = 0, hn = 0, r = 0, dtau = 1, w0 = 0, w1 = 0;
-  bool tin = false;
-  int ph0 = 0;
+  DtsCell<2> c{};
+  int ph0 = SPIN;
   if (lane < K) {
-    const uint8_t f = fl[a + lane];
-    rn0 = rho[a + lane]; rn1 = mom[a + lane]; hn = h[a + lane];
-    tin = f & F_TINY;
-    ph0 = phase_of(e, rn0);
-    const double theta = tin ? hn / p.h_av : p.theta_nb;  // theta_k = alpha = h_k^n / h_av (R12)
-    dtau = theta * dt;
-    r = dtau / dt;
-    w0 = rn0; w1 = rn1;
-    W0[lane] = w0; W1[lane] = w1; Wu[lane] = w1 / w0;
+    c.un[0] = rho[a + lane]; c.un[1] = mom[a + lane]; c.hn = h[a + lane];
+    const bool tin = fl[a + lane] & F_TINY;
+    ph0 = phase_of(e, c.un[0]);
+    c.theta = tin ? c.hn / p.h_av : p.theta_nb;  // theta_k = alpha = h_k^n / h_av (R12)
+    c.tol = tin ? p.tol_tiny : p.tol_nb;
   }
-  // loop invariants of the relaxed update and of the residual (one reciprocal each)
-  const double i1r = 1.0 / (1.0 + r), qr = r * i1r, rsc = (1.0 + r) / dtau;
-  const double tol_l = tin ? p.tol_tiny : p.tol_nb;  // this lane's stop threshold
-  // phases of U^n by cell (the edges' HLL / boundary choice is fixed for the step)
-  const unsigned vapm = __ballot_sync(0xffffffffu, lane < K && ph0 == VAP);
-  const unsigned liqm = __ballot_sync(0xffffffffu, lane < K && ph0 == LIQ);
-  auto phase_n = [&](int c) { return (vapm >> c & 1u) ? VAP : ((liqm >> c & 1u) ? LIQ : SPIN); };
-  __syncwarp();
-  long long l = 0;
-  int err = 0;
-  bool prev_cont_robust = true;  // decision margin of the last "continue"
-#ifdef EIS_DTS_CLOCK
-  long long dc0 = clock64();
-  if (lane == 0) sh.dclk[3] += 1;
-#endif
-  for (int part = 0; part < 2 && !err; ++part) {  // part 0: Part 1 iterations; part 1: fluxes at U*
-    for (;;) {
-      for (int j0 = 1; j0 < K; j0 += 2) {  // (a) interior edges at W^l, two per round
-        const int j = j0 + half;
-        if (j < K) {
-          const double rl = W0[j - 1], ml = W1[j - 1], rr = W0[j], mr = W1[j], ul = Wu[j - 1], ur = Wu[j];
-          const int pl = phase_n(j - 1), pr = phase_n(j);  // phases of U^n
-          if (pl != pr) {
-            IfaceSol s = iface_solve_hw(e, p, rl, ul, rr, ur, pl == VAP, xs0[j], xs1[j], hmask, hl, half * 16);
-            if (hl == 0) {
-              if (s.iters < 0) err = ST_NEWTON;
-              Fe0[j] = s.F0; Fe1[j] = s.F1; we[j] = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
-              ++solves;
-#ifdef EIS_DTS_CLOCK
-              atomicAdd(reinterpret_cast<unsigned long long*>(&sh.dclk[4]), (unsigned long long)s.iters);
-#endif
-            }
-          } else if (hl == 0) {
-            hll(e, pl, rl, ml, ul, rr, mr, ur, Fe0[j], Fe1[j]);
-            we[j] = 0.0;
-          }
-        }
-      }
-      err = __reduce_max_sync(0xffffffffu, err);
-      __syncwarp();
-#ifdef EIS_DTS_CLOCK
-      { const long long c = clock64(); if (lane == 0) sh.dclk[0] += c - dc0; dc0 = c; }
-#endif
-      if (err || part == 1) break;
-      bool conv = true, rstop = true, rcont = false;  // (b) relaxed moving-cell update (R13) and this lane's residual
-      int bad = 0;
-      if (lane < K) {
-        const double hl_ = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
-        if (!(hl_ > 0.0)) bad = ST_WIDTH;
-        const double ih = 1.0 / hl_, a0 = hn * ih, a1 = dt * ih;
-        const double fL0 = Fe0[lane], fR0 = Fe0[lane + 1], fL1 = Fe1[lane], fR1 = Fe1[lane + 1];
-        const double n0 = w0 * i1r + qr * (a0 * rn0 - a1 * (fR0 - fL0));
-        const double n1 = w1 * i1r + qr * (a0 * rn1 - a1 * (fR1 - fL1));
-        // res = |(1 + r)(W^{l+1} - W^l)| / (dtau max(|W^l|, 1)) < tol, multiplied out (no division)
-        const double d0 = fabs(rsc * (n0 - w0)), d1 = fabs(rsc * (n1 - w1));
-        const double t0 = tol_l * fmax(fabs(w0), 1.0), t1 = tol_l * fmax(fabs(w1), 1.0);
-        conv = d0 < t0 && d1 < t1;
-        // decision margins: the rounding-error bound of W^{l+1} - W^l on the residual's scale
-        const double e0 = MARGIN_EPS * rsc * (fabs(w0) + qr * (fabs(a0 * rn0) + a1 * (fabs(fL0) + fabs(fR0))));
-        const double e1 = MARGIN_EPS * rsc * (fabs(w1) + qr * (fabs(a0 * rn1) + a1 * (fabs(fL1) + fabs(fR1))));
-        rstop = d0 < t0 - e0 && d1 < t1 - e1;
-        rcont = d0 >= t0 + e0 || d1 >= t1 + e1;
-        w0 = n0; w1 = n1;
-        if (!(w0 > 0.0) || phase_of(e, w0) != ph0) bad = bad ? bad : ST_SPINODAL;
-      }
-      // max over tiny cells < tol_tiny and over the others < tol_nb  <=>  every lane below its own
-      conv = __all_sync(0xffffffffu, conv);
-      rstop = __all_sync(0xffffffffu, rstop);
-      rcont = __any_sync(0xffffffffu, rcont);
-      if (conv && (!rstop || !prev_cont_robust)) marg += 1;
-      prev_cont_robust = rcont;
-      bad = __reduce_max_sync(0xffffffffu, bad);
-      if (lane < K) { W0[lane] = w0; W1[lane] = w1; Wu[lane] = w1 / w0; }
-      __syncwarp();
-      ++l;
-#ifdef EIS_DTS_CLOCK
-      { const long long c = clock64(); if (lane == 0) { sh.dclk[1] += c - dc0; sh.dclk[2] += 1; } dc0 = c; }
-#endif
-      if (bad) { err = bad; break; }
-      if (conv) break;
-      if (l >= p.dts_max_iter) { err = ST_DTS_CAP; break; }
-    }
-  }
+  TwoPhaseDts S{e, p, __ballot_sync(0xffffffffu, lane < K && ph0 == VAP), __ballot_sync(0xffffffffu, lane < K && ph0 == LIQ), 0};
+  double u1[2] = {0.0, 0.0}, hn1 = 0.0;
+  const int err = dts_warp(S, sc, K, dt, p.dts_max_iter, c, u1, hn1, it_out, marg);
+  solves += S.solves;
   bool wm = false;  // width decision margin of this lane's cell
-  if (!err && lane < K) {  // Part 2 (b): conservative update with F_left, F*, F_right
-    const double hn1 = __dadd_rn(hn, __dmul_rn(we[lane + 1] - we[lane], dt));
-    if (!(hn1 > 0.0)) err = ST_WIDTH;
-    else {
-      wm = hn1 != hn && (width_marginal(hn1, p.eps_tiny * p.h_av) || width_marginal(hn1, p.eps_split * p.h_av));
-      rho[a + lane] = (hn / hn1) * rn0 - (dt / hn1) * (Fe0[lane + 1] - Fe0[lane]);
-      mom[a + lane] = (hn / hn1) * rn1 - (dt / hn1) * (Fe1[lane + 1] - Fe1[lane]);
-      h[a + lane] = hn1;
-      if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
-    }
+  if (!err && lane < K) {
+    wm = hn1 != c.hn && (width_marginal(hn1, p.eps_tiny * p.h_av) || width_marginal(hn1, p.eps_split * p.h_av));
+    rho[a + lane] = u1[0]; mom[a + lane] = u1[1]; h[a + lane] = hn1;
+    if (hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av) remesh = 1;
   }
   marg += __popc(__ballot_sync(0xffffffffu, wm));
   if (lane >= 1 && lane < K && !err) {  // keep the converged boundary states for the next step
     Ifc* s = const_cast<Ifc*>(find_ifc(sh, a + lane));
-    if (s) { s->pV = xs0[lane]; s->pL = xs1[lane]; }
+    if (s) { s->pV = sc[TwoPhaseDts::XS0 + lane]; s->pL = sc[TwoPhaseDts::XS1 + lane]; }
   }
-  err = __reduce_max_sync(0xffffffffu, err);
   __syncwarp();
-  it_out = l;
   return err;
+}
+
+// The same system for the per-thread loop (dts_thread): one lane owns a whole block; the
+// boundary solver runs on that lane (iface_solve_t, the half warp's iteration in one thread).
+template <int KMAX>
+struct TwoPhaseDtsT {
+  static constexpr int NV = 2;
+  const Eos& e;
+  const Prm& p;
+  unsigned vapm, liqm;  // phases of U^n by cell
+  int solves;
+  double xs0[KMAX + 1], xs1[KMAX + 1];  // star pressures of the interior boundaries (warm starts)
+  double Wu[KMAX];                      // velocities of the iterate
+  __device__ __forceinline__ int phase_n(int c) const { return (vapm >> c & 1u) ? VAP : ((liqm >> c & 1u) ? LIQ : SPIN); }
+  __device__ __forceinline__ int edge(int j, const double (&Wl)[2], const double (&Wr)[2], double (&F)[2], double& w) {
+    const int pl = phase_n(j - 1), pr = phase_n(j);
+    if (pl != pr) {
+      IfaceSol s = iface_solve_t(e, p, Wl[0], Wu[j - 1], Wr[0], Wu[j], pl == VAP, xs0[j], xs1[j]);
+      F[0] = s.F0; F[1] = s.F1; w = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
+      ++solves;
+      return s.iters < 0 ? ST_NEWTON : 0;
+    }
+    hll(e, pl, Wl[0], Wl[1], Wu[j - 1], Wr[0], Wr[1], Wu[j], F[0], F[1]);
+    w = 0.0;
+    return 0;
+  }
+  __device__ __forceinline__ int check(int i, const double (&w)[2]) const {
+    return (!(w[0] > 0.0) || phase_of(e, w[0]) != phase_n(i)) ? ST_SPINODAL : 0;
+  }
+  __device__ __forceinline__ void store(int i, const double (&w)[2]) { Wu[i] = w[1] / w[0]; }
+};
+
+// one DTS job by this thread: U^n, h^n, outer edges and warm starts from the record, results
+// (U^{n+1}, h^{n+1}, converged boundary states, counts, status) back into it
+template <int KMAX>
+__device__ __forceinline__ void run_dts_job(const Eos& e, const Prm& p, DtsJob& J) {
+  const int K = J.K;
+  DtsCell<2> c[KMAX];
+  double Fe[KMAX + 1][2], we[KMAX + 1], u1[KMAX][2], h1[KMAX];
+  TwoPhaseDtsT<KMAX> S{e, p, 0u, 0u, 0};
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    c[i].un[0] = c[i].un[1] = 0.0; c[i].hn = 1.0; c[i].theta = 1.0; c[i].tol = 1.0;
+    if (i < K) {
+      c[i].un[0] = J.un[i][0]; c[i].un[1] = J.un[i][1]; c[i].hn = J.hn[i];
+      const bool tin = (J.tiny >> i) & 1;
+      c[i].theta = tin ? c[i].hn / p.h_av : p.theta_nb;  // theta_k = alpha = h_k^n / h_av (R12)
+      c[i].tol = tin ? p.tol_tiny : p.tol_nb;
+      const int ph = phase_of(e, c[i].un[0]);
+      S.vapm |= (ph == VAP ? 1u : 0u) << i;
+      S.liqm |= (ph == LIQ ? 1u : 0u) << i;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j <= KMAX; ++j) {
+    we[j] = 0.0; Fe[j][0] = Fe[j][1] = 0.0;
+    S.xs0[j] = (j >= 1 && j < K) ? J.xs[j][0] : -1.0;
+    S.xs1[j] = (j >= 1 && j < K) ? J.xs[j][1] : -1.0;
+    if (j == 0) { Fe[0][0] = J.Fo[0][0]; Fe[0][1] = J.Fo[0][1]; we[0] = J.wo[0]; }
+    if (j == K) { Fe[j][0] = J.Fo[1][0]; Fe[j][1] = J.Fo[1][1]; we[j] = J.wo[1]; }
+  }
+  long long it = 0;
+  int marg = 0;
+  const int err = dts_thread<TwoPhaseDtsT<KMAX>, KMAX>(S, K, J.dt, p.dts_max_iter, c, Fe, we, u1, h1, it, marg);
+  J.it = it; J.solves = S.solves; J.status = err; J.marg = marg;
+  if (err) return;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+    if (i < K) { J.un[i][0] = u1[i][0]; J.un[i][1] = u1[i][1]; J.hn[i] = h1[i]; }
+#pragma unroll
+  for (int j = 1; j < KMAX; ++j)
+    if (j < K) { J.xs[j][0] = S.xs0[j]; J.xs[j][1] = S.xs1[j]; }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -773,6 +784,9 @@ struct Zone {
   double dt_given;       // > 0: this dt (tiles: the global CFL step); else the grid's own CFL dt
   double s_given;        // > 0: the S_max of that step (tiles, LTS mode); else the grid's own
   bool left_real, right_real;  // the smem grid ends are domain ends (transmissive, R15)
+  DtsJob* djobs = nullptr;     // window split (step_body<1>): blocks are exported as DTS jobs
+  int* djn = nullptr;          //   job counter
+  int djcap = 0;               //   job capacity
 };
 struct Arr {
   double *rho, *mom, *h, *F0, *F1, *X;
@@ -942,8 +956,44 @@ __device__ __noinline__ void bulk_p2(const Prm& p, const CtaShared& sh, double* 
   }
 }
 
-__device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShared& sh, Arr& A, double t, double t_end,
-                                            const Zone& Z) {
+// window split part B: the results of this window's DTS jobs into the grid (as dts_block's
+// epilogue: cells, width decisions, warm starts, counters of blocks owned by this window)
+__device__ __forceinline__ void apply_dts_jobs(const Prm& p, CtaShared& sh, Arr& A, const Zone& Z, const DtsJob* jobs) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < sh.nblk; ++k) {
+    const int jd = sh.dj[k];
+    if (jd < 0) continue;
+    const DtsJob& J = jobs[jd];
+    const int a = sh.blkA[k], K = J.K;
+    if (J.status) { if (lane == 0) set_status(sh, J.status); continue; }
+    bool wm = false, rm = false;
+    if (lane < K) {
+      const double hn = A.h[a + lane], hn1 = J.hn[lane];
+      wm = hn1 != hn && (width_marginal(hn1, p.eps_tiny * p.h_av) || width_marginal(hn1, p.eps_split * p.h_av));
+      A.rho[a + lane] = J.un[lane][0]; A.mom[a + lane] = J.un[lane][1]; A.h[a + lane] = hn1;
+      rm = hn1 < p.eps_tiny * p.h_av || hn1 > p.eps_split * p.h_av;
+    }
+    if (lane >= 1 && lane < K) {  // keep the converged boundary states for the next step
+      Ifc* f = const_cast<Ifc*>(find_ifc(sh, a + lane));
+      if (f) { f->pV = J.xs[lane][0]; f->pL = J.xs[lane][1]; }
+    }
+    const int mg = J.marg + __popc(__ballot_sync(0xffffffffu, wm));
+    if (__any_sync(0xffffffffu, rm) && lane == 0) sh.remesh = 1;
+    if (a >= Z.own_lo && a < Z.own_hi && lane == 0) {  // count a block once (its first cell's owner)
+      sh.c_dts += (unsigned long long)J.it; sh.c_regions += 1ull;
+      if ((unsigned long long)J.it > sh.c_dtsmax) sh.c_dtsmax = (unsigned long long)J.it;
+      sh.c_margin += (unsigned long long)mg;
+      sh.c_solves += (unsigned long long)J.solves;
+    }
+    __syncwarp();
+  }
+  for (int k = lane; k < sh.nifc; k += 32) { sh.ws0[k] = sh.ifc[k].pV; sh.ws1[k] = sh.ifc[k].pL; }
+  __syncwarp();
+}
+
+// The end of a large step: status check, remesh (a10; R9, R10), counters and the new cell count.
+__device__ __forceinline__ double step_tail(const Eos& e, const Prm& p, CtaShared& sh, Arr& A, int n, const int ntrg,
+                                            const double dt, const Zone& Z) {
   double* const rho = A.rho;
   double* const mom = A.mom;
   double* const h = A.h;
@@ -951,8 +1001,169 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
   double* const F1 = A.F1;
   double* const X = A.X;
   uint8_t* const fl = A.fl;
-  int n = A.n;
   const int C = A.C;
+  const int tid = threadIdx.x, T = blockDim.x;
+  {
+    const int stop2 = sh.status;
+    __syncthreads();
+    if (stop2) return -1.0;
+  }
+  // ---------------- remesh (a10; R9, R10): events -> shifts -> scatter ----------------
+  int n_new = n;
+  EIS_FCLK(5);
+  if (sh.remesh) {
+    if (tid == 0) { sh.nmev = 0; sh.nsev = 0; sh.ngrp = 0; }
+    __syncthreads();
+    for (int i = tid; i < n; i += T) {
+      const double r_ = rho[i];
+      const int ph = phase_of(e, r_);
+      if (!(r_ > 0.0)) zone_status(sh, Z, i, ST_NONPOS);
+      else if (ph == SPIN) zone_status(sh, Z, i, ST_SPINODAL);
+      if (h[i] < p.eps_tiny * p.h_av) {  // merge partner: same-phase neighbour; both -> smaller, ties left
+        const bool sl = i > 0 && !created_at(sh, ntrg, i) && phase_of(e, rho[i - 1]) == ph;
+        const bool sr = i < n - 1 && !created_at(sh, ntrg, i + 1) && phase_of(e, rho[i + 1]) == ph;
+        int j = -1;
+        if (sl && sr) j = (h[i + 1] < h[i - 1]) ? i : i - 1;
+        else if (sl) j = i - 1;
+        else if (sr) j = i;
+        if (j >= 0) { const int k = atomicAdd(&sh.nmev, 1); if (k < MAXEV) sh.mev[k] = j; else set_status(sh, ST_CAPACITY); }
+      }
+      if (h[i] > p.eps_split * p.h_av) {
+        const int k = atomicAdd(&sh.nsev, 1);
+        if (k < MAXEV) sh.sev[k] = i; else set_status(sh, ST_CAPACITY);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && sh.status == 0) {  // small serial bookkeeping: groups, splits, new size
+      int nm = sh.nmev, ns = sh.nsev;
+      for (int a = 1; a < nm; ++a) { int v = sh.mev[a], b = a - 1; while (b >= 0 && sh.mev[b] > v) { sh.mev[b + 1] = sh.mev[b]; --b; } sh.mev[b + 1] = v; }
+      for (int a = 1; a < ns; ++a) { int v = sh.sev[a], b = a - 1; while (b >= 0 && sh.sev[b] > v) { sh.sev[b + 1] = sh.sev[b]; --b; } sh.sev[b + 1] = v; }
+      int ng = 0, merges = 0, splits = 0, im = 0, is = 0;
+      // walk merge edges (deduplicated) and split cells in increasing cell order
+      while (im < nm || is < ns) {
+        const int jm = im < nm ? sh.mev[im] : (1 << 29), js = is < ns ? sh.sev[is] : (1 << 29);
+        Grp gr;
+        if (jm <= js) {  // merge group [jm, g1]: consecutive merge edges (R10)
+          int g1 = jm + 1;
+          ++im;
+          while (im < nm && sh.mev[im] <= g1) { if (sh.mev[im] == g1) ++g1; ++im; }
+          double hs = 0.0, s0 = 0.0, s1 = 0.0;
+          for (int k = jm; k <= g1; ++k) { hs += h[k]; s0 += h[k] * rho[k]; s1 += h[k] * mom[k]; }
+          gr.g0 = jm; gr.g1 = g1; gr.h = hs; gr.r = s0 / hs; gr.m = s1 / hs;
+          gr.split = hs > p.eps_split * p.h_av;
+          merges += g1 - jm;
+          while (is < ns && sh.sev[is] <= g1) ++is;  // split candidates inside the group
+        } else {
+          gr.g0 = gr.g1 = js; gr.h = h[js]; gr.r = rho[js]; gr.m = mom[js]; gr.split = 1;
+          ++is;
+        }
+        splits += gr.split;
+        if (ng < MAXEV) sh.grp[ng++] = gr; else set_status(sh, ST_CAPACITY);
+      }
+      sh.ngrp = ng;
+      int ncre = 0;
+      for (int k = 0; k < ntrg; ++k) ncre += sh.trg[k].acc;
+      int nn = n + ncre;
+      for (int k = 0; k < ng; ++k) nn += sh.grp[k].split - (sh.grp[k].g1 - sh.grp[k].g0);
+      if (nn > C) set_status(sh, ST_CAPACITY);
+      sh.n_new = nn;
+      sh.c_merges += merges;
+      sh.c_splits += splits;
+    }
+    __syncthreads();
+    if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
+    __syncthreads();
+    if (sh.status == 0 && (sh.ngrp > 0 || sh.c_creations > 0)) {
+      if (tid == 0) { sh.olo = 1 << 30; sh.ohi = -1; }
+      __syncthreads();
+      for (int i = tid; i < n; i += T) {  // scatter into (F0, F1, X)
+        int kg = -1;
+        for (int k = 0; k < sh.ngrp; ++k)
+          if (sh.grp[k].g0 <= i && i <= sh.grp[k].g1) kg = k;
+        if (kg >= 0 && sh.grp[kg].g0 != i) continue;  // merged into its group head
+        int pos = i + remesh_shift(sh, ntrg, i);
+        if (created_at(sh, ntrg, i)) {  // created cell, width (w_r - w_l) dt
+          const Trg* tr = find_trg(sh, ntrg, i);
+          F0[pos - 1] = tr->rB; F1[pos - 1] = tr->mB; X[pos - 1] = (tr->wr - tr->wl) * dt;
+          if (Z.own_lo < i && i <= Z.own_hi) {  // owned edge
+            atomicMin(&sh.olo, pos - 1); atomicMax(&sh.ohi, pos); atomicAdd(&sh.o_cre, 1);
+          }
+        }
+        if (Z.own_lo <= i && i < Z.own_hi) {  // owned head: its outputs are owned
+          atomicMin(&sh.olo, pos);
+          atomicMax(&sh.ohi, pos + ((kg >= 0 && sh.grp[kg].split) ? 2 : 1));
+          if (kg >= 0) { atomicAdd(&sh.o_merges, sh.grp[kg].g1 - sh.grp[kg].g0); atomicAdd(&sh.o_splits, sh.grp[kg].split); }
+        }
+        if (kg >= 0) {
+          const Grp& gr = sh.grp[kg];
+          if (gr.split) {
+            const double hh = 0.5 * gr.h;
+            F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = hh;
+            F0[pos + 1] = gr.r; F1[pos + 1] = gr.m; X[pos + 1] = hh;
+          } else { F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = gr.h; }
+        } else { F0[pos] = rho[i]; F1[pos] = mom[i]; X[pos] = h[i]; }
+      }
+      // boundary list: old boundaries shift with their right cell; each creation adds two
+      __syncthreads();
+      if (tid == 0) {
+        int nif = sh.nifc;
+        for (int k = 0; k < nif; ++k) sh.ifc[k].e += remesh_shift(sh, ntrg, sh.ifc[k].e);
+        for (int k = 0; k < ntrg; ++k) {
+          if (!sh.trg[k].acc) continue;
+          const int pc = sh.trg[k].e + remesh_shift(sh, ntrg, sh.trg[k].e) - 1;  // created cell
+          for (int q = 0; q < 2; ++q) {
+            if (nif >= MAXIF) { set_status(sh, ST_CAPACITY); break; }
+            int b = nif - 1;
+            while (b >= 0 && sh.ifc[b].e > pc + q) { sh.ifc[b + 1] = sh.ifc[b]; --b; }
+            sh.ifc[b + 1].e = pc + q;
+            ++nif;
+          }
+        }
+        sh.nifc = nif;
+        if (sh.c_creations) sh.wsn = -1;  // ordinals changed: no warm start next step
+        sh.nblk = 0;                      // flags are rebuilt below
+      }
+      n_new = sh.n_new;
+      __syncthreads();
+      for (int i = tid; i < n_new; i += T) { rho[i] = F0[i]; mom[i] = F1[i]; h[i] = X[i]; }  // copy back
+      for (int i = tid; i <= C; i += T) fl[i] = 0;
+      __syncthreads();
+      for (int k = tid; k < sh.nifc; k += T) fl[sh.ifc[k].e] = F_IF;
+    }
+  }
+  __syncthreads();
+  EIS_FCLK(6);
+  if (tid == 0) {
+    EIS_TCLK(5);
+    MemberStats& st = sh.st;
+    st.steps += 1;
+    st.cell_updates += n;
+    st.creations += sh.o_cre;
+    st.merges += sh.o_merges;
+    st.splits += sh.o_splits;
+    if (st.steps == 1 || dt < st.dt_min) st.dt_min = dt;
+    if (dt > st.dt_max) st.dt_max = dt;
+    sh.n = n_new;
+    sh.ntrg = 0; sh.remesh = 0;
+    sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
+    sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
+  }
+  n = n_new;
+  A.n = n;
+  __syncthreads();
+  return dt;
+  }
+
+template <int PH = 0>  // 0: the whole step; 1: window split part A (blocks exported as DTS jobs, no remesh)
+__device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShared& sh, Arr& A, double t, double t_end,
+                                            const Zone& Z) {
+  double* const rho = A.rho;
+  double* const mom = A.mom;
+  double* const h = A.h;
+  double* const F0 = A.F0;
+  double* const F1 = A.F1;
+  uint8_t* const fl = A.fl;
+  int n = A.n;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const int SW = nw - 1;  // solver warp
   const int half = lane >> 4, hl = lane & 15;
@@ -1070,6 +1281,36 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       if (lane == 0) sh.tclk[6] = clock64();
 #endif
       const int nblk = sh.nblk;
+      if constexpr (PH == 1) {  // window split: each block becomes a DTS job (dts_jobs, one lane)
+        for (int k = 0; k < nblk; ++k) {
+          const int a = sh.blkA[k], b = sh.blkB[k], K = b - a + 1;
+          if (lane == 0) sh.dj[k] = -1;
+          if (b < Z.zlo || a >= Z.zhi) continue;  // a block wholly in the halo is not needed
+          if (K > MAXB || b < a) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
+          int jd = 0;
+          if (lane == 0) jd = atomicAdd(Z.djn, 1);
+          jd = __shfl_sync(0xffffffffu, jd, 0);
+          if (jd >= Z.djcap) { if (lane == 0) set_status(sh, ST_CAPACITY); continue; }
+          DtsJob& J = Z.djobs[jd];
+          if (lane < K) { J.un[lane][0] = rho[a + lane]; J.un[lane][1] = mom[a + lane]; J.hn[lane] = h[a + lane]; }
+          if (lane >= 1 && lane < K) {  // warm start of interior boundaries from the last step
+            const Ifc* f = find_ifc(sh, a + lane);
+            J.xs[lane][0] = f ? f->pV : -1.0;
+            J.xs[lane][1] = f ? f->pL : -1.0;
+          }
+          const unsigned tb = __ballot_sync(0xffffffffu, lane < K && (fl[a + lane] & F_TINY));
+          if (lane == 0) {  // outer edges: the explicit step's fluxes and speeds
+            double g0, g1, w;
+            edge_view(sh, fl, F0, F1, a, 1, g0, g1, w);
+            J.Fo[0][0] = g0; J.Fo[0][1] = g1; J.wo[0] = w;
+            edge_view(sh, fl, F0, F1, b + 1, 0, g0, g1, w);
+            J.Fo[1][0] = g0; J.Fo[1][1] = g1; J.wo[1] = w;
+            J.dt = dt; J.K = K; J.tiny = (int)tb;
+            sh.dj[k] = jd;
+          }
+          __syncwarp();
+        }
+      } else
       for (int k = 0; k < nblk; ++k) {
         const int a = sh.blkA[k], b = sh.blkB[k];
         if (b < Z.zlo || a >= Z.zhi) continue;  // tiles: a block wholly in the halo is not needed
@@ -1160,155 +1401,13 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
       if (tid == 0) sh.remesh = 1;
       __syncthreads();
     }
-    {
+    if constexpr (PH == 1) {  // window split, part A: the blocks were exported; remesh after the DTS jobs
       const int stop2 = sh.status;
       __syncthreads();
-      if (stop2) return -1.0;
+      return stop2 ? -1.0 : dt;
+    } else {
+      return step_tail(e, p, sh, A, n, ntrg, dt, Z);
     }
-    // ---------------- remesh (a10; R9, R10): events -> shifts -> scatter ----------------
-    int n_new = n;
-    EIS_FCLK(5);
-    if (sh.remesh) {
-      if (tid == 0) { sh.nmev = 0; sh.nsev = 0; sh.ngrp = 0; }
-      __syncthreads();
-      for (int i = tid; i < n; i += T) {
-        const double r_ = rho[i];
-        const int ph = phase_of(e, r_);
-        if (!(r_ > 0.0)) zone_status(sh, Z, i, ST_NONPOS);
-        else if (ph == SPIN) zone_status(sh, Z, i, ST_SPINODAL);
-        if (h[i] < p.eps_tiny * p.h_av) {  // merge partner: same-phase neighbour; both -> smaller, ties left
-          const bool sl = i > 0 && !created_at(sh, ntrg, i) && phase_of(e, rho[i - 1]) == ph;
-          const bool sr = i < n - 1 && !created_at(sh, ntrg, i + 1) && phase_of(e, rho[i + 1]) == ph;
-          int j = -1;
-          if (sl && sr) j = (h[i + 1] < h[i - 1]) ? i : i - 1;
-          else if (sl) j = i - 1;
-          else if (sr) j = i;
-          if (j >= 0) { const int k = atomicAdd(&sh.nmev, 1); if (k < MAXEV) sh.mev[k] = j; else set_status(sh, ST_CAPACITY); }
-        }
-        if (h[i] > p.eps_split * p.h_av) {
-          const int k = atomicAdd(&sh.nsev, 1);
-          if (k < MAXEV) sh.sev[k] = i; else set_status(sh, ST_CAPACITY);
-        }
-      }
-      __syncthreads();
-      if (tid == 0 && sh.status == 0) {  // small serial bookkeeping: groups, splits, new size
-        int nm = sh.nmev, ns = sh.nsev;
-        for (int a = 1; a < nm; ++a) { int v = sh.mev[a], b = a - 1; while (b >= 0 && sh.mev[b] > v) { sh.mev[b + 1] = sh.mev[b]; --b; } sh.mev[b + 1] = v; }
-        for (int a = 1; a < ns; ++a) { int v = sh.sev[a], b = a - 1; while (b >= 0 && sh.sev[b] > v) { sh.sev[b + 1] = sh.sev[b]; --b; } sh.sev[b + 1] = v; }
-        int ng = 0, merges = 0, splits = 0, im = 0, is = 0;
-        // walk merge edges (deduplicated) and split cells in increasing cell order
-        while (im < nm || is < ns) {
-          const int jm = im < nm ? sh.mev[im] : (1 << 29), js = is < ns ? sh.sev[is] : (1 << 29);
-          Grp gr;
-          if (jm <= js) {  // merge group [jm, g1]: consecutive merge edges (R10)
-            int g1 = jm + 1;
-            ++im;
-            while (im < nm && sh.mev[im] <= g1) { if (sh.mev[im] == g1) ++g1; ++im; }
-            double hs = 0.0, s0 = 0.0, s1 = 0.0;
-            for (int k = jm; k <= g1; ++k) { hs += h[k]; s0 += h[k] * rho[k]; s1 += h[k] * mom[k]; }
-            gr.g0 = jm; gr.g1 = g1; gr.h = hs; gr.r = s0 / hs; gr.m = s1 / hs;
-            gr.split = hs > p.eps_split * p.h_av;
-            merges += g1 - jm;
-            while (is < ns && sh.sev[is] <= g1) ++is;  // split candidates inside the group
-          } else {
-            gr.g0 = gr.g1 = js; gr.h = h[js]; gr.r = rho[js]; gr.m = mom[js]; gr.split = 1;
-            ++is;
-          }
-          splits += gr.split;
-          if (ng < MAXEV) sh.grp[ng++] = gr; else set_status(sh, ST_CAPACITY);
-        }
-        sh.ngrp = ng;
-        int ncre = 0;
-        for (int k = 0; k < ntrg; ++k) ncre += sh.trg[k].acc;
-        int nn = n + ncre;
-        for (int k = 0; k < ng; ++k) nn += sh.grp[k].split - (sh.grp[k].g1 - sh.grp[k].g0);
-        if (nn > C) set_status(sh, ST_CAPACITY);
-        sh.n_new = nn;
-        sh.c_merges += merges;
-        sh.c_splits += splits;
-      }
-      __syncthreads();
-      if (tid == 0) { sh.olo = Z.own_lo; sh.ohi = Z.own_hi; }
-      __syncthreads();
-      if (sh.status == 0 && (sh.ngrp > 0 || sh.c_creations > 0)) {
-        if (tid == 0) { sh.olo = 1 << 30; sh.ohi = -1; }
-        __syncthreads();
-        for (int i = tid; i < n; i += T) {  // scatter into (F0, F1, X)
-          int kg = -1;
-          for (int k = 0; k < sh.ngrp; ++k)
-            if (sh.grp[k].g0 <= i && i <= sh.grp[k].g1) kg = k;
-          if (kg >= 0 && sh.grp[kg].g0 != i) continue;  // merged into its group head
-          int pos = i + remesh_shift(sh, ntrg, i);
-          if (created_at(sh, ntrg, i)) {  // created cell, width (w_r - w_l) dt
-            const Trg* tr = find_trg(sh, ntrg, i);
-            F0[pos - 1] = tr->rB; F1[pos - 1] = tr->mB; X[pos - 1] = (tr->wr - tr->wl) * dt;
-            if (Z.own_lo < i && i <= Z.own_hi) {  // owned edge
-              atomicMin(&sh.olo, pos - 1); atomicMax(&sh.ohi, pos); atomicAdd(&sh.o_cre, 1);
-            }
-          }
-          if (Z.own_lo <= i && i < Z.own_hi) {  // owned head: its outputs are owned
-            atomicMin(&sh.olo, pos);
-            atomicMax(&sh.ohi, pos + ((kg >= 0 && sh.grp[kg].split) ? 2 : 1));
-            if (kg >= 0) { atomicAdd(&sh.o_merges, sh.grp[kg].g1 - sh.grp[kg].g0); atomicAdd(&sh.o_splits, sh.grp[kg].split); }
-          }
-          if (kg >= 0) {
-            const Grp& gr = sh.grp[kg];
-            if (gr.split) {
-              const double hh = 0.5 * gr.h;
-              F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = hh;
-              F0[pos + 1] = gr.r; F1[pos + 1] = gr.m; X[pos + 1] = hh;
-            } else { F0[pos] = gr.r; F1[pos] = gr.m; X[pos] = gr.h; }
-          } else { F0[pos] = rho[i]; F1[pos] = mom[i]; X[pos] = h[i]; }
-        }
-        // boundary list: old boundaries shift with their right cell; each creation adds two
-        __syncthreads();
-        if (tid == 0) {
-          int nif = sh.nifc;
-          for (int k = 0; k < nif; ++k) sh.ifc[k].e += remesh_shift(sh, ntrg, sh.ifc[k].e);
-          for (int k = 0; k < ntrg; ++k) {
-            if (!sh.trg[k].acc) continue;
-            const int pc = sh.trg[k].e + remesh_shift(sh, ntrg, sh.trg[k].e) - 1;  // created cell
-            for (int q = 0; q < 2; ++q) {
-              if (nif >= MAXIF) { set_status(sh, ST_CAPACITY); break; }
-              int b = nif - 1;
-              while (b >= 0 && sh.ifc[b].e > pc + q) { sh.ifc[b + 1] = sh.ifc[b]; --b; }
-              sh.ifc[b + 1].e = pc + q;
-              ++nif;
-            }
-          }
-          sh.nifc = nif;
-          if (sh.c_creations) sh.wsn = -1;  // ordinals changed: no warm start next step
-          sh.nblk = 0;                      // flags are rebuilt below
-        }
-        n_new = sh.n_new;
-        __syncthreads();
-        for (int i = tid; i < n_new; i += T) { rho[i] = F0[i]; mom[i] = F1[i]; h[i] = X[i]; }  // copy back
-        for (int i = tid; i <= C; i += T) fl[i] = 0;
-        __syncthreads();
-        for (int k = tid; k < sh.nifc; k += T) fl[sh.ifc[k].e] = F_IF;
-      }
-    }
-    __syncthreads();
-    EIS_FCLK(6);
-    if (tid == 0) {
-      EIS_TCLK(5);
-      MemberStats& st = sh.st;
-      st.steps += 1;
-      st.cell_updates += n;
-      st.creations += sh.o_cre;
-      st.merges += sh.o_merges;
-      st.splits += sh.o_splits;
-      if (st.steps == 1 || dt < st.dt_min) st.dt_min = dt;
-      if (dt > st.dt_max) st.dt_max = dt;
-      sh.n = n_new;
-      sh.ntrg = 0; sh.remesh = 0;
-      sh.c_merges = 0; sh.c_splits = 0; sh.c_creations = 0;
-      sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
-    }
-    n = n_new;
-    A.n = n;
-    __syncthreads();
-    return dt;
   }
 
 // ------------------------------------------------------------------------------------------

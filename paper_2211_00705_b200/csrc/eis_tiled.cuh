@@ -55,11 +55,16 @@ struct Tiles {
   int poll;                        // a window kernel polls beside tiled_fast (EIS_WIN_POLL_PER_SM)
   int M, tpm;                      // members (independent grids) and tiles per member: tile k
                                    // belongs to member k / tpm; halos never cross members
+  int split;                       // window split: part A, dts_jobs (one lane per block), part B
+  int djcap;                       //   DTS job capacity
+  DtsJob* djobs;                   //   DTS jobs of the step (counter ctl[10])
+  unsigned char* wsave;            //   per window job: its grid between parts A and B (WSAVE bytes)
 };
 constexpr int SCS = 8, MCS = 4;
 // ctl: [1] any member status  [2] done-counter  [3] launches  [4] tile-list length  [5] next tile job
 //      [6] window-list length  [7] next window job  [8] window jobs of the last step
 //      [9] tiled_fast CTAs finished (the window kernel running beside tiled_fast polls it)
+//      [10] DTS jobs of the step (window split)  [11] next window job of part B
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -109,7 +114,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
     tl.ctl[8] = tl.ctl[6];  // window jobs of this step (diagnostics)
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
     if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
       tl.xbuf[XB_DT] = -s;
       tl.xbuf[XB_DT + 1] = hm;
@@ -688,19 +693,50 @@ __device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, doubl
   }
 }
 
+// Window split (tl.split): part A (PH = 1) runs the step body up to the remesh with the blocks
+// exported as DTS jobs and saves the window (CtaShared, n, dt, rho / mom / h) to the job's
+// slot; dts_jobs solves every job of the step, one lane each; part B (PH = 2) restores the slot,
+// applies the DTS results, finishes the step (remesh) and assembles the tile output.
+constexpr size_t WSAVE_SH = (sizeof(CtaShared) + 15) & ~size_t(15);
+constexpr size_t WSAVE = WSAVE_SH + 16 + 3 * 8 * (size_t)WCAP;
+__device__ __forceinline__ void window_save(const Tiles& tl, const CtaShared& sh, const Arr& A, int j, double dt) {
+  unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&sh);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(slot);
+  for (int i = threadIdx.x; i < (int)(sizeof(CtaShared) / 8); i += blockDim.x) dst[i] = src[i];
+  double* d = reinterpret_cast<double*>(slot + WSAVE_SH);
+  if (threadIdx.x == 0) { d[0] = (double)A.n; d[1] = dt; }
+  for (int i = threadIdx.x; i < A.n; i += blockDim.x) {
+    d[2 + i] = A.rho[i]; d[2 + WCAP + i] = A.mom[i]; d[2 + 2 * WCAP + i] = A.h[i];
+  }
+}
+__device__ __forceinline__ double window_restore(const Tiles& tl, CtaShared& sh, Arr& A, int j) {
+  const unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(slot);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sh);
+  for (int i = threadIdx.x; i < (int)(sizeof(CtaShared) / 8); i += blockDim.x) dst[i] = src[i];
+  const double* d = reinterpret_cast<const double*>(slot + WSAVE_SH);
+  const int n = (int)d[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    A.rho[i] = d[2 + i]; A.mom[i] = d[2 + WCAP + i]; A.h[i] = d[2 + 2 * WCAP + i];
+  }
+  A.n = n;
+  return d[1];
+}
+
 // PF: after the step body, thread 0 claims the next window job and loads its list entry into
 // registers (jn, kn, wan, wbn; jn = -1 when the list is exhausted); the loads complete during the
 // assembly and the caller publishes them, so the next job starts without those round trips.
-template <bool PF>
+template <bool PF, int PH = 0>
 __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
-                                            int k, int wa, int wb, double t_end, int& jn, int& kn, int& wan,
+                                            int j, int k, int wa, int wb, double t_end, int& jn, int& kn, int& wan,
                                             int& wbn) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const TGeo g = tile_geo_spec(tl, k);
   const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int nL = g.nL, cnt = g.cnt;
   const int s0 = max(0, wa - HALO), s1 = min(g.n, wb + HALO), n = s1 - s0;
-  if (tid == 0) {
+  if (PH != 2 && tid == 0) {
     sh.status = 0;
     reset_counters(sh);
     memset(&sh.st, 0, sizeof(sh.st));
@@ -712,23 +748,25 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     for (int q = 0; q < MAXIF; ++q) { sh.ws0[q] = ws[q]; sh.ws1[q] = ws[MAXIF + q]; }
   }
   const int huL = g.huL, huR = g.huR;
-  for (int i = tid; i < n; i += T) {
-    const int v = s0 + i;
-    long long mo;
-    const double* pr = vcell(tl, g, v, mo);
-    A.rho[i] = pr[0];
-    A.mom[i] = pr[mo];
-    double hh;
-    if (v < nL) hh = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + v]);
-    else if (v < nL + cnt) hh = g.hu_in ? p.h_av : tl.h[g.in][g.base + v - nL];
-    else hh = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + v - nL - cnt]);
-    A.h[i] = hh;
+  if (PH != 2) {
+    for (int i = tid; i < n; i += T) {
+      const int v = s0 + i;
+      long long mo;
+      const double* pr = vcell(tl, g, v, mo);
+      A.rho[i] = pr[0];
+      A.mom[i] = pr[mo];
+      double hh;
+      if (v < nL) hh = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + v]);
+      else if (v < nL + cnt) hh = g.hu_in ? p.h_av : tl.h[g.in][g.base + v - nL];
+      else hh = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + v - nL - cnt]);
+      A.h[i] = hh;
+    }
+    for (int i = tid; i <= capw; i += T) A.fl[i] = 0;
+    A.n = n;
+    __syncthreads();
+    if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, n);
+    __syncthreads();
   }
-  for (int i = tid; i <= capw; i += T) A.fl[i] = 0;
-  A.n = n;
-  __syncthreads();
-  if (warp == nw - 1) build_boundary_list(e, sh, A.rho, A.fl, n);
-  __syncthreads();
   EIS_TCLK(0);
   Zone Z;
   Z.own_lo = wa - s0; Z.own_hi = wb - s0;
@@ -737,9 +775,31 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   Z.s_given = tl.scal[SCS * g.m + 5];
   Z.left_real = (g.first && !tl.nbr_left && s0 == 0);
   Z.right_real = (g.last && !tl.nbr_right && s1 == g.n);
-  const double dt = step_body(e, p, sh, A, t, t_end, Z);
+  Z.djobs = tl.djobs; Z.djn = &tl.ctl[10]; Z.djcap = tl.djcap;
+  double dt;
+  if constexpr (PH == 0) {
+    dt = step_body<0>(e, p, sh, A, t, t_end, Z);
+  } else if constexpr (PH == 1) {  // part A: up to the remesh, blocks exported; the window saved
+    dt = step_body<1>(e, p, sh, A, t, t_end, Z);
+    window_save(tl, sh, A, j, dt);
+    if (PF && tid == 0) {
+      jn = atomicAdd(&tl.ctl[7], 1);
+      if (jn < tl.ctl[6]) { kn = tl.wlist[4 * jn]; wan = tl.wlist[4 * jn + 1]; wbn = tl.wlist[4 * jn + 2]; }
+      else jn = -1;
+    }
+    __syncthreads();
+    return;
+  } else {  // part B: the saved window, the DTS results, the rest of the step
+    dt = window_restore(tl, sh, A, j);
+    __syncthreads();
+    if (dt >= 0.0 && sh.status == 0) {
+      apply_dts_jobs(p, sh, A, Z, tl.djobs);
+      __syncthreads();
+      dt = step_tail(e, p, sh, A, A.n, sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG, dt, Z);
+    }
+  }
   if (PF && tid == 0) {
-    jn = atomicAdd(&tl.ctl[7], 1);
+    jn = atomicAdd(&tl.ctl[PH == 2 ? 11 : 7], 1);
     if (jn < tl.ctl[6]) { kn = tl.wlist[4 * jn]; wan = tl.wlist[4 * jn + 1]; wbn = tl.wlist[4 * jn + 2]; }
     else jn = -1;
   }
@@ -846,10 +906,24 @@ __device__ __forceinline__ void window_dbg(const Tiles& tl, const CtaShared& sh,
 // tiled_fast on a second stream): a job index is waited for until its entry carries this step's
 // tag, or until every tiled_fast CTA has finished and the index is past the list (or a status
 // was raised).  The instance launched after tiled_fast (POLL = false) drains the same list.
-template <int MAXT, int MINB, bool POLL>
+// dts_jobs (window split): Algorithm 2 on every block exported by the window kernel's part A
+// this step, one lane per block (dts_thread: the boundary solves of a block run on its lane),
+// so the blocks of all windows iterate side by side instead of one block per window warp.
+__global__ void __launch_bounds__(32)
+dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl) {
+  const int n = tl.ctl[10] < tl.djcap ? tl.ctl[10] : tl.djcap;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    DtsJob& J = tl.djobs[q];
+    if (J.K == 3) run_dts_job<3>(e, p, J);  // one tiny cell: the usual block
+    else run_dts_job<MAXB>(e, p, J);
+  }
+}
+
+template <int MAXT, int MINB, bool POLL, int PH = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
           double t_end) {
+  static_assert(!POLL || PH == 0, "the polling instance runs the whole window step");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
   Arr A = carve(smem_raw, WCAP);
@@ -858,7 +932,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   volatile int* vctl = tl.ctl;
   if constexpr (!POLL) {  // the next job is claimed during the current one's assembly (tile_window<true>)
     if (tid == 0) {
-      const int j = atomicAdd(&tl.ctl[7], 1);
+      const int j = atomicAdd(&tl.ctl[PH == 2 ? 11 : 7], 1);
       const bool ok = j < tl.ctl[6];
       sh.pf_j = ok ? j : -1;
       if (ok) { sh.pf_k = tl.wlist[4 * j]; sh.pf_wa = tl.wlist[4 * j + 1]; sh.pf_wb = tl.wlist[4 * j + 2]; }
@@ -870,7 +944,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       __syncthreads();  // every lane has read the job before thread 0 replaces it
       const long long c0 = clock64();
       int jn = -1, kn = 0, wan = 0, wbn = 0;
-      tile_window<true>(e, p, tl, sh, A, WCAP, k, wa, wb, t_end, jn, kn, wan, wbn);
+      tile_window<true, PH>(e, p, tl, sh, A, WCAP, j, k, wa, wb, t_end, jn, kn, wan, wbn);
       if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, wa, wb, c0);
       if (tid == 0) { sh.pf_j = jn; sh.pf_k = kn; sh.pf_wa = wan; sh.pf_wb = wbn; }
       __syncthreads();
@@ -908,7 +982,7 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       if (j < 0) break;
       const long long c0 = clock64();
       int jn, kn, wan, wbn;
-      tile_window<false>(e, p, tl, sh, A, WCAP, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
+      tile_window<false>(e, p, tl, sh, A, WCAP, j, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
                          wan, wbn);
       if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
     }
@@ -931,7 +1005,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   const bool one = tl.M == 1;  // one grid: this kernel folds the CFL partials and ends the step
   const double t = tl.scal[0], dt_given = tl.scal[1];
   if (one && (tl.mctl[1] != 0 || !(t < t_end))) {  // uniform across the grid: nothing to do
-    if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }  // (a no-op step's counters)
+    if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }  // (a no-op step's counters)
     return;
   }
   double dt = dt_given;
@@ -972,7 +1046,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (last) {
     __threadfence();
     if (tl.mctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
-    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; }
+    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }
   }
 }
 
@@ -1071,7 +1145,7 @@ __global__ void tiled_members_finish(const __grid_constant__ Prm p, const __grid
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     tl.ctl[8] = tl.ctl[6];
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
+    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
     if (after_step) tl.ctl[3] += 1;
   }
   if (m >= tl.M) return;
@@ -1129,7 +1203,7 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
     tl.mctl[2] += 1;
     tl.ctl[3] += 1;
   }
-  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0;
+  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
   double dt = p.cfl * hm / S;
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;
