@@ -95,6 +95,8 @@ struct CtaShared {
   int olo, ohi;  // tiles: owned output range after the remesh
   int pf_j, pf_k, pf_wa, pf_wb;  // tiles: the next window job, claimed during the current one
   int fbits;     // tiles: phase bits of the smem grid (fast-path test)
+  int sv_n;      // window split: the grid's cell count and dt, saved with it between parts A and B
+  double sv_dt;
   int o_cre, o_merges, o_splits;  // events owned by this grid (tiles: not the halo's)
   unsigned long long c_dts, c_solves, c_regions, c_dtsmax, c_margin;
   MemberStats st;

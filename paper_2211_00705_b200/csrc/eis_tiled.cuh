@@ -210,6 +210,9 @@ __device__ __forceinline__ const double* vcell(const Tiles& tl, const TGeo& g, i
 #ifndef EIS_FAST_PIPE
 #define EIS_FAST_PIPE 0
 #endif
+// (Measured, round 2: four cells per lane -- 120-cell windows, 80 registers, 6 CTAs/SM, no
+// spills -- is 20 % slower on C5 (1.22 vs 1.01 ms): the kernel needs the warps more than it saves
+// on shuffles and per-window overhead.)
 constexpr int FB = EIS_FB;  // windows per warp per batch
 constexpr int FW = 60;      // cells updated per window: the pairs of lanes 1..30
 
@@ -698,30 +701,41 @@ __device__ __forceinline__ void fast_part_pass(const Eos& e, double* orho, doubl
 // slot; dts_jobs solves every job of the step, one lane each; part B (PH = 2) restores the slot,
 // applies the DTS results, finishes the step (remesh) and assembles the tile output.
 constexpr size_t WSAVE_SH = (sizeof(CtaShared) + 15) & ~size_t(15);
-constexpr size_t WSAVE = WSAVE_SH + 16 + 3 * 8 * (size_t)WCAP;
-__device__ __forceinline__ void window_save(const Tiles& tl, const CtaShared& sh, const Arr& A, int j, double dt) {
-  unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&sh);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(slot);
-  for (int i = threadIdx.x; i < (int)(sizeof(CtaShared) / 8); i += blockDim.x) dst[i] = src[i];
-  double* d = reinterpret_cast<double*>(slot + WSAVE_SH);
-  if (threadIdx.x == 0) { d[0] = (double)A.n; d[1] = dt; }
-  for (int i = threadIdx.x; i < A.n; i += blockDim.x) {
-    d[2 + i] = A.rho[i]; d[2 + WCAP + i] = A.mom[i]; d[2 + 2 * WCAP + i] = A.h[i];
+// the saved prefix of the window CTA's shared memory: CtaShared | rho | mom | h (carve layout)
+constexpr size_t WSAVE = (WSAVE_SH + 3 * 8 * (size_t)(WCAP + 1) + 15) & ~size_t(15);
+// one TMA bulk copy each way (cp.async.bulk, shared <-> global): a window is saved and restored
+// in one transfer instead of a loop of dependent loads
+__device__ __forceinline__ void window_save(const Tiles& tl, CtaShared& sh, const Arr& A, int j, double dt) {
+  if (threadIdx.x == 0) { sh.sv_n = A.n; sh.sv_dt = dt; }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(slot), "r"((unsigned)__cvta_generic_to_shared(&sh)), "r"((unsigned)WSAVE) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory free for the next job
   }
+  __syncthreads();
 }
 __device__ __forceinline__ double window_restore(const Tiles& tl, CtaShared& sh, Arr& A, int j) {
-  const unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(slot);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sh);
-  for (int i = threadIdx.x; i < (int)(sizeof(CtaShared) / 8); i += blockDim.x) dst[i] = src[i];
-  const double* d = reinterpret_cast<const double*>(slot + WSAVE_SH);
-  const int n = (int)d[0];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    A.rho[i] = d[2 + i]; A.mom[i] = d[2 + WCAP + i]; A.h[i] = d[2 + 2 * WCAP + i];
+  __shared__ __align__(8) unsigned long long wbar;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&wbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  A.n = n;
-  return d[1];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)WSAVE) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(&sh)), "l"(slot), "r"((unsigned)WSAVE), "r"(bar) : "memory");
+  }
+  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+               " @!P1 bra WAIT_%=;\n}" ::"r"(bar) : "memory");
+  A.n = sh.sv_n;
+  return sh.sv_dt;
 }
 
 // PF: after the step body, thread 0 claims the next window job and loads its list entry into
@@ -749,17 +763,28 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
   }
   const int huL = g.huL, huR = g.huR;
   if (PH != 2) {
-    for (int i = tid; i < n; i += T) {
-      const int v = s0 + i;
-      long long mo;
-      const double* pr = vcell(tl, g, v, mo);
-      A.rho[i] = pr[0];
-      A.mom[i] = pr[mo];
-      double hh;
-      if (v < nL) hh = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + v]);
-      else if (v < nL + cnt) hh = g.hu_in ? p.h_av : tl.h[g.in][g.base + v - nL];
-      else hh = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + v - nL - cnt]);
-      A.h[i] = hh;
+    // the window's cells: every load of the thread first, then the shared-memory stores (the
+    // loads of one thread are independent, so they are all in flight together)
+    constexpr int LU = (WCAP + 31) / 32;
+    double lr[LU], lm[LU], lh[LU];
+#pragma unroll
+    for (int u = 0; u < LU; ++u) {
+      const int i = tid + 32 * u, v = s0 + i;
+      lr[u] = 0.0; lm[u] = 0.0; lh[u] = 0.0;
+      if (i < n) {
+        long long mo;
+        const double* pr = vcell(tl, g, v, mo);
+        lr[u] = pr[0];
+        lm[u] = pr[mo];
+        if (v < nL) lh[u] = g.xl ? pr[2 * HALO] : (huL ? p.h_av : tl.h[g.in][g.bl + g.cl - nL + v]);
+        else if (v < nL + cnt) lh[u] = g.hu_in ? p.h_av : tl.h[g.in][g.base + v - nL];
+        else lh[u] = g.xr ? pr[2 * HALO] : (huR ? p.h_av : tl.h[g.in][g.br + v - nL - cnt]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < LU; ++u) {
+      const int i = tid + 32 * u;
+      if (i < n) { A.rho[i] = lr[u]; A.mom[i] = lm[u]; A.h[i] = lh[u]; }
     }
     for (int i = tid; i <= capw; i += T) A.fl[i] = 0;
     A.n = n;
@@ -909,6 +934,8 @@ __device__ __forceinline__ void window_dbg(const Tiles& tl, const CtaShared& sh,
 // dts_jobs (window split): Algorithm 2 on every block exported by the window kernel's part A
 // this step, one lane per block (dts_thread: the boundary solves of a block run on its lane),
 // so the blocks of all windows iterate side by side instead of one block per window warp.
+// (Tried: two lanes per block, each solving every other interior edge with the fluxes exchanged
+// by shuffles -- 4 % slower on C5: the per-lane chain is the boundary solver's math either way.)
 __global__ void __launch_bounds__(32)
 dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl) {
   const int n = tl.ctl[10] < tl.djcap ? tl.ctl[10] : tl.djcap;

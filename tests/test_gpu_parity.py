@@ -505,6 +505,43 @@ def test_c5_virtual_ranks_bitwise(P, world):
     np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c5_virtual_ranks_cut_at_cavitating_segments(P, world):
+    """SURVEY §8(e)'s hard case: rank cuts ON cavitating 4096-cell segment boundaries (tile 1024,
+    24 segments: the cuts of 2, 4 and 8 ranks fall on boundaries whose velocity jumps of 36-275
+    m/s open a bubble at step 1), so the creation, its implicit block and the merges straddle the
+    rank cut.  The rank slices exchanged by device copies reproduce the 1-rank run bit for bit."""
+    from paper_2211_00705_b200.decomp import VirtualRanks, rank_slice
+    n, steps, tile = 24 * 4096, 150, 1024
+    w = W.c5(n_cells=n)
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=tile)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)
+    ctx.set_state(rho, mom)
+    ctx.step(1)
+    cuts = [rank_slice(n, tile, r, world)[0] for r in range(1, world)]
+    xs = [i["x"] for i in ctx.interfaces()]  # (edge indices shift with every creation to the left)
+    hav = h_av(w)
+    assert any(any(abs(x - (w["x_left"] + c * hav)) <= 2 * hav for x in xs) for c in cuts), cuts  # a bubble at a cut
+    ctx.set_state(rho, mom)
+    st = ctx.step(steps, stats=True)
+    assert st["creations"] >= 1 and st["regions"] >= 1
+    g = ctx.get_state()
+    n1 = int(g["n"][0])
+    vr = VirtualRanks(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], world, tile=tile,
+                      stream=torch.cuda.current_stream())
+    vr.set_state(rho[:w["N"]], mom[:w["N"]])
+    vr.step(steps)
+    v = vr.get_state()
+    assert v["status"] == [0] * world
+    assert all(t == g["t"][0] for t in v["t"])
+    assert v["rho"].shape[0] == n1
+    np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
+    np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
+    np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
+
+
 @pytest.mark.parametrize("n,steps", [(40 * 940 + 517, 200)])
 def test_c5_window_path_matches_whole_tile_path(P, oracle_mod, n, steps, monkeypatch):
     """The windowed full step (tiled_win: step body on <= 160 owned cells around a tile's special
