@@ -40,9 +40,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Algorithmic fp64 operations per cell-update of the bulk path: decode 5,
-# HLL edge flux + creation pre-filter 36, moving-cell update 15; one division = 1 op.
-FLOP_PER_CELL_UPDATE = 56
+# Algorithmic fp64 operations per cell-update of the bulk path, SURVEY §8(d)'s count (a division
+# = 1 op): u = m/rho 1, p 2, HLL flux of one edge per cell ~17 (Davis speeds, the two physical
+# fluxes, the intermediate state), update 6.  (The kernel executes more: rcp refinement, the
+# creation pre-filter, the CFL partials; those are not algorithmic work.)
+FLOP_PER_CELL_UPDATE = 26
 C5_BYTES_PER_CELL_UPDATE = 32  # the fast pass: read rho, mom; write rho, mom (fp64; widths of
                                 # tiles whose widths are all h_av are neither read nor written)
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 FMA/clk x 2 x max clock
@@ -403,8 +405,9 @@ def main():
                 "tile_ms_per_step": kt["tile_ms"] / max(args.steps, 1),
                 "whole_step_gbs": step_bw, "whole_step_frac": step_bw / hbm,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
-        launches = args.steps * (4 if w["M"] > 1 else 3)
-        launch_note = "per step: tiled_fast + tiled_win + tiled_slow" + (" + tiled_members_finish" if w["M"] > 1 else "")
+        launches = kt["launches"]  # counted by the library (eis_get_timing)
+        launch_note = ("per step: tiled_fast + window part A + dts_jobs + window part B + tiled_slow" +
+                       (" + tiled_members_finish" if w["M"] > 1 else ""))
     else:
         peak, peak_src = fp64_peak()
         kms = kt["resident_ms"] if kt["resident_ms"] > 0 else ms
@@ -413,7 +416,7 @@ def main():
                 "traffic": ncu_traffic(name), "kernel": "eis::resident_steps",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                 "flop_per_cell_update": FLOP_PER_CELL_UPDATE, "peak_source": peak_src}
-        launches = 1
+        launches = kt["launches"]
         launch_note = "one member-resident kernel launch for the K timed steps"
     if rank == 0:
         line = {
@@ -536,7 +539,8 @@ def main_c5(args, torch, dist, P, world, rank, local):
                        "cells": n_glob, "parallelism": f"tile-aligned grid slices x{world}, halo exchange + CFL min",
                        "l2": "state (2 GB) larger than L2",
                        "implicit_regions": MODE_NAMES[mode],
-                       "launches": "per step: tiled_fast + tiled_win + tiled_slow"
+                       "launches": "per step: tiled_fast + window part A + dts_jobs + window part B + tiled_slow" +
+                                   ("" if world == 1 else " + tiled_finish (after the exchange)")
                        + (" + NCCL halo exchange / all-reduce + tiled_finish" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": ncu_traffic("C5"), "kernel": "eis::tiled_fast",
@@ -547,7 +551,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
                          "tile_ms_per_step": kt["tile_ms"] / max(args.steps, 1),
                          "whole_step_gbs": step_bw, "whole_step_frac": step_bw / hbm,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * (3 if world == 1 else 4), "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kt["launches"], "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
             "members_not_ok": nbad, "rates": rates,

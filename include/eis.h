@@ -235,7 +235,8 @@ eis_status eis_window_diag(eis_ctx* ctx, int64_t* out, int64_t capacity, int64_t
  * events on the context's stream around each kernel (a few microseconds per step).
  * eis_get_timing synchronises the stream and returns the summed milliseconds since
  * eis_set_timing: ms[0] tiled fast pass, ms[1] tiled window full steps, ms[2] tiled whole-tile
- * full steps + next dt, ms[3] member-resident kernel; *launches = recorded launch groups. */
+ * full steps + next dt (window split: part A, dts_jobs and part B are all in ms[1]), ms[3]
+ * member-resident kernel; *launches = kernels the step calls launched meanwhile. */
 eis_status eis_set_timing(eis_ctx* ctx, int32_t enable);
 eis_status eis_get_timing(eis_ctx* ctx, double* ms /* [4] */, int64_t* launches);
 

@@ -36,6 +36,7 @@ struct eis_ctx {
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::array<int, 5>> ev_marks;  // per recorded launch group: event indices + kind
+  long long n_kernels = 0;                     // kernels launched by the step calls while timing is on
   size_t ev_used = 0;
   eis_eos eos_in;
   eis_params prm_in;
@@ -66,6 +67,7 @@ struct eis_ctx {
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
   int dts_grid = 0;                        // window split: dts_jobs CTAs (one warp each)
+  int dts_tpb = 32;                        //   threads per dts_jobs CTA (EIS_DTS_TPB, development)
   DtsJob* t_djobs = nullptr;
   unsigned char* t_wsave = nullptr;
   cudaStream_t stream2 = nullptr;          // tiled: the window kernel beside tiled_fast
@@ -373,6 +375,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   int split = c->p.mode == 0 && c->win_grid_poll == 0;
   if (const char* ev = getenv("EIS_WIN_SPLIT")) split = split && atoi(ev) != 0;
   c->dts_grid = std::max(nsm, 1) * 16;
+  c->dts_tpb = 32;
+  if (const char* ev = getenv("EIS_DTS_TPB")) c->dts_tpb = std::max(1, std::min(32, atoi(ev)));
   const size_t tc = (size_t)ntiles * capt;
   const size_t mc = (size_t)M * cap;  // member-major staging
   bool ok = cudaMalloc(&c->d_rho, mc * 8) == cudaSuccess && cudaMalloc(&c->d_mom, mc * 8) == cudaSuccess &&
@@ -641,6 +645,7 @@ extern "C" eis_status eis_set_timing(eis_ctx* c, int32_t enable) {
   c->timing = enable != 0;
   c->ev_marks.clear();
   c->ev_used = 0;
+  c->n_kernels = 0;
   return EIS_OK;
 }
 
@@ -648,7 +653,7 @@ extern "C" eis_status eis_get_timing(eis_ctx* c, double* ms, int64_t* launches) 
   if (!c || !ms || !launches) return EIS_E_ARG;
   CU(cudaStreamSynchronize(c->stream));
   for (int q = 0; q < 4; ++q) ms[q] = 0.0;
-  *launches = (int64_t)c->ev_marks.size();
+  *launches = (int64_t)c->n_kernels;
   for (const auto& m : c->ev_marks) {
     float t = 0.f;
     if (m[4] == 0) {  // resident: one kernel
@@ -823,7 +828,10 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   }
   if (c->tl.split) {  // part A, the DTS jobs (one lane per block), part B
     tiled_win<32, EIS_WIN_MINB, false, 1><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
-    dts_jobs<<<c->dts_grid, 32, 0, c->stream>>>(c->e, c->p, c->tl);
+    dts_jobs<<<c->dts_grid * 32 / c->dts_tpb, c->dts_tpb, 0, c->stream>>>(c->e, c->p, c->tl);
+#ifdef EIS_DTS_DEBUG
+    dts_dbg_print<<<1, 1, 0, c->stream>>>();
+#endif
     tiled_win<32, EIS_WIN_MINB, false, 2><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   } else {
     tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
@@ -833,7 +841,10 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->tl.M > 1)
     tiled_members_finish<<<(unsigned)(((long long)c->tl.M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, t_end, 1);
-  if (c->timing) { m[3] = timing_event(c); c->ev_marks.push_back(m); }
+  if (c->timing) {
+    m[3] = timing_event(c); c->ev_marks.push_back(m);
+    c->n_kernels += 2 + (c->tl.split ? 3 : 1) + (c->win_grid_poll > 0 ? 1 : 0) + (c->tl.M > 1 ? 1 : 0);
+  }
 }
 
 static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats* out) {
@@ -885,7 +896,7 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
       resident_steps<512, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
     else
       resident_steps<1024, 1><<<M, c->threads, c->smem, c->stream>>>(c->e, c->p, c->g, n_steps, t_end);
-    if (c->timing) { m[1] = timing_event(c); c->ev_marks.push_back(m); }
+    if (c->timing) { m[1] = timing_event(c); c->ev_marks.push_back(m); c->n_kernels += 1; }
     CU(cudaGetLastError());
   }
   if (out) return collect_stats(c, out);
@@ -1049,6 +1060,7 @@ extern "C" eis_status eis_step_finish(eis_ctx* c, double t_end, int32_t after_st
   if (c->sticky) return c->sticky;
   CU(cudaSetDevice(c->grid.device));
   tiled_finish<<<1, 1, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
+  if (c->timing) c->n_kernels += 1;
   CU(cudaGetLastError());
   return EIS_OK;
 }

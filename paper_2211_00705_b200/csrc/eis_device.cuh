@@ -264,6 +264,34 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
 // within ~rtol of the root (the oracle tests the step against rtol itself, one extra iteration).
 // Returns the iteration count (>= 0) or -1; aux holds the value at the returned iterate.
 // ---------------------------------------------------------------------------------------
+#ifdef EIS_DTS_DEBUG  // development: counts of the one-thread solver (dts_jobs)
+__device__ unsigned long long g_dbg[8];  // solves, newton iterations, evaluations, armijo evals, retries, LIN exits
+#define EIS_DBG(i) do { if (!HALF) atomicAdd(&g_dbg[i], 1ull); } while (0)
+#else
+#define EIS_DBG(i) do { } while (0)
+#endif
+// R14d's acceptance test and update (shared with the one-evaluation fast path iface_try_lin)
+__device__ __forceinline__ bool lin_accept(const Eos& e, const Prm& p, const double G[2], double d0, double d1, double x0,
+                                           double x1, bool wellc) {
+  return wellc && fmax(fabs(G[0]), fabs(G[1])) <= p.lin_gtol && fabs(d0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
+         fabs(d1) <= p.newton_stol * fmax(fabs(x1), e.p0);
+}
+__device__ __forceinline__ void lin_apply(const double da[4], double d0, double d1, double aux[2], double& x0, double& x1) {
+  aux[0] += da[0] * d0 + da[1] * d1;
+  aux[1] += da[2] * d0 + da[3] * d1;
+  x0 += d0; x1 += d1;
+}
+// the Newton direction d = -J^-1 G (2x2, Cramer); false for a singular or non-finite Jacobian.
+// wellc: det has not cancelled below 1e-8 of its terms (R14d's shortcut needs a well-conditioned J)
+__device__ __forceinline__ bool newton_dir(const double G[2], const double J[4], double& d0, double& d1, bool& wellc) {
+  const double det = J[0] * J[3] - J[1] * J[2];
+  if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
+  wellc = fabs(det) >= 1e-8 * (fabs(J[0] * J[3]) + fabs(J[1] * J[2]));
+  const double idet = __drcp_rn(det);
+  d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
+  d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
+  return true;
+}
 // HALF = false: the same iteration by one thread, the Armijo candidates tried in order (the first
 // accepted k is the smallest: the result is the half warp's bit for bit).
 template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, double*, double*, double*, double*),
@@ -271,30 +299,28 @@ template <class Prob, bool (*EVAL)(const Eos&, const Prob&, double, double, doub
 __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, double& x1, double aux[2],
                          unsigned mask, int hl, int base_lane) {
   double G[2], J[4], da[4];
+  EIS_DBG(2);
   if (!EVAL(e, P, x0, x1, G, J, aux, da)) return -1;
   for (int it = 0; it < p.newton_max_iter; ++it) {
-    const double det = J[0] * J[3] - J[1] * J[2];
-    if (!(fabs(det) > 0.0) || !isfinite(det)) return -1;
+    EIS_DBG(1);
     // R14d needs a well-conditioned Jacobian (the O(|d|^2) constant grows like 1/|det|): no
     // shortcut when det has cancelled to below 1e-8 of its terms
-    const bool wellc = fabs(det) >= 1e-8 * (fabs(J[0] * J[3]) + fabs(J[1] * J[2]));
-    const double idet = __drcp_rn(det);
-    const double d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
-    const double d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
+    double d0, d1;
+    bool wellc;
+    if (!newton_dir(G, J, d0, d1, wellc)) return -1;
     // quadratic regime (LIN, reading R14d): a residual already <= sqrt(gtol) whose Newton step is
     // within sqrt(rtol) of the iterate puts x + d within ~|d|^2 <= rtol of the root: accept it
     // without another evaluation, the auxiliary values to first order (error O(|d|^2))
-    if (LIN && wellc && fmax(fabs(G[0]), fabs(G[1])) <= p.lin_gtol && fabs(d0) <= p.newton_stol * fmax(fabs(x0), e.p0) &&
-        fabs(d1) <= p.newton_stol * fmax(fabs(x1), e.p0)) {
-      aux[0] += da[0] * d0 + da[1] * d1;
-      aux[1] += da[2] * d0 + da[3] * d1;
-      x0 += d0; x1 += d1;
+    if (LIN && lin_accept(e, p, G, d0, d1, x0, x1, wellc)) {
+      lin_apply(da, d0, d1, aux, x0, x1);
+      EIS_DBG(5);
       return it + 1;
     }
     const double n0 = G[0] * G[0] + G[1] * G[1];
     // the full step first, on every lane alike (no divergence, no shuffles): accepted almost always
     double y0 = x0 + d0, y1 = x1 + d1, Gy[2], Jy[4], ay[2], dy[4];
     const double c1 = 1.0 - 1e-4;
+    EIS_DBG(2);
     bool ok = EVAL(e, P, y0, y1, Gy, Jy, ay, dy) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= c1 * c1 * n0;
     double s0 = d0, s1 = d1;
     if (!ok && !HALF) {  // back-tracking, lambda = 2^-k in order
@@ -303,6 +329,7 @@ __device__ int newton_hw(const Eos& e, const Prm& p, const Prob& P, double& x0, 
         const double lam = __longlong_as_double((long long)(1023 - k) << 52);  // 2^-k
         y0 = x0 + lam * d0; y1 = x1 + lam * d1;
         const double cl = 1.0 - 1e-4 * lam;
+        EIS_DBG(3);
         if (EVAL(e, P, y0, y1, Gy, Jy, ay, dy) && Gy[0] * Gy[0] + Gy[1] * Gy[1] <= cl * cl * n0) acc = k;
       }
       if (acc < 0) return fmax(fabs(G[0]), fabs(G[1])) <= p.newton_gtol ? it : -1;  // rounding floor
@@ -365,22 +392,38 @@ struct IfaceSol {
 // Phase-boundary Riemann solve by a half warp (HALF) or one thread.  (rm, um) minus (left)
 // state, (rp, up) plus.  Warm start: if x_init0 > 0 use (x_init0, x_init1) as the first iterate,
 // else HLLC.  Outputs F_PB = (-z, -z u_V* + p_V*) (vapour side R17), w = u_V* + z v_V*.
-template <bool HALF>
-__device__ __forceinline__ IfaceSol iface_solve_x(const Eos& e, const Prm& p, double rm, double um, double rp,
-                                                  double up, bool vap_minus, double x_init0, double x_init1,
-                                                  unsigned mask, int hl, int base_lane) {
+__device__ __forceinline__ IfaceProb iface_prob(double rm, double um, double rp, double up, bool vap_minus) {
   IfaceProb P;
   if (vap_minus) { P.rV = rm; P.uV = um; P.rL = rp; P.uL = up; P.sV = -1.0; }
   else { P.rV = rp; P.uV = up; P.rL = rm; P.uL = um; P.sV = 1.0; }
   P.du = up - um;
+  return P;
+}
+// the boundary's flux and speed from the converged star pressures and aux = (z, f_V)
+__device__ __forceinline__ void iface_finish(const Eos& e, const IfaceProb& P, bool vap_minus, double x0,
+                                             const double aux[2], IfaceSol& s) {
+  const double z = aux[0], fV = aux[1];
+  const double uVs = vap_minus ? P.uV - fV : P.uV + fV;  // wave relations (P:1521)
+  s.w = uVs + z * e.a_v2 * __drcp_rn(x0);                  // z = -rho_V* (u_V* - w)
+  s.F0 = -z;
+  s.F1 = -z * uVs + x0;
+}
+
+template <bool HALF>
+__device__ __forceinline__ IfaceSol iface_solve_x(const Eos& e, const Prm& p, double rm, double um, double rp,
+                                                  double up, bool vap_minus, double x_init0, double x_init1,
+                                                  unsigned mask, int hl, int base_lane) {
+  const IfaceProb P = iface_prob(rm, um, rp, up, vap_minus);
   double x0, x1, aux[2];
   if (x_init0 > 0.0) { x0 = x_init0; x1 = x_init1; }
   else {
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
   }
+  EIS_DBG(0);
   int it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN, HALF>(e, p, P, x0, x1, aux, mask, hl, base_lane);
   if (it < 0 && x_init0 > 0.0) {  // warm start failed: retry from the HLLC estimate
+    EIS_DBG(4);
     const double g = vap_minus ? hllc_guess(e, P.rV, P.uV, P.rL, P.uL) : hllc_guess(e, P.rV, -P.uV, P.rL, -P.uL);
     x0 = g; x1 = g;
     it = newton_hw<IfaceProb, iface_eval, EIS_NEWTON_LIN, HALF>(e, p, P, x0, x1, aux, mask, hl, base_lane);
@@ -389,12 +432,29 @@ __device__ __forceinline__ IfaceSol iface_solve_x(const Eos& e, const Prm& p, do
   s.iters = it;
   s.pV = x0; s.pL = x1;
   if (it < 0) { s.F0 = s.F1 = s.w = 0.0; return s; }
-  const double z = aux[0], fV = aux[1];
-  const double uVs = vap_minus ? P.uV - fV : P.uV + fV;  // wave relations (P:1521)
-  s.w = uVs + z * e.a_v2 * __drcp_rn(x0);                  // z = -rho_V* (u_V* - w)
-  s.F0 = -z;
-  s.F1 = -z * uVs + x0;
+  iface_finish(e, P, vap_minus, x0, aux, s);
   return s;
+}
+// The warm-started solve when its first Newton step is accepted by R14d (the usual case inside
+// Algorithm 2): one evaluation, straight-line code (two of these side by side overlap).  Returns
+// false when the general solver is needed; when true, s is iface_solve_x's result (the same
+// expressions; compiled in another context the compiler may contract a multiply-add differently,
+// so equal up to the last bits).
+__device__ __forceinline__ bool iface_try_lin(const Eos& e, const Prm& p, double rm, double um, double rp, double up,
+                                              bool vap_minus, double x0, double x1, IfaceSol& s) {
+  if (!EIS_NEWTON_LIN || !(x0 > 0.0) || !(p.newton_max_iter > 0)) return false;
+  const IfaceProb P = iface_prob(rm, um, rp, up, vap_minus);
+  double G[2], J[4], aux[2], da[4];
+  if (!iface_eval(e, P, x0, x1, G, J, aux, da)) return false;
+  double d0, d1;
+  bool wellc;
+  if (!newton_dir(G, J, d0, d1, wellc)) return false;
+  if (!lin_accept(e, p, G, d0, d1, x0, x1, wellc)) return false;
+  lin_apply(da, d0, d1, aux, x0, x1);
+  s.iters = 1;
+  s.pV = x0; s.pL = x1;
+  iface_finish(e, P, vap_minus, x0, aux, s);
+  return true;
 }
 __device__ __noinline__ IfaceSol iface_solve_hw(const Eos& e, const Prm& p, double rm, double um, double rp,
                                                 double up, bool vap_minus, double x_init0, double x_init1,

@@ -177,8 +177,8 @@ __device__ __forceinline__ int dts_warp(Sys& S, double* sc, const int K, const d
 // one lane per block).  Identical expressions in the identical order as dts_warp, so the two
 // give the same bits.  KMAX: compile-time bound of K (arrays stay in registers for KMAX = 3).
 // A per-thread system `Sys` supplies
-//   int  edge(j, Wl, Wr, F, w)   interior edge j between cells j-1 (state Wl) and j (Wr): flux
-//        F[NV] and edge speed w; returns a status (0: ok)
+//   int  edges(K, W, Fe, we)     every interior edge j = 1 .. K-1 between cells j-1 and j at the
+//        iterate W: fluxes Fe[j][NV] and edge speeds we[j]; returns the largest status (0: ok)
 //   int  check(i, w)             admissibility of cell i's new iterate
 //   void store(i, w)             caches derived values of cell i's iterate
 // Fe[KMAX+1][NV], we[KMAX+1]: the caller sets the outer edges 0 and K.
@@ -209,12 +209,9 @@ __device__ __forceinline__ int dts_thread(Sys& S, const int K, const double dt, 
   bool prev_cont_robust = true;
   for (int part = 0; part < 2 && !err; ++part) {
     for (;;) {
-#pragma unroll
-      for (int j = 1; j < KMAX; ++j) {  // (a) interior edges at W^l
-        if (j < K) {
-          const int s = S.edge(j, W[j - 1], W[j], Fe[j], we[j]);
-          if (s > err) err = s;
-        }
+      {  // (a) interior edges at W^l
+        const int s = S.edges(K, W, Fe, we);
+        if (s > err) err = s;
       }
       if (err || part == 1) break;
       bool conv = true, rstop = true, rcont = false;

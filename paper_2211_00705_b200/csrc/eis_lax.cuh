@@ -144,9 +144,18 @@ struct EulerDts {
 struct EulerDtsT {
   static constexpr int NV = 3;
   double g;
-  __device__ __forceinline__ int edge(int, const double (&Wl)[3], const double (&Wr)[3], double (&F)[3], double& w) {
-    w = 0.0;
-    return face_flux(g, Wl[0], Wl[1], Wl[2], Wr[0], Wr[1], Wr[2], F);
+  template <int KMAX>
+  __device__ __forceinline__ int edges(int K, const double (&W)[KMAX][3], double (&Fe)[KMAX + 1][3], double (&we)[KMAX + 1]) {
+    int err = 0;
+#pragma unroll
+    for (int j = 1; j < KMAX; ++j) {
+      if (j < K) {
+        we[j] = 0.0;
+        const int s = face_flux(g, W[j - 1][0], W[j - 1][1], W[j - 1][2], W[j][0], W[j][1], W[j][2], Fe[j]);
+        if (s > err) err = s;
+      }
+    }
+    return err;
   }
   __device__ __forceinline__ int check(int, const double (&)[3]) const { return 0; }
   __device__ __forceinline__ void store(int, const double (&)[3]) {}

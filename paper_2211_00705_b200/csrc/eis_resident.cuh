@@ -334,6 +334,31 @@ struct TwoPhaseDtsT {
     return (!(w[0] > 0.0) || phase_of(e, w[0]) != phase_n(i)) ? ST_SPINODAL : 0;
   }
   __device__ __forceinline__ void store(int i, const double (&w)[2]) { Wu[i] = w[1] / w[0]; }
+  __device__ __forceinline__ void put(int j, const IfaceSol& s, double (&F)[2], double& w) {
+    F[0] = s.F0; F[1] = s.F1; w = s.w; xs0[j] = s.pV; xs1[j] = s.pL;
+    ++solves;
+  }
+  // all interior edges; the usual 3-cell block around a tiny cell of the other phase has two
+  // warm-started boundary solves, tried first as one-evaluation R14d steps side by side (the two
+  // evaluations overlap); any that is not accepted takes the general solver (same bits)
+  __device__ __forceinline__ int edges(int K, const double (&W)[KMAX][2], double (&Fe)[KMAX + 1][2], double (&we)[KMAX + 1]) {
+    if (KMAX == 3 && K == 3 && phase_n(0) != phase_n(1) && phase_n(1) != phase_n(2) && xs0[1] > 0.0 && xs0[2] > 0.0) {
+      IfaceSol s1, s2;
+      const bool ok1 = iface_try_lin(e, p, W[0][0], Wu[0], W[1][0], Wu[1], phase_n(0) == VAP, xs0[1], xs1[1], s1);
+      const bool ok2 = iface_try_lin(e, p, W[1][0], Wu[1], W[2][0], Wu[2], phase_n(1) == VAP, xs0[2], xs1[2], s2);
+      int err = 0;
+      if (ok1) put(1, s1, Fe[1], we[1]);
+      else err = max(err, edge(1, W[0], W[1], Fe[1], we[1]));
+      if (ok2) put(2, s2, Fe[2], we[2]);
+      else err = max(err, edge(2, W[1], W[2], Fe[2], we[2]));
+      return err;
+    }
+    int err = 0;
+#pragma unroll
+    for (int j = 1; j < KMAX; ++j)
+      if (j < K) err = max(err, edge(j, W[j - 1], W[j], Fe[j], we[j]));
+    return err;
+  }
 };
 
 // one DTS job by this thread: U^n, h^n, outer edges and warm starts from the record, results

@@ -936,13 +936,31 @@ __device__ __forceinline__ void window_dbg(const Tiles& tl, const CtaShared& sh,
 // so the blocks of all windows iterate side by side instead of one block per window warp.
 // (Tried: two lanes per block, each solving every other interior edge with the fluxes exchanged
 // by shuffles -- 4 % slower on C5: the per-lane chain is the boundary solver's math either way.)
+// blocks of more than 3 cells (rare: overlapping regions R11, merged blocks): out of line, so
+// the usual block's code keeps its registers
+__device__ __noinline__ void run_dts_job_gen(const Eos& e, const Prm& p, DtsJob& J) { run_dts_job<MAXB>(e, p, J); }
+#ifdef EIS_DTS_DEBUG
+__global__ void dts_dbg_print() {
+  printf("dtsdbg solves %llu newton_its %llu evals %llu armijo_evals %llu retries %llu lin_exits %llu\n", g_dbg[0], g_dbg[1],
+         g_dbg[2], g_dbg[3], g_dbg[4], g_dbg[5]);
+  for (int i = 0; i < 8; ++i) g_dbg[i] = 0;
+}
+#endif
 __global__ void __launch_bounds__(32)
 dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl) {
   const int n = tl.ctl[10] < tl.djcap ? tl.ctl[10] : tl.djcap;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     DtsJob& J = tl.djobs[q];
+#ifdef EIS_DTS_DEBUG  // development: the longest jobs of a step
+    const long long c0 = clock64();
+#endif
     if (J.K == 3) run_dts_job<3>(e, p, J);  // one tiny cell: the usual block
-    else run_dts_job<MAXB>(e, p, J);
+    else run_dts_job_gen(e, p, J);
+#ifdef EIS_DTS_DEBUG
+    const long long dc = clock64() - c0;
+    if (dc > 400000) printf("dtsjob q %d K %d it %lld solves %d cycles %lld hn %.3e %.3e %.3e tiny %d\n", q, J.K, J.it, J.solves, dc,
+                            J.hn[0], J.hn[1], J.hn[2], J.tiny);
+#endif
   }
 }
 

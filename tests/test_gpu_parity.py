@@ -993,11 +993,14 @@ def test_dts_cap_freezes_only_its_member(P, oracle_mod):
 
 
 @pytest.mark.parametrize("cfg", ["c5_65k", "c5_262k", "c4"])
-def test_window_split_is_bitwise_the_one_kernel_window_step(P, cfg, monkeypatch):
+def test_window_split_matches_the_one_kernel_window_step(P, cfg, monkeypatch):
     """The window split (part A up to the remesh with the implicit blocks exported, dts_jobs with
-    one lane per block -- dts_thread and the one-thread boundary solver -- then part B) gives the
-    bits of the one-kernel window step (dts_warp, half-warp solver): same expressions in the same
-    order, so states, widths, clocks and every counter agree exactly."""
+    one lane per block -- dts_thread, the one-thread boundary solver and its one-evaluation R14d
+    path -- then part B) against the one-kernel window step (dts_warp, half-warp solver): the same
+    method in the same order, so the same events and the same states to the last bits (the two
+    solvers are compiled in different contexts, where the compiler may contract a multiply-add
+    differently, and Algorithm 2's iterates carry such differences along): element-wise (R32) to
+    1e-11, clocks to 1e-12, DTS stop decisions equal unless one was within its rounding margin."""
     if cfg == "c4":
         w = W.c4(members=np.array([0, 1, 2, 3, 5, 777, 9999, 12345]))
         steps, layout = 120, P.LAYOUT_TILED
@@ -1011,11 +1014,18 @@ def test_window_split_is_bitwise_the_one_kernel_window_step(P, cfg, monkeypatch)
         out[split] = g
     a, b = out["1"], out["0"]
     assert a["stats"]["regions"] > 0 and a["stats"]["dts_iters"] > 0
-    for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits", "merges", "regions",
-              "decision_margin_warnings"):
+    for k in ("cell_updates", "creations", "splits", "merges", "regions"):
         assert a["stats"][k] == b["stats"][k], (k, a["stats"][k], b["stats"][k])
+    marg = a["stats"]["decision_margin_warnings"] + b["stats"]["decision_margin_warnings"]
+    for k in ("dts_iters", "iface_solves"):
+        assert a["stats"][k] == b["stats"][k] or marg > 0, (k, a["stats"][k], b["stats"][k])
     np.testing.assert_array_equal(a["status"], b["status"])
     np.testing.assert_array_equal(a["n"], b["n"])
-    np.testing.assert_array_equal(a["t"], b["t"])
-    for k in ("rho", "mom", "h"):
-        np.testing.assert_array_equal(a[k], b[k])
+    np.testing.assert_allclose(a["t"], b["t"], rtol=1e-12)
+    hav = h_av(w)
+    for m in range(w["M"]):
+        n = int(a["n"][m])
+        for k in ("rho", "mom"):
+            el = el_err(a[k][m, :n], b[k][m, :n], b["h"][m, :n], hav, b["rho"][m, :n] if k == "mom" else None)
+            assert el.max() <= 1e-11, (m, k, float(el.max()), int(el.argmax()))
+        assert np.abs(a["h"][m, :n] - b["h"][m, :n]).max() <= 1e-11 * hav
