@@ -448,9 +448,13 @@ def main_c5(args, torch, dist, P, world, rank, local):
     n_glob = args.members or (1 << 27)   # --members: profiling only, fewer cells
     w = with_mode(W.c5(n_cells=n_glob))
     stream = torch.cuda.current_stream()
+    # world > 1: the per-step sequence (step_local, NCCL halo exchange + CFL all-reduce,
+    # step_finish) replayed as CUDA graphs of EIS_RANK_GRAPH steps on the grid's own stream
+    gsteps = int(os.environ.get("EIS_RANK_GRAPH", "10")) if world > 1 else 0
     rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
                   tile=int(os.environ.get("EIS_TILE", "1400")),
-                  stream=stream)
+                  stream=stream, graph_steps=gsteps)
+    stream = rg.stream if rg.stream is not None else stream  # the library's stream: events go there
     rho_l = np.zeros(rg.cap)
     mom_l = np.zeros(rg.cap)
     rho_l[:rg.n] = w["rho"][0, rg.c0:rg.c1]
@@ -469,7 +473,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    rg.ctx.set_timing(True)  # CUDA events around each kernel on the library's (this) stream
+    rg.ctx.set_timing(gsteps == 0)  # CUDA events around each kernel on the library's (this) stream
     torch.cuda.synchronize()
     e0.record(stream)
     rg.step(args.steps)
@@ -479,9 +483,16 @@ def main_c5(args, torch, dist, P, world, rank, local):
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    if gsteps:  # graph replays record no per-kernel events: the kernel times of the same steps, eager
+        st_timed = rg.ctx.member_stats()[0]
+        rg.set_state(rho_d, mom_d)
+        torch.cuda.synchronize()
+        rg.ctx.set_timing(True)
+        rg.step(args.steps, graph=False)
+        torch.cuda.synchronize()
     kt = rg.ctx.get_timing()
     rg.ctx.set_timing(False)
-    st = rg.ctx.step(0, stats=True) if world == 1 else rg.ctx.member_stats()[0]
+    st = rg.ctx.step(0, stats=True) if world == 1 else (st_timed if gsteps else rg.ctx.member_stats()[0])
     cu_local = st["cell_updates"]
     nbad = int(rg.ctx.member_status()[0] != 0)
     cu = st["cell_updates"]

@@ -201,6 +201,10 @@ eis_status eis_member_stats(eis_ctx* ctx, eis_stats* out);
  *                       rank's recv_left; min-allreduce of the 2-double CFL pair)
  *   eis_step_finish(after_step = 1)
  * and after eis_set_state: exchange, then eis_step_finish(after_step = 0) (initial dt).
+ * eis_step_local and eis_step_finish only enqueue work on the context's stream (no host
+ * synchronisation, no allocation), so the per-step sequence, the exchange's NCCL calls included,
+ * can be captured into a CUDA graph on that stream and replayed (decomp.RankGrid); steps issued
+ * during a capture record no eis_set_timing events.
  * Exchange buffer: EIS_XB_DOUBLES doubles of device memory owned by the caller, borrowed for
  * the context's lifetime: records of EIS_HALO cells (rho[EIS_HALO], mom[..], h[..], count)
  * at offsets EIS_XB_SEND_LEFT, _SEND_RIGHT, _RECV_LEFT, _RECV_RIGHT, then the pair

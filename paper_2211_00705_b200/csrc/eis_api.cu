@@ -815,6 +815,12 @@ static int timing_event(eis_ctx* c, cudaStream_t st = nullptr) {  // an event fr
 
 static void tiled_launch(eis_ctx* c, double t_end) {
   std::array<int, 5> m{-1, -1, -1, -1, 1};
+  // a step captured into a CUDA graph (rank mode: step_local -> halo exchange -> step_finish
+  // replayed without the host) records no timing events: the pool's events belong to eager steps
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cap);
+  const int timing_saved = c->timing;
+  if (cap != cudaStreamCaptureStatusNone) c->timing = 0;
   // tiled_fast, then (side stream, high priority) a window kernel that takes window jobs as
   // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
   if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
@@ -845,6 +851,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     m[3] = timing_event(c); c->ev_marks.push_back(m);
     c->n_kernels += 2 + (c->tl.split ? 3 : 1) + (c->win_grid_poll > 0 ? 1 : 0) + (c->tl.M > 1 ? 1 : 0);
   }
+  c->timing = timing_saved;
 }
 
 static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats* out) {
@@ -1060,7 +1067,9 @@ extern "C" eis_status eis_step_finish(eis_ctx* c, double t_end, int32_t after_st
   if (c->sticky) return c->sticky;
   CU(cudaSetDevice(c->grid.device));
   tiled_finish<<<1, 1, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
-  if (c->timing) c->n_kernels += 1;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cap);
+  if (c->timing && cap == cudaStreamCaptureStatusNone) c->n_kernels += 1;
   CU(cudaGetLastError());
   return EIS_OK;
 }

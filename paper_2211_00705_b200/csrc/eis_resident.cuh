@@ -118,12 +118,12 @@ struct CtaShared {
 #define EIS_ARRIVE(i) do { if ((threadIdx.x & 31) == 0) { if (warp == SW) sh.tclk[i] = clock64(); if (warp == 0) sh.tclk[(i) + 1] = clock64(); } } while (0)
 #else
 #define EIS_TCLK(i) do { } while (0)
+#define EIS_ARRIVE(i) do { } while (0)
 #endif
 #ifdef EIS_FINE_CLOCK
 #define EIS_FCLK(i) do { if (threadIdx.x == 0) sh.fclk[i] = clock64(); } while (0)
 #else
 #define EIS_FCLK(i) do { } while (0)
-#define EIS_ARRIVE(i) do { } while (0)
 #endif
 
 __device__ __forceinline__ void set_status(CtaShared& sh, int code) { atomicCAS(&sh.status, 0, code); }

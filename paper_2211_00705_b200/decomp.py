@@ -51,12 +51,54 @@ def exchange_halos(xbuf: torch.Tensor, rank: int, world: int, group=None) -> Non
         dist.all_reduce(xbuf[XB_DT:XB_DT + 2], op=dist.ReduceOp.MIN, group=group)
 
 
+def capture_steps(step_once, k: int, stream):
+    """A CUDA graph of k calls of step_once() captured on `stream` (a torch.cuda.Stream, the
+    stream the library's contexts were created with): every call must only enqueue work on it
+    (library steps, torch device ops, NCCL collectives).  Replaying it runs k whole steps with no
+    host round trip between the per-step launches."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(k):
+            step_once()
+    return g
+
+
+class StepGraphs:
+    """Steps of a rank-mode grid as CUDA-graph replays: `graph_steps` steps per graph, captured
+    once per t_end (the launch arguments are part of the graph); a remainder runs eagerly."""
+
+    def __init__(self, step_once, stream, graph_steps: int):
+        self.step_once, self.stream, self.k = step_once, stream, graph_steps
+        self.graphs = {}
+
+    def run(self, n_steps: int, t_end: float):
+        g = self.graphs.get(t_end)
+        if g is None and n_steps >= self.k:
+            g = self.graphs[t_end] = capture_steps(lambda: self.step_once(t_end), self.k, self.stream)
+        while g is not None and n_steps >= self.k:
+            g.replay()
+            n_steps -= self.k
+        for _ in range(n_steps):
+            self.step_once(t_end)
+
+
 class RankGrid:
-    """This rank's slice of one tiled grid.  For world == 1 it is a plain tiled context."""
+    """This rank's slice of one tiled grid.  For world == 1 it is a plain tiled context.
+
+    graph_steps > 0 (world > 1): the per-step sequence step_local -> exchange -> step_finish is
+    captured into a CUDA graph of graph_steps steps on a stream of the grid's own and replayed,
+    so the host issues one replay per graph_steps steps instead of four calls per step.
+    The first step (eager) initialises the NCCL communicators before any capture."""
 
     def __init__(self, eos: dict, params: dict, n_global: int, x_left: float, x_right: float, rank: int,
-                 world: int, tile: int = 1400, device: int = 0, stream=None, group=None, slack: int = 16):
+                 world: int, tile: int = 1400, device: int = 0, stream=None, group=None, slack: int = 16,
+                 graph_steps: int = 0):
         self.rank, self.world, self.group = rank, world, group
+        self.graph_steps = graph_steps if world > 1 else 0
+        if self.graph_steps and (stream is None or stream == torch.cuda.default_stream(device)):
+            stream = torch.cuda.Stream(device)  # capture needs a stream other than the default one
+        self.stream = stream
+        self._graphs = None
         self.c0, self.c1 = rank_slice(n_global, tile, rank, world)
         self.n = self.c1 - self.c0
         self.h_av = (x_right - x_left) / n_global
@@ -69,23 +111,42 @@ class RankGrid:
             self.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
             self.ctx.set_exchange_buffer(self.xbuf)
 
+    def _on_stream(self):
+        """torch's current stream = the library's stream (NCCL and torch ops ordered with the kernels)"""
+        import contextlib
+        return torch.cuda.stream(self.stream) if hasattr(self.stream, "cuda_stream") else contextlib.nullcontext()
+
     def exchange(self):
-        exchange_halos(self.xbuf, self.rank, self.world, self.group)
+        with self._on_stream():
+            exchange_halos(self.xbuf, self.rank, self.world, self.group)
 
     def set_state(self, rho_local, mom_local, t_end: float = float("inf")):
         """rho/mom: this rank's cells [c0, c1) (padded to cap), device or host buffers."""
-        self.ctx.set_state(rho_local, mom_local)
-        if self.world > 1:
-            self.exchange()
-            self.ctx.step_finish(t_end, after_step=False)
+        with self._on_stream():
+            self.ctx.set_state(rho_local, mom_local)
+            if self.world > 1:
+                self.exchange()
+                self.ctx.step_finish(t_end, after_step=False)
 
-    def step(self, n_steps: int, t_end: float = float("inf")):
+    def _step_once(self, t_end: float):
+        self.ctx.step_local(t_end)
+        self.exchange()
+        self.ctx.step_finish(t_end, after_step=True)
+
+    def step(self, n_steps: int, t_end: float = float("inf"), graph: bool = True):
+        """graph=False: eager steps even when graph_steps > 0 (e.g. for per-kernel timing)."""
         if self.world == 1:
             return self.ctx.step(n_steps) if t_end == float("inf") else self.ctx.run_to(t_end, n_steps)
-        for _ in range(n_steps):
-            self.ctx.step_local(t_end)
-            self.exchange()
-            self.ctx.step_finish(t_end, after_step=True)
+        with self._on_stream():
+            if graph and self.graph_steps and n_steps > 0:
+                if self._graphs is None:
+                    self._step_once(t_end)  # eager: communicators and lazy module loads before capture
+                    n_steps -= 1
+                    self._graphs = StepGraphs(self._step_once, self.stream, self.graph_steps)
+                self._graphs.run(n_steps, t_end)
+                return
+            for _ in range(n_steps):
+                self._step_once(t_end)
 
 
 class VirtualRanks:
@@ -93,6 +154,8 @@ class VirtualRanks:
     waits on another): exercises the rank-mode library path against the 1-rank run."""
 
     def __init__(self, eos, params, n_global, x_left, x_right, world, tile=1400, device=0, stream=None):
+        self.stream = stream
+        self._graphs = None
         self.parts = []
         for r in range(world):
             g = RankGrid.__new__(RankGrid)
@@ -121,6 +184,11 @@ class VirtualRanks:
 
     def set_state(self, rho_global, mom_global, t_end=float("inf")):
         """rho/mom: the whole grid as 1-D device tensors."""
+        import contextlib
+        with torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext():
+            self._set_state(rho_global, mom_global, t_end)
+
+    def _set_state(self, rho_global, mom_global, t_end):
         for g in self.parts:
             r = torch.zeros(g.cap, dtype=torch.float64, device=rho_global.device)
             m = torch.zeros_like(r)
@@ -131,13 +199,27 @@ class VirtualRanks:
         for g in self.parts:
             g.ctx.step_finish(t_end, after_step=False)
 
-    def step(self, n_steps, t_end=float("inf")):
-        for _ in range(n_steps):
-            for g in self.parts:
-                g.ctx.step_local(t_end)
-            self._exchange()
-            for g in self.parts:
-                g.ctx.step_finish(t_end, after_step=True)
+    def _step_once(self, t_end):
+        for g in self.parts:
+            g.ctx.step_local(t_end)
+        self._exchange()
+        for g in self.parts:
+            g.ctx.step_finish(t_end, after_step=True)
+
+    def step(self, n_steps, t_end=float("inf"), graph_steps: int = 0):
+        """graph_steps > 0: as RankGrid, the steps as replays of a captured CUDA graph (the
+        contexts must have been created on a non-default torch stream, self.stream)."""
+        import contextlib
+        with torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext():
+            if graph_steps and n_steps > 0:
+                if self._graphs is None:
+                    self._step_once(t_end)
+                    n_steps -= 1
+                    self._graphs = StepGraphs(self._step_once, self.stream, graph_steps)
+                self._graphs.run(n_steps, t_end)
+                return
+            for _ in range(n_steps):
+                self._step_once(t_end)
 
     def get_state(self):
         outs = [g.ctx.get_state() for g in self.parts]

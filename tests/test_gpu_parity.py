@@ -542,6 +542,34 @@ def test_c5_virtual_ranks_cut_at_cavitating_segments(P, world):
     np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
 
 
+@pytest.mark.parametrize("world,graph_steps", [(2, 8), (4, 5)])
+def test_c5_virtual_ranks_cuda_graph_replay_bitwise(P, world, graph_steps):
+    """SURVEY §8(e), the decomposed step off the host: the per-step sequence of every rank slice
+    (step_local, the halo exchange, step_finish) captured once into a CUDA graph and replayed
+    (decomp.StepGraphs) gives the eager steps' results bit for bit, so the library's rank-mode
+    calls only enqueue work (a host synchronisation or allocation inside would break the capture).
+    Rank cuts on cavitating segment boundaries (tile 1024); 61 steps = 1 eager + replays + an
+    eager remainder."""
+    from paper_2211_00705_b200.decomp import VirtualRanks
+    n, steps, tile = 24 * 4096, 61, 1024
+    w = W.c5(n_cells=n)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)[:w["N"]]
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)[:w["N"]]
+    out = []
+    for gs in (0, graph_steps):
+        s = torch.cuda.Stream()
+        vr = VirtualRanks(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], world, tile=tile, stream=s)
+        vr.set_state(rho, mom)
+        vr.step(steps, graph_steps=gs)
+        torch.cuda.synchronize()
+        out.append(vr.get_state())
+    e, g = out
+    assert e["status"] == [0] * world and g["status"] == [0] * world
+    assert e["t"] == g["t"]
+    for k in ("rho", "mom", "h"):
+        np.testing.assert_array_equal(g[k], e[k])
+
+
 @pytest.mark.parametrize("n,steps", [(40 * 940 + 517, 200)])
 def test_c5_window_path_matches_whole_tile_path(P, oracle_mod, n, steps, monkeypatch):
     """The windowed full step (tiled_win: step body on <= 160 owned cells around a tile's special

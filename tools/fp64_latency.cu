@@ -13,9 +13,9 @@
     ++k;                                                                \
   }
 
-__global__ void lat(double* out, double* cyc, double seed) {
+__global__ void lat(double* out, double* cyc, double seed, double ca, double cb) {
   int k = 0;
-  CHAIN("dfma", fma(x, 1.0000001, 1e-9));
+  CHAIN("dfma", fma(x, ca, cb));
   CHAIN("ddiv", 1.0000001 / x);
   CHAIN("drcp_rn", __drcp_rn(x));
   CHAIN("dsqrt", sqrt(x + 1.0));
@@ -37,9 +37,9 @@ int main() {
   double *out, *cyc;
   cudaMallocManaged(&out, 64 * 8);
   cudaMallocManaged(&cyc, 64 * 8);
-  lat<<<1, 1>>>(out, cyc, 1.5);
+  lat<<<1, 1>>>(out, cyc, 1.5, 1.0000001, 1e-9);
   cudaDeviceSynchronize();
-  lat<<<1, 1>>>(out, cyc, 1.5);
+  lat<<<1, 1>>>(out, cyc, 1.5, 1.0000001, 1e-9);
   cudaDeviceSynchronize();
   const char* names[] = {"dfma", "ddiv", "drcp_rn", "dsqrt", "dlog", "dlog1p", "dexp", "logf", "fdiv"};
   printf("{");

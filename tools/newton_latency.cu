@@ -59,10 +59,10 @@ __global__ void k_eval(const __grid_constant__ Eos e, int R, long long* cyc, dou
 __global__ void k_eval(const __grid_constant__ Eos e, int R, long long* cyc, double* out) {
   IfaceProb P;
   P.rV = 0.01; P.uV = 0.0; P.rL = 999.0; P.uL = -150.0; P.sV = 1.0; P.du = 150.0;
-  double G[2], J[4], aux[2], acc = 0, x0 = 500.0 + threadIdx.x, x1 = 600.0;
+  double G[2], J[4], aux[2], da[4], acc = 0, x0 = 500.0 + threadIdx.x, x1 = 600.0;
   long long t0 = clock64();
   for (int r = 0; r < R; ++r) {
-    iface_eval(e, P, x0, x1, G, J, aux);
+    iface_eval(e, P, x0, x1, G, J, aux, da);
     x0 += 1e-9 * G[0]; x1 += 1e-9 * J[3];  // dependent chain
     acc += aux[0];
   }
@@ -70,7 +70,30 @@ __global__ void k_eval(const __grid_constant__ Eos e, int R, long long* cyc, dou
   if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / R; out[0] = acc + x0 + x1; }
 }
 
+__global__ void k_lin(const __grid_constant__ Eos e, const __grid_constant__ Prm p, int R, long long* cyc, double* out) {
+  // warm-started one-evaluation solve (iface_try_lin, the DTS inner solve): start at the root
+  double rl = 999.0, ul = -150.0, rv = 0.01, uv = 0.0;
+  IfaceSol s0 = iface_solve_t(e, p, rl, ul, rv, uv, false, -1.0, -1.0);
+  double x0 = s0.pV, x1 = s0.pL, acc = 0;
+  int ok = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < R; ++r) {
+    IfaceSol s;
+    const bool b = iface_try_lin(e, p, rl, ul + 1e-12 * (r & 7) + 1e-13 * acc, rv, uv, false, x0, x1, s);
+    ok += b;
+    acc += 1e-30 * s.F1;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / R; out[0] = acc + ok; out[1] = ok; }
+}
 int main_eval_only(Eos& e, long long* cyc, double* out) {
+  Prm p;
+  p.cfl = 0.9; p.eps_split = 2; p.eps_tiny = 0.5; p.theta_nb = 0.9; p.tol_nb = 1e-3; p.tol_tiny = 0.1;
+  p.newton_rtol = 1e-13; p.newton_gtol = 1e-12; p.newton_stol = sqrt(1e-13); p.h_av = 1e-3; p.dts_max_iter = 1000000; p.newton_max_iter = 50;
+  p.armijo_max = 30; p.mode = 0; p.lin_gtol = 1e-6;
+  k_lin<<<1, 1>>>(e, p, 200, cyc, out);
+  cudaDeviceSynchronize();
+  printf("{\"try_lin_cycles\": %lld, \"accepted\": %.0f}\n", cyc[0], out[1]);
 
   for (int th : {1, 32}) {
     k_eval<<<1, th>>>(e, 200, cyc, out);
