@@ -453,7 +453,8 @@ def main_c5(args, torch, dist, P, world, rank, local):
     gsteps = int(os.environ.get("EIS_RANK_GRAPH", "10")) if world > 1 else 0
     rg = RankGrid(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], rank, world, device=local,
                   tile=int(os.environ.get("EIS_TILE", "1400")),
-                  stream=stream, graph_steps=gsteps)
+                  stream=stream, graph_steps=gsteps,
+                  peer=os.environ.get("EIS_RANK_PEER", "1") != "0")  # the exchange over peer memory
     stream = rg.stream if rg.stream is not None else stream  # the library's stream: events go there
     rho_l = np.zeros(rg.cap)
     mom_l = np.zeros(rg.cap)
@@ -551,8 +552,9 @@ def main_c5(args, torch, dist, P, world, rank, local):
                        "l2": "state (2 GB) larger than L2",
                        "implicit_regions": MODE_NAMES[mode],
                        "launches": "per step: tiled_fast + window part A + dts_jobs + window part B + tiled_slow" +
-                                   ("" if world == 1 else " + tiled_finish (after the exchange)")
-                       + (" + NCCL halo exchange / all-reduce + tiled_finish" if world > 1 else "")},
+                                   ("" if world == 1 else (" + tiled_finish (peer-memory exchange by the kernels)"
+                                                           if rg.peer else " + NCCL halo exchange / all-reduce + tiled_finish"))
+                                   + (f"; CUDA graphs of {gsteps} steps" if gsteps else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": ncu_traffic("C5"), "kernel": "eis::tiled_fast",
                          "bytes_per_cell_update": C5_BYTES_PER_CELL_UPDATE,

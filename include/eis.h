@@ -218,6 +218,23 @@ eis_status eis_member_stats(eis_ctx* ctx, eis_stats* out);
 #define EIS_XB_DT (4 * EIS_XB_REC)
 #define EIS_XB_DOUBLES (4 * EIS_XB_REC + 2)
 eis_status eis_set_exchange_buffer(eis_ctx* ctx, double* dev_xbuf);
+/* Peer mode (the exchange inside the kernels, over NVLink peer memory): every
+ * rank's exchange buffer holds EIS_XB_DOUBLES_PEER doubles, zero-initialised, device memory that
+ * every rank's device can access (peer-mapped / symmetric memory).  `left` / `right`: the left /
+ * right neighbour's buffer (NULL exactly where nbr_left / nbr_right is 0), `all[q]`: rank q's
+ * buffer (host array of `world` <= EIS_XB_MAXRANKS device pointers; all[rank] is this context's
+ * own).  Then the step's last CTA writes this rank's send records into the neighbours' receive
+ * slots and its CFL pair into every rank's pair table (double-buffered by the parity of a
+ * publication count, tagged after a system-scope fence); eis_step_finish waits for every rank's
+ * tag (one warp; a peer that never publishes ends the wait after ~2 s with member status
+ * EIS_E_INTERNAL), folds the pairs (min) and moves the records into the receive slots.  The
+ * caller runs no collective: per step eis_step_local -> eis_step_finish(after_step = 1), and
+ * after eis_set_state eis_step_finish(after_step = 0).  Every rank must issue the same sequence
+ * of calls.  Returns EIS_E_ARG for inconsistent pointers or world. */
+#define EIS_XB_MAXRANKS 8
+#define EIS_XB_DOUBLES_PEER (EIS_XB_DOUBLES + 4 * EIS_XB_REC + 8 * EIS_XB_MAXRANKS)
+eis_status eis_set_exchange_peers(eis_ctx* ctx, double* left, double* right, double* const* all, int32_t rank,
+                                  int32_t world);
 eis_status eis_step_local(eis_ctx* ctx, double t_end);
 eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
 

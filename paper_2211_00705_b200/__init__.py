@@ -76,7 +76,8 @@ class Thresholds(C.Structure):
 # exported symbols of libeis.so (checked by tests/test_abi.py against include/eis.h)
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
-           "eis_set_exchange_buffer", "eis_step_local", "eis_step_finish", "eis_tile_info", "eis_set_timing",
+           "eis_set_exchange_buffer", "eis_set_exchange_peers", "eis_step_local", "eis_step_finish",
+           "eis_tile_info", "eis_set_timing",
            "eis_get_timing", "eis_window_diag", "eis_lax_run")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
@@ -84,6 +85,8 @@ XB_REC = 3 * HALO + 1
 XB_SEND_LEFT, XB_SEND_RIGHT, XB_RECV_LEFT, XB_RECV_RIGHT = 0, XB_REC, 2 * XB_REC, 3 * XB_REC
 XB_DT = 4 * XB_REC
 XB_DOUBLES = 4 * XB_REC + 2
+XB_MAXRANKS = 8
+XB_DOUBLES_PEER = XB_DOUBLES + 4 * XB_REC + 8 * XB_MAXRANKS  # peer mode (eis_set_exchange_peers)
 
 _lib = None
 
@@ -113,6 +116,7 @@ def lib():
         L.eis_last_error.restype = C.c_char_p
         L.eis_destroy.argtypes = [vp]
         L.eis_set_exchange_buffer.argtypes = [vp, vp]
+        L.eis_set_exchange_peers.argtypes = [vp, vp, vp, P(vp), i32, i32]
         L.eis_step_local.argtypes = [vp, d]
         L.eis_step_finish.argtypes = [vp, d, i32]
         L.eis_lax_run.argtypes = [P(LaxCase), i64, i64, vp, vp, vp, P(LaxStats), vp]
@@ -286,6 +290,15 @@ class Context:
         """xbuf: a device tensor of XB_DOUBLES float64 owned by the caller (kept alive by it)."""
         self._xbuf = xbuf
         self._check(lib().eis_set_exchange_buffer(self._ctx, xbuf.data_ptr()), "eis_set_exchange_buffer")
+
+    def set_exchange_peers(self, left_ptr, right_ptr, all_ptrs, rank: int, world: int):
+        """Peer mode: device addresses (ints) of the neighbours' exchange buffers (None at the
+        domain ends) and of every rank's, each XB_DOUBLES_PEER float64 (this rank's own buffer,
+        set with set_exchange_buffer, must be all_ptrs[rank])."""
+        arr = (C.c_void_p * len(all_ptrs))(*[int(a) for a in all_ptrs])
+        self._check(lib().eis_set_exchange_peers(self._ctx, C.c_void_p(left_ptr) if left_ptr else None,
+                                                 C.c_void_p(right_ptr) if right_ptr else None, arr,
+                                                 int(rank), int(world)), "eis_set_exchange_peers")
 
     def step_local(self, t_end: float = float("inf")):
         self._check(lib().eis_step_local(self._ctx, float(t_end)), "eis_step_local")

@@ -66,6 +66,7 @@ struct eis_ctx {
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
+  double** d_xpeers = nullptr;  // peer mode: the ranks' exchange buffers (device array)
   int dts_grid = 0;                        // window split: dts_jobs CTAs (one warp each)
   int dts_tpb = 32;                        //   threads per dts_jobs CTA (EIS_DTS_TPB, development)
   DtsJob* t_djobs = nullptr;
@@ -404,7 +405,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (ok && split)
     ok = cudaMalloc(&c->t_djobs, (size_t)djcap * sizeof(DtsJob)) == cudaSuccess &&
          cudaMalloc(&c->t_wsave, (size_t)ntiles * WSAVE) == cudaSuccess;
-  if (!ok) { eis_destroy(c); return EIS_E_CUDA; }
+  if (!ok || cudaMemset(c->t_ctl, 0, 16 * 4) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
   c->g.dbg = nullptr;
@@ -425,6 +426,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   tl.mctl = c->t_mctl;
   tl.ntiles = (int)ntiles; tl.capt = capt; tl.M = (int)M; tl.tpm = (int)tpm;
   tl.xbuf = nullptr;
+  tl.xpeer_l = nullptr; tl.xpeer_r = nullptr; tl.xpeers = nullptr; tl.xrank = 0; tl.xworld = 1;
   tl.nbr_left = grid->nbr_left != 0; tl.nbr_right = grid->nbr_right != 0;
   *out = c;
   return EIS_OK;
@@ -432,7 +434,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m == 0) for (int q = 0; q < 16; ++q) tl.ctl[q] = 0;
+  if (m == 0) for (int q = 0; q < 16; ++q) if (q != 12) tl.ctl[q] = 0;  // [12]: peer-mode publications,
+                                                                        // counted over the context's life
   if (m >= tl.M) return;
   if (status[m]) atomicCAS(&tl.ctl[1], 0, status[m]);
   int* mc = tl.mctl + MCS * m;
@@ -632,6 +635,7 @@ extern "C" void eis_destroy(eis_ctx* c) {
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
   cudaFree(c->t_djobs); cudaFree(c->t_wsave);
+  cudaFree(c->d_xpeers);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_mctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -1045,6 +1049,24 @@ extern "C" eis_status eis_member_stats(eis_ctx* c, eis_stats* out) {
 // ------------------------------------------------------------------------------------------
 // rank mode (one tiled grid decomposed over ranks): exchange buffer + split step
 // ------------------------------------------------------------------------------------------
+static_assert(EIS_XB_DOUBLES_PEER == XB_DOUBLES_PEER && EIS_XB_MAXRANKS == XB_MAXRANKS, "exchange layout (include/eis.h)");
+// peer mode: the neighbours' exchange buffers and every rank's (device pointers this context's
+// device can access: peer-mapped / symmetric memory), each of EIS_XB_DOUBLES_PEER doubles
+extern "C" eis_status eis_set_exchange_peers(eis_ctx* c, double* left, double* right, double* const* all,
+                                             int32_t rank, int32_t world) {
+  if (!c || !c->tiled || !c->tl.xbuf || !all || world < 1 || world > XB_MAXRANKS || rank < 0 || rank >= world)
+    return EIS_E_ARG;
+  if ((c->tl.nbr_left != 0) != (left != nullptr) || (c->tl.nbr_right != 0) != (right != nullptr)) return EIS_E_ARG;
+  for (int q = 0; q < world; ++q) if (!all[q]) return EIS_E_ARG;
+  if (all[rank] != c->tl.xbuf) return EIS_E_ARG;  // this rank's entry is its own exchange buffer
+  CU(cudaSetDevice(c->grid.device));
+  if (!c->d_xpeers) CU(cudaMalloc(&c->d_xpeers, XB_MAXRANKS * sizeof(double*)));
+  CU(cudaMemcpy(c->d_xpeers, all, world * sizeof(double*), cudaMemcpyHostToDevice));
+  c->tl.xpeer_l = left; c->tl.xpeer_r = right;
+  c->tl.xpeers = c->d_xpeers; c->tl.xrank = rank; c->tl.xworld = world;
+  return EIS_OK;
+}
+
 extern "C" eis_status eis_set_exchange_buffer(eis_ctx* c, double* xbuf) {
   if (!c || !c->tiled || !xbuf) return EIS_E_ARG;
   c->tl.xbuf = xbuf;
@@ -1066,7 +1088,7 @@ extern "C" eis_status eis_step_finish(eis_ctx* c, double t_end, int32_t after_st
   if (!c || !c->tiled || !c->tl.xbuf) return EIS_E_ARG;
   if (c->sticky) return c->sticky;
   CU(cudaSetDevice(c->grid.device));
-  tiled_finish<<<1, 1, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
+  tiled_finish<<<1, 32, 0, c->stream>>>(c->p, c->tl, t_end, after_step);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cap);
   if (c->timing && cap == cudaStreamCaptureStatusNone) c->n_kernels += 1;

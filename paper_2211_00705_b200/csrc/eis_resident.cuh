@@ -830,94 +830,96 @@ __device__ __forceinline__ void zone_status_e(CtaShared& sh, const Zone& Z, int 
 
 // ------------------------------------------------------------------------------------------
 // Bulk pass P1 (own register allocation: the loop invariants stay in registers).
-// window w: 64 cells, two per lane, c0 = 62w-2+2l and c1 = c0+1 (lane 0 is the left halo,
-// transmissive ghosts at the ends, R15); lane l >= 1 owns c0, c1, the LEFT edge of c0 and the
-// edge between c0 and c1: HLL flux (a3), creation trigger (a4), S_max / h_min partials (a2).
-// One reciprocal per cell (u = m/rho); the left neighbour's state arrives by shuffle.
-// Interior windows skip the ghost clamps.  Flagged cells are re-checked in full (rare).
+// window w: 32 CPL cells, CPL per lane, c_j = 31 CPL w - CPL + CPL l + j (lane 0 is the left
+// halo; transmissive ghosts at the ends, R15); lane l >= 1 owns its CPL cells, the LEFT edge of
+// its first cell and its internal edges: HLL flux (a3), creation trigger (a4), S_max / h_min
+// partials (a2).  One reciprocal per cell (u = m/rho); the left neighbour's state arrives by
+// shuffle.  Interior windows skip the ghost clamps.  Flagged cells are re-checked in full (rare).
+// (EIS_P1_CPL: cells per lane, 2; 4 measured 5 % slower on C3 in round 2.)
 // ------------------------------------------------------------------------------------------
-__device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
-                                     const double* __restrict__ rho, const double* __restrict__ mom,
-                                     const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
-                                     const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
+#ifndef EIS_P1_CPL
+#define EIS_P1_CPL 2
+#endif
+template <int CPL>
+__device__ __forceinline__ void bulk_p1_t(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
+                                          const double* __restrict__ rho, const double* __restrict__ mom,
+                                          const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
+                                          const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
   const Eos e = e_ref;  // constants into registers once (not a generic load per use)
   const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
   const double a_v = e.a_v, a_l = e.a_l, rmin2 = e.rho_min * e.rho_min, inv_rt = 1.0 / e.rho_tilde;
   const double eps_h = p_ref.eps_tiny * p_ref.h_av;
   const bool explicit_mode = p_ref.mode == 1;
   const int lane = threadIdx.x & 31;
+  constexpr int WW = 31 * CPL;  // owned cells (and left edges) per window
   double s_part = 0.0, h_part = INFINITY;
   bool bad = false;      // a non-positive or spinodal density somewhere (reported below, rare)
   bool special = false;  // a trigger candidate or a phase change (handled below, rare)
-  // main pass: windows of 64 cells, two per lane (c0 = 62w-2+2l, c1 = c0+1); lanes >= 1 own
-  // c0, c1, the left edge of c0 (left state by shuffle) and the internal edge c1
-  const int nwp = (n + 62) / 62;  // edges 0..n
+  const int nwp = (n + WW) / WW;  // edges 0..n
   for (int w = warp; w < nwp; w += nbulk) {
-    const int c0 = 62 * w - 2 + 2 * lane, c1 = c0 + 1;
-    const bool interior_win = w > 0 && 62 * w + 62 < n;  // c0 .. c1 + 1 all exist
-    int i0 = c0, i1 = c1;
-    if (!interior_win) {
-      i0 = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0);
-      i1 = c1 < 0 ? 0 : (c1 >= n ? n - 1 : c1);
+    const int cb = WW * w - CPL + CPL * lane;  // this lane's first cell
+    const bool interior_win = w > 0 && WW * w + WW < n;  // every cell of the window and its right neighbour exist
+    double r[CPL], m[CPL], u[CPL], q[CPL], a[CPL];
+    unsigned ph[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      int i = cb + j;
+      if (!interior_win) i = i < 0 ? 0 : (i >= n ? n - 1 : i);
+      r[j] = rho[i]; m[j] = mom[i];
     }
-    const double r0 = rho[i0], m0 = mom[i0], r1 = rho[i1], m1 = mom[i1];
-    const double u0 = m0 * rcp_fast(r0), u1 = m1 * rcp_fast(r1);
-    const bool v0 = r0 <= rho_tilde, l0 = r0 >= rho_min, v1 = r1 <= rho_tilde, l1 = r1 >= rho_min;
-    const unsigned ph0 = v0 ? 1u : (l0 ? 2u : 0u), ph1 = v1 ? 1u : (l1 ? 2u : 0u);
-    const double q0 = v0 ? a_v2 * r0 : p0 + a_l2 * (r0 - rho0);
-    const double q1 = v1 ? a_v2 * r1 : p0 + a_l2 * (r1 - rho0);
-    const double a0 = v0 ? a_v : a_l, a1 = v1 ? a_v : a_l;
-    const double rl = __shfl_up_sync(0xffffffffu, r1, 1), ml = __shfl_up_sync(0xffffffffu, m1, 1);
-    const double ul = __shfl_up_sync(0xffffffffu, u1, 1), pl = __shfl_up_sync(0xffffffffu, q1, 1);
-    const unsigned phl = __shfl_up_sync(0xffffffffu, ph1, 1);
-    unsigned phr = __shfl_down_sync(0xffffffffu, ph0, 1);
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      u[j] = m[j] * rcp_fast(r[j]);
+      const bool v = r[j] <= rho_tilde, l = r[j] >= rho_min;
+      ph[j] = v ? 1u : (l ? 2u : 0u);
+      q[j] = v ? a_v2 * r[j] : p0 + a_l2 * (r[j] - rho0);
+      a[j] = v ? a_v : a_l;
+    }
+    const double rl = __shfl_up_sync(0xffffffffu, r[CPL - 1], 1), ml = __shfl_up_sync(0xffffffffu, m[CPL - 1], 1);
+    const double ul = __shfl_up_sync(0xffffffffu, u[CPL - 1], 1), pl = __shfl_up_sync(0xffffffffu, q[CPL - 1], 1);
+    const unsigned phl = __shfl_up_sync(0xffffffffu, ph[CPL - 1], 1);
+    unsigned phr = __shfl_down_sync(0xffffffffu, ph[0], 1);
     if (lane == 31) {
-      const double rr = rho[c1 + 1 < n ? c1 + 1 : n - 1];
+      const int ir = cb + CPL;
+      const double rr = rho[ir < n ? ir : n - 1];
       phr = rr <= rho_tilde ? 1u : (rr >= rho_min ? 2u : 0u);
     }
     if (lane >= 1) {
-      if (c0 < n) {  // cell c0: S_max, h_min partials
-        bad |= !(r0 > 0.0) || ph0 == 0u;
-        const double su = fabs(u0) + a0;
-        s_part = su > s_part ? su : s_part;  // S over all cells (R5)
-        const double hc = h[c0];
-        const bool same_l = c0 > 0 && phl == ph0, same_r = c0 + 1 < n && ph1 == ph0;
-        const bool tiny = hc < eps_h && !same_l && !same_r;
-        const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
-        h_part = hh < h_part ? hh : h_part;  // h_min over non-tiny cells (R6)
-      }
-      if (c1 < n) {  // cell c1
-        bad |= !(r1 > 0.0) || ph1 == 0u;
-        const double su = fabs(u1) + a1;
-        s_part = su > s_part ? su : s_part;
-        const double hc = h[c1];
-        const bool same_l = ph0 == ph1, same_r = c1 + 1 < n && phr == ph1;
-        const bool tiny = hc < eps_h && !same_l && !same_r;
-        const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
-        h_part = hh < h_part ? hh : h_part;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {  // cell c_j: S_max, h_min partials
+        const int c = cb + j;
+        if (c < n) {
+          bad |= !(r[j] > 0.0) || ph[j] == 0u;
+          const double su = fabs(u[j]) + a[j];
+          s_part = su > s_part ? su : s_part;  // S over all cells (R5)
+          const double hc = h[c];
+          const bool same_l = j == 0 ? (c > 0 && phl == ph[0]) : ph[j - 1] == ph[j];
+          const bool same_r = c + 1 < n && (j == CPL - 1 ? phr : ph[j + 1]) == ph[j];
+          const bool tiny = hc < eps_h && !same_l && !same_r;
+          const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
+          h_part = hh < h_part ? hh : h_part;  // h_min over non-tiny cells (R6)
+        }
       }
       // creation pre-filters (R7), exact bounds with a 1e-9 m/s margin: liquid, both waves
       // rarefactions and ln y <= y - 1; vapour, both shocks and sqrt(rt r) <= rt, so
       // Phi(rt) >= du + a_v (2 - (r_L + r_R)/rt)
-      if (c0 <= n && phl == ph0 && ph0 != 0u) {  // edge c0 between cells c0-1 and c0
-        double f0, f1;
-        hll_fast(a0, rl, ml, ul, pl, r0, m0, u0, q0, f0, f1);
-        F0[c0] = f0; F1[c0] = f1;
-        const double du = u0 - ul, x = rl * r0;
-        const bool cand = l0 ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (rl + r0) * inv_rt) + 1e-9);
-        special |= cand && c0 > 0 && c0 < n;
-      } else if (c0 > 0 && c0 < n && phl != ph0) {
-        special |= !(fl[c0] & F_IF);  // a phase change must be a listed boundary
-      }
-      if (c1 <= n && ph0 == ph1 && ph1 != 0u) {  // edge c1 between cells c0 and c1
-        double f0, f1;
-        hll_fast(a1, r0, m0, u0, q0, r1, m1, u1, q1, f0, f1);
-        F0[c1] = f0; F1[c1] = f1;
-        const double du = u1 - u0, x = r0 * r1;
-        const bool cand = l1 ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x) : (du < -a_v * (2.0 - (r0 + r1) * inv_rt) + 1e-9);
-        special |= cand && c1 < n;
-      } else if (c1 < n && ph0 != ph1) {
-        special |= !(fl[c1] & F_IF);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {  // edge c_j between cells c_j - 1 and c_j
+        const int c = cb + j;
+        const double rL = j == 0 ? rl : r[j - 1], mL = j == 0 ? ml : m[j - 1];
+        const double uL = j == 0 ? ul : u[j - 1], pL = j == 0 ? pl : q[j - 1];
+        const unsigned phL = j == 0 ? phl : ph[j - 1];
+        if (c <= n && phL == ph[j] && ph[j] != 0u) {
+          double f0, f1;
+          hll_fast(a[j], rL, mL, uL, pL, r[j], m[j], u[j], q[j], f0, f1);
+          F0[c] = f0; F1[c] = f1;
+          const double du = u[j] - uL, x = rL * r[j];
+          const bool cand = ph[j] == 2u ? !(du * x <= a_l * (x - rmin2) - 1e-9 * x)
+                                        : (du < -a_v * (2.0 - (rL + r[j]) * inv_rt) + 1e-9);
+          special |= cand && c > 0 && c < n;
+        } else if (c > 0 && c < n && phL != ph[j]) {
+          special |= !(fl[c] & F_IF);  // a phase change must be a listed boundary
+        }
       }
     }
   }
@@ -925,31 +927,37 @@ __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShar
   parts[1] = h_part;
   if (__any_sync(0xffffffffu, bad || special)) {  // rare: redo this warp's cells and edges in full
     for (int w = warp; w < nwp; w += nbulk) {
-      for (int q = 0; q < 2; ++q) {
-        const int cj = 62 * w - 2 + 2 * lane + q;
+      for (int qq = 0; qq < CPL; ++qq) {
+        const int cj = WW * w - CPL + CPL * lane + qq;
         if (lane < 1 || cj >= n) continue;
         const double rc = rho[cj];
         const int pc = phase_of(e, rc);
         if (!(rc > 0.0)) zone_status(sh, Z, cj, ST_NONPOS);
         else if (pc == SPIN) zone_status(sh, Z, cj, ST_SPINODAL);
         if (cj < 1) continue;
-        const double rl = rho[cj - 1];
-        const int pl = phase_of(e, rl);
-        if (pl == pc && pc != SPIN) {
-          const double uc = mom[cj] / rc, ul = mom[cj - 1] / rl;
+        const double rL = rho[cj - 1];
+        const int pL = phase_of(e, rL);
+        if (pL == pc && pc != SPIN) {
+          const double uc = mom[cj] / rc, uL = mom[cj - 1] / rL;
           bool marg = false;
           if (cj - 1 >= Z.zlo && cj < Z.zhi && !region_at(e, p_ref, rho, h, n, cj - 1) &&
-              !region_at(e, p_ref, rho, h, n, cj) && creation_trigger(e, pc, rl, ul, rc, uc, marg)) {  // R16
+              !region_at(e, p_ref, rho, h, n, cj) && creation_trigger(e, pc, rL, uL, rc, uc, marg)) {  // R16
             const int k = atomicAdd(&sh.ntrg, 1);
             if (k < MAXTRG) { sh.trg[k].e = cj; sh.trg[k].acc = 0; } else set_status(sh, ST_CAPACITY);
           }
           if (marg && Z.own_lo < cj && cj <= Z.own_hi) atomicAdd(&sh.c_margin, 1ull);  // owned edge
-        } else if (pl != pc && !(fl[cj] & F_IF)) {
+        } else if (pL != pc && !(fl[cj] & F_IF)) {
           zone_status_e(sh, Z, cj, ST_INTERNAL);  // a phase boundary missing from the list
         }
       }
     }
   }
+}
+__device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
+                                     const double* __restrict__ rho, const double* __restrict__ mom,
+                                     const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
+                                     const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
+  bulk_p1_t<EIS_P1_CPL>(e_ref, p_ref, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts);
 }
 
 // Bulk pass P2: explicit update of the cells with two HLL edges (a7); h^{n+1} = h^n there, so

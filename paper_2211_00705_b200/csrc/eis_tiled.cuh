@@ -47,6 +47,13 @@ struct Tiles {
   int* wlist;                      // work list of (tile, window begin, window end, ready tag)
   double* partf;                   // per window tile: S_max, h_min, all-h_av of its fast cells
   double* part2;                   // per tiled_slow CTA: S_max, h_min
+  // peer mode (eis_set_exchange_peers): the exchange done by the kernels themselves over peer
+  // memory (NVLink): xpeer_l / xpeer_r are the neighbours' exchange buffers (null at the domain
+  // ends), xpeers[q] rank q's (for the CFL pair); null xpeers: the caller exchanges (NCCL)
+  double* xpeer_l;
+  double* xpeer_r;
+  double* const* xpeers;
+  int xrank, xworld;
   long long* wdbg;                 // diagnostics (EIS_WINDOW_DEBUG): per window job of the last step
                                    // {cycles, dts iterations, window cells, boundaries, start clock,
                                    //  6 phase cycles (EIS_PHASE_CLOCK builds, else 0)}
@@ -73,6 +80,15 @@ constexpr int XB_REC = 3 * HALO + 1;
 constexpr int XB_SEND_LEFT = 0, XB_SEND_RIGHT = XB_REC, XB_RECV_LEFT = 2 * XB_REC, XB_RECV_RIGHT = 3 * XB_REC;
 constexpr int XB_DT = 4 * XB_REC;
 constexpr int XB_DOUBLES = 4 * XB_REC + 2;
+// peer mode, appended (double-buffered by the parity of the publication tag, so a neighbour one
+// publication ahead never overwrites what this rank has not consumed yet): the neighbours'
+// records [parity][left, right][XB_REC] and the ranks' CFL pairs [parity][rank][-S_max, h_min,
+// tag, status]
+constexpr int XB_MAXRANKS = 8;
+constexpr int XB_PREC = XB_DOUBLES;                          // + (2 par + side) * XB_REC
+constexpr int XB_PPAIR = XB_PREC + 4 * XB_REC;               // + (par * XB_MAXRANKS + rank) * 4
+constexpr int XB_DOUBLES_PEER = XB_PPAIR + 2 * XB_MAXRANKS * 4;
+// ctl[12]: publications of this rank (init + every step) = the tag of the last one
 
 constexpr int WS_STRIDE = 2 * MAXIF + 1;
 
@@ -98,6 +114,35 @@ __device__ __forceinline__ void cfl_partials(const Eos& e, const Prm& p, const d
   h_out = warp_min(hm);
 }
 
+// Peer mode: this rank's step-end exchange, by one CTA after every record of the step is written
+// (the last CTA of tiled_slow / tiled_init_dt): its send records into the neighbours' receive
+// slots, its CFL pair (-S_max, h_min) and status into every rank's pair table, then -- after a
+// system-scope fence -- the tag.  Consumed by tiled_finish (eis_step_finish).
+__device__ void xpublish(const Tiles& tl, double neg_s, double hm, int status) {
+  __shared__ long long tag_s;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid == 0) tag_s = (long long)(++tl.ctl[12]);
+  __syncthreads();
+  const long long tag = tag_s;
+  const int par = (int)(tag & 1);
+  for (int q = tid; q < XB_REC; q += blockDim.x) {  // my send-left -> left rank's right slot, etc.
+    if (tl.xpeer_l) tl.xpeer_l[XB_PREC + (2 * par + 1) * XB_REC + q] = tl.xbuf[XB_SEND_LEFT + q];
+    if (tl.xpeer_r) tl.xpeer_r[XB_PREC + (2 * par + 0) * XB_REC + q] = tl.xbuf[XB_SEND_RIGHT + q];
+  }
+  for (int q = tid; q < tl.xworld; q += blockDim.x) {
+    double* pr = tl.xpeers[q] + XB_PPAIR + (par * XB_MAXRANKS + tl.xrank) * 4;
+    pr[0] = neg_s; pr[1] = hm; pr[3] = (double)status;
+  }
+  __threadfence_system();
+  __syncthreads();
+  for (int q = tid; q < tl.xworld; q += blockDim.x) {
+    volatile double* pt = tl.xpeers[q] + XB_PPAIR + (par * XB_MAXRANKS + tl.xrank) * 4 + 2;
+    *pt = (double)tag;
+  }
+  __threadfence_system();
+}
+
 // Last CTA of a step: fold the per-CTA partials into the next dt, advance t.
 __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, double dt_used, double t_end) {
   __shared__ double rs[32], rh[32];
@@ -115,13 +160,19 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
     tl.ctl[8] = tl.ctl[6];  // window jobs of this step (diagnostics)
     tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
-    if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
+  }
+  if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
+    if (tid == 0) {
       tl.xbuf[XB_DT] = -s;
       tl.xbuf[XB_DT + 1] = hm;
       tl.scal[4] = dt_used;
       __threadfence();
-      return;
     }
+    __syncthreads();
+    if (tl.xpeers) xpublish(tl, tl.xbuf[XB_DT], tl.xbuf[XB_DT + 1], 0);
+    return;
+  }
+  if (tid == 0) {
     const double t_new = tl.scal[0] + dt_used;
     double dt = p.cfl * hm / s;
     if (t_new + dt > t_end) dt = t_end - t_new;
@@ -1051,6 +1102,9 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   const double t = tl.scal[0], dt_given = tl.scal[1];
   if (one && (tl.mctl[1] != 0 || !(t < t_end))) {  // uniform across the grid: nothing to do
     if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }  // (a no-op step's counters)
+    // peer mode: a stopped rank still publishes a neutral pair while the others step (t is
+    // global, so at t_end every rank stops together and nobody waits)
+    if (blockIdx.x == 0 && tl.xbuf && tl.xpeers && t < t_end) xpublish(tl, 0.0, INFINITY, tl.mctl[1]);
     return;
   }
   double dt = dt_given;
@@ -1091,7 +1145,10 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   if (last) {
     __threadfence();
     if (tl.mctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
-    else if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }
+    else {
+      if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }
+      if (tl.xbuf && tl.xpeers) xpublish(tl, 0.0, INFINITY, tl.mctl[1]);  // (neutral pair, status)
+    }
   }
 }
 
@@ -1128,6 +1185,28 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
   hm = warp_min(hm);
   if (lane == 0) { rs[warp] = s; rh[warp] = hm; }
   __syncthreads();
+  // initial halos for the first exchange (before the last-CTA election: peer mode publishes
+  // them with the initial CFL pair)
+  if (tl.xbuf && (k == 0 || k == tl.ntiles - 1)) {  // initial halos for the first exchange
+    const int cur2 = tl.mctl[0];
+    if (k == 0 && tl.nbr_left) {
+      double* sb = tl.xbuf + XB_SEND_LEFT;
+      for (int i = tid; i < HALO; i += blockDim.x) {
+        sb[i] = tl.rho[cur2][base + i]; sb[HALO + i] = tl.mom[cur2][base + i];
+        sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][base + i];
+      }
+      if (tid == 0) sb[3 * HALO] = HALO;
+    }
+    if (k == tl.ntiles - 1 && tl.nbr_right) {
+      double* sb = tl.xbuf + XB_SEND_RIGHT;
+      for (int i = tid; i < HALO; i += blockDim.x) {
+        const long long j = base + cnt - HALO + i;
+        sb[i] = tl.rho[cur2][j]; sb[HALO + i] = tl.mom[cur2][j]; sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][j];
+      }
+      if (tid == 0) sb[3 * HALO] = HALO;
+    }
+  }
+  __syncthreads();
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
     tl.part[2 * k] = s;
@@ -1158,25 +1237,8 @@ tiled_init_dt(const __grid_constant__ Eos e, const __grid_constant__ Prm p, cons
       }
       tl.ctl[2] = 0;
     }
-  }
-  if (tl.xbuf && (k == 0 || k == tl.ntiles - 1)) {  // initial halos for the first exchange
-    const int cur2 = tl.mctl[0];
-    if (k == 0 && tl.nbr_left) {
-      double* sb = tl.xbuf + XB_SEND_LEFT;
-      for (int i = tid; i < HALO; i += blockDim.x) {
-        sb[i] = tl.rho[cur2][base + i]; sb[HALO + i] = tl.mom[cur2][base + i];
-        sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][base + i];
-      }
-      if (tid == 0) sb[3 * HALO] = HALO;
-    }
-    if (k == tl.ntiles - 1 && tl.nbr_right) {
-      double* sb = tl.xbuf + XB_SEND_RIGHT;
-      for (int i = tid; i < HALO; i += blockDim.x) {
-        const long long j = base + cnt - HALO + i;
-        sb[i] = tl.rho[cur2][j]; sb[HALO + i] = tl.mom[cur2][j]; sb[2 * HALO + i] = tl.hu[cur2][k] ? p.h_av : tl.h[cur2][j];
-      }
-      if (tid == 0) sb[3 * HALO] = HALO;
-    }
+    __syncthreads();
+    if (tl.xbuf && tl.xpeers) xpublish(tl, tl.xbuf[XB_DT], tl.xbuf[XB_DT + 1], tl.mctl[1]);
   }
 }
 
@@ -1234,12 +1296,53 @@ __global__ void tiled_members_active(const __grid_constant__ Tiles tl, double t_
 
 // rank mode, after the exchange: dt from the min-reduced pair; after a step also advance t and
 // flip the buffers (what the last CTA does in single-rank mode)
+// (one warp)  Peer mode: wait until every rank's publication of this step has arrived (its tag in
+// this rank's pair table; a system-scope acquire), fold the ranks' pairs into XB_DT and copy the
+// neighbours' records into the receive slots the next step's kernels read.  A rank that never
+// publishes (a dead peer) ends the wait after ~2 s with status ST_INTERNAL instead of a hang.
+__device__ bool xconsume(const Tiles& tl) {
+  const int lane = threadIdx.x & 31;
+  const long long tag = (long long)tl.ctl[12];  // publications so far: the same on every rank
+  const int par = (int)(tag & 1);
+  bool ok = true;
+  if (lane < tl.xworld) {
+    volatile const double* pt = tl.xbuf + XB_PPAIR + (par * XB_MAXRANKS + lane) * 4 + 2;
+    const long long c0 = clock64();
+    while (*pt != (double)tag)
+      if (clock64() - c0 > 4000000000ll) { ok = false; break; }
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok) {
+    if (lane == 0) { atomicCAS(&tl.mctl[1], 0, (int)ST_INTERNAL); atomicCAS(&tl.ctl[1], 0, (int)ST_INTERNAL); }
+    return false;
+  }
+  __threadfence_system();
+  double ns = INFINITY, hm = INFINITY;  // the min over ranks of (-S_max_r, h_min_r), as the all-reduce
+  if (lane < tl.xworld) {
+    volatile const double* pr = tl.xbuf + XB_PPAIR + (par * XB_MAXRANKS + lane) * 4;
+    ns = pr[0]; hm = pr[1];
+  }
+  ns = warp_min(ns);  // (compare-select: exact, order-free)
+  hm = warp_min(hm);
+  if (lane == 0) { tl.xbuf[XB_DT] = ns; tl.xbuf[XB_DT + 1] = hm; }
+  for (int q = lane; q < XB_REC; q += 32) {
+    volatile const double* rl = tl.xbuf + XB_PREC + (2 * par + 0) * XB_REC;
+    volatile const double* rr = tl.xbuf + XB_PREC + (2 * par + 1) * XB_REC;
+    if (tl.nbr_left) tl.xbuf[XB_RECV_LEFT + q] = rl[q];
+    if (tl.nbr_right) tl.xbuf[XB_RECV_RIGHT + q] = rr[q];
+  }
+  __syncwarp();
+  return true;
+}
+
 __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constant__ Tiles tl, double t_end, int after_step) {
   if (tl.mctl[1] != 0) return;
+  if (after_step && !(tl.scal[0] < t_end)) return;  // the step was a no-op (on every rank: t is global)
+  if (tl.xpeers && !xconsume(tl)) return;
+  if (threadIdx.x != 0) return;
   const double S = -tl.xbuf[XB_DT], hm = tl.xbuf[XB_DT + 1];
   double t_new = tl.scal[0];
   if (after_step) {
-    if (!(t_new < t_end)) return;  // the step was a no-op
     const double dt_used = tl.scal[4];
     t_new += dt_used;
     if (tl.mctl[2] == 0 || dt_used < tl.scal[2]) tl.scal[2] = dt_used;

@@ -12,8 +12,8 @@ import math
 
 import torch
 
-from . import (HALO, LAYOUT_TILED, XB_DOUBLES, XB_DT, XB_REC, XB_RECV_LEFT, XB_RECV_RIGHT,
-               XB_SEND_LEFT, XB_SEND_RIGHT, Context)
+from . import (HALO, LAYOUT_TILED, XB_DOUBLES, XB_DOUBLES_PEER, XB_DT, XB_MAXRANKS, XB_REC, XB_RECV_LEFT,
+               XB_RECV_RIGHT, XB_SEND_LEFT, XB_SEND_RIGHT, Context)
 
 
 def tile_count(n: int, tile: int) -> int:
@@ -92,7 +92,7 @@ class RankGrid:
 
     def __init__(self, eos: dict, params: dict, n_global: int, x_left: float, x_right: float, rank: int,
                  world: int, tile: int = 1400, device: int = 0, stream=None, group=None, slack: int = 16,
-                 graph_steps: int = 0):
+                 graph_steps: int = 0, peer: bool = False):
         self.rank, self.world, self.group = rank, world, group
         self.graph_steps = graph_steps if world > 1 else 0
         if self.graph_steps and (stream is None or stream == torch.cuda.default_stream(device)):
@@ -107,9 +107,40 @@ class RankGrid:
                            x_left + self.c1 * self.h_av, device=device, stream=stream, layout=LAYOUT_TILED,
                            tile_cells=tile, nbr_left=rank > 0, nbr_right=rank < world - 1, h_av=self.h_av)
         self.xbuf = None
+        self.peer = False
         if world > 1:
-            self.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
-            self.ctx.set_exchange_buffer(self.xbuf)
+            if peer:
+                self.peer = self._setup_peers(device)
+            if not self.peer:
+                self.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
+                self.ctx.set_exchange_buffer(self.xbuf)
+
+    def _setup_peers(self, device) -> bool:
+        """Peer mode over torch symmetric memory (NVLink-mapped buffers of every rank): the
+        kernels write the halo records and the CFL pair into the peers' buffers themselves and
+        eis_step_finish waits for them -- no collective per step.  False (NCCL exchange) when
+        symmetric memory is unavailable."""
+        if self.world > XB_MAXRANKS:
+            return False
+        try:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(XB_DOUBLES_PEER, dtype=torch.float64, device=f"cuda:{device}")
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
+            ptrs = [int(p_) for p_ in hdl.buffer_ptrs]
+            torch.cuda.synchronize(device)
+            dist.barrier(group=self.group)  # every buffer zeroed before any rank publishes
+        except Exception as exc:  # noqa: BLE001 -- no symmetric memory: the NCCL exchange
+            import warnings
+            warnings.warn(f"peer exchange unavailable ({exc}); using the NCCL exchange")
+            return False
+        self.xbuf, self._hdl = buf, hdl
+        self.ctx.set_exchange_buffer(buf)
+        r = self.rank
+        self.ctx.set_exchange_peers(ptrs[r - 1] if r > 0 else None, ptrs[r + 1] if r < self.world - 1 else None,
+                                    ptrs, r, self.world)
+        return True
 
     def _on_stream(self):
         """torch's current stream = the library's stream (NCCL and torch ops ordered with the kernels)"""
@@ -117,6 +148,8 @@ class RankGrid:
         return torch.cuda.stream(self.stream) if hasattr(self.stream, "cuda_stream") else contextlib.nullcontext()
 
     def exchange(self):
+        if self.peer:  # the kernels exchanged over peer memory; eis_step_finish consumes it
+            return
         with self._on_stream():
             exchange_halos(self.xbuf, self.rank, self.world, self.group)
 
@@ -153,8 +186,13 @@ class VirtualRanks:
     """P rank slices of one grid on ONE device, exchanged by device copies (no NCCL, no kernel
     waits on another): exercises the rank-mode library path against the 1-rank run."""
 
-    def __init__(self, eos, params, n_global, x_left, x_right, world, tile=1400, device=0, stream=None):
+    def __init__(self, eos, params, n_global, x_left, x_right, world, tile=1400, device=0, stream=None,
+                 peer: bool = False):
+        """peer=True: the slices exchange through eis_set_exchange_peers (the kernels write into
+        the neighbours' buffers, eis_step_finish consumes) instead of device copies; every rank's
+        step_local is enqueued before any step_finish, so no kernel waits on a later one."""
         self.stream = stream
+        self.peer = peer
         self._graphs = None
         self.parts = []
         for r in range(world):
@@ -167,11 +205,18 @@ class VirtualRanks:
             g.ctx = Context(eos, params, 1, g.n, g.cap, x_left + g.c0 * g.h_av, x_left + g.c1 * g.h_av,
                             device=device, stream=stream, layout=LAYOUT_TILED, tile_cells=tile,
                             nbr_left=r > 0, nbr_right=r < world - 1, h_av=g.h_av)
-            g.xbuf = torch.zeros(XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
+            g.xbuf = torch.zeros(XB_DOUBLES_PEER if peer else XB_DOUBLES, dtype=torch.float64, device=f"cuda:{device}")
             g.ctx.set_exchange_buffer(g.xbuf)
             self.parts.append(g)
+        if peer:
+            ptrs = [g.xbuf.data_ptr() for g in self.parts]
+            for r, g in enumerate(self.parts):
+                g.ctx.set_exchange_peers(ptrs[r - 1] if r > 0 else None, ptrs[r + 1] if r < world - 1 else None,
+                                         ptrs, r, world)
 
     def _exchange(self):
+        if self.peer:
+            return
         P = self.parts
         for r, g in enumerate(P):
             if r > 0:

@@ -542,6 +542,64 @@ def test_c5_virtual_ranks_cut_at_cavitating_segments(P, world):
     np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
 
 
+@pytest.mark.parametrize("world,graph_steps", [(2, 0), (4, 0), (8, 0), (4, 6)])
+def test_c5_virtual_ranks_peer_exchange_bitwise(P, world, graph_steps):
+    """SURVEY §8(e), the exchange inside the kernels (eis_set_exchange_peers): the last CTA of
+    every rank's step writes its halo records into the neighbours' exchange buffers and its CFL
+    pair into every rank's pair table, eis_step_finish folds them -- no copy or collective in
+    between.  Rank cuts on cavitating segment boundaries (tile 1024); the slices reproduce the
+    1-rank run bit for bit (also replayed from a captured CUDA graph), and the publication tags
+    of the double-buffered tables advance once per step on every rank."""
+    from paper_2211_00705_b200.decomp import VirtualRanks
+    n, steps, tile = 24 * 4096, 61, 1024
+    w = W.c5(n_cells=n)
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=tile)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)[:w["N"]]
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)[:w["N"]]
+    ctx.set_state(rho, mom)
+    st = ctx.step(steps, stats=True)
+    assert st["creations"] >= 1 and st["regions"] >= 1
+    g = ctx.get_state()
+    n1 = int(g["n"][0])
+    s = torch.cuda.Stream() if graph_steps else torch.cuda.current_stream()
+    vr = VirtualRanks(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], world, tile=tile, stream=s, peer=True)
+    vr.set_state(rho, mom)
+    vr.step(steps, graph_steps=graph_steps)
+    torch.cuda.synchronize()
+    v = vr.get_state()
+    assert v["status"] == [0] * world
+    assert all(t == g["t"][0] for t in v["t"])
+    assert v["rho"].shape[0] == n1
+    np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
+    np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
+    np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
+    # tags: 1 (set_state) + one per step, in both parity halves of every rank's pair table
+    for part in vr.parts:
+        tags = part.xbuf[P.XB_DOUBLES + 4 * P.XB_REC:].reshape(2, P.XB_MAXRANKS, 4)[:, :world, 2].cpu().numpy()
+        assert sorted(set(tags.max(axis=0).tolist())) == [steps + 1]
+        assert sorted(set(tags.min(axis=0).tolist())) == [steps]
+
+
+def test_peer_exchange_arguments_rejected(P):
+    """eis_set_exchange_peers validates its pointers against the rank mode of the context."""
+    w = W.c5(n_cells=8 * 1024)
+    ctx = P.Context(w["eos"], w["params"], 1, w["N"], w["cap"], w["x_left"], w["x_right"],
+                    stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=1024, nbr_left=True)
+    xb = torch.zeros(P.XB_DOUBLES_PEER, dtype=torch.float64, device="cuda")
+    other = torch.zeros_like(xb)
+    with pytest.raises(P.EisError):  # before set_exchange_buffer
+        ctx.set_exchange_peers(other.data_ptr(), None, [other.data_ptr(), xb.data_ptr()], 1, 2)
+    ctx.set_exchange_buffer(xb)
+    with pytest.raises(P.EisError):  # a left neighbour exists: its buffer is required
+        ctx.set_exchange_peers(None, None, [other.data_ptr(), xb.data_ptr()], 1, 2)
+    with pytest.raises(P.EisError):  # all[rank] must be this context's buffer
+        ctx.set_exchange_peers(other.data_ptr(), None, [xb.data_ptr(), other.data_ptr()], 1, 2)
+    with pytest.raises(P.EisError):  # too many ranks
+        ctx.set_exchange_peers(other.data_ptr(), None, [other.data_ptr()] * 8 + [xb.data_ptr()], 8, 9)
+    ctx.set_exchange_peers(other.data_ptr(), None, [other.data_ptr(), xb.data_ptr()], 1, 2)
+
+
 @pytest.mark.parametrize("world,graph_steps", [(2, 8), (4, 5)])
 def test_c5_virtual_ranks_cuda_graph_replay_bitwise(P, world, graph_steps):
     """SURVEY §8(e), the decomposed step off the host: the per-step sequence of every rank slice
