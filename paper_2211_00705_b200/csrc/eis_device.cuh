@@ -40,15 +40,74 @@ __device__ __forceinline__ double pres(const Eos& e, int ph, double rho) {
 }
 __device__ __forceinline__ double sound(const Eos& e, int ph) { return ph == VAP ? e.a_v : e.a_l; }
 
+// Reciprocal for the bulk passes: the hardware seed (rcp.approx.ftz.f64, ~2^-23 relative)
+// and one cubic refinement r (1 + e + e^2), e = 1 - x r, relative error ~e^3 before rounding,
+// so within an ulp of the correctly rounded value; 4 instructions, deterministic.  Arguments
+// are positive normal numbers (densities, HLL speed spans) wherever the result is kept.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+#ifndef EIS_FAST_RCP
+#define EIS_FAST_RCP 1
+#endif
+// the reciprocals of the interface solver's evaluation chain: rcp_fast (within an ulp, a shorter
+// dependent chain; the default since round 2, DESIGN R14e), or correctly rounded (__drcp_rn) in
+// EIS_FAST_RCP=0 builds
+__device__ __forceinline__ double rcp_sel(double x) {
+#if EIS_FAST_RCP
+  return rcp_fast(x);
+#else
+  return __drcp_rn(x);
+#endif
+}
+
+// ln x for a positive normal x, written for latency (the default; EIS_FAST_LOG=0: log()): x = 2^k m with m in
+// [1/sqrt2, sqrt2), ln m = 2 atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.172), the series
+// 2 s (1 + s^2/3 + ... + s^22/23) (truncation < 1e-19 relative) in Estrin form, k ln2 in two
+// parts.  Within a few ulp of log(x).
+__device__ __forceinline__ double log_fast(double x) {
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  int k = (hi >> 20) - 1023;
+  hi = (hi & 0x000fffff) | 0x3ff00000;
+  if (hi >= 0x3ff6a09e) { hi -= 0x00100000; ++k; }
+  const double m = __hiloint2double(hi, lo), f = m - 1.0;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(2.0 + f));
+  const double e1 = fma(-(2.0 + f), r, 1.0);
+  const double s = f * fma(r, fma(e1, e1, e1), r);
+  const double z = s * s, z2 = z * z, z4 = z2 * z2, z8 = z4 * z4;
+  const double p0 = fma(z, 1.0 / 3, 1.0), p1 = fma(z, 1.0 / 7, 1.0 / 5), p2 = fma(z, 1.0 / 11, 1.0 / 9);
+  const double p3 = fma(z, 1.0 / 15, 1.0 / 13), p4 = fma(z, 1.0 / 19, 1.0 / 17), p5 = fma(z, 1.0 / 23, 1.0 / 21);
+  const double q0 = fma(z2, p1, p0), q1 = fma(z2, p3, p2), q2 = fma(z2, p5, p4);
+  const double poly = fma(z8, q2, fma(z4, q1, q0));
+  const double kd = (double)k;
+  return fma(kd, 6.93147180369123816490e-01, fma(2.0 * s, poly, kd * 1.90821492927058770002e-10));
+}
+#ifndef EIS_FAST_LOG
+#define EIS_FAST_LOG 1
+#endif
+__device__ __forceinline__ double log_sel(double x) {
+#if EIS_FAST_LOG
+  return log_fast(x);
+#else
+  return log(x);
+#endif
+}
+
 // ln(a/b) for a/b near 1 (liquid densities, |a/b - 1| < 1e-2): 9-term series of ln(1 + x),
 // truncation < 1e-19 relative; otherwise log.  Exact reciprocals use __drcp_rn (correctly rounded,
 // so 1/x bit-for-bit, at half the latency of a division).
 __device__ __forceinline__ double ln_ratio(double a, double b) {
-  const double x = (a - b) * __drcp_rn(b);
+  const double x = (a - b) * rcp_sel(b);
   if (fabs(x) < 1e-2) {
     return x * (1.0 + x * (-0.5 + x * (1.0 / 3 + x * (-0.25 + x * (0.2 + x * (-1.0 / 6 + x * (1.0 / 7 + x * (-0.125 + x * (1.0 / 9)))))))));
   }
-  return log(a * __drcp_rn(b));
+  return log_sel(a * rcp_sel(b));
 }
 
 // Outer-wave function in density form (P:1496-1503 with R19): rarefaction a ln(r*/r_K),
@@ -57,10 +116,10 @@ __device__ __forceinline__ void wave_fd(double a, double rs, double rk, double& 
   if (rs > rk) {
     const double iq = rsqrt(rs * rk);
     f = a * (rs - rk) * iq;
-    df = 0.5 * a * (rs + rk) * iq * __drcp_rn(rs);
+    df = 0.5 * a * (rs + rk) * iq * rcp_sel(rs);
   } else {
     f = a * ln_ratio(rs, rk);
-    df = a * __drcp_rn(rs);
+    df = a * rcp_sel(rs);
   }
 }
 __device__ __forceinline__ double wave_f(double a, double rs, double rk) {
@@ -89,7 +148,7 @@ __device__ __forceinline__ void hll_p(double a, double rl, double ml, double ul,
   const double SL = fmin(ul, ur) - a, SR = fmax(ul, ur) + a;
   if (SL >= 0.0) { F0 = ml; F1 = FL1; return; }
   if (SR <= 0.0) { F0 = mr; F1 = FR1; return; }
-  const double inv = __drcp_rn(SR - SL), SLSR = SL * SR;
+  const double inv = rcp_sel(SR - SL), SLSR = SL * SR;
   F0 = (SR * ml - SL * mr + SLSR * (rr - rl)) * inv;
   F1 = (SR * FL1 - SL * FR1 + SLSR * (mr - ml)) * inv;
 }
@@ -98,17 +157,6 @@ __device__ __forceinline__ void hll_p(double a, double rl, double ml, double ul,
 // HLL formula always evaluated, the upwind cases selected afterwards.
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
-// Reciprocal for the bulk passes: the hardware seed (rcp.approx.ftz.f64, ~2^-23 relative)
-// and one cubic refinement r (1 + e + e^2), e = 1 - x r, relative error ~e^3 before rounding,
-// so within an ulp of the correctly rounded value; 4 instructions, deterministic.  Arguments
-// are positive normal numbers (densities, HLL speed spans) wherever the result is kept.
-__device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
-
 __device__ __forceinline__ void hll_fast(double a, double rl, double ml, double ul, double pl, double rr, double mr,
                                          double ur, double pr, double& F0, double& F1) {
   const double FL1 = ml * ul + pl, FR1 = mr * ur + pr;
@@ -171,8 +219,8 @@ __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, dou
   const double rVs = pV * e.inv_av2;
   const double rLs = e.rho0 + (pL - e.p0) * e.inv_al2;
   if (!(rLs > 0.0)) return false;
-  const double vV = e.a_v2 * __drcp_rn(pV), vL = __drcp_rn(rLs);
-  const double gV = e.a_v2 * log(pV * e.inv_p0), gL = e.a_l2 * ln_ratio(rLs, e.rho0);
+  const double vV = e.a_v2 * rcp_sel(pV), vL = rcp_sel(rLs);
+  const double gV = e.a_v2 * log_sel(pV * e.inv_p0), gL = e.a_l2 * ln_ratio(rLs, e.rho0);
   const double sV = P.sV, sL = -P.sV;
   const double jp = sV * pV + sL * pL, jv = sV * vV + sL * vL;
   const double jv2 = sV * vV * vV + sL * vL * vL, jg = sV * gV + sL * gL;
@@ -181,7 +229,7 @@ __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, dou
   const double disc = 1.0 - 4.0 * A * B;
   if (!(disc > 0.0)) return false;
   const double sq = sqrt(disc);
-  const double z = 2.0 * B * __drcp_rn(1.0 + sq);
+  const double z = 2.0 * B * rcp_sel(1.0 + sq);
   double fV, dfV, fL, dfL;
   wave_fd(e.a_v, rVs, P.rV, fV, dfV);
   wave_fd(e.a_l, rLs, P.rL, fL, dfL);
@@ -194,7 +242,7 @@ __device__ __forceinline__ bool iface_eval(const Eos& e, const IfaceProb& P, dou
   const double dA_L = tp * sL * vL * dvL;
   const double dB_V = e.tau * jg + tp * sV * vV;                         // dg/dp = v
   const double dB_L = tp * sL * vL;
-  const double isq = __drcp_rn(sq), z2 = z * z;
+  const double isq = rcp_sel(sq), z2 = z * z;
   const double zV = (dA_V * z2 + dB_V) * isq, zL = (dA_L * z2 + dB_L) * isq;
   J[0] = (sV + 2.0 * z * zV * jv + z2 * sV * dvV) * e.inv_p0;
   J[1] = (sL + 2.0 * z * zL * jv + z2 * sL * dvL) * e.inv_p0;
@@ -229,7 +277,7 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
   const double disc = 1.0 - 4.0 * A * B;
   if (!(disc > 0.0)) return false;
   const double sq = sqrt(disc);
-  const double z = 2.0 * B * __drcp_rn(1.0 + sq);
+  const double z = 2.0 * B * rcp_sel(1.0 + sq);
   const double aA = cav ? e.a_l : e.a_v;
   double f1, df1, f2, df2;
   wave_fd(aA, rA, P.rl, f1, df1);
@@ -244,7 +292,7 @@ __device__ __forceinline__ bool create_eval(const Eos& e, const CreateProb& P, d
   const double dA_B = (cav ? 0.5 * e.tau * jv2 : 0.0) - tp * vB * dvB;
   const double dB_A = (cav ? 0.0 : e.tau * jg) + tp * vA;
   const double dB_B = (cav ? e.tau * jg : 0.0) - tp * vB;
-  const double isq = __drcp_rn(sq), z2 = z * z;
+  const double isq = rcp_sel(sq), z2 = z * z;
   const double zA = (dA_A * z2 + dB_A) * isq, zB = (dA_B * z2 + dB_B) * isq;
   J[0] = (1.0 + 2.0 * z * zA * jv + z2 * dvA) * e.inv_p0;
   J[1] = (-1.0 + 2.0 * z * zB * jv - z2 * dvB) * e.inv_p0;
@@ -287,7 +335,7 @@ __device__ __forceinline__ bool newton_dir(const double G[2], const double J[4],
   const double det = J[0] * J[3] - J[1] * J[2];
   if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
   wellc = fabs(det) >= 1e-8 * (fabs(J[0] * J[3]) + fabs(J[1] * J[2]));
-  const double idet = __drcp_rn(det);
+  const double idet = rcp_sel(det);
   d0 = -(J[3] * G[0] - J[1] * G[1]) * idet;
   d1 = -(-J[2] * G[0] + J[0] * G[1]) * idet;
   return true;
@@ -404,7 +452,7 @@ __device__ __forceinline__ void iface_finish(const Eos& e, const IfaceProb& P, b
                                              const double aux[2], IfaceSol& s) {
   const double z = aux[0], fV = aux[1];
   const double uVs = vap_minus ? P.uV - fV : P.uV + fV;  // wave relations
-  s.w = uVs + z * e.a_v2 * __drcp_rn(x0);                  // z = -rho_V* (u_V* - w)
+  s.w = uVs + z * e.a_v2 * rcp_sel(x0);                  // z = -rho_V* (u_V* - w)
   s.F0 = -z;
   s.F1 = -z * uVs + x0;
 }
