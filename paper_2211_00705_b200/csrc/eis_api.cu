@@ -349,7 +349,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
-      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
@@ -373,7 +374,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->win_grid_poll = 0;
   if (const char* ev = getenv("EIS_WIN_POLL_PER_SM")) c->win_grid_poll = std::max(0, atoi(ev)) * std::max(1, nsm);
   // window split (dual time stepping only; EIS_WIN_SPLIT=0: every window step in one kernel)
-  int split = c->p.mode == 0 && c->win_grid_poll == 0;
+  int split = c->p.mode == 0;  // (with a polling instance: part A polls beside tiled_fast)
   if (const char* ev = getenv("EIS_WIN_SPLIT")) split = split && atoi(ev) != 0;
   c->dts_grid = std::max(nsm, 1) * 16;
   c->dts_tpb = 32;
@@ -833,11 +834,15 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
-    tiled_win<32, EIS_WIN_MINB, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
+    if (c->tl.split)  // part A of the windows as tiled_fast publishes them
+      tiled_win<32, EIS_WIN_MINB, true, 1><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
+    else
+      tiled_win<32, EIS_WIN_MINB, true><<<c->win_grid_poll, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
     cudaEventRecord(c->ev_join, c->stream2);
   }
   if (c->tl.split) {  // part A, the DTS jobs (one lane per block), part B
     tiled_win<32, EIS_WIN_MINB, false, 1><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+    if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);  // every part A done
     dts_jobs<<<c->dts_grid * 32 / c->dts_tpb, c->dts_tpb, 0, c->stream>>>(c->e, c->p, c->tl);
 #ifdef EIS_DTS_DEBUG
     dts_dbg_print<<<1, 1, 0, c->stream>>>();
@@ -846,7 +851,7 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   } else {
     tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   }
-  if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+  if (c->win_grid_poll > 0 && !c->tl.split) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
   if (c->tl.M > 1)

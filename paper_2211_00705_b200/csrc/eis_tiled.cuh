@@ -1019,7 +1019,7 @@ template <int MAXT, int MINB, bool POLL, int PH = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
           double t_end) {
-  static_assert(!POLL || PH == 0, "the polling instance runs the whole window step");
+  static_assert(!POLL || PH <= 1, "a polling instance runs the whole window step or part A");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
   Arr A = carve(smem_raw, WCAP);
@@ -1078,8 +1078,8 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       if (j < 0) break;
       const long long c0 = clock64();
       int jn, kn, wan, wbn;
-      tile_window<false>(e, p, tl, sh, A, WCAP, j, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end, jn, kn,
-                         wan, wbn);
+      tile_window<false, PH>(e, p, tl, sh, A, WCAP, j, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end,
+                             jn, kn, wan, wbn);
       if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
     }
   }
