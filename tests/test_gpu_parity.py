@@ -581,6 +581,30 @@ def test_c5_virtual_ranks_peer_exchange_bitwise(P, world, graph_steps):
         assert sorted(set(tags.min(axis=0).tolist())) == [steps]
 
 
+def test_peer_exchange_with_a_stopped_rank_does_not_wait(P):
+    """Peer mode with a rank whose member is stopped (a spinodal cell in its slice at set_state):
+    the stopped rank keeps publishing neutral pairs, so the other ranks' eis_step_finish never
+    waits for it (no ~2 s timeouts: the steps return promptly) and its status is reported."""
+    import time
+    from paper_2211_00705_b200.decomp import VirtualRanks
+    n, tile, world = 12 * 4096, 1024, 3
+    w = W.c5(n_cells=n)
+    rho = torch.tensor(w["rho"], device="cuda").reshape(-1)[:w["N"]].clone()
+    mom = torch.tensor(w["mom"], device="cuda").reshape(-1)[:w["N"]].clone()
+    vr = VirtualRanks(w["eos"], w["params"], w["N"], w["x_left"], w["x_right"], world, tile=tile,
+                      stream=torch.cuda.current_stream(), peer=True)
+    mid = vr.parts[1]
+    rho[(mid.c0 + mid.c1) // 2] = 500.0  # between rho_tilde and rho_min: spinodal
+    vr.set_state(rho, mom)
+    t0 = time.perf_counter()
+    vr.step(10)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 5.0
+    st = vr.get_state()["status"]
+    assert P.STATUS[st[1]] == "E_SPINODAL", st
+    assert all(P.STATUS[s] != "E_INTERNAL" for s in st), st  # (E_INTERNAL: a peer-wait timeout)
+
+
 def test_peer_exchange_arguments_rejected(P):
     """eis_set_exchange_peers validates its pointers against the rank mode of the context."""
     w = W.c5(n_cells=8 * 1024)
