@@ -434,11 +434,34 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
-            "members_not_ok": nbad, "rates": rates,
+            "members_not_ok": nbad, "rates": rates, "context": paper_context(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def paper_context():
+    """The paper's speed-up of the split scheme over fully explicit local time stepping (north_star:
+    quoted with its hardware -- unstated -- as context, not a target), and the same comparison
+    measured on this GPU by tools/dts_vs_lts.py (profiles/r02_dts_vs_lts.json) when present."""
+    ctx = {"paper_split_vs_explicit_lts": {
+        "cavitation_E2": {"wall_time": 4.93 / 2.94, "local_iterations": 1941 / 355, "cite": "P:1324-1325"},
+        "nucleation_E3": {"wall_time": 9811 / 509, "local_iterations": 27154016 / 1367460, "cite": "P:1435-1436"},
+        "hardware": "unstated (1D CPU runs, ~400 cells)"}}
+    f = os.path.join(ROOT, "profiles", "r02_dts_vs_lts.json")
+    if os.path.exists(f):
+        try:
+            d = json.loads(open(f).read().strip().splitlines()[-1])
+            ctx["gpu_split_vs_explicit_lts"] = {
+                "cavitation_E2": {"gpu_time": d["E2_ratio"]["gpu_time_lts_over_dts"],
+                                  "local_iterations": d["E2_ratio"]["local_iterations_lts_over_dts"]},
+                "nucleation_E3_first_7_steps": {"gpu_time": d["E3_ratio"]["gpu_time_lts_over_dts"],
+                                                "local_iterations": d["E3_ratio"]["local_iterations_lts_over_dts"]},
+                "source": "profiles/r02_dts_vs_lts.json (one B200)"}
+        except (ValueError, KeyError):
+            pass
+    return ctx
 
 
 def main_c5(args, torch, dist, P, world, rank, local):
@@ -567,7 +590,7 @@ def main_c5(args, torch, dist, P, world, rank, local):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kt["launches"], "clocks": clk,
             "stats": {k: st[k] for k in ("cell_updates", "dts_iters", "iface_solves", "creations", "splits",
                                          "merges", "regions")},
-            "members_not_ok": nbad, "rates": rates,
+            "members_not_ok": nbad, "rates": rates, "context": paper_context(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
