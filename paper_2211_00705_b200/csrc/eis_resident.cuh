@@ -844,8 +844,7 @@ template <int CPL>
 __device__ __forceinline__ void bulk_p1_t(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
                                           const double* __restrict__ rho, const double* __restrict__ mom,
                                           const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
-                                          const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts,
-                                          bool want_parts) {
+                                          const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
   const Eos e = e_ref;  // constants into registers once (not a generic load per use)
   const double rho_tilde = e.rho_tilde, rho_min = e.rho_min, a_v2 = e.a_v2, a_l2 = e.a_l2, p0 = e.p0, rho0 = e.rho0;
   const double a_v = e.a_v, a_l = e.a_l, rmin2 = e.rho_min * e.rho_min, inv_rt = 1.0 / e.rho_tilde;
@@ -891,7 +890,6 @@ __device__ __forceinline__ void bulk_p1_t(const Eos& e_ref, const Prm& p_ref, Ct
         const int c = cb + j;
         if (c < n) {
           bad |= !(r[j] > 0.0) || ph[j] == 0u;
-          if (!want_parts) continue;  // (this step's dt is known: member_partials / the tile's dt)
           const double su = fabs(u[j]) + a[j];
           s_part = su > s_part ? su : s_part;  // S over all cells (R5)
           const double hc = h[c];
@@ -958,42 +956,8 @@ __device__ __forceinline__ void bulk_p1_t(const Eos& e_ref, const Prm& p_ref, Ct
 __device__ __noinline__ void bulk_p1(const Eos& e_ref, const Prm& p_ref, CtaShared& sh, const Zone& Z,
                                      const double* __restrict__ rho, const double* __restrict__ mom,
                                      const double* __restrict__ h, double* __restrict__ F0, double* __restrict__ F1,
-                                     const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts,
-                                     bool want_parts) {
-  bulk_p1_t<EIS_P1_CPL>(e_ref, p_ref, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts, want_parts);
-}
-
-// S_max and h_min (non-tiny cells; every cell in EXPLICIT mode) of a member grid in shared
-// memory, by all threads: the partials bulk_p1 would compute at the start of the next step, with
-// its expressions (u = m rcp(rho), the phase codes of P:134 with spinodal as a code of its own),
-// so the dt is the same bits.  The member-resident kernel computes them after each step's remesh
-// (and once at the start), so P1 -- on the step's critical path -- does not (R5, R6).
-__device__ void member_partials(const Eos& e, const Prm& p, CtaShared& sh, const double* rho, const double* mom,
-                                const double* h, int n, double& smax, double& hmin) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const double eps_h = p.eps_tiny * p.h_av;
-  const bool explicit_mode = p.mode == 1;
-  auto code = [&](double r) { return r <= e.rho_tilde ? 1u : (r >= e.rho_min ? 2u : 0u); };
-  double s = 0.0, hm = INFINITY;
-  for (int c = tid; c < n; c += blockDim.x) {
-    const double r = rho[c];
-    const unsigned ph = code(r);
-    const double su = fabs(mom[c] * rcp_fast(r)) + (ph == 1u ? e.a_v : e.a_l);
-    s = su > s ? su : s;
-    const double hc = h[c];
-    const bool same_l = c > 0 && code(rho[c - 1]) == ph, same_r = c + 1 < n && code(rho[c + 1]) == ph;
-    const bool tiny = hc < eps_h && !same_l && !same_r;
-    const double hh = (explicit_mode || !tiny) ? hc : INFINITY;
-    hm = hh < hm ? hh : hm;
-  }
-  s = warp_max(s);
-  hm = warp_min(hm);
-  __syncthreads();  // (part_s / part_h of the step body are free)
-  if (lane == 0) { sh.part_s[warp] = s; sh.part_h[warp] = hm; }
-  __syncthreads();
-  smax = warp_max(lane < nw ? sh.part_s[lane] : 0.0);
-  hmin = warp_min(lane < nw ? sh.part_h[lane] : INFINITY);
-  __syncthreads();
+                                     const uint8_t* __restrict__ fl, int n, int warp, int nbulk, double* parts) {
+  bulk_p1_t<EIS_P1_CPL>(e_ref, p_ref, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts);
 }
 
 // Bulk pass P2: explicit update of the cells with two HLL edges (a7); h^{n+1} = h^n there, so
@@ -1324,7 +1288,7 @@ __device__ __forceinline__ double step_body(const Eos& e, const Prm& p, CtaShare
     // ---------------- P1: edges (HLL a3, trigger a4), dt partials (a2) ----------------
     if (warp < nbulk) {
       double parts[2];
-      bulk_p1(e, p, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts, !(Z.dt_given > 0.0 && Z.s_given > 0.0));
+      bulk_p1(e, p, sh, Z, rho, mom, h, F0, F1, fl, n, warp, nbulk, parts);
       s_part = parts[0];
       h_part = parts[1];
     }
@@ -1503,9 +1467,6 @@ __device__ __forceinline__ void reset_counters(CtaShared& sh) {
   sh.o_cre = 0; sh.o_merges = 0; sh.o_splits = 0;
 }
 
-#ifndef EIS_RESIDENT_PARTIALS
-#define EIS_RESIDENT_PARTIALS 1  // the member-resident kernel's CFL partials after each step, not in P1
-#endif
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
 resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Members g,
@@ -1537,16 +1498,11 @@ resident_steps(const __grid_constant__ Eos e, const __grid_constant__ Prm p, con
   Zone Z;
   Z.zlo = 0; Z.zhi = 1 << 30; Z.own_lo = 0; Z.own_hi = 1 << 30; Z.dt_given = -1.0; Z.s_given = -1.0;
   Z.left_real = true; Z.right_real = true;
-  // this step's CFL partials, computed after the previous step (or here): P1 skips them
-  double smax = 0.0, hmin = INFINITY;
-  if (EIS_RESIDENT_PARTIALS) member_partials(e, p, sh, A.rho, A.mom, A.h, A.n, smax, hmin);
   for (long long step = 0; step < n_steps; ++step) {
     const bool stop = sh.status != 0 || !(t < t_end);
     __syncthreads();  // every thread has read sh.status before anyone can write it
     if (stop) break;
-    if (EIS_RESIDENT_PARTIALS) { Z.dt_given = p.cfl * hmin / smax; Z.s_given = smax; }
     const double dt = step_body(e, p, sh, A, t, t_end, Z);
-    if (EIS_RESIDENT_PARTIALS && dt >= 0.0) member_partials(e, p, sh, A.rho, A.mom, A.h, A.n, smax, hmin);
 #ifdef EIS_PHASE_CLOCK
     if (g.dbg && tid == 0) {
       long long* d = g.dbg + 8 * m;
