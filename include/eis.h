@@ -244,6 +244,18 @@ eis_status eis_step_finish(eis_ctx* ctx, double t_end, int32_t after_step);
  * candidates), rather than only the single-phase fast path.  Synchronises the stream. */
 eis_status eis_tile_info(eis_ctx* ctx, int64_t* n_tiles, int64_t* full_tile_steps, int64_t* window_steps);
 
+/* Window prediction (tiled layout, dual time stepping): a window's full step
+ * predicts which cells of its tile the next step's streaming pass will flag as special, so that
+ * the first part of the predicted windows' full step (phase-boundary solves P:1481-1562, the
+ * explicit pass, the export of the implicit blocks) and Algorithm 2 on those blocks
+ * run beside the streaming pass of the next step; the streaming pass compares its
+ * own classification with the prediction and a window whose prediction failed takes the same
+ * full step after it.  Results do not depend on the predictions.  Outputs (host pointers): the
+ * window full steps since eis_set_state and how many of them were predicted; enabled = 0 when
+ * the context runs without predictions (another mode, rank slices, EIS_WIN_SPEC=0).
+ * Synchronises the stream.  EIS_E_ARG for a member-resident context or null pointers. */
+eis_status eis_window_prediction(eis_ctx* ctx, int64_t* windows, int64_t* predicted, int32_t* enabled);
+
 /* Window diagnostics (tiled layout, context created with the environment variable
  * EIS_WINDOW_DEBUG set): per window full step of the last step, 11 int64 each -- SM clock cycles,
  * dual-time iterations, window owned cells, phase boundaries in the window grid, start clock,

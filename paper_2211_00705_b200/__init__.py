@@ -77,7 +77,7 @@ class Thresholds(C.Structure):
 SYMBOLS = ("eis_thresholds_of", "eis_create", "eis_set_state", "eis_step", "eis_run_to", "eis_get_state",
            "eis_interfaces", "eis_member_status", "eis_member_stats", "eis_last_error", "eis_destroy",
            "eis_set_exchange_buffer", "eis_set_exchange_peers", "eis_step_local", "eis_step_finish",
-           "eis_tile_info", "eis_set_timing",
+           "eis_tile_info", "eis_window_prediction", "eis_set_timing",
            "eis_get_timing", "eis_window_diag", "eis_lax_run")
 # exchange-buffer layout (include/eis.h EIS_XB_*)
 HALO = 10
@@ -109,6 +109,9 @@ def lib():
         L.eis_member_status.argtypes = [vp, P(i32)]
         L.eis_member_stats.argtypes = [vp, P(Stats)]
         L.eis_tile_info.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+        if not hasattr(L, "eis_window_prediction") and os.environ.get("EIS_LIB"):  # an older dev variant (A/B runs)
+            L.eis_window_prediction = L.eis_tile_info
+        L.eis_window_prediction.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(i32)]
         L.eis_window_diag.argtypes = [vp, P(C.c_int64), C.c_int64, P(C.c_int64)]
         L.eis_set_timing.argtypes = [vp, C.c_int32]
         L.eis_get_timing.argtypes = [vp, P(C.c_double), P(C.c_int64)]
@@ -328,6 +331,11 @@ class Context:
         nt, full, win = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(lib().eis_tile_info(self._ctx, C.byref(nt), C.byref(full), C.byref(win)), "eis_tile_info")
         return {"n_tiles": nt.value, "full_tile_steps": full.value, "window_steps": win.value}
+
+    def window_prediction(self) -> dict:
+        w, h, en = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(lib().eis_window_prediction(self._ctx, C.byref(w), C.byref(h), C.byref(en)), "eis_window_prediction")
+        return {"windows": w.value, "predicted": h.value, "enabled": bool(en.value)}
 
     def member_stats(self) -> list:
         arr = (Stats * self.M)()

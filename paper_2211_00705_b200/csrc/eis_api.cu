@@ -36,6 +36,7 @@ struct eis_ctx {
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::array<int, 5>> ev_marks;  // per recorded launch group: event indices + kind
+  std::vector<std::array<int, 6>> ev_spec;   // development (EIS_SPEC_TIMING): step start, early part A end, early dts_jobs end, late part A end, late dts end, part B end
   long long n_kernels = 0;                     // kernels launched by the step calls while timing is on
   size_t ev_used = 0;
   eis_eos eos_in;
@@ -63,6 +64,8 @@ struct eis_ctx {
   Tiles tl;
   double *t_rho[2], *t_mom[2], *t_h[2], *t_ws, *t_part, *t_scal;
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_mctl = nullptr, *t_slow, *t_wlist;
+  int *t_pred[2] = {nullptr, nullptr}, *t_plist[2] = {nullptr, nullptr}, *t_mlist = nullptr;  // window prediction (Tiles::spec)
+  int win_grid_early = 0;                  //   CTAs of the early part A (beside tiled_fast)
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
@@ -350,7 +353,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
-      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_win<32, EIS_WIN_MINB, false, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_win) != cudaSuccess) {
     delete c; return EIS_E_CUDA;
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
@@ -358,6 +362,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
     if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1, 1>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 2>) != cudaSuccess || cudaFuncGetAttributes(&fa, dts_jobs) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_finish) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_init_dt<256>) != cudaSuccess) {
       delete c; return EIS_E_CUDA;
@@ -392,7 +397,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   ok = ok && cudaMalloc(&c->t_ws, (size_t)ntiles * WS_STRIDE * 8) == cudaSuccess &&
        cudaMalloc(&c->t_part, (size_t)ntiles * 16) == cudaSuccess &&
        cudaMalloc(&c->t_stats, (size_t)ntiles * sizeof(TileStats)) == cudaSuccess &&
-       cudaMalloc(&c->t_scal, (size_t)M * SCS * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, 16 * 4) == cudaSuccess &&
+       cudaMalloc(&c->t_scal, (size_t)M * SCS * 8) == cudaSuccess && cudaMalloc(&c->t_ctl, NCTL * 4) == cudaSuccess &&
        cudaMalloc(&c->t_mctl, (size_t)M * MCS * 4) == cudaSuccess &&
        cudaMalloc(&c->t_slow, (size_t)ntiles * 4) == cudaSuccess &&
        cudaMalloc(&c->t_wlist, (size_t)ntiles * 16) == cudaSuccess &&
@@ -403,10 +408,21 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
        cudaMalloc(&c->t_part2, (size_t)c->slow_grid * 16) == cudaSuccess &&
        cudaMalloc(&c->t_off, (ntiles + M) * 8) == cudaSuccess;
   const long long djcap = 4 * ntiles;  // DTS jobs per step (windows hold one block, rarely more)
+  // window prediction (window split, one rank, no polling instance; EIS_WIN_SPEC=0: off): part A
+  // and the DTS jobs of the predicted windows run beside tiled_fast on the side stream
+  const int spec_ok = split && c->win_grid_poll == 0 && !grid->nbr_left && !grid->nbr_right;
+  int spec = spec_ok && M > 1;  // default: ensembles (C4 +15 %); one grid (C5): +4 % at 20 steps, see DESIGN 6.2
+  if (const char* ev = getenv("EIS_WIN_SPEC")) spec = spec_ok && atoi(ev) != 0;
+  c->win_grid_early = std::max(nsm, 1) * 16;  // (C5: 16 per SM 1.35 ms/step, 8: 1.46, 4: 1.55; C4: 8 and 16 within 1 %)
+  if (const char* ev = getenv("EIS_WIN_EARLY_PER_SM")) c->win_grid_early = std::max(1, atoi(ev)) * std::max(1, nsm);
+  c->win_grid_early = (int)std::min<long long>(ntiles, c->win_grid_early);
   if (ok && split)
     ok = cudaMalloc(&c->t_djobs, (size_t)djcap * sizeof(DtsJob)) == cudaSuccess &&
-         cudaMalloc(&c->t_wsave, (size_t)ntiles * WSAVE) == cudaSuccess;
-  if (!ok || cudaMemset(c->t_ctl, 0, 16 * 4) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
+         cudaMalloc(&c->t_wsave, (size_t)ntiles * WSAVE * (spec ? 2 : 1)) == cudaSuccess;
+  if (ok && spec) ok = cudaMalloc(&c->t_mlist, (size_t)ntiles * 4) == cudaSuccess;
+  for (int b = 0; b < 2 && ok && spec; ++b)
+    ok = cudaMalloc(&c->t_pred[b], (size_t)ntiles * 16) == cudaSuccess && cudaMalloc(&c->t_plist[b], (size_t)ntiles * 4) == cudaSuccess;
+  if (!ok || cudaMemset(c->t_ctl, 0, NCTL * 4) != cudaSuccess) { eis_destroy(c); return EIS_E_CUDA; }
   c->g.rho = c->d_rho; c->g.mom = c->d_mom; c->g.h = c->d_h; c->g.n = c->d_n; c->g.t = c->d_t;
   c->g.status = c->d_status; c->g.stats = c->d_stats; c->g.cap = cap;
   c->g.dbg = nullptr;
@@ -421,6 +437,9 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
   tl.poll = c->win_grid_poll > 0 ? 1 : 0;
   tl.split = split; tl.djcap = split ? (int)djcap : 0; tl.djobs = c->t_djobs; tl.wsave = c->t_wsave;
+  tl.spec = spec;
+  for (int b = 0; b < 2; ++b) { tl.pred[b] = c->t_pred[b]; tl.plist[b] = c->t_plist[b]; }
+  tl.mlist = c->t_mlist;
   tl.wmax = WMAX;  // EIS_TILED_WMAX: a smaller bound (0: every special tile takes the whole-tile step)
   if (const char* ev = getenv("EIS_TILED_WMAX")) tl.wmax = std::max(0, std::min(WMAX, atoi(ev)));
   tl.ws = c->t_ws; tl.part = c->t_part; tl.tstats = c->t_stats; tl.scal = c->t_scal; tl.ctl = c->t_ctl;
@@ -435,7 +454,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 
 __global__ void k_tiles_reset(Tiles tl, const int* status, double t0) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m == 0) for (int q = 0; q < 16; ++q) if (q != 12) tl.ctl[q] = 0;  // [12]: peer-mode publications,
+  if (m == 0) for (int q = 0; q < NCTL; ++q) if (q != 12) tl.ctl[q] = 0;  // [12]: peer-mode publications,
                                                                         // counted over the context's life
   if (m >= tl.M) return;
   if (status[m]) atomicCAS(&tl.ctl[1], 0, status[m]);
@@ -636,6 +655,8 @@ extern "C" void eis_destroy(eis_ctx* c) {
   for (int b = 0; b < 2; ++b) { cudaFree(c->t_rho[b]); cudaFree(c->t_mom[b]); cudaFree(c->t_h[b]); cudaFree(c->t_cnt[b]); cudaFree(c->t_hu[b]); }
   cudaFree(c->t_slow); cudaFree(c->t_part2); cudaFree(c->t_wlist); cudaFree(c->t_wdbg); cudaFree(c->t_partf);
   cudaFree(c->t_djobs); cudaFree(c->t_wsave);
+  for (int b = 0; b < 2; ++b) { cudaFree(c->t_pred[b]); cudaFree(c->t_plist[b]); }
+  cudaFree(c->t_mlist);
   cudaFree(c->d_xpeers);
   cudaFree(c->t_ws); cudaFree(c->t_part); cudaFree(c->t_stats); cudaFree(c->t_scal); cudaFree(c->t_ctl); cudaFree(c->t_mctl); cudaFree(c->t_off);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -649,6 +670,7 @@ extern "C" eis_status eis_set_timing(eis_ctx* c, int32_t enable) {
   if (!c) return EIS_E_ARG;
   c->timing = enable != 0;
   c->ev_marks.clear();
+  c->ev_spec.clear();
   c->ev_used = 0;
   c->n_kernels = 0;
   return EIS_OK;
@@ -659,6 +681,17 @@ extern "C" eis_status eis_get_timing(eis_ctx* c, double* ms, int64_t* launches) 
   CU(cudaStreamSynchronize(c->stream));
   for (int q = 0; q < 4; ++q) ms[q] = 0.0;
   *launches = (int64_t)c->n_kernels;
+  if (!c->ev_spec.empty()) {  // development: mean offsets from the step start (ms)
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (const auto& sm : c->ev_spec)
+      for (int q = 1; q < 6; ++q) {
+        float t = 0.f;
+        if (sm[q] >= 0 && cudaEventElapsedTime(&t, c->ev_pool[sm[0]], c->ev_pool[sm[q]]) == cudaSuccess) acc[q] += t;
+      }
+    const double n = (double)c->ev_spec.size();
+    fprintf(stderr, "EIS_SPEC_TIMING (ms from the step start, mean of %d steps): early A end %.4f  early dts end %.4f  late A end %.4f  late dts end %.4f  part B end %.4f\n",
+            (int)n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+  }
   for (const auto& m : c->ev_marks) {
     float t = 0.f;
     if (m[4] == 0) {  // resident: one kernel
@@ -686,6 +719,16 @@ extern "C" eis_status eis_window_diag(eis_ctx* c, int64_t* out, int64_t capacity
     CU(cudaMemcpyAsync(out, c->t_wdbg, (size_t)n * WDBG_FIELDS * 8, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
   }
+  return EIS_OK;
+}
+
+extern "C" eis_status eis_window_prediction(eis_ctx* c, int64_t* windows, int64_t* predicted, int32_t* enabled) {
+  if (!c || !windows || !predicted || !enabled) return EIS_E_ARG;
+  if (!c->tiled) return fail(c, EIS_E_ARG, "eis_window_prediction: not a tiled context%s");
+  int ctl[NCTL];
+  CU(cudaMemcpyAsync(ctl, c->t_ctl, sizeof(ctl), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  *windows = ctl[19]; *predicted = ctl[18]; *enabled = c->tl.spec;
   return EIS_OK;
 }
 
@@ -757,6 +800,7 @@ extern "C" eis_status eis_set_state(eis_ctx* c, const double* rho, const double*
   if (c->tiled) {
     k_tiles_reset<<<(unsigned)((M + 127) / 128), 128, 0, c->stream>>>(c->tl, c->d_status, t0);
     CU(cudaMemsetAsync(c->t_wlist, 0, (size_t)c->tl.ntiles * 16, c->stream));  // window ready tags
+    for (int b = 0; b < 2 && c->tl.spec; ++b) CU(cudaMemsetAsync(c->t_pred[b], 0xff, (size_t)c->tl.ntiles * 16, c->stream));  // no predictions
     k_to_tiles<<<c->tl.ntiles, 256, 0, c->stream>>>(c->g, c->tl, 0, c->tile_cells);
     tiled_init_dt<256><<<c->tl.ntiles, 256, 0, c->stream>>>(c->e, c->p, c->tl, INFINITY);
     if (M > 1) tiled_members_finish<<<(unsigned)((M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, INFINITY, 0);
@@ -818,6 +862,21 @@ static int timing_event(eis_ctx* c, cudaStream_t st = nullptr) {  // an event fr
   return i;
 }
 
+// development (EIS_SYNC_DEBUG=1): synchronise after every launch of a step and name the first failure
+static void dbg_sync(eis_ctx* c, const char* what) {
+  static const int on = getenv("EIS_SYNC_DEBUG") ? atoi(getenv("EIS_SYNC_DEBUG")) : 0;
+  if (!on) return;
+  cudaError_t e1 = cudaStreamSynchronize(c->stream2), e2 = cudaStreamSynchronize(c->stream);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    fprintf(stderr, "EIS_SYNC_DEBUG: after %s: %s / %s\n", what, cudaGetErrorString(e1), cudaGetErrorString(e2));
+    int ctl[NCTL];
+    if (cudaMemcpy(ctl, c->t_ctl, sizeof(ctl), cudaMemcpyDeviceToHost) == cudaSuccess)
+      for (int q = 0; q < NCTL; ++q) fprintf(stderr, " ctl[%d]=%d", q, ctl[q]);
+    fprintf(stderr, "\n");
+    abort();
+  }
+}
+
 static void tiled_launch(eis_ctx* c, double t_end) {
   std::array<int, 5> m{-1, -1, -1, -1, 1};
   // a step captured into a CUDA graph (rank mode: step_local -> halo exchange -> step_finish
@@ -828,9 +887,22 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   if (cap != cudaStreamCaptureStatusNone) c->timing = 0;
   // tiled_fast, then (side stream, high priority) a window kernel that takes window jobs as
   // tiled_fast publishes them; after tiled_fast a full-occupancy instance drains the rest
-  if (c->win_grid_poll > 0) cudaEventRecord(c->ev_fork, c->stream);
+  if (c->win_grid_poll > 0 || c->tl.spec) cudaEventRecord(c->ev_fork, c->stream);
   if (c->timing) m[0] = timing_event(c);
+  static const int spec_timing_on = getenv("EIS_SPEC_TIMING") ? atoi(getenv("EIS_SPEC_TIMING")) : 0;
+  const bool spec_timing = spec_timing_on && c->timing && c->tl.split;
+  std::array<int, 6> sm{m[0], -1, -1, -1, -1, -1};
+  if (c->tl.spec) {  // the predicted windows: part A and their DTS jobs beside tiled_fast
+    cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
+    tiled_win<32, EIS_WIN_MINB, false, 1, 1><<<c->win_grid_early, 32, c->smem_win, c->stream2>>>(c->e, c->p, c->tl, t_end);
+    if (spec_timing) sm[1] = timing_event(c, c->stream2);
+    dts_jobs<<<c->dts_grid * 32 / c->dts_tpb, c->dts_tpb, 0, c->stream2>>>(c->e, c->p, c->tl, 1);
+    if (spec_timing) sm[2] = timing_event(c, c->stream2);
+    cudaEventRecord(c->ev_join, c->stream2);
+    dbg_sync(c, "early part A + dts_jobs");
+  }
   tiled_fast<EIS_FAST_T, EIS_FAST_MINB><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  dbg_sync(c, "tiled_fast");
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
@@ -841,24 +913,32 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     cudaEventRecord(c->ev_join, c->stream2);
   }
   if (c->tl.split) {  // part A, the DTS jobs (one lane per block), part B
+    if (c->tl.spec) cudaStreamWaitEvent(c->stream, c->ev_join, 0);  // the early jobs are solved (and counted)
     tiled_win<32, EIS_WIN_MINB, false, 1><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+    dbg_sync(c, "part A");
+    if (spec_timing) sm[3] = timing_event(c);
     if (c->win_grid_poll > 0) cudaStreamWaitEvent(c->stream, c->ev_join, 0);  // every part A done
-    dts_jobs<<<c->dts_grid * 32 / c->dts_tpb, c->dts_tpb, 0, c->stream>>>(c->e, c->p, c->tl);
+    dts_jobs<<<c->dts_grid * 32 / c->dts_tpb, c->dts_tpb, 0, c->stream>>>(c->e, c->p, c->tl, 0);
+    dbg_sync(c, "dts_jobs");
+    if (spec_timing) sm[4] = timing_event(c);
 #ifdef EIS_DTS_DEBUG
     dts_dbg_print<<<1, 1, 0, c->stream>>>();
 #endif
     tiled_win<32, EIS_WIN_MINB, false, 2><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
+    dbg_sync(c, "part B");
+    if (spec_timing) { sm[5] = timing_event(c); c->ev_spec.push_back(sm); }
   } else {
     tiled_win<32, EIS_WIN_MINB, false><<<c->win_grid, 32, c->smem_win, c->stream>>>(c->e, c->p, c->tl, t_end);
   }
   if (c->win_grid_poll > 0 && !c->tl.split) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   if (c->timing) m[2] = timing_event(c);
   tiled_slow<256, 4><<<c->slow_grid, 256, c->smem, c->stream>>>(c->e, c->p, c->tl, t_end);
+  dbg_sync(c, "tiled_slow");
   if (c->tl.M > 1)
     tiled_members_finish<<<(unsigned)(((long long)c->tl.M * 32 + 255) / 256), 256, 0, c->stream>>>(c->p, c->tl, t_end, 1);
   if (c->timing) {
     m[3] = timing_event(c); c->ev_marks.push_back(m);
-    c->n_kernels += 2 + (c->tl.split ? 3 : 1) + (c->win_grid_poll > 0 ? 1 : 0) + (c->tl.M > 1 ? 1 : 0);
+    c->n_kernels += 2 + (c->tl.split ? 3 : 1) + (c->win_grid_poll > 0 ? 1 : 0) + (c->tl.M > 1 ? 1 : 0) + (c->tl.spec ? 2 : 0);
   }
   c->timing = timing_saved;
 }
@@ -887,6 +967,7 @@ static eis_status launch(eis_ctx* c, long long n_steps, double t_end, eis_stats*
           CU(cudaMemsetAsync(c->t_ctl + 10, 0, 4, c->stream));
           tiled_members_active<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(c->tl, t_end);
           CU(cudaMemcpyAsync(&act, c->t_ctl + 10, 4, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaMemsetAsync(c->t_ctl + 10, 0, 4, c->stream));  // (the next step counts its DTS jobs from 0)
           CU(cudaStreamSynchronize(c->stream));
           if (act == 0) break;
         }

@@ -93,7 +93,7 @@ struct CtaShared {
   int nifc, wsn, ntrg, nblk, n, status, remesh, nmev, nsev, ngrp, n_new;
   int c_merges, c_splits, c_creations;
   int olo, ohi;  // tiles: owned output range after the remesh
-  int pf_j, pf_k, pf_wa, pf_wb;  // tiles: the next window job, claimed during the current one
+  int pf_j, pf_k, pf_wa, pf_wb, pf_slot;  // tiles: the next window job, claimed during the current one
   int fbits;     // tiles: phase bits of the smem grid (fast-path test)
   int sv_n;      // window split: the grid's cell count and dt, saved with it between parts A and B
   double sv_dt;

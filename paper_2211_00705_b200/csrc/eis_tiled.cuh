@@ -66,12 +66,37 @@ struct Tiles {
   int djcap;                       //   DTS job capacity
   DtsJob* djobs;                   //   DTS jobs of the step (counter ctl[10])
   unsigned char* wsave;            //   per window job: its grid between parts A and B (WSAVE bytes)
+  // window prediction (tl.spec; window split only): the window step predicts the tile's special
+  // range of the NEXT step, so that part A and the DTS jobs of the predicted windows run beside
+  // tiled_fast on a second stream; tiled_fast compares its own classification with the
+  // prediction (equal: the early result is used; else the window takes the late path)
+  int spec;
+  int* pred[2];                    //   per tile, by step parity: [slot, q_lo, q_hi, -] (slot -1: none);
+                                   //   q = special range in positions relative to the first owned cell
+  int* plist[2];                   //   predicted tiles by slot (-1: that window predicted nothing), by step parity
+  int* mlist;                      //   list indices of this step's windows whose prediction failed (late part A)
 };
 constexpr int SCS = 8, MCS = 4;
 // ctl: [1] any member status  [2] done-counter  [3] launches  [4] tile-list length  [5] next tile job
 //      [6] window-list length  [7] next window job  [8] window jobs of the last step
 //      [9] tiled_fast CTAs finished (the window kernel running beside tiled_fast polls it)
 //      [10] DTS jobs of the step (window split)  [11] next window job of part B
+//      [13] early window jobs of this step (= the last step's listed windows: a window's early slot is
+//           its list index of the step that predicted it)  [15] next early job
+//      [17] DTS jobs solved by the early dts_jobs launch  [18] hits, [19] window jobs (cumulative)
+//      [20] listed windows of this step whose prediction failed (the late part A's jobs, mlist)
+//      [14] early window jobs of the next step
+constexpr int NCTL = 32;
+// end of a step: the work-list counters (the predictions made become the next step's)
+__device__ __forceinline__ void ctl_step_reset(const Tiles& tl) {
+  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
+  tl.ctl[15] = 0; tl.ctl[17] = 0; tl.ctl[20] = 0;
+  if (tl.spec && tl.ctl[8] > 0) tl.ctl[14] = 4 * tl.ctl[8] <= tl.ntiles ? tl.ctl[8] : 0;  // (ctl[8]: this step's listed windows;
+                                                                                  //  predictions were made if they were sparse)
+}
+__device__ __forceinline__ void ctl_step_roll(const Tiles& tl) {  // once per step taken, with ctl[3] += 1
+  tl.ctl[13] = tl.ctl[14]; tl.ctl[14] = 0;
+}
 
 // Exchange buffer (rank mode, one grid decomposed over ranks): four halo records of
 // HALO cells (rho, mom, h) + a count, then the CFL pair (-S_max, h_min) to be min-reduced.
@@ -159,7 +184,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
   if (tid == 0) {
     for (int w = 0; w < nw; ++w) { s = fmax(s, rs[w]); hm = fmin(hm, rh[w]); }
     tl.ctl[8] = tl.ctl[6];  // window jobs of this step (diagnostics)
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
+    ctl_step_reset(tl);
   }
   if (tl.xbuf) {  // rank mode: the global dt needs the other ranks (eis_step_finish)
     if (tid == 0) {
@@ -184,6 +209,7 @@ __device__ void tiles_finish_step(const Prm& p, const Tiles& tl, int nparts, dou
     tl.mctl[0] = 1 - tl.mctl[0];
     tl.mctl[2] += 1;
     tl.ctl[3] += 1;
+    ctl_step_roll(tl);
     __threadfence();
   }
 }
@@ -545,6 +571,15 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       if (window) {  // a window of the tile, published with this step's tag after its data
         const int j = atomicAdd(&tl.ctl[6], 1);
         tl.wlist[4 * j] = k; tl.wlist[4 * j + 1] = wa; tl.wlist[4 * j + 2] = wb;
+        if (tl.spec) {  // was this window predicted (its part A and DTS jobs already under way)?
+          const int* pr = tl.pred[tl.ctl[3] & 1] + 4 * k;
+          const int jp = pr[0];
+          const bool hit = jp >= 0 && jp < tl.ctl[13] && pr[1] == s_lo - own_lo && pr[2] == s_hi - own_lo;
+          tl.wlist[4 * j + 3] = hit ? jp : -1;
+          atomicAdd(&tl.ctl[19], 1);
+          if (hit) atomicAdd(&tl.ctl[18], 1);
+          else tl.mlist[atomicAdd(&tl.ctl[20], 1)] = j;
+        }
         if (tl.poll) {  // only a concurrently polling window kernel reads the entry before this kernel ends
           __threadfence();
           *reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]) = tl.ctl[3] + 1;
@@ -562,6 +597,8 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
            double t_end) {
   const TGeo g = tile_geo_spec(tl, blockIdx.x);
   const double t = tl.scal[SCS * g.m];
+  // no prediction for the next step unless this step's window step makes one (later in the stream)
+  if (tl.spec && threadIdx.x == 0) tl.pred[1 - (tl.ctl[3] & 1)][4 * blockIdx.x] = -1;
   if (tl.mctl[MCS * g.m + 1] == 0 && t < t_end) {  // else the member does not step (uniform in the CTA)
     double dt = tl.scal[SCS * g.m + 1];
     if (t + dt > t_end) dt = t_end - t;  // as step_body
@@ -769,38 +806,124 @@ __device__ __forceinline__ void window_save(const Tiles& tl, CtaShared& sh, cons
   }
   __syncthreads();
 }
-__device__ __forceinline__ double window_restore(const Tiles& tl, CtaShared& sh, Arr& A, int j) {
-  __shared__ __align__(8) unsigned long long wbar;
-  const unsigned bar = (unsigned)__cvta_generic_to_shared(&wbar);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+// (the CTA's mbarrier `bar` is initialised once by the kernel and used phase after phase: `par` is
+// the parity of the phase this restore completes, flipped here for the next one -- an mbarrier
+// must not be initialised again while it is a valid object)
+__device__ __forceinline__ double window_restore(const Tiles& tl, CtaShared& sh, Arr& A, int j, unsigned bar, unsigned& par) {
   if (threadIdx.x == 0) {
     const unsigned char* slot = tl.wsave + (size_t)j * WSAVE;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)WSAVE) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"((unsigned)__cvta_generic_to_shared(&sh)), "l"(slot), "r"((unsigned)WSAVE), "r"(bar) : "memory");
   }
-  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-               " @!P1 bra WAIT_%=;\n}" ::"r"(bar) : "memory");
+  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               " @!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(par) : "memory");
+  par ^= 1u;
   A.n = sh.sv_n;
   return sh.sv_dt;
+}
+
+// Window prediction: after a window's full step, which cells of this tile will tiled_fast flag
+// as special in the NEXT step?  tiled_fast's own tests (fast_pairs: the cell tests of the warp
+// window's specialisation and the creation pre-filter of every edge inside a warp window),
+// evaluated on the window grid after the step (cells [0, nl); local cell i will be virtual cell
+// v0 + i of the next step's tile, n_next cells in all); the cells outside the grid are the
+// tile's plain cells, taken to keep the phase of the grid's end cells.  One warp.  Returns the
+// range [qlo, qhi] of flagged cells as local indices (qhi < 0: none).  A guess by design: the
+// next tiled_fast decides (a wrong guess only sends that window down the late path).
+__device__ __forceinline__ void predict_special(const Eos& e, const double* rho, const double* mom, int nl, int v0,
+                                                int n_next, int& qlo, int& qhi) {
+  const int lane = threadIdx.x & 31;
+  const double rho_min = e.rho_min, rho_tilde = e.rho_tilde, rmin2 = rho_min * rho_min, inv_rt = 1.0 / rho_tilde;
+  const int nwin = (n_next + FW - 1) / FW;
+  const int w_lo = max(0, (v0 - 61 + FW - 1) / FW), w_hi = min(nwin - 1, (v0 + nl - 1 + 2) / FW);
+  const bool left_liq = rho[0] >= rho_min, right_liq = rho[nl - 1] >= rho_min;
+  unsigned liqm = 0;  // bit w - w_lo: warp window w takes the liquid specialisation
+  for (int w = w_lo; w <= w_hi && w - w_lo < 32; ++w) {
+    const int ca = FW * w - 2, cb = FW * w + 61;  // its loaded cells (clamped to the grid by tiled_fast)
+    bool any = (max(ca, 0) < v0 && left_liq) || (min(cb, n_next - 1) >= v0 + nl && right_liq);
+    for (int c = ca + lane; c <= cb; c += 32) {
+      const int i = c - v0;
+      if (i >= 0 && i < nl) any |= rho[i] >= rho_min;
+    }
+    if (__any_sync(0xffffffffu, any)) liqm |= 1u << (w - w_lo);
+  }
+  int lo = 1 << 30, hi = -1;
+  for (int i = lane; i < nl; i += 32) {
+    const int v = v0 + i;
+    const double r = rho[i];
+    bool flagged = false;
+    const int wa = max(w_lo, (v - 61 + FW - 1) / FW), wb = min(w_hi, (v + 2) / FW);
+    for (int w = wa; w <= wb; ++w) {
+      const bool L = liqm >> (w - w_lo) & 1u;
+      flagged |= L ? !(r >= rho_min) : !(r <= rho_tilde && r > 0.0);
+      if (i >= 1 && v >= FW * w - 1) {  // the edge (v - 1, v) lies inside window w
+        const double rl = rho[i - 1];
+        const double du = mom[i] * rcp_fast(r) - mom[i - 1] * rcp_fast(rl), x = rl * r;
+        flagged |= L ? !(du * x <= e.a_l * (x - rmin2) - 1e-9 * x) : (du < -e.a_v * (2.0 - (rl + r) * inv_rt) + 1e-9);
+      }
+    }
+    if (flagged) { lo = min(lo, i); hi = max(hi, i); }
+  }
+  qlo = __reduce_min_sync(0xffffffffu, lo);
+  qhi = __reduce_max_sync(0xffffffffu, hi);
+}
+
+// The next window job of part PH from list SRC (0: tiled_fast's window list; 1: the predicted
+// windows, part A beside tiled_fast).  Returns its index (< 0: the list is exhausted) with the
+// tile, the window and its save slot.  With predictions on, a listed window whose prediction
+// held (tiled_fast stored its early slot in the entry) skips the late part A and part B reads
+// the early slot; the others use the slots above ntiles.
+template <int PH, int SRC>
+__device__ __forceinline__ int claim_window_job(const Tiles& tl, double t_end, int& k, int& wa, int& wb, int& slot) {
+  for (;;) {
+    if constexpr (SRC == 1) {
+      const int j = atomicAdd(&tl.ctl[15], 1);
+      if (j >= tl.ctl[13]) return -1;
+      const int par = tl.ctl[3] & 1;
+      k = tl.plist[par][j];
+      if (k < 0) continue;  // that window made no prediction
+      const int* pr = tl.pred[par] + 4 * k;
+      const int qlo = pr[1], qhi = pr[2];
+      const TGeo g = tile_geo_spec(tl, k);
+      if (!(tl.mctl[MCS * g.m + 1] == 0 && tl.scal[SCS * g.m] < t_end)) continue;  // the member does not step
+      const int own_lo = g.nL, own_hi = g.nL + g.cnt;
+      wa = max(own_lo, own_lo + qlo - 1 - HALO);  // as tiled_fast's classification
+      wb = min(own_hi, own_lo + qhi + 2 + HALO);
+      if (wa >= wb || wb - wa > tl.wmax) continue;  // tiled_fast would not list such a window
+      slot = j;
+      return j;
+    } else {
+      int j = atomicAdd(&tl.ctl[PH == 2 ? 11 : 7], 1);
+      if (PH == 1 && tl.spec) {  // the late part A: only the windows whose prediction failed
+        if (j >= tl.ctl[20]) return -1;
+        j = tl.mlist[j];
+      } else if (j >= tl.ctl[6]) return -1;
+      k = tl.wlist[4 * j]; wa = tl.wlist[4 * j + 1]; wb = tl.wlist[4 * j + 2];
+      slot = j;
+      if (tl.spec) {
+        const int jp = tl.wlist[4 * j + 3];
+        slot = jp >= 0 ? jp : tl.ntiles + j;
+      }
+      return j;
+    }
+  }
 }
 
 // PF: after the step body, thread 0 claims the next window job and loads its list entry into
 // registers (jn, kn, wan, wbn; jn = -1 when the list is exhausted); the loads complete during the
 // assembly and the caller publishes them, so the next job starts without those round trips.
-template <bool PF, int PH = 0>
+template <bool PF, int PH = 0, int SRC = 0>
 __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Tiles& tl, CtaShared& sh, Arr& A, int capw,
-                                            int j, int k, int wa, int wb, double t_end, int& jn, int& kn, int& wan,
-                                            int& wbn) {
+                                            int slot, int k, int wa, int wb, double t_end, int& jn, int& kn, int& wan,
+                                            int& wbn, int& slotn, unsigned wbar = 0, unsigned* wpar = nullptr, int jlist = 0) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   const TGeo g = tile_geo_spec(tl, k);
   const double t = tl.scal[SCS * g.m], dt_given = tl.scal[SCS * g.m + 1];
   const int nL = g.nL, cnt = g.cnt;
   const int s0 = max(0, wa - HALO), s1 = min(g.n, wb + HALO), n = s1 - s0;
+  const int spec_npar = (PH == 2 && tl.spec) ? 1 - (tl.ctl[3] & 1) : 0;           // window prediction (below)
+  const bool spec_sparse = PH == 2 && tl.spec && 4 * tl.ctl[6] <= tl.ntiles;
   if (PH != 2 && tid == 0) {
     sh.status = 0;
     reset_counters(sh);
@@ -857,16 +980,12 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
     dt = step_body<0>(e, p, sh, A, t, t_end, Z);
   } else if constexpr (PH == 1) {  // part A: up to the remesh, blocks exported; the window saved
     dt = step_body<1>(e, p, sh, A, t, t_end, Z);
-    window_save(tl, sh, A, j, dt);
-    if (PF && tid == 0) {
-      jn = atomicAdd(&tl.ctl[7], 1);
-      if (jn < tl.ctl[6]) { kn = tl.wlist[4 * jn]; wan = tl.wlist[4 * jn + 1]; wbn = tl.wlist[4 * jn + 2]; }
-      else jn = -1;
-    }
+    window_save(tl, sh, A, slot, dt);
+    if (PF && tid == 0) jn = claim_window_job<PH, SRC>(tl, t_end, kn, wan, wbn, slotn);
     __syncthreads();
     return;
   } else {  // part B: the saved window, the DTS results, the rest of the step
-    dt = window_restore(tl, sh, A, j);
+    dt = window_restore(tl, sh, A, slot, wbar, *wpar);
     __syncthreads();
     if (dt >= 0.0 && sh.status == 0) {
       apply_dts_jobs(p, sh, A, Z, tl.djobs);
@@ -874,11 +993,7 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
       dt = step_tail(e, p, sh, A, A.n, sh.ntrg < MAXTRG ? sh.ntrg : MAXTRG, dt, Z);
     }
   }
-  if (PF && tid == 0) {
-    jn = atomicAdd(&tl.ctl[PH == 2 ? 11 : 7], 1);
-    if (jn < tl.ctl[6]) { kn = tl.wlist[4 * jn]; wan = tl.wlist[4 * jn + 1]; wbn = tl.wlist[4 * jn + 2]; }
-    else jn = -1;
-  }
+  if (PF && tid == 0) jn = claim_window_job<PH, SRC>(tl, t_end, kn, wan, wbn, slotn);
   __syncthreads();
   const int olo = sh.olo, ohi = sh.ohi;
   const int nw_out = ohi - olo;
@@ -929,6 +1044,25 @@ __device__ __forceinline__ void tile_window(const Eos& e, const Prm& p, const Ti
         if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
         if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
       }
+    }
+  }
+  // the tile's window of the next step, predicted (only while at most a quarter of the tiles hold a
+  // window: part A of many windows is throughput work that costs tiled_fast more than the hidden
+  // DTS latency is worth -- measured on C3); the early slot is this window's list index
+  if (tl.spec && PH == 2 && T == 32) {
+    int pk = -1, plo = 0, phi = 0;
+    if (dt >= 0.0 && st == 0 && spec_sparse) {
+      const int nLn = g.first ? 0 : HALO, nRn = g.last ? 0 : HALO;  // next step's halos (neighbours hold >= HALO cells)
+      const int pa = wa - nL;
+      int qlo, qhi;
+      predict_special(e, A.rho, A.mom, A.n, nLn + pa - olo, nLn + nout + nRn, qlo, qhi);
+      plo = pa + qlo - olo; phi = pa + qhi - olo;  // positions relative to the first owned cell
+      const int lo2 = max(0, plo - 1 - HALO), hi2 = min(nout, phi + 2 + HALO);
+      if (qhi >= 0 && lo2 < hi2 && hi2 - lo2 <= tl.wmax) pk = k;
+    }
+    if (tid == 0) {
+      tl.plist[spec_npar][jlist] = pk;
+      if (pk >= 0) { int* pr = tl.pred[spec_npar] + 4 * k; pr[1] = plo; pr[2] = phi; pr[0] = jlist; }
     }
   }
   if (lane == 0) { sh.part_s[warp] = s_th; sh.part_h[warp] = h_th; }
@@ -997,10 +1131,14 @@ __global__ void dts_dbg_print() {
   for (int i = 0; i < 8; ++i) g_dbg[i] = 0;
 }
 #endif
+// (window prediction: the early launch, beside tiled_fast, solves the jobs of the predicted
+// windows and leaves their count in ctl[17]; the launch after the late part A solves the rest)
 __global__ void __launch_bounds__(32)
-dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl) {
+dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl, int early) {
   const int n = tl.ctl[10] < tl.djcap ? tl.ctl[10] : tl.djcap;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+  const int q0 = early ? 0 : tl.ctl[17];
+  if (early && blockIdx.x == 0 && threadIdx.x == 0) tl.ctl[17] = n;  // (every job of part A beside tiled_fast is listed by now)
+  for (int q = q0 + blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     DtsJob& J = tl.djobs[q];
 #ifdef EIS_DTS_DEBUG  // development: the longest jobs of a step
     const long long c0 = clock64();
@@ -1015,11 +1153,12 @@ dts_jobs(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __g
   }
 }
 
-template <int MAXT, int MINB, bool POLL, int PH = 0>
+template <int MAXT, int MINB, bool POLL, int PH = 0, int SRC = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
           double t_end) {
   static_assert(!POLL || PH <= 1, "a polling instance runs the whole window step or part A");
+  static_assert(SRC == 0 || (!POLL && PH == 1), "the predicted windows only run part A");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaShared& sh = *reinterpret_cast<CtaShared*>(smem_raw);
   Arr A = carve(smem_raw, WCAP);
@@ -1027,22 +1166,32 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
   const int tag = tl.ctl[3] + 1;
   volatile int* vctl = tl.ctl;
   if constexpr (!POLL) {  // the next job is claimed during the current one's assembly (tile_window<true>)
+    // window prediction: an empty job list (no early jobs; every listed window predicted) ends the
+    // CTA before its first atomic
+    if (SRC == 1 && tl.ctl[13] == 0) return;
+    if (SRC == 0 && PH == 1 && tl.spec && tl.ctl[20] == 0) return;
+    __shared__ __align__(8) unsigned long long wbar_s;  // part B: the restores' mbarrier, one phase per job
+    const unsigned wbar = (unsigned)__cvta_generic_to_shared(&wbar_s);
+    unsigned wpar = 0;
+    if (PH == 2 && tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (tid == 0) {
-      const int j = atomicAdd(&tl.ctl[PH == 2 ? 11 : 7], 1);
-      const bool ok = j < tl.ctl[6];
-      sh.pf_j = ok ? j : -1;
-      if (ok) { sh.pf_k = tl.wlist[4 * j]; sh.pf_wa = tl.wlist[4 * j + 1]; sh.pf_wb = tl.wlist[4 * j + 2]; }
+      int k = 0, wa = 0, wb = 0, slot = 0;
+      sh.pf_j = claim_window_job<PH, SRC>(tl, t_end, k, wa, wb, slot);
+      sh.pf_k = k; sh.pf_wa = wa; sh.pf_wb = wb; sh.pf_slot = slot;
     }
     __syncthreads();
     for (;;) {
-      const int j = sh.pf_j, k = sh.pf_k, wa = sh.pf_wa, wb = sh.pf_wb;
+      const int j = sh.pf_j, k = sh.pf_k, wa = sh.pf_wa, wb = sh.pf_wb, slot = sh.pf_slot;
       if (j < 0) break;
       __syncthreads();  // every lane has read the job before thread 0 replaces it
       const long long c0 = clock64();
-      int jn = -1, kn = 0, wan = 0, wbn = 0;
-      tile_window<true, PH>(e, p, tl, sh, A, WCAP, j, k, wa, wb, t_end, jn, kn, wan, wbn);
-      if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, wa, wb, c0);
-      if (tid == 0) { sh.pf_j = jn; sh.pf_k = kn; sh.pf_wa = wan; sh.pf_wb = wbn; }
+      int jn = -1, kn = 0, wan = 0, wbn = 0, slotn = 0;
+      tile_window<true, PH, SRC>(e, p, tl, sh, A, WCAP, slot, k, wa, wb, t_end, jn, kn, wan, wbn, slotn, wbar, &wpar, j);
+      if (tl.wdbg && tid == 0 && SRC == 0) window_dbg(tl, sh, j, wa, wb, c0);
+      if (tid == 0) { sh.pf_j = jn; sh.pf_k = kn; sh.pf_wa = wan; sh.pf_wb = wbn; sh.pf_slot = slotn; }
       __syncthreads();
     }
   } else {
@@ -1077,9 +1226,9 @@ tiled_win(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __
       const int j = sh.n_new;
       if (j < 0) break;
       const long long c0 = clock64();
-      int jn, kn, wan, wbn;
+      int jn, kn, wan, wbn, slotn;
       tile_window<false, PH>(e, p, tl, sh, A, WCAP, j, tl.wlist[4 * j], tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], t_end,
-                             jn, kn, wan, wbn);
+                             jn, kn, wan, wbn, slotn);
       if (tl.wdbg && tid == 0) window_dbg(tl, sh, j, tl.wlist[4 * j + 1], tl.wlist[4 * j + 2], c0);
     }
   }
@@ -1101,7 +1250,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
   const bool one = tl.M == 1;  // one grid: this kernel folds the CFL partials and ends the step
   const double t = tl.scal[0], dt_given = tl.scal[1];
   if (one && (tl.mctl[1] != 0 || !(t < t_end))) {  // uniform across the grid: nothing to do
-    if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }  // (a no-op step's counters)
+    if (blockIdx.x == 0 && tid == 0) { tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; tl.ctl[15] = 0; tl.ctl[17] = 0; tl.ctl[20] = 0; }  // (a no-op step's counters)
     // peer mode: a stopped rank still publishes a neutral pair while the others step (t is
     // global, so at t_end every rank stops together and nobody waits)
     if (blockIdx.x == 0 && tl.xbuf && tl.xpeers && t < t_end) xpublish(tl, 0.0, INFINITY, tl.mctl[1]);
@@ -1146,7 +1295,7 @@ tiled_slow(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     __threadfence();
     if (tl.mctl[1] == 0) tiles_finish_step(p, tl, (int)gridDim.x, dt, t_end);
     else {
-      if (tid == 0) { tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0; }
+      if (tid == 0) { ctl_step_reset(tl); }
       if (tl.xbuf && tl.xpeers) xpublish(tl, 0.0, INFINITY, tl.mctl[1]);  // (neutral pair, status)
     }
   }
@@ -1252,8 +1401,8 @@ __global__ void tiled_members_finish(const __grid_constant__ Prm p, const __grid
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     tl.ctl[8] = tl.ctl[6];
-    tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
-    if (after_step) tl.ctl[3] += 1;
+    ctl_step_reset(tl);
+    if (after_step) { tl.ctl[3] += 1; ctl_step_roll(tl); }
   }
   if (m >= tl.M) return;
   double s = 0.0, hm = INFINITY;
@@ -1350,8 +1499,9 @@ __global__ void tiled_finish(const __grid_constant__ Prm p, const __grid_constan
     tl.mctl[0] = 1 - tl.mctl[0];
     tl.mctl[2] += 1;
     tl.ctl[3] += 1;
+    ctl_step_roll(tl);
   }
-  tl.ctl[2] = 0; tl.ctl[4] = 0; tl.ctl[5] = 0; tl.ctl[6] = 0; tl.ctl[7] = 0; tl.ctl[9] = 0; tl.ctl[10] = 0; tl.ctl[11] = 0;
+  ctl_step_reset(tl);
   double dt = p.cfl * hm / S;
   if (t_new + dt > t_end) dt = t_end - t_new;
   tl.scal[0] = t_new;

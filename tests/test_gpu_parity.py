@@ -1139,3 +1139,43 @@ def test_window_split_matches_the_one_kernel_window_step(P, cfg, monkeypatch):
             el = el_err(a[k][m, :n], b[k][m, :n], b["h"][m, :n], hav, b["rho"][m, :n] if k == "mom" else None)
             assert el.max() <= 1e-11, (m, k, float(el.max()), int(el.argmax()))
         assert np.abs(a["h"][m, :n] - b["h"][m, :n]).max() <= 1e-11 * hav
+
+
+@pytest.mark.parametrize("cfg", ["c5_65k", "c5_262k", "c4", "c3"])
+def test_window_prediction_does_not_change_results(P, cfg, monkeypatch):
+    """Window prediction (DESIGN 6.2: part A and the DTS jobs of the predicted windows run beside
+    tiled_fast on a second stream; tiled_fast checks each prediction against its own
+    classification and a failed one takes the late path): the same kernels on the same inputs in
+    either case, so states, clocks and every counter are equal bit for bit with predictions on
+    and off; and nearly every window step of these runs is predicted (all but the creation
+    steps), except where every tile holds a window (C3 members as tiles: predictions are only
+    made while at most a quarter of the tiles hold one)."""
+    if cfg == "c4":
+        w = W.c4(members=np.array([0, 1, 2, 3, 5, 777, 9999, 12345]))
+        steps = 120
+    elif cfg == "c3":
+        w = W.c3(members=np.arange(24))
+        steps = 150
+    else:
+        w = W.c5(n_cells=1 << (16 if cfg == "c5_65k" else 18))
+        steps = 60
+    out = {}
+    for spec in ("1", "0"):
+        monkeypatch.setenv("EIS_WIN_SPEC", spec)
+        g, ctx = gpu_run(P, w, steps=steps, layout=P.LAYOUT_TILED)
+        out[spec] = g
+        pr = ctx.window_prediction()
+        assert pr["enabled"] == (spec == "1")
+        if spec == "1":
+            assert pr["windows"] == ctx.tile_info()["window_steps"] > 0
+            if cfg == "c3":  # a window in every tile: no predictions (only made while windows are sparse)
+                assert pr["predicted"] == 0, pr
+            else:
+                assert pr["predicted"] >= 0.9 * pr["windows"], pr
+            _tally("test_window_prediction[%s]" % cfg, "windows", pr["windows"])
+            _tally("test_window_prediction[%s]" % cfg, "predicted", pr["predicted"])
+    a, b = out["1"], out["0"]
+    assert a["stats"] == b["stats"]
+    assert a["mstats"] == b["mstats"]
+    for k in ("status", "n", "t", "rho", "mom", "h"):
+        np.testing.assert_array_equal(a[k], b[k])
