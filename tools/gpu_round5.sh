@@ -1,23 +1,23 @@
 #!/bin/bash
-# session-5 evidence: full GPU suite, then C5 (driver's command and 500 steps) with predictions off / on, C4, C3
+# session-5 evidence: full GPU suite, smoke, the bench lines (C5 driver's command, C5 500 steps, C4, C3),
+# then the ncu launch list of the C4 command (after it exited 0 without ncu)
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r5_tests.log 2>&1; tail -3 gpurun_out/r5_tests.log
-run() { # name, args..., env via ENVV
-  name=$1; shift
-  env $ENVV timeout 900 python bench.py "$@" > gpurun_out/r5_$name.json 2> gpurun_out/r5_$name.err
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+run() { name=$1; shift
+  timeout 900 python bench.py "$@" > gpurun_out/r5_$name.json 2> gpurun_out/r5_$name.err
   echo "$name rc=$?"
   python - <<P
 import json
 try:
     d=json.loads(open("gpurun_out/r5_$name.json").read().strip().splitlines()[-1])
-    print("  ", "%.4e" % d["value"], "%.4f ms" % d["ms_per_step"], d["members_not_ok"], "frac %.4f" % d["roofline"]["frac"], {k:round(v,4) for k,v in d["roofline"].items() if "ms" in k}, "e2e", (d.get("e2e") or {}).get("value"), "cpu", (d.get("cpu_baseline") or {}).get("value"))
+    print("  ", "%.4e" % d["value"], "%.4f ms" % d["ms_per_step"], d["members_not_ok"], "frac %.4f" % d["roofline"]["frac"], {k:round(v,4) for k,v in d["roofline"].items() if "ms" in k}, "e2e", (d.get("e2e") or {}).get("value"), "cpu", (d.get("cpu_baseline") or {}).get("value"), "launches", d.get("gpu_launches"))
 except Exception as ex: print("  no json", ex); print(open("gpurun_out/r5_$name.err").read()[-600:])
 P
 }
-ENVV="EIS_WIN_SPEC=0" run c5_500_spec0 --workload C5 --steps 500 --no-cpu --no-e2e
-ENVV="EIS_WIN_SPEC=1" run c5_500_spec1 --workload C5 --steps 500 --no-cpu --no-e2e
-ENVV="EIS_WIN_SPEC=1" run c5_20_spec1 --workload C5 --steps 20 --warmup 5 --no-cpu --no-e2e
-ENVV="EIS_WIN_SPEC=0" run c4_spec0 --workload C4 --no-cpu --no-e2e
-ENVV="X=1" run c4 --workload C4
-ENVV="X=1" run c5 --steps 20 --warmup 5
+run c5 --steps 20 --warmup 5
+run c5_500 --no-cpu --no-e2e
+run c4 --workload C4
+run c3 --workload C3 --no-cpu
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r5_ncu_launches_c4.csv python bench.py --workload C4 --steps 60 --warmup 3 --no-cpu --no-e2e > gpurun_out/r5_ncu_c4.log 2>&1; echo "ncu rc=$?"; tail -1 gpurun_out/r5_ncu_launches_c4.csv | cut -c1-200
