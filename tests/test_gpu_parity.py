@@ -1179,3 +1179,55 @@ def test_window_prediction_does_not_change_results(P, cfg, monkeypatch):
     assert a["mstats"] == b["mstats"]
     for k in ("status", "n", "t", "rho", "mom", "h"):
         np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_window_prediction_defaults_and_resets(P, monkeypatch):
+    """Where window prediction runs (DESIGN 6.2): by default for ensembles on the tiled layout,
+    not for one grid; never for rank slices (the neighbours' halos arrive between the two halves
+    of the step), for the other time-stepping modes (no DTS jobs) or on the member-resident
+    layout (EIS_E_ARG); eis_set_state starts its counters again; and a rank-sliced grid with
+    EIS_WIN_SPEC=1 still reproduces the 1-rank run with predictions bit for bit."""
+    from paper_2211_00705_b200.decomp import VirtualRanks
+    monkeypatch.delenv("EIS_WIN_SPEC", raising=False)
+    w4 = W.c4(members=np.array([0, 1, 2, 3, 5, 777, 9999, 12345]))
+    g4, c4 = gpu_run(P, w4, steps=40, layout=P.LAYOUT_TILED)
+    assert c4.window_prediction()["enabled"]
+    n, tile = 40 * 960 + 517, 960
+    w5 = W.c5(n_cells=n)
+    rho = torch.tensor(w5["rho"], device="cuda").reshape(-1)
+    mom = torch.tensor(w5["mom"], device="cuda").reshape(-1)
+    c5 = P.Context(w5["eos"], w5["params"], 1, w5["N"], w5["cap"], w5["x_left"], w5["x_right"],
+                   stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=tile)
+    assert not c5.window_prediction()["enabled"]  # one grid: off unless asked for
+    wl = dict(w5, params=dict(w5["params"], mode=P.MODE_LTS))
+    monkeypatch.setenv("EIS_WIN_SPEC", "1")
+    cl = P.Context(wl["eos"], wl["params"], 1, wl["N"], wl["cap"], wl["x_left"], wl["x_right"],
+                   stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=tile)
+    assert not cl.window_prediction()["enabled"]
+    w3 = W.c3(members=np.arange(4))
+    cr = P.Context(w3["eos"], w3["params"], w3["M"], w3["N"], w3["cap"], w3["x_left"], w3["x_right"],
+                   stream=torch.cuda.current_stream(), layout=P.LAYOUT_RESIDENT)
+    with pytest.raises(P.EisError):
+        cr.window_prediction()
+    c5 = P.Context(w5["eos"], w5["params"], 1, w5["N"], w5["cap"], w5["x_left"], w5["x_right"],
+                   stream=torch.cuda.current_stream(), layout=P.LAYOUT_TILED, tile_cells=tile)
+    assert c5.window_prediction()["enabled"]
+    c5.set_state(rho, mom)
+    c5.step(120)
+    p1 = c5.window_prediction()
+    assert p1["windows"] > 0 and p1["predicted"] >= 0.9 * p1["windows"]
+    c5.set_state(rho, mom)
+    assert c5.window_prediction()["windows"] == 0
+    c5.step(120)
+    assert c5.window_prediction() == p1
+    g = c5.get_state()
+    n1 = int(g["n"][0])
+    vr = VirtualRanks(w5["eos"], w5["params"], w5["N"], w5["x_left"], w5["x_right"], 3, tile=tile,
+                      stream=torch.cuda.current_stream())
+    assert not any(r.ctx.window_prediction()["enabled"] for r in vr.parts)
+    vr.set_state(rho[:w5["N"]], mom[:w5["N"]])
+    vr.step(120)
+    v = vr.get_state()
+    np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
+    np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
+    np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
