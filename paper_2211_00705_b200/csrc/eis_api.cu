@@ -353,6 +353,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
 #if EIS_FAST_TMA
   c->smem_fast = 2 * sizeof(double) * (size_t)((capt + 1) & ~1);
   if (cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess) { delete c; return EIS_E_CUDA; }
 #endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
@@ -366,7 +368,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
+    if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1, 1>) != cudaSuccess ||
@@ -908,7 +910,10 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     cudaEventRecord(c->ev_join, c->stream2);
     dbg_sync(c, "early part A + dts_jobs");
   }
-  tiled_fast<EIS_FAST_T, EIS_FAST_MINB><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  if (c->tl.spec)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   dbg_sync(c, "tiled_fast");
   if (c->timing) m[1] = timing_event(c);
   if (c->win_grid_poll > 0) {

@@ -372,7 +372,9 @@ __device__ __forceinline__ void fast_pairs(const Eos& e, const double2 (&rv)[FB]
 #endif
 constexpr int WMAX = EIS_WMAX;  // owned cells of a full-step window (larger: the whole tile)
 
-template <bool HU, int IN>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
+// SPEC: window prediction compiled in (a template parameter: the kernel of contexts without
+// predictions keeps the round-2 code generation -- 1 % on C5)
+template <bool HU, int IN, bool SPEC>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
   const int BIN = IN >= 0 ? IN : g.in, BOUT = 1 - BIN;  // IN = -1: dynamic
   __shared__ double ps[32], ph[32];
@@ -571,7 +573,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       if (window) {  // a window of the tile, published with this step's tag after its data
         const int j = atomicAdd(&tl.ctl[6], 1);
         tl.wlist[4 * j] = k; tl.wlist[4 * j + 1] = wa; tl.wlist[4 * j + 2] = wb;
-        if (tl.spec) {  // was this window predicted (its part A and DTS jobs already under way)?
+        if (SPEC) {  // was this window predicted (its part A and DTS jobs already under way)?
           const int* pr = tl.pred[tl.ctl[3] & 1] + 4 * k;
           const int jp = pr[0];
           const bool hit = jp >= 0 && jp < tl.ctl[13] && pr[1] == s_lo - own_lo && pr[2] == s_hi - own_lo;
@@ -591,28 +593,28 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   }
 }
 
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, bool SPEC = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
   const TGeo g = tile_geo_spec(tl, blockIdx.x);
   const double t = tl.scal[SCS * g.m];
   // no prediction for the next step unless this step's window step makes one (later in the stream)
-  if (tl.spec && threadIdx.x == 0) tl.pred[1 - (tl.ctl[3] & 1)][4 * blockIdx.x] = -1;
+  if (SPEC && threadIdx.x == 0) tl.pred[1 - (tl.ctl[3] & 1)][4 * blockIdx.x] = -1;
   if (tl.mctl[MCS * g.m + 1] == 0 && t < t_end) {  // else the member does not step (uniform in the CTA)
     double dt = tl.scal[SCS * g.m + 1];
     if (t + dt > t_end) dt = t_end - t;  // as step_body
 #if EIS_FAST_STATIC_IN
     if (g.in) {
-      if (g.hu_in) tiled_fast_body<true, 1>(e, p, tl, g, dt);
-      else tiled_fast_body<false, 1>(e, p, tl, g, dt);
+      if (g.hu_in) tiled_fast_body<true, 1, SPEC>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 1, SPEC>(e, p, tl, g, dt);
     } else {
-      if (g.hu_in) tiled_fast_body<true, 0>(e, p, tl, g, dt);
-      else tiled_fast_body<false, 0>(e, p, tl, g, dt);
+      if (g.hu_in) tiled_fast_body<true, 0, SPEC>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 0, SPEC>(e, p, tl, g, dt);
     }
 #else
-    if (g.hu_in) tiled_fast_body<true, -1>(e, p, tl, g, dt);
-    else tiled_fast_body<false, -1>(e, p, tl, g, dt);
+    if (g.hu_in) tiled_fast_body<true, -1, SPEC>(e, p, tl, g, dt);
+    else tiled_fast_body<false, -1, SPEC>(e, p, tl, g, dt);
 #endif
   }
   if (tl.poll) {  // count finished CTAs for the polling window kernel (every CTA, always)
