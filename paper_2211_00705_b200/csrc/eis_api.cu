@@ -355,6 +355,10 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   if (cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess) { delete c; return EIS_E_CUDA; }
 #endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
@@ -368,7 +372,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   }
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
+    if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1, 1>) != cudaSuccess ||
@@ -910,8 +915,14 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     cudaEventRecord(c->ev_join, c->stream2);
     dbg_sync(c, "early part A + dts_jobs");
   }
-  if (c->tl.spec)
+  static const int plain_ok = getenv("EIS_FAST_PLAIN") ? atoi(getenv("EIS_FAST_PLAIN")) : 1;
+  const bool plain = plain_ok && !c->tl.nbr_left && !c->tl.nbr_right && !c->tl.poll;  // (no exchange buffer, no polling kernel)
+  if (c->tl.spec && plain)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (c->tl.spec)
     tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (plain)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   else
     tiled_fast<EIS_FAST_T, EIS_FAST_MINB><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   dbg_sync(c, "tiled_fast");

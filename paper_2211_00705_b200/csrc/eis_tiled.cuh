@@ -374,8 +374,11 @@ constexpr int WMAX = EIS_WMAX;  // owned cells of a full-step window (larger: th
 
 // SPEC: window prediction compiled in (a template parameter: the kernel of contexts without
 // predictions keeps the round-2 code generation -- 1 % on C5)
-template <bool HU, int IN, bool SPEC>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
+// PLAIN: one rank and no polling window kernel (the usual context): the exchange-buffer halos,
+// send records, fences and ready tags are compiled out
+template <bool HU, int IN, bool SPEC, bool PLAIN>  // IN: the buffer read (static, so the array bases stay parameter-bank operands)
 __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, const Tiles& tl, const TGeo& g, double dt) {
+  const bool gxl = !PLAIN && g.xl, gxr = !PLAIN && g.xr, tpoll = !PLAIN && tl.poll;
   const int BIN = IN >= 0 ? IN : g.in, BOUT = 1 - BIN;  // IN = -1: dynamic
   __shared__ double ps[32], ph[32];
   __shared__ int fl_or, s_lo, s_hi;
@@ -419,11 +422,11 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   }
 #endif
   // segment bases of the virtual array: left halo | own | right halo (density; momentum at +mo)
-  const double* const segL = g.xl ? tl.xbuf + XB_RECV_LEFT + HALO - g.nL : rin + g.bl + g.cl - g.nL;
-  const long long moL = g.xl ? HALO : mo_t;
+  const double* const segL = gxl ? tl.xbuf + XB_RECV_LEFT + HALO - g.nL : rin + g.bl + g.cl - g.nL;
+  const long long moL = gxl ? HALO : mo_t;
   const double* const segO = rin + g.base - g.nL;
-  const double* const segR = g.xr ? tl.xbuf + XB_RECV_RIGHT - own_hi : rin + g.br - own_hi;
-  const long long moR = g.xr ? HALO : mo_t;
+  const double* const segR = gxr ? tl.xbuf + XB_RECV_RIGHT - own_hi : rin + g.br - own_hi;
+  const long long moR = gxr ? HALO : mo_t;
   double* const orho = tl.rho[BOUT] + g.base - own_lo;  // indexed by the virtual cell
   double* const omom = tl.mom[BOUT] + g.base - own_lo;
   double* const oh = tl.h[BOUT] + g.base - own_lo;
@@ -524,7 +527,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   unif = !(f & 8);
   if (window) {  // partials and width uniformity of the fast cells (outside [wa, wb)), from the
                  // output just written (the window full step only moves them): as cfl_partials
-    if (tl.poll) __threadfence();  // output read by a window CTA running concurrently (polling mode)
+    if (tpoll) __threadfence();  // output read by a window CTA running concurrently (polling mode)
     double sf = 0.0, hf = INFINITY;
     bool uf = true;
     for (int c = own_lo + tid; c < own_hi; c += blockDim.x) {
@@ -545,10 +548,10 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       tl.partf[3 * k] = s; tl.partf[3 * k + 1] = hm; tl.partf[3 * k + 2] = (fl_or & 16) ? 0.0 : 1.0;
     }
   }
-  if (fast && (g.xl || g.xr)) {  // rank mode: send records of the first / last HALO owned cells
+  if (fast && (gxl || gxr)) {  // rank mode: send records of the first / last HALO owned cells
     for (int q = tid; q < 2 * HALO; q += blockDim.x) {
       const bool left = q < HALO;
-      if (left ? !g.xl : !g.xr) continue;
+      if (left ? !gxl : !gxr) continue;
       const int c = left ? own_lo + q : own_hi - 2 * HALO + q;
       double* sb = tl.xbuf + (left ? XB_SEND_LEFT : XB_SEND_RIGHT) + (left ? q : q - HALO);
       sb[0] = orho[c]; sb[HALO] = omom[c]; sb[2 * HALO] = HU ? h_av : oh[c];
@@ -565,8 +568,8 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
       tl.ws[(size_t)k * WS_STRIDE + 2 * MAXIF] = 0.0;  // no boundary: no warm start
       // fire-and-forget reduction: no load in the CTA's last instructions
       atomicAdd(reinterpret_cast<unsigned long long*>(&tl.tstats[k].cell_updates), (unsigned long long)g.cnt);
-      if (g.xl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
-      if (g.xr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
+      if (gxl) tl.xbuf[XB_SEND_LEFT + 3 * HALO] = HALO;
+      if (gxr) tl.xbuf[XB_SEND_RIGHT + 3 * HALO] = HALO;
     } else {
       tl.part[2 * k] = 0.0;  // neutral: the full-step kernels fold this tile's own partials
       tl.part[2 * k + 1] = INFINITY;
@@ -582,7 +585,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
           if (hit) atomicAdd(&tl.ctl[18], 1);
           else tl.mlist[atomicAdd(&tl.ctl[20], 1)] = j;
         }
-        if (tl.poll) {  // only a concurrently polling window kernel reads the entry before this kernel ends
+        if (tpoll) {  // only a concurrently polling window kernel reads the entry before this kernel ends
           __threadfence();
           *reinterpret_cast<volatile int*>(&tl.wlist[4 * j + 3]) = tl.ctl[3] + 1;
         }
@@ -593,7 +596,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   }
 }
 
-template <int MAXT, int MINB, bool SPEC = false>
+template <int MAXT, int MINB, bool SPEC = false, bool PLAIN = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
@@ -606,18 +609,18 @@ tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const _
     if (t + dt > t_end) dt = t_end - t;  // as step_body
 #if EIS_FAST_STATIC_IN
     if (g.in) {
-      if (g.hu_in) tiled_fast_body<true, 1, SPEC>(e, p, tl, g, dt);
-      else tiled_fast_body<false, 1, SPEC>(e, p, tl, g, dt);
+      if (g.hu_in) tiled_fast_body<true, 1, SPEC, PLAIN>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 1, SPEC, PLAIN>(e, p, tl, g, dt);
     } else {
-      if (g.hu_in) tiled_fast_body<true, 0, SPEC>(e, p, tl, g, dt);
-      else tiled_fast_body<false, 0, SPEC>(e, p, tl, g, dt);
+      if (g.hu_in) tiled_fast_body<true, 0, SPEC, PLAIN>(e, p, tl, g, dt);
+      else tiled_fast_body<false, 0, SPEC, PLAIN>(e, p, tl, g, dt);
     }
 #else
-    if (g.hu_in) tiled_fast_body<true, -1, SPEC>(e, p, tl, g, dt);
-    else tiled_fast_body<false, -1, SPEC>(e, p, tl, g, dt);
+    if (g.hu_in) tiled_fast_body<true, -1, SPEC, PLAIN>(e, p, tl, g, dt);
+    else tiled_fast_body<false, -1, SPEC, PLAIN>(e, p, tl, g, dt);
 #endif
   }
-  if (tl.poll) {  // count finished CTAs for the polling window kernel (every CTA, always)
+  if (!PLAIN && tl.poll) {  // count finished CTAs for the polling window kernel (every CTA, always)
     __syncthreads();
     if (threadIdx.x == 0) { __threadfence(); atomicAdd(&tl.ctl[9], 1); }
   }
