@@ -359,6 +359,14 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
       cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess ||
       cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)c->smem_fast) != cudaSuccess ||
+      cudaFuncSetAttribute(tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)c->smem_fast) != cudaSuccess) { delete c; return EIS_E_CUDA; }
 #endif
   c->smem_win = ((sizeof(CtaShared) + 15) & ~size_t(15)) + 6 * 8 * (size_t)(WCAP + 1) + (((size_t)WCAP + 1 + 15) & ~size_t(15));
@@ -373,7 +381,9 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   {  // load every tiled kernel now (CUDA lazy loading would load one at its first launch)
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true>) != cudaSuccess ||
-        cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 1>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 1>) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 2>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 2>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, true>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false>) != cudaSuccess || cudaFuncGetAttributes(&fa, tiled_slow<256, 4>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1>) != cudaSuccess ||
         cudaFuncGetAttributes(&fa, tiled_win<32, EIS_WIN_MINB, false, 1, 1>) != cudaSuccess ||
@@ -917,7 +927,17 @@ static void tiled_launch(eis_ctx* c, double t_end) {
   }
   static const int plain_ok = getenv("EIS_FAST_PLAIN") ? atoi(getenv("EIS_FAST_PLAIN")) : 1;
   const bool plain = plain_ok && !c->tl.nbr_left && !c->tl.nbr_right && !c->tl.poll;  // (no exchange buffer, no polling kernel)
-  if (c->tl.spec && plain)
+  static const int one_ok = getenv("EIS_FAST_ONE") ? atoi(getenv("EIS_FAST_ONE")) : 1;
+  const bool one = one_ok && plain && c->tl.M == 1;
+  if (one && c->tl.spec)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 1><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (one)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 1><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (one_ok && plain && c->tl.M <= 65535 && c->tl.spec)  // ensembles: (tile in member, member) as a 2D grid
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 2><<<dim3((unsigned)c->tl.tpm, (unsigned)c->tl.M), EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (one_ok && plain && c->tl.M <= 65535)
+    tiled_fast<EIS_FAST_T, EIS_FAST_MINB, false, true, 2><<<dim3((unsigned)c->tl.tpm, (unsigned)c->tl.M), EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
+  else if (c->tl.spec && plain)
     tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);
   else if (c->tl.spec)
     tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);

@@ -226,9 +226,14 @@ struct TGeo {
 };
 // (the tile metadata of both buffers is loaded before `cur` is known: one dependent global
 // round trip fewer at the start of every tile)
-__device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
-  const int m = k / tl.tpm;
-  const bool hasl = k % tl.tpm != 0, hasr = (k + 1) % tl.tpm != 0;
+// (PLAIN: no rank neighbour, the exchange buffer is never read; GEO = 1: one grid, GEO = 2: the
+// member m2 and the tile j2 within it given (a 2D launch) -- no division by the tiles per member
+// at the start of every CTA: tiled_fast's instantiations for the usual contexts)
+template <bool PLAIN = false, int GEO = 0>
+__device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k, int m2 = 0, int j2 = 0) {
+  const int m = GEO == 1 ? 0 : (GEO == 2 ? m2 : k / tl.tpm);
+  const bool hasl = GEO == 1 ? k != 0 : (GEO == 2 ? j2 != 0 : k % tl.tpm != 0);
+  const bool hasr = GEO == 1 ? k + 1 != tl.ntiles : (GEO == 2 ? j2 + 1 != tl.tpm : (k + 1) % tl.tpm != 0);
   const int c0 = tl.cnt[0][k], c1 = tl.cnt[1][k], h0 = tl.hu[0][k], h1 = tl.hu[1][k];
   const int l0 = hasl ? tl.cnt[0][k - 1] : 0, l1 = hasl ? tl.cnt[1][k - 1] : 0;
   const int r0 = hasr ? tl.cnt[0][k + 1] : 0, r1 = hasr ? tl.cnt[1][k + 1] : 0;
@@ -243,7 +248,7 @@ __device__ __forceinline__ TGeo tile_geo_spec(const Tiles& tl, int k) {
   g.hu_in = (cur ? h1 : h0) != 0;
   g.huL = (cur ? hl1 : hl0) != 0;
   g.huR = (cur ? hr1 : hr0) != 0;
-  g.xl = (g.first && tl.nbr_left); g.xr = (g.last && tl.nbr_right);
+  g.xl = !PLAIN && (g.first && tl.nbr_left); g.xr = !PLAIN && (g.last && tl.nbr_right);
   g.cl = cur ? l1 : l0;
   g.nL = hasl ? min(HALO, g.cl) : (g.xl ? (int)tl.xbuf[XB_RECV_LEFT + 3 * HALO] : 0);
   g.nR = hasr ? min(HALO, cur ? r1 : r0) : (g.xr ? (int)tl.xbuf[XB_RECV_RIGHT + 3 * HALO] : 0);
@@ -493,7 +498,7 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
     else if (!lmask)
       fast_pairs<HU, false, false>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
                                    vmask, slo, shi, unif, snum, sden, h_part);
-    else {  // a batch whose windows differ in phase (rare): each window with its own
+    else if constexpr (FB > 1) {  // a batch whose windows differ in phase (rare): each window with its own
       fast_pairs<HU, true, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
                                  lmask, slo, shi, unif, snum, sden, h_part);
       fast_pairs<HU, false, true>(e, rv, mv, w0, nw, nwin, n, own_lo, own_hi, dt, dt_hav, h_av, ih, orho, omom, oh,
@@ -596,14 +601,15 @@ __device__ __forceinline__ void tiled_fast_body(const Eos& e, const Prm& p, cons
   }
 }
 
-template <int MAXT, int MINB, bool SPEC = false, bool PLAIN = false>
+template <int MAXT, int MINB, bool SPEC = false, bool PLAIN = false, int GEO = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
 tiled_fast(const __grid_constant__ Eos e, const __grid_constant__ Prm p, const __grid_constant__ Tiles tl,
            double t_end) {
-  const TGeo g = tile_geo_spec(tl, blockIdx.x);
+  const int kt = GEO == 2 ? (int)blockIdx.y * tl.tpm + (int)blockIdx.x : (int)blockIdx.x;
+  const TGeo g = tile_geo_spec<PLAIN, GEO>(tl, kt, (int)blockIdx.y, (int)blockIdx.x);
   const double t = tl.scal[SCS * g.m];
   // no prediction for the next step unless this step's window step makes one (later in the stream)
-  if (SPEC && threadIdx.x == 0) tl.pred[1 - (tl.ctl[3] & 1)][4 * blockIdx.x] = -1;
+  if (SPEC && threadIdx.x == 0) tl.pred[1 - (tl.ctl[3] & 1)][4 * kt] = -1;
   if (tl.mctl[MCS * g.m + 1] == 0 && t < t_end) {  // else the member does not step (uniform in the CTA)
     double dt = tl.scal[SCS * g.m + 1];
     if (t + dt > t_end) dt = t_end - t;  // as step_body
