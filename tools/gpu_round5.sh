@@ -23,4 +23,4 @@ run c4 --workload C4
 run c3 --workload C3 --no-cpu
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r5_ncu_launches_c4.csv python bench.py --workload C4 --steps 60 --warmup 3 --no-cpu --no-e2e > gpurun_out/r5_ncu_c4.log 2>&1; echo "ncu c4 rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r5_ncu_launches_c5.csv python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e > gpurun_out/r5_ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tiled_fast -s 40 -c 1 -o gpurun_out/r5_ncu_full_tiled_fast python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e > gpurun_out/r5_ncu_full.log 2>&1; echo "ncu full rc=$?"; ls -la gpurun_out/r5_ncu_full_tiled_fast.ncu-rep
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tiled_fast -s 15 -c 1 -o gpurun_out/r5_ncu_full_tiled_fast python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e > gpurun_out/r5_ncu_full.log 2>&1; echo "ncu full rc=$?"; ls -la gpurun_out/r5_ncu_full_tiled_fast.ncu-rep
