@@ -66,6 +66,7 @@ struct eis_ctx {
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_mctl = nullptr, *t_slow, *t_wlist;
   int *t_pred[2] = {nullptr, nullptr}, *t_plist[2] = {nullptr, nullptr}, *t_mlist = nullptr;  // window prediction (Tiles::spec)
   int win_grid_early = 0;                  //   CTAs of the early part A (beside tiled_fast)
+  int fast_plain = 1, fast_one = 1;        // tiled_fast instantiations (EIS_FAST_PLAIN / EIS_FAST_ONE = 0: the general ones)
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
@@ -440,6 +441,8 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->win_grid_early = std::max(nsm, 1) * (M > 1 ? 8 : 16);  // (C5: 16 per SM 1.35 ms/step, 8: 1.46, 4: 1.55; C4: 8 0.591, 16 0.597)
   if (const char* ev = getenv("EIS_WIN_EARLY_PER_SM")) c->win_grid_early = std::max(1, atoi(ev)) * std::max(1, nsm);
   c->win_grid_early = (int)std::min<long long>(ntiles, c->win_grid_early);
+  if (const char* ev = getenv("EIS_FAST_PLAIN")) c->fast_plain = atoi(ev) != 0;
+  if (const char* ev = getenv("EIS_FAST_ONE")) c->fast_one = atoi(ev) != 0;
   if (ok && split)
     ok = cudaMalloc(&c->t_djobs, (size_t)djcap * sizeof(DtsJob)) == cudaSuccess &&
          cudaMalloc(&c->t_wsave, (size_t)ntiles * WSAVE * (spec ? 2 : 1)) == cudaSuccess;
@@ -925,9 +928,8 @@ static void tiled_launch(eis_ctx* c, double t_end) {
     cudaEventRecord(c->ev_join, c->stream2);
     dbg_sync(c, "early part A + dts_jobs");
   }
-  static const int plain_ok = getenv("EIS_FAST_PLAIN") ? atoi(getenv("EIS_FAST_PLAIN")) : 1;
+  const int plain_ok = c->fast_plain, one_ok = c->fast_one;
   const bool plain = plain_ok && !c->tl.nbr_left && !c->tl.nbr_right && !c->tl.poll;  // (no exchange buffer, no polling kernel)
-  static const int one_ok = getenv("EIS_FAST_ONE") ? atoi(getenv("EIS_FAST_ONE")) : 1;
   const bool one = one_ok && plain && c->tl.M == 1;
   if (one && c->tl.spec)
     tiled_fast<EIS_FAST_T, EIS_FAST_MINB, true, true, 1><<<c->tl.ntiles, EIS_FAST_T, c->smem_fast, c->stream>>>(c->e, c->p, c->tl, t_end);

@@ -1231,3 +1231,30 @@ def test_window_prediction_defaults_and_resets(P, monkeypatch):
     np.testing.assert_array_equal(v["rho"], g["rho"][0, :n1])
     np.testing.assert_array_equal(v["mom"], g["mom"][0, :n1])
     np.testing.assert_array_equal(v["h"], g["h"][0, :n1])
+
+
+@pytest.mark.parametrize("cfg", ["c5_65k", "c4"])
+def test_tiled_fast_instantiations_agree(P, cfg, monkeypatch):
+    """tiled_fast is instantiated per kind of context (DESIGN 6.2: without the rank-mode / polling
+    code, with the tile geometry of one grid or of a 2D ensemble launch, with or without the
+    prediction code); the general instantiations (EIS_FAST_ONE=0, EIS_FAST_PLAIN=0) run the same
+    arithmetic: states, clocks and counters bit for bit equal."""
+    if cfg == "c4":
+        w = W.c4(members=np.array([0, 1, 2, 3, 5, 777, 9999, 12345]))
+        steps = 80
+    else:
+        w = W.c5(n_cells=1 << 16)
+        steps = 60
+    out = []
+    for one, plain, spec in (("1", "1", "1"), ("0", "1", "1"), ("0", "0", "1"), ("1", "1", "0"), ("0", "0", "0")):
+        monkeypatch.setenv("EIS_FAST_ONE", one)
+        monkeypatch.setenv("EIS_FAST_PLAIN", plain)
+        monkeypatch.setenv("EIS_WIN_SPEC", spec)
+        g, _ = gpu_run(P, w, steps=steps, layout=P.LAYOUT_TILED)
+        out.append(g)
+    a = out[0]
+    assert a["stats"]["creations"] > 0
+    for b in out[1:]:
+        assert a["stats"] == b["stats"]
+        for k in ("status", "n", "t", "rho", "mom", "h"):
+            np.testing.assert_array_equal(a[k], b[k])
