@@ -66,7 +66,7 @@ struct eis_ctx {
   int *t_cnt[2], *t_hu[2], *t_ctl, *t_mctl = nullptr, *t_slow, *t_wlist;
   int *t_pred[2] = {nullptr, nullptr}, *t_plist[2] = {nullptr, nullptr}, *t_mlist = nullptr;  // window prediction (Tiles::spec)
   int win_grid_early = 0;                  //   CTAs of the early part A (beside tiled_fast)
-  int fast_plain = 1, fast_one = 1;        // tiled_fast instantiations (EIS_FAST_PLAIN / EIS_FAST_ONE = 0: the general ones)
+  int fast_plain, fast_one;                // tiled_fast instantiations (EIS_FAST_PLAIN / EIS_FAST_ONE = 0: the general ones)
   long long* t_wdbg = nullptr;
   double *t_part2, *t_partf;
   int slow_grid, win_grid, win_grid_poll;
@@ -441,6 +441,7 @@ static eis_status create_tiled(eis_ctx* c, eis_ctx** out) {
   c->win_grid_early = std::max(nsm, 1) * (M > 1 ? 8 : 16);  // (C5: 16 per SM 1.35 ms/step, 8: 1.46, 4: 1.55; C4: 8 0.591, 16 0.597)
   if (const char* ev = getenv("EIS_WIN_EARLY_PER_SM")) c->win_grid_early = std::max(1, atoi(ev)) * std::max(1, nsm);
   c->win_grid_early = (int)std::min<long long>(ntiles, c->win_grid_early);
+  c->fast_plain = 1; c->fast_one = 1;  // (eis_create zero-fills the context: defaults are set here)
   if (const char* ev = getenv("EIS_FAST_PLAIN")) c->fast_plain = atoi(ev) != 0;
   if (const char* ev = getenv("EIS_FAST_ONE")) c->fast_one = atoi(ev) != 0;
   if (ok && split)
